@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the Hilbert-reordered SEM leapfrog step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One "step" = one leapfrog time step of the whole hot path (stiffness apply with
+gather + conflict-free scatter, M^-1 scaling, Ricker source, update) over the
+configured mesh.  Workload: BASELINE.json configs[3] (C4, 2048 x 2048 cells per
+GPU, P3) -- the weak-scaling configuration the metric's 1/2/4/8-GPU numbers and
+the >= 60 % HBM roofline target are quoted on; its per-step working set
+(~1.75 GB) is far larger than the 126 MB L2, so no flush is needed between
+steps.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "element-updates/sec per time step and achieved HBM GB/s fraction, 1/2/4/8 B200"
+UNIT = "element-updates/s"
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def problem_for(name: str, world: int):
+    from paper_2104_08416_b200 import meshgen as mg
+    return mg.config(name, 1, gpus=world) if name == "C4" else mg.config(name, 1)
+
+
+def k7_bytes(info):
+    """Algorithmic bytes per launch of K7 / K8."""
+    E, Np, N = info["n_elements"], info["nodes_per_elem"], info["n_nodes"]
+    Nint, Nsh = info["n_interior_nodes"], info["n_shared_nodes"]
+    k7 = E * (4 * Np + 24) + 8 * N + 24 * Nint
+    k8 = 24 * Nsh
+    return float(k7), float(k8)
+
+
+def run_ours(args):
+    import torch
+    from paper_2104_08416_b200 import sem as S
+    from paper_2104_08416_b200 import meshgen as mg
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = args.gpus if world == 1 else world
+    torch.cuda.set_device(local)
+    dist = None
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    peak, peak_src, peaks = load_peak()
+
+    pb = problem_for(args.config, 1)  # replicas: every rank runs the per-GPU workload
+    m = pb.mesh
+    ctx = S.SemContext(local, stream=stream.cuda_stream)
+    r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
+    ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt)
+    info = ctx.sem_get_info()
+    E = info["n_elements"]
+
+    # warm-up (untimed)
+    ctx.sem_step_n(args.warmup)
+    ctx.sem_sync()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ctx.sem_set_kernel_timing(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0.record(stream)
+    ctx.sem_step_n(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    kt = ctx.sem_kernel_times()
+    ctx.sem_set_kernel_timing(False)
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    U, nstep = ctx.sem_read_field()
+    finite = bool(np.isfinite(U).all())
+
+    ms_step = ms / args.steps
+    value = E * world * args.steps / (ms / 1e3)
+    b7, b8 = k7_bytes(info)
+    k7_avg = kt["k7_ms"] / max(kt["k7_launches"], 1)
+    k8_avg = kt["k8_ms"] / max(kt["k8_launches"], 1)
+    achieved = b7 / (k7_avg * 1e-3) / 1e9
+    step_gbs = info["bytes_alg_per_step"] / (ms_step * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded meshgen recipe, DESIGN.md)",
+        "config": {"workload": "%s: %s" % (args.config, WORKLOADS.get(args.config, "")),
+                   "elements_per_gpu": E, "nodes_per_gpu": info["n_nodes"], "degree": pb.P,
+                   "ordering": "hilbert elements + first-touch nodes", "parallelism": "replicas" if world > 1 else "1 GPU",
+                   "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (info["bytes_alg_per_step"] / 1e9),
+                   "chunk_elems": info["chunk_elems"], "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
+                   "max_colors": info["max_colors"], "dt": pb.dt},
+        "roofline": {"bound": "hbm", "kernel": "k7_step (stiffness apply + fused leapfrog)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_src, "traffic": None,
+                     "bytes_per_launch": b7, "avg_launch_ms": k7_avg,
+                     "k7_share_of_step": kt["k7_ms"] / max(ms, 1e-9),
+                     "k8_avg_launch_ms": k8_avg, "k8_bytes_per_launch": b8},
+        "step_alg_gbs": step_gbs, "step_alg_frac": step_gbs / peak,
+        "step_alg_frac_of_8tbs": step_gbs / 8000.0,
+        "gpu_launches": int(kt["k7_launches"] + kt["k8_launches"]),
+        "clocks": clk,
+        "prep_ms": {"mesh_reorder": info["prep_reorder_ms"], "build_operators": info["prep_build_ms"]},
+        "field_finite": finite,
+    }
+    if rank == 0 and args.orderings and world == 1:
+        out["orderings"] = orderings(ctx, pb, args, S)
+    if rank == 0 and args.e2e:
+        out["e2e"] = e2e(pb, args, S, local, stream)
+    ctx.close()
+    if rank == 0 and world == 1 and args.cpu:
+        out["cpu_baseline"] = cpu_baseline(pb)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+WORKLOADS = {
+    "C1": "32x32 cells [0,1]^2 +-0.2h jitter, P2, c=1, Ricker 10 Hz",
+    "C2": "512x512 cells [0,4000]^2 m +-0.25h jitter, P3, c=2000 m/s, Ricker 15 Hz",
+    "C3": "graded 2000x1000 cells over [0,8000]x[0,4000] m, 3 layers, P3, Ricker 10 Hz",
+    "C4": "2048x2048 cells per GPU (h=7.8125 m) +-0.25h jitter, P3, c=2000 m/s, Ricker 15 Hz",
+    "C5": "graded 16384x8192 cells, 10 random layers, P2, Ricker 10 Hz",
+}
+
+
+def orderings(ctx, pb, args, S):
+    """Hilbert vs random vs natural, same physical mesh (1 GPU)."""
+    import torch
+    res = {}
+    K = max(50, min(args.steps, 400))
+    variants = [
+        ("hilbert", pb.mesh, pb.c, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH),
+        ("hilbert_canonical_nodes", pb.mesh, pb.c, S.SEM_ORDER_HILBERT, S.SEM_NODES_CANONICAL),
+        ("natural", pb.natural, pb.c_natural, S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
+        ("random", pb.mesh, pb.c, S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
+    ]
+    stream = torch.cuda.current_stream()
+    for name, m, c, eo, no in variants:
+        ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, eo, no)
+        src = pb.src_vertex if m is pb.mesh else int(pb.mesh.vert_perm[pb.src_vertex])
+        ctx.sem_build_operators(c, src, pb.f0, pb.t0, pb.amplitude, pb.dt)
+        ctx.sem_step_n(5)
+        ctx.sem_set_kernel_timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ctx.sem_step_n(K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / K
+        kt = ctx.sem_kernel_times()
+        ctx.sem_set_kernel_timing(False)
+        info = ctx.sem_get_info()
+        res[name] = {"element_updates_per_s": info["n_elements"] / (ms * 1e-3), "ms_per_step": ms,
+                     "alg_gbs": info["bytes_alg_per_step"] / (ms * 1e-3) / 1e9,
+                     "k7_ms": kt["k7_ms"] / max(kt["k7_launches"], 1),
+                     "k8_ms": kt["k8_ms"] / max(kt["k8_launches"], 1),
+                     "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
+                     "max_chunk_nodes": info["max_chunk_nodes"], "steps": K}
+    return res
+
+
+def e2e(pb, args, S, device, stream):
+    """The whole job through the public C ABI from pinned host buffers:
+    mesh H2D + reorder + operators + K steps + field D2H, timed on the host
+    around synchronising calls (inputs start in host memory)."""
+    import torch
+    m = pb.mesh
+    vxy = torch.from_numpy(m.vxy).pin_memory()
+    tri = torch.from_numpy(m.tri).pin_memory()
+    c = torch.from_numpy(pb.c).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx = S.SemContext(device, stream=stream.cuda_stream)
+    r = ctx.sem_mesh_reorder(vxy.numpy(), tri.numpy(), pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
+    ctx.sem_build_operators(c.numpy(), pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt)
+    out = torch.empty(r["n_nodes"], dtype=torch.float64).pin_memory()
+    ctx.sem_step_n(args.steps)
+    ctx.sem_read_field(out=out.numpy())
+    t1 = time.perf_counter()
+    ctx.close()
+    E = m.ne
+    h2d = m.vxy.nbytes + m.tri.nbytes + pb.c.nbytes
+    d2h = out.numel() * 8 + E * 8 + r["n_nodes"] * 4
+    return {"value": E * args.steps / (t1 - t0), "unit": UNIT, "seconds": t1 - t0,
+            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+            "includes": "sem_mesh_reorder + sem_build_operators + sem_step_n(K) + sem_read_field"}
+
+
+def cpu_baseline(pb, steps=2):
+    """The oracle, as it stands, on this host's cores: a bounded sample of the
+    same workload (a few leapfrog steps of the full mesh)."""
+    from oracle import core
+    from oracle.core import OracleSEM
+    m = pb.mesh
+    t0 = time.perf_counter()
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    setup = time.perf_counter() - t0
+    o.leapfrog(pb.dt, 1, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)  # warm-up
+    t0 = time.perf_counter()
+    o.leapfrog(pb.dt, steps, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
+    dt = time.perf_counter() - t0
+    return {"value": m.ne * steps / dt, "unit": UNIT, "cores": core.num_threads(), "kind": "oracle",
+            "sample": "%d leapfrog steps of the full %s mesh (%d elements), oracle setup %.1f s excluded"
+                      % (steps, pb.name, m.ne, setup),
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the reference arm of this tier), timed as it
+    stands on the host cores, on a bounded sample of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import core
+    from oracle.core import OracleSEM
+    from paper_2104_08416_b200 import meshgen as mg
+    # sample: the same recipe at reduced size so W + K oracle steps take ~1-2 min
+    budget_s = 90.0
+    scale = 1
+    nthr = core.num_threads()
+    per_elem_s = 1.2e-6 / max(nthr, 1)  # rough oracle cost per element-update
+    while (2048 // scale) ** 2 * 2 * per_elem_s * (args.steps + args.warmup) > budget_s and scale < 256:
+        scale *= 2
+    pb = mg.config(args.config, scale) if args.config != "C4" else mg.config("C4", scale)
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    U, Up = o.leapfrog(pb.dt, args.warmup, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
+    t0 = time.perf_counter()
+    o.leapfrog(pb.dt, args.steps, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0, U=U, Uprev=Up,
+               step0=args.warmup)
+    dt = time.perf_counter() - t0
+    value = m.ne * args.steps / dt
+    sample = "%s recipe at 1/%d cell count per axis (%d elements), %d steps" % (args.config, scale, m.ne, args.steps)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": "%s: %s" % (args.config, WORKLOADS.get(args.config, "")),
+                                           "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthr, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-orderings", dest="orderings", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,214 @@
+/*
+ * sem.h -- C ABI of libsem.so, the B200 (sm_100a) hot path of arxiv 2104.08416:
+ * the explicit spectral-element leapfrog step for the 2D acoustic wave equation
+ * on unstructured triangles, after the mesh is reordered along a generalized
+ * Hilbert curve.
+ *
+ * Call order (the paper's problem statement, PAPER.md:540 mesh -> SEM nodes,
+ * :296-321 reorder, :240-263 operators, :269 explicit stepping):
+ *
+ *   sem_create -> sem_mesh_reorder -> sem_build_operators -> sem_step_n* ->
+ *   sem_read_field -> sem_free
+ *
+ * Conventions (all entry points):
+ *  - Pointers named *_host are HOST memory, borrowed for the duration of the
+ *    call only; the library copies what it needs.  Outputs are caller-allocated.
+ *    Device memory is owned by the context and released by sem_free.
+ *  - Index arrays are int32 (E*Np and N must be < 2^31).
+ *  - Every call returns a sem_status; on error sem_last_error() holds a message
+ *    naming the element, node or step involved.  SEM_E_CUDA is sticky: the
+ *    context is unusable afterwards.  No C++ exception crosses the ABI.
+ *  - Work is enqueued on the context's CUDA stream; calls that return host
+ *    data synchronise that stream.
+ *  - A context is not thread-safe; use one per process/GPU.
+ *  - There is no CPU fallback: without a usable sm_100 device sem_create fails.
+ */
+#ifndef SEM_H
+#define SEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sem_ctx sem_ctx;
+
+typedef enum {
+    SEM_OK = 0,
+    SEM_E_ARG = 1,          /* invalid argument (range, NULL, c <= 0, dt <= 0 ...) */
+    SEM_E_STATE = 2,        /* call out of order (e.g. step before build)          */
+    SEM_E_MESH = 3,         /* degenerate / inconsistent mesh                      */
+    SEM_E_UNSUPPORTED = 4,  /* degree not in {2, 3}, unknown ordering ...           */
+    SEM_E_CUDA = 5,         /* CUDA error (sticky)                                 */
+    SEM_E_NCCL = 6,         /* NCCL error                                          */
+    SEM_E_OOM = 7,          /* device or host allocation failed                    */
+    SEM_E_NONFINITE = 8     /* non-finite value in the field (step index in msg)   */
+} sem_status;
+
+/* Element orderings (§6.1).  INPUT = the paper's "None"
+ * (file order); HILBERT = §4.3 steps 1-4; RANDOM = stable
+ * sort of element ids by splitmix64(seed ^ id) (reading R16). */
+enum { SEM_ORDER_INPUT = 0, SEM_ORDER_HILBERT = 1, SEM_ORDER_RANDOM = 2 };
+
+/* Node numberings.  FIRST_TOUCH = PAPER.md:316 step 1 (each node gets the next
+ * label the first time an element in the new order touches it); CANONICAL =
+ * the input numbering of DESIGN.md reading R13 (vertex ids, then edge nodes,
+ * then interior nodes). */
+enum { SEM_NODES_FIRST_TOUCH = 0, SEM_NODES_CANONICAL = 2 };
+
+/* Numbering of node arrays crossing the ABI (read_field / write_state).
+ * CANONICAL = reading R13 input numbering; INTERNAL = the reordered labels
+ * chosen by sem_mesh_reorder (node_perm_out maps them to CANONICAL). */
+enum { SEM_NUMBERING_CANONICAL = 0, SEM_NUMBERING_INTERNAL = 1 };
+
+/*
+ * Create a context on CUDA device `device`.
+ *  rank, world_size : this process's place in a multi-GPU run (world_size = 1
+ *                     for one GPU).  world_size > 1 requires nccl_unique_id.
+ *  nccl_unique_id   : 128-byte ncclUniqueId from rank 0 (NULL iff world_size==1).
+ *  cuda_stream      : cudaStream_t to enqueue on (e.g. torch's current stream),
+ *                     or NULL for a stream owned by the context.
+ * Errors: SEM_E_ARG (bad rank/world/device), SEM_E_CUDA (no sm_100 device),
+ *         SEM_E_UNSUPPORTED (world_size > 1 in a build without NCCL).
+ */
+sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
+                      const void *nccl_unique_id, void *cuda_stream);
+
+/* Release every device buffer and the context.  NULL is a no-op. */
+void sem_free(sem_ctx *ctx);
+
+/* Last error message of this context ("" if none).  Owned by the context. */
+const char *sem_last_error(const sem_ctx *ctx);
+
+/*
+ * Build the SEM mesh and reorder it.
+ *
+ *  vxy_host   [n_vertices][2] fp64 vertex coordinates.
+ *  tri_host   [n_elements][3] int32 vertex ids of linear triangles.  A
+ *             clockwise triangle is fixed by swapping its 2nd and 3rd vertex
+ *             (the centroid used for the SFC key is taken before the fix).
+ *  degree     polynomial order P in {2, 3}: Np = 6 or 10 local nodes,
+ *             placed per DESIGN.md reading R3 (P2 midpoints; P3 Gauss-Lobatto
+ *             edge points + centroid).
+ *  elem_order SEM_ORDER_*.  HILBERT follows PAPER.md:299-305: centroids ->
+ *             bounding box w_b = ceil(sqrt(E)), h_b = ceil(sqrt(E)/r) of the
+ *             vertex extents (r = w_m/h_m) -> generalized Hilbert curve over
+ *             w_b x h_b (docs/hilbert.md) -> elements sorted stably by the
+ *             curve position of their centroid's sub-rectangle.
+ *  node_order SEM_NODES_* (PAPER.md:312-321 first part; reading R12).
+ *  seed       used by SEM_ORDER_RANDOM only.
+ *
+ * Outputs (caller-allocated host memory, any may be NULL):
+ *  hilbert_key_out [E]  curve position of each element (INPUT numbering);
+ *                       zeros unless elem_order == HILBERT.
+ *  elem_perm_out   [E]  elem_perm_out[k] = input id of the element placed k-th.
+ *  node_perm_out   [N]  node_perm_out[i] = canonical id of internal node i.
+ *                       (N is not known before the call: pass NULL and read
+ *                       n_nodes_out, or size it as V + 3E(P-1) + E*nI.)
+ *  n_nodes_out          N, the number of global SEM nodes.
+ *  grid_wh_out     [2]  (w_b, h_b) for HILBERT, else (0, 0).
+ *
+ * Errors: SEM_E_UNSUPPORTED (degree, ordering), SEM_E_MESH ("element e has zero
+ * area", "vertex v is not used by any element"), SEM_E_ARG, SEM_E_CUDA, SEM_E_OOM.
+ * Resets any operators/state of an earlier mesh.
+ */
+sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vertices,
+                            const int32_t *tri_host, int64_t n_elements, int degree,
+                            int elem_order, int node_order, uint64_t seed,
+                            uint32_t *hilbert_key_out, int32_t *elem_perm_out,
+                            int32_t *node_perm_out, int64_t *n_nodes_out,
+                            int32_t grid_wh_out[2]);
+
+/*
+ * Build the per-element operators and the lumped mass (PAPER.md:163-171 element
+ * map, :206 inverse Jacobian, :240-250 lumped M-bar), and set the source.
+ *
+ *  c_elem_host [E] wave speed per element, INPUT element numbering, > 0.
+ *              Reading R2: M^(e) = 1, F^(e) = c_e^2 I, B = -I, so
+ *              the element stiffness is K^e = sum_ab G_ab S_ab with
+ *              G = c^2 detJ J^-1 J^-T (reading R5).
+ *  src_vertex  input vertex id (= canonical node id) of the Ricker point source
+ *              (Algorithm 3); -1 for no source.
+ *  f0, t0, amplitude: source A * r(t), r(t) = (1 - 2 pi^2 f0^2 tau^2)
+ *              exp(-pi^2 f0^2 tau^2), tau = t - t0 (reading R7).
+ *  dt          time step (> 0), used as dt^2 / M-bar.
+ * Resets the state to U^0 = U^-1 = 0 at step 0.
+ * Errors: SEM_E_STATE (no mesh), SEM_E_ARG (c <= 0 names the element, dt <= 0,
+ * src out of range), SEM_E_CUDA.
+ */
+sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t src_vertex,
+                               double f0, double t0, double amplitude, double dt);
+
+/*
+ * Advance n_steps leapfrog steps (north_star; reading R1):
+ *   U^{n+1} = 2 U^n - U^{n-1} + (dt^2 / M-bar) (A r(n dt) e_src - K U^n)
+ * where K U^n is the element-by-element stiffness apply with gather and
+ * conflict-free scatter (Algorithms 1-2, fused).
+ * Enqueued on the context stream; returns without synchronising.
+ * Errors: SEM_E_STATE (no operators), SEM_E_ARG (n_steps < 0), SEM_E_CUDA.
+ */
+sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps);
+
+/*
+ * Copy U^n to out_host[N] (fp64) in the requested numbering and return the
+ * step index n.  Synchronises.  Errors: SEM_E_STATE, SEM_E_ARG, SEM_E_CUDA,
+ * SEM_E_NONFINITE ("non-finite field at step n").
+ */
+sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t *step_out);
+
+/*
+ * Test/checkpoint hook: overwrite (U^n, U^{n-1}) from host arrays [N] in the
+ * given numbering; the step index is left unchanged.  Either pointer may be
+ * NULL to set that array to zero.  Errors: SEM_E_STATE, SEM_E_ARG, SEM_E_CUDA.
+ */
+sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double *u_prev_host,
+                           int numbering);
+
+/* Set the step index n (used with sem_write_state to resume a run). */
+sem_status sem_set_step(sem_ctx *ctx, int64_t step);
+
+/* Synchronise the context stream and surface asynchronous errors. */
+sem_status sem_sync(sem_ctx *ctx);
+
+/* Descriptive numbers of the built problem (for the bench and tests). */
+typedef struct {
+    int64_t n_elements;       /* E (this rank) */
+    int64_t n_nodes;          /* N (this rank's local nodes) */
+    int64_t n_nodes_global;   /* N of the whole mesh */
+    int32_t degree;           /* P */
+    int32_t nodes_per_elem;   /* Np */
+    int64_t n_chunks;         /* CTAs of the step kernel */
+    int32_t chunk_elems;      /* elements per chunk */
+    int32_t max_chunk_nodes;  /* largest chunk-local node table */
+    int64_t n_interior_nodes; /* finalised inside the step kernel */
+    int64_t n_shared_nodes;   /* finalised by the fix-up kernel */
+    int64_t n_partial_slots;  /* partial sums written per step */
+    int32_t max_colors;       /* largest per-chunk colour count */
+    int32_t launches_per_step;/* kernels launched per leapfrog step */
+    int64_t step;             /* current step index n */
+    double bytes_alg_per_step;/* E (4 Np + 24) + 32 N */
+    double prep_reorder_ms;   /* last sem_mesh_reorder wall time */
+    double prep_build_ms;     /* last sem_build_operators wall time */
+} sem_info;
+
+sem_status sem_get_info(sem_ctx *ctx, sem_info *out);
+
+/*
+ * Kernel timing: when enabled, CUDA events on the context stream bracket every
+ * launch of the stiffness/update kernel (K7) and the fix-up kernel (K8);
+ * sem_kernel_times returns their accumulated device milliseconds and launch
+ * counts since the last reset.  Synchronises.
+ */
+sem_status sem_set_kernel_timing(sem_ctx *ctx, int enable);
+sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches,
+                            double *k8_ms, int64_t *k8_launches);
+
+/* Library version string. */
+const char *sem_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_H */

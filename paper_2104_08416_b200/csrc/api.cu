@@ -1,0 +1,627 @@
+// api.cu -- the C ABI of libsem.so (include/sem.h).  Orchestrates the kernels
+// of reorder.cu / step.cu and owns all device memory of a context.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.h"
+#include "sem.h"
+#include "sem_internal.h"
+
+using namespace sem;
+
+namespace {
+int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
+constexpr int kChunkElems = 256;
+}  // namespace
+
+struct sem_ctx {
+    int device = 0, rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    bool dead = false;
+
+    // mesh
+    bool have_mesh = false, have_ops = false;
+    int P = 0, Np = 0;
+    int64_t nv = 0, E = 0, N = 0;
+    int32_t grid[2] = {0, 0};
+    RefTables T;
+    std::vector<void *> mesh_allocs, ops_allocs;
+    double *d_vxy = nullptr;
+    int32_t *d_tri_or = nullptr;  // oriented triangles, INPUT order
+    int32_t *d_perm = nullptr;    // new -> input
+    int32_t *d_int_to_can = nullptr, *d_int_to_ft = nullptr;
+    std::vector<int32_t> can_to_int;
+    DevChunks dch{};
+    ChunkMeta meta_info;  // counts only (vectors released after upload)
+
+    // operators / state
+    double *d_Grr = nullptr, *d_Gss = nullptr, *d_Grs = nullptr, *d_dt2M = nullptr;
+    double *d_U[2] = {nullptr, nullptr};
+    double *d_partial = nullptr;
+    int cur = 0;
+    int32_t src_int = -1;
+    double amp = 0, f0 = 1, t0 = 0, dt = 0;
+    int64_t step = 0;
+
+    // timing
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev7, ev8, pool;
+    double t7 = 0, t8 = 0;
+    int64_t n7 = 0, n8 = 0;
+    double prep_reorder_ms = 0, prep_build_ms = 0;
+};
+
+namespace {
+
+sem_status fail(sem_ctx *c, sem_status s, const std::string &msg) {
+    c->err = msg;
+    return s;
+}
+
+sem_status cuda_fail(sem_ctx *c, cudaError_t e, const char *where) {
+    c->dead = true;
+    c->err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    return SEM_E_CUDA;
+}
+
+#define CK(call)                                                        \
+    do {                                                                \
+        cudaError_t _e = (call);                                        \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call);        \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(std::vector<void *> &list, T **p, size_t count) {
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, sizeof(T) * (count ? count : 1));
+    if (e != cudaSuccess) return e;
+    list.push_back(q);
+    *p = (T *)q;
+    return cudaSuccess;
+}
+
+void free_list(std::vector<void *> &l) {
+    for (void *p : l) cudaFree(p);
+    l.clear();
+}
+
+void reset_ops(sem_ctx *ctx) {
+    free_list(ctx->ops_allocs);
+    ctx->d_Grr = ctx->d_Gss = ctx->d_Grs = ctx->d_dt2M = nullptr;
+    ctx->d_U[0] = ctx->d_U[1] = nullptr;
+    ctx->d_partial = nullptr;
+    ctx->have_ops = false;
+    ctx->step = 0;
+    ctx->cur = 0;
+}
+
+void reset_mesh(sem_ctx *ctx) {
+    reset_ops(ctx);
+    free_list(ctx->mesh_allocs);
+    ctx->have_mesh = false;
+    ctx->can_to_int.clear();
+    ctx->dch = DevChunks{};
+}
+
+double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+template <typename T>
+cudaError_t upload(std::vector<void *> &list, T **dst, const std::vector<T> &src, cudaStream_t s) {
+    cudaError_t e = dalloc(list, dst, src.size());
+    if (e != cudaSuccess) return e;
+    if (src.empty()) return cudaSuccess;
+    return cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s);
+}
+
+sem_status ensure_tables(sem_ctx *ctx) {
+    if (g_const_P != ctx->P) {
+        CK(upload_ref_tables(ctx->T, ctx->stream));
+        g_const_P = ctx->P;
+    }
+    return SEM_OK;
+}
+
+sem_status record(sem_ctx *ctx, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &list, bool start) {
+    if (start) {
+        std::pair<cudaEvent_t, cudaEvent_t> ev;
+        if (!ctx->pool.empty()) { ev = ctx->pool.back(); ctx->pool.pop_back(); }
+        else {
+            CK(cudaEventCreate(&ev.first));
+            CK(cudaEventCreate(&ev.second));
+        }
+        list.push_back(ev);
+        CK(cudaEventRecord(ev.first, ctx->stream));
+    } else {
+        CK(cudaEventRecord(list.back().second, ctx->stream));
+    }
+    return SEM_OK;
+}
+
+sem_status drain_events(sem_ctx *ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto *lst : {&ctx->ev7, &ctx->ev8}) {
+        for (auto &ev : *lst) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ev.first, ev.second));
+            if (lst == &ctx->ev7) { ctx->t7 += ms; ctx->n7++; }
+            else { ctx->t8 += ms; ctx->n8++; }
+            ctx->pool.push_back(ev);
+        }
+        lst->clear();
+    }
+    return SEM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sem_version(void) { return "sem-hilbert-b200 0.1 (sm_100a)"; }
+
+sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
+                      const void *nccl_unique_id, void *cuda_stream) {
+    if (!out) return SEM_E_ARG;
+    *out = nullptr;
+    if (world_size < 1 || rank < 0 || rank >= world_size || device < 0) return SEM_E_ARG;
+    if (world_size > 1) return SEM_E_UNSUPPORTED;  // multi-GPU halo: not in this build yet
+    (void)nccl_unique_id;
+    sem_ctx *ctx = new (std::nothrow) sem_ctx();
+    if (!ctx) return SEM_E_OOM;
+    ctx->device = device;
+    ctx->rank = rank;
+    ctx->world = world_size;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device >= ndev) {
+        *out = ctx;
+        ctx->dead = true;
+        ctx->err = "no CUDA device available (libsem has no CPU fallback)";
+        return SEM_E_CUDA;
+    }
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess || prop.major != 10) {
+        *out = ctx;
+        ctx->dead = true;
+        ctx->err = "device is not sm_100 (B200); this library is built for sm_100a only";
+        return SEM_E_CUDA;
+    }
+    if ((e = cudaSetDevice(device)) != cudaSuccess) {
+        *out = ctx;
+        return cuda_fail(ctx, e, "cudaSetDevice");
+    }
+    if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
+    else {
+        if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            *out = ctx;
+            return cuda_fail(ctx, e, "cudaStreamCreate");
+        }
+        ctx->own_stream = true;
+    }
+    *out = ctx;
+    return SEM_OK;
+}
+
+void sem_free(sem_ctx *ctx) {
+    if (!ctx) return;
+    if (!ctx->dead) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+    }
+    reset_mesh(ctx);
+    for (auto *lst : {&ctx->ev7, &ctx->ev8, &ctx->pool})
+        for (auto &ev : *lst) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *sem_last_error(const sem_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vertices,
+                            const int32_t *tri_host, int64_t n_elements, int degree,
+                            int elem_order, int node_order, uint64_t seed,
+                            uint32_t *hilbert_key_out, int32_t *elem_perm_out,
+                            int32_t *node_perm_out, int64_t *n_nodes_out,
+                            int32_t grid_wh_out[2]) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    if (degree != 2 && degree != 3)
+        return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) + " (2 or 3)");
+    if (elem_order < 0 || elem_order > 2)
+        return fail(ctx, SEM_E_UNSUPPORTED, "unknown element ordering " + std::to_string(elem_order));
+    if (node_order != SEM_NODES_FIRST_TOUCH && node_order != SEM_NODES_CANONICAL)
+        return fail(ctx, SEM_E_UNSUPPORTED, "unknown node ordering " + std::to_string(node_order));
+    if (!vxy_host || !tri_host || n_vertices < 3 || n_elements < 1)
+        return fail(ctx, SEM_E_ARG, "empty or missing mesh arrays");
+    const int Np = (degree + 1) * (degree + 2) / 2;
+    if (n_elements * Np >= (int64_t)INT_MAX || n_vertices >= INT_MAX)
+        return fail(ctx, SEM_E_ARG, "mesh too large for 32-bit indices");
+    for (int64_t i = 0; i < 3 * n_elements; i++)
+        if (tri_host[i] < 0 || tri_host[i] >= n_vertices)
+            return fail(ctx, SEM_E_MESH, "element " + std::to_string(i / 3) + " has a vertex id out of range");
+    try {
+        CK(cudaSetDevice(ctx->device));
+        reset_mesh(ctx);
+        const double t_start = now_ms();
+        cudaStream_t s = ctx->stream;
+        ctx->P = degree;
+        ctx->Np = Np;
+        ctx->nv = n_vertices;
+        ctx->E = n_elements;
+        if (!build_ref_tables(degree, ctx->T)) return fail(ctx, SEM_E_UNSUPPORTED, "reference tables");
+        const int64_t E = n_elements, nv = n_vertices;
+        std::vector<void *> tmp;  // freed at the end of this call
+        struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+
+        CK(dalloc(ctx->mesh_allocs, &ctx->d_vxy, 2 * nv));
+        CK(cudaMemcpyAsync(ctx->d_vxy, vxy_host, sizeof(double) * 2 * nv, cudaMemcpyHostToDevice, s));
+        int32_t *d_tri = nullptr, *d_bad = nullptr;
+        CK(dalloc(tmp, &d_tri, 3 * E));
+        CK(dalloc(tmp, &d_bad, 1));
+        CK(cudaMemcpyAsync(d_tri, tri_host, sizeof(int32_t) * 3 * E, cudaMemcpyHostToDevice, s));
+        CK(dalloc(ctx->mesh_allocs, &ctx->d_tri_or, 3 * E));
+        CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
+        CK(launch_orient(ctx->d_vxy, d_tri, E, ctx->d_tri_or, d_bad, s));
+        int32_t bad = 0;
+        CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has zero area");
+
+        // ---- element order (list L) ----
+        CK(dalloc(ctx->mesh_allocs, &ctx->d_perm, E));
+        int32_t *d_ids = nullptr;
+        CK(dalloc(tmp, &d_ids, E));
+        CK(launch_iota(d_ids, E, s));
+        ctx->grid[0] = ctx->grid[1] = 0;
+        if (elem_order == SEM_ORDER_INPUT) {
+            CK(cudaMemcpyAsync(ctx->d_perm, d_ids, sizeof(int32_t) * E, cudaMemcpyDeviceToDevice, s));
+            if (hilbert_key_out) std::memset(hilbert_key_out, 0, sizeof(uint32_t) * E);
+        } else if (elem_order == SEM_ORDER_HILBERT) {
+            double *d_bb = nullptr;
+            CK(dalloc(tmp, &d_bb, 4));
+            CK(launch_bbox(ctx->d_vxy, nv, d_bb, s));
+            double bb[4];
+            CK(cudaMemcpyAsync(bb, d_bb, sizeof(bb), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            // PAPER.md:301 step 2 with reading R9 (same operation order as written)
+            const double wm = bb[2] - bb[0], hm = bb[3] - bb[1];
+            if (!(wm > 0.0) || !(hm > 0.0)) return fail(ctx, SEM_E_MESH, "mesh has zero width or height");
+            const double r = wm / hm;
+            const double sq = std::sqrt((double)E);
+            const double wbd = std::ceil(sq), hbd = std::ceil(sq / r);
+            const int64_t wb = wbd < 1.0 ? 1 : (int64_t)wbd, hb = hbd < 1.0 ? 1 : (int64_t)hbd;
+            if (wb * hb > (int64_t)0xFFFFFFFFLL || wb > INT_MAX / 4 || hb > INT_MAX / 4)
+                return fail(ctx, SEM_E_ARG, "SFC grid too large");
+            const double ws = (double)wb / wm, hs = (double)hb / hm;
+            ctx->grid[0] = (int32_t)wb;
+            ctx->grid[1] = (int32_t)hb;
+            uint32_t *d_keys = nullptr, *d_keys2 = nullptr;
+            CK(dalloc(tmp, &d_keys, E));
+            CK(dalloc(tmp, &d_keys2, E));
+            CK(launch_hilbert_keys(ctx->d_vxy, d_tri, E, bb[0], bb[1], ws, hs, (int32_t)wb,
+                                   (int32_t)hb, d_keys, s));
+            int bits = 1;
+            while (bits < 32 && ((int64_t)1 << bits) < wb * hb) bits++;
+            CK(sort_pairs_u32(d_keys, d_ids, d_keys2, ctx->d_perm, E, bits, s));
+            if (hilbert_key_out)
+                CK(cudaMemcpyAsync(hilbert_key_out, d_keys, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, s));
+        } else {
+            uint64_t *d_k = nullptr, *d_k2 = nullptr;
+            CK(dalloc(tmp, &d_k, E));
+            CK(dalloc(tmp, &d_k2, E));
+            CK(launch_random_keys(E, seed, d_k, s));
+            CK(sort_pairs_u64(d_k, d_ids, d_k2, ctx->d_perm, E, 64, s));
+            if (hilbert_key_out) std::memset(hilbert_key_out, 0, sizeof(uint32_t) * E);
+        }
+
+        // ---- canonical SEM nodes, relabel ----
+        int32_t *d_mu_can = nullptr, *d_mu_new = nullptr, *d_mu_ft = nullptr, *d_node_perm = nullptr;
+        CK(dalloc(tmp, &d_mu_can, E * Np));
+        int64_t nedges = 0, nunused = 0;
+        int32_t first_unused = 0;
+        CK(canonical_nodes(ctx->d_tri_or, nv, E, degree, d_mu_can, &nedges, &nunused, &first_unused, s));
+        if (nunused)
+            return fail(ctx, SEM_E_MESH, "vertex " + std::to_string(first_unused) + " is not used by any element");
+        const int nI = (degree - 1) * (degree - 2) / 2;
+        const int64_t N = nv + nedges * (degree - 1) + E * nI;
+        if (N >= INT_MAX) return fail(ctx, SEM_E_ARG, "too many nodes for 32-bit indices");
+        ctx->N = N;
+        CK(dalloc(tmp, &d_mu_new, E * Np));
+        CK(launch_permute_rows(d_mu_can, ctx->d_perm, E, Np, d_mu_new, s));
+        CK(dalloc(tmp, &d_node_perm, N));
+        if (node_order == SEM_NODES_FIRST_TOUCH) {
+            CK(dalloc(tmp, &d_mu_ft, E * Np));
+            int64_t nl = 0;
+            CK(first_touch(d_mu_new, E, Np, N, d_node_perm, d_mu_ft, &nl, s));
+            if (nl != N) return fail(ctx, SEM_E_MESH, "first-touch labelled " + std::to_string(nl) +
+                                                          " of " + std::to_string(N) + " nodes");
+        } else {
+            CK(launch_iota(d_node_perm, N, s));
+            d_mu_ft = d_mu_new;
+        }
+
+        // ---- host outputs ----
+        std::vector<int32_t> node_perm(N), mu_h((size_t)E * Np);
+        CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(mu_h.data(), d_mu_ft, sizeof(int32_t) * E * Np, cudaMemcpyDeviceToHost, s));
+        if (elem_perm_out)
+            CK(cudaMemcpyAsync(elem_perm_out, ctx->d_perm, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        free_list(tmp);
+        if (node_perm_out) std::memcpy(node_perm_out, node_perm.data(), sizeof(int32_t) * N);
+        if (n_nodes_out) *n_nodes_out = N;
+        if (grid_wh_out) { grid_wh_out[0] = ctx->grid[0]; grid_wh_out[1] = ctx->grid[1]; }
+
+        // ---- chunk metadata for the step kernel ----
+        ChunkMeta m;
+        std::string err;
+        if (!build_chunks(mu_h.data(), E, Np, N, kChunkElems, m, err)) return fail(ctx, SEM_E_MESH, err);
+        std::vector<int32_t>().swap(mu_h);
+        DevChunks &d = ctx->dch;
+        d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
+        d.N_int = m.N_int; d.N_sh = m.N_sh; d.n_slots = m.n_slots; d.max_local = m.max_local;
+        auto &L = ctx->mesh_allocs;
+        CK(upload(L, &d.int_start, m.int_start, s));
+        CK(upload(L, &d.shl_start, m.shl_start, s));
+        CK(upload(L, &d.shl_node, m.shl_node, s));
+        CK(upload(L, &d.shl_slot, m.shl_slot, s));
+        CK(upload(L, &d.sh_pstart, m.sh_pstart, s));
+        CK(upload(L, &d.lidx, m.lidx, s));
+        CK(upload(L, &d.color, m.color, s));
+        CK(upload(L, &d.ncolors, m.ncolors, s));
+        {
+            std::vector<int32_t> i2ft(N), i2can(N);
+            ctx->can_to_int.assign(N, -1);
+            for (int64_t g = 0; g < N; g++) {
+                const int32_t i = m.int_of[g];
+                i2ft[i] = (int32_t)g;
+                i2can[i] = node_perm[g];
+                ctx->can_to_int[node_perm[g]] = i;
+            }
+            CK(upload(L, &ctx->d_int_to_ft, i2ft, s));
+            CK(upload(L, &ctx->d_int_to_can, i2can, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        ctx->meta_info = ChunkMeta();
+        ctx->meta_info.B = m.B; ctx->meta_info.Np = m.Np; ctx->meta_info.E = m.E; ctx->meta_info.N = m.N;
+        ctx->meta_info.nchunks = m.nchunks; ctx->meta_info.N_int = m.N_int; ctx->meta_info.N_sh = m.N_sh;
+        ctx->meta_info.n_slots = m.n_slots; ctx->meta_info.max_local = m.max_local;
+        ctx->meta_info.max_colors = m.max_colors;
+        ctx->have_mesh = true;
+        ctx->prep_reorder_ms = now_ms() - t_start;
+        return SEM_OK;
+    } catch (const std::bad_alloc &) {
+        return fail(ctx, SEM_E_OOM, "host allocation failed in sem_mesh_reorder");
+    }
+}
+
+sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t src_vertex,
+                               double f0, double t0, double amplitude, double dt) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    if (!ctx->have_mesh) return fail(ctx, SEM_E_STATE, "sem_build_operators before sem_mesh_reorder");
+    if (!c_elem_host) return fail(ctx, SEM_E_ARG, "c_elem is NULL");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(ctx, SEM_E_ARG, "dt must be > 0");
+    if (!(f0 > 0.0) && src_vertex >= 0) return fail(ctx, SEM_E_ARG, "f0 must be > 0");
+    if (src_vertex < -1 || src_vertex >= ctx->nv)
+        return fail(ctx, SEM_E_ARG, "source vertex " + std::to_string(src_vertex) + " out of range");
+    for (int64_t e = 0; e < ctx->E; e++)
+        if (!(c_elem_host[e] > 0.0) || !std::isfinite(c_elem_host[e]))
+            return fail(ctx, SEM_E_ARG, "element " + std::to_string(e) + " has wave speed c <= 0");
+    try {
+        CK(cudaSetDevice(ctx->device));
+        reset_ops(ctx);
+        const double t_start = now_ms();
+        cudaStream_t s = ctx->stream;
+        const DevChunks &d = ctx->dch;
+        const int64_t Epad = d.nchunks * d.B;
+        auto &L = ctx->ops_allocs;
+        std::vector<void *> tmp;
+        struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+        double *d_c = nullptr, *d_detJ = nullptr;
+        int32_t *d_bad = nullptr;
+        CK(dalloc(tmp, &d_c, ctx->E));
+        CK(dalloc(tmp, &d_detJ, Epad));
+        CK(dalloc(tmp, &d_bad, 1));
+        CK(cudaMemcpyAsync(d_c, c_elem_host, sizeof(double) * ctx->E, cudaMemcpyHostToDevice, s));
+        CK(dalloc(L, &ctx->d_Grr, Epad));
+        CK(dalloc(L, &ctx->d_Gss, Epad));
+        CK(dalloc(L, &ctx->d_Grs, Epad));
+        CK(dalloc(L, &ctx->d_dt2M, ctx->N));
+        CK(dalloc(L, &ctx->d_U[0], ctx->N));
+        CK(dalloc(L, &ctx->d_U[1], ctx->N));
+        CK(dalloc(L, &ctx->d_partial, d.n_slots));
+        CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
+        CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm, d_c, ctx->E, Epad, ctx->d_Grr,
+                           ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
+        g_const_P = 0;
+        sem_status st = ensure_tables(ctx);
+        if (st != SEM_OK) return st;
+        CK(assemble_mass(d, d_detJ, dt, ctx->d_partial, ctx->d_dt2M, s));
+        CK(cudaMemsetAsync(ctx->d_U[0], 0, sizeof(double) * ctx->N, s));
+        CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * ctx->N, s));
+        int32_t bad = 0;
+        CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has detJ <= 0");
+        ctx->src_int = src_vertex >= 0 ? ctx->can_to_int[src_vertex] : -1;
+        ctx->amp = amplitude;
+        ctx->f0 = f0;
+        ctx->t0 = t0;
+        ctx->dt = dt;
+        ctx->step = 0;
+        ctx->cur = 0;
+        ctx->have_ops = true;
+        ctx->prep_build_ms = now_ms() - t_start;
+        return SEM_OK;
+    } catch (const std::bad_alloc &) {
+        return fail(ctx, SEM_E_OOM, "host allocation failed in sem_build_operators");
+    }
+}
+
+sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_step_n before sem_build_operators");
+    if (n_steps < 0) return fail(ctx, SEM_E_ARG, "n_steps < 0");
+    CK(cudaSetDevice(ctx->device));
+    sem_status st = ensure_tables(ctx);
+    if (st != SEM_OK) return st;
+    StepParams p;
+    p.Grr = ctx->d_Grr; p.Gss = ctx->d_Gss; p.Grs = ctx->d_Grs; p.dt2M = ctx->d_dt2M;
+    p.partial = ctx->d_partial;
+    p.src = ctx->src_int; p.amp = ctx->amp; p.f0 = ctx->f0; p.t0 = ctx->t0; p.dt = ctx->dt;
+    for (int64_t k = 0; k < n_steps; k++) {
+        p.U = ctx->d_U[ctx->cur];
+        p.Uprev = ctx->d_U[1 - ctx->cur];
+        p.n = ctx->step;
+        if (ctx->timing) { st = record(ctx, ctx->ev7, true); if (st) return st; }
+        CK(launch_k7(ctx->dch, p, ctx->stream));
+        if (ctx->timing) { st = record(ctx, ctx->ev7, false); if (st) return st; }
+        if (ctx->dch.N_sh > 0) {
+            if (ctx->timing) { st = record(ctx, ctx->ev8, true); if (st) return st; }
+            CK(launch_k8(ctx->dch, p, ctx->stream));
+            if (ctx->timing) { st = record(ctx, ctx->ev8, false); if (st) return st; }
+        }
+        ctx->cur = 1 - ctx->cur;
+        ctx->step++;
+        if (ctx->timing && ctx->ev7.size() >= 4096) { st = drain_events(ctx); if (st) return st; }
+    }
+    return SEM_OK;
+}
+
+sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t *step_out) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_read_field before sem_build_operators");
+    if (!out_host) return fail(ctx, SEM_E_ARG, "out is NULL");
+    if (numbering != SEM_NUMBERING_CANONICAL && numbering != SEM_NUMBERING_INTERNAL)
+        return fail(ctx, SEM_E_ARG, "unknown numbering");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::vector<void *> tmp;
+    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    double *d_out = nullptr;
+    int32_t *d_flag = nullptr;
+    CK(dalloc(tmp, &d_out, ctx->N));
+    CK(dalloc(tmp, &d_flag, 1));
+    const int32_t *map = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_int_to_can : ctx->d_int_to_ft;
+    CK(launch_scatter_f64(ctx->d_U[ctx->cur], map, ctx->N, d_out, s));
+    CK(launch_fill_i32(d_flag, 1, INT_MAX, s));
+    CK(launch_nonfinite(d_out, ctx->N, d_flag, s));
+    int32_t flag = 0;
+    CK(cudaMemcpyAsync(out_host, d_out, sizeof(double) * ctx->N, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&flag, d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (step_out) *step_out = ctx->step;
+    if (flag != INT_MAX)
+        return fail(ctx, SEM_E_NONFINITE, "non-finite field at step " + std::to_string(ctx->step) +
+                                              " (node " + std::to_string(flag) + ")");
+    return SEM_OK;
+}
+
+sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double *u_prev_host,
+                           int numbering) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_write_state before sem_build_operators");
+    if (numbering != SEM_NUMBERING_CANONICAL && numbering != SEM_NUMBERING_INTERNAL)
+        return fail(ctx, SEM_E_ARG, "unknown numbering");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::vector<void *> tmp;
+    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    double *d_in = nullptr;
+    CK(dalloc(tmp, &d_in, ctx->N));
+    const int32_t *map = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_int_to_can : ctx->d_int_to_ft;
+    const double *src[2] = {u_curr_host, u_prev_host};
+    double *dst[2] = {ctx->d_U[ctx->cur], ctx->d_U[1 - ctx->cur]};
+    for (int k = 0; k < 2; k++) {
+        if (!src[k]) { CK(cudaMemsetAsync(dst[k], 0, sizeof(double) * ctx->N, s)); continue; }
+        CK(cudaMemcpyAsync(d_in, src[k], sizeof(double) * ctx->N, cudaMemcpyHostToDevice, s));
+        CK(launch_gather_f64(d_in, map, ctx->N, dst[k], s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return SEM_OK;
+}
+
+sem_status sem_set_step(sem_ctx *ctx, int64_t step) {
+    if (!ctx) return SEM_E_ARG;
+    if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_set_step before sem_build_operators");
+    if (step < 0) return fail(ctx, SEM_E_ARG, "step < 0");
+    ctx->step = step;
+    return SEM_OK;
+}
+
+sem_status sem_sync(sem_ctx *ctx) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    return SEM_OK;
+}
+
+sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
+    if (!ctx || !o) return SEM_E_ARG;
+    std::memset(o, 0, sizeof(*o));
+    if (!ctx->have_mesh) return fail(ctx, SEM_E_STATE, "no mesh");
+    const ChunkMeta &m = ctx->meta_info;
+    o->n_elements = ctx->E;
+    o->n_nodes = ctx->N;
+    o->n_nodes_global = ctx->N;
+    o->degree = ctx->P;
+    o->nodes_per_elem = ctx->Np;
+    o->n_chunks = m.nchunks;
+    o->chunk_elems = m.B;
+    o->max_chunk_nodes = m.max_local;
+    o->n_interior_nodes = m.N_int;
+    o->n_shared_nodes = m.N_sh;
+    o->n_partial_slots = m.n_slots;
+    o->max_colors = m.max_colors;
+    o->launches_per_step = 1 + (m.N_sh > 0 ? 1 : 0);
+    o->step = ctx->step;
+    o->bytes_alg_per_step = (double)ctx->E * (4.0 * ctx->Np + 24.0) + 32.0 * (double)ctx->N;
+    o->prep_reorder_ms = ctx->prep_reorder_ms;
+    o->prep_build_ms = ctx->prep_build_ms;
+    return SEM_OK;
+}
+
+sem_status sem_set_kernel_timing(sem_ctx *ctx, int enable) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    sem_status st = drain_events(ctx);
+    if (st) return st;
+    ctx->timing = enable != 0;
+    ctx->t7 = ctx->t8 = 0;
+    ctx->n7 = ctx->n8 = 0;
+    return SEM_OK;
+}
+
+sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches, double *k8_ms,
+                            int64_t *k8_launches) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    sem_status st = drain_events(ctx);
+    if (st) return st;
+    if (k7_ms) *k7_ms = ctx->t7;
+    if (k7_launches) *k7_launches = ctx->n7;
+    if (k8_ms) *k8_ms = ctx->t8;
+    if (k8_launches) *k8_launches = ctx->n8;
+    return SEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// kernels.h -- host launchers of the sm_100a kernels (product path).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sem_internal.h"
+
+namespace sem {
+
+// ----------------------------- reorder.cu ---------------------------------
+// Vertex bounding box {xmin, ymin, xmax, ymax} -> out4 (device).
+cudaError_t launch_bbox(const double *vxy, int64_t nv, double *out4, cudaStream_t s);
+// Orientation fix (det < 0 -> swap v1,v2); *bad = min element with det == 0.
+cudaError_t launch_orient(const double *vxy, const int32_t *tri, int64_t E, int32_t *tri_or,
+                          int32_t *bad, cudaStream_t s);
+// K1: generalized-Hilbert key of every element's centroid cell.
+cudaError_t launch_hilbert_keys(const double *vxy, const int32_t *tri, int64_t E, double xm0,
+                                double xm1, double ws, double hs, int32_t wb, int32_t hb,
+                                uint32_t *keys, cudaStream_t s);
+cudaError_t launch_random_keys(int64_t E, uint64_t seed, uint64_t *keys, cudaStream_t s);
+cudaError_t launch_iota(int32_t *a, int64_t n, cudaStream_t s);
+cudaError_t launch_fill_i32(int32_t *a, int64_t n, int32_t v, cudaStream_t s);
+// K2: stable radix sort of (key, id) pairs -> perm (CUB onesweep).
+cudaError_t sort_pairs_u32(const uint32_t *keys, const int32_t *vals, uint32_t *keys_out,
+                           int32_t *vals_out, int64_t n, int end_bit, cudaStream_t s);
+cudaError_t sort_pairs_u64(const uint64_t *keys, const int32_t *vals, uint64_t *keys_out,
+                           int32_t *vals_out, int64_t n, int end_bit, cudaStream_t s);
+// K4: canonical SEM node numbering (reading R13).  Returns n_edges via host ptr.
+cudaError_t canonical_nodes(const int32_t *tri_or, int64_t nv, int64_t E, int P,
+                            int32_t *mu_can, int64_t *n_edges, int64_t *n_unused,
+                            int32_t *first_unused, cudaStream_t s);
+// K3: rows of src [E][w] permuted: dst[k] = src[perm[k]].
+cudaError_t launch_permute_rows(const int32_t *src, const int32_t *perm, int64_t E, int w,
+                                int32_t *dst, cudaStream_t s);
+// K5: first-touch renumbering.  node_perm[new] = old;
+// mu_out = relabelled mu.  Returns number of labels via host ptr.
+cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t *node_perm,
+                        int32_t *mu_out, int64_t *n_labels, cudaStream_t s);
+
+// ------------------------------- step.cu -----------------------------------
+struct DevChunks {  // device copy of ChunkMeta
+    int B, Np;
+    int64_t E, N, nchunks, N_int, N_sh, n_slots;
+    int max_local;
+    int32_t *int_start, *shl_start, *shl_node, *shl_slot, *sh_pstart;
+    uint16_t *lidx;
+    uint8_t *color, *ncolors;
+};
+
+cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s);
+// K6: per element (new order) G = c^2 detJ J^-1 J^-T and detJ.
+cudaError_t launch_geometry(const double *vxy, const int32_t *tri_or_in, const int32_t *perm,
+                            const double *c_in, int64_t E, int64_t Epad, double *Grr,
+                            double *Gss, double *Grs, double *detJ, int32_t *bad,
+                            cudaStream_t s);
+// Lumped mass, assembled with the chunk machinery; writes dt2M = dt^2 / Mbar.
+cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *partial,
+                          double *dt2M, cudaStream_t s);
+
+struct StepParams {
+    const double *Grr, *Gss, *Grs;
+    const double *dt2M;
+    const double *U;   // U^n
+    double *Uprev;     // U^{n-1} in, U^{n+1} out
+    double *partial;
+    int32_t src;       // internal node id of the source (-1 none)
+    double amp, f0, t0, dt;
+    int64_t n;         // step index of U
+};
+cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, cudaStream_t s);
+cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s);
+
+// Node-array permutations for I/O: out[map[i]] = in[i] / out[i] = in[map[i]].
+cudaError_t launch_scatter_f64(const double *in, const int32_t *map, int64_t n, double *out,
+                               cudaStream_t s);
+cudaError_t launch_gather_f64(const double *in, const int32_t *map, int64_t n, double *out,
+                              cudaStream_t s);
+cudaError_t launch_nonfinite(const double *a, int64_t n, int32_t *flag, cudaStream_t s);
+
+}  // namespace sem

@@ -1,0 +1,63 @@
+// sem_internal.h -- private declarations of libsem.so (product path).
+// Nothing here is shared with oracle/.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "sem.h"
+
+namespace sem {
+
+constexpr int kMaxNp = 10;
+
+// ---------------------------------------------------------------------------
+// Reference triangle tables, derived on the host in long double (refelem.cpp).
+// Readings R3 (node sets, lattice order) and R4 (weights) of DESIGN.md.
+// ---------------------------------------------------------------------------
+struct RefTables {
+    int P = 0, Np = 0;
+    double node[kMaxNp][2];
+    double wK[kMaxNp];         // stiffness quadrature weights  = int N_p
+    double wM[kMaxNp];         // mass lumping weights (HRZ for P2)
+    double Dr[kMaxNp][kMaxNp]; // Dr[k][p] = dN_p/dr at node k
+    double Ds[kMaxNp][kMaxNp];
+    // Element stiffness factors: K^e = Grr*Srr + Gss*Sss + Grs*Srs with
+    // G = c^2 detJ J^-1 J^-T (Grs = off-diagonal entry).
+    double Srr[kMaxNp][kMaxNp], Sss[kMaxNp][kMaxNp], Srs[kMaxNp][kMaxNp];
+};
+bool build_ref_tables(int P, RefTables &out);
+
+// Local node kinds of the lattice order (R3): kind 0 = vertex (which = local
+// vertex), 1 = edge (which = local edge 0:v0v1 1:v0v2 2:v1v2, m = position from
+// the edge's first listed vertex), 2 = interior (m = index).
+struct LocalNode { int kind, which, m; };
+const LocalNode *local_nodes(int P);
+
+// ---------------------------------------------------------------------------
+// Chunk metadata for the deterministic chunk-owned scatter (chunks.cpp).
+// Elements are cut into chunks of B consecutive elements (one CTA each).
+// Nodes touched by exactly one chunk are "interior" and get contiguous
+// internal ids per chunk; all other nodes are "shared" and live at the end.
+// ---------------------------------------------------------------------------
+struct ChunkMeta {
+    int B = 0, Np = 0;
+    int64_t E = 0, N = 0, nchunks = 0;
+    int64_t N_int = 0, N_sh = 0, n_slots = 0;
+    int max_local = 0, max_colors = 0;
+    std::vector<int32_t> int_start;  // [nchunks+1] internal id range of interior nodes
+    std::vector<int32_t> shl_start;  // [nchunks+1] range in shl_node / shl_slot
+    std::vector<int32_t> shl_node;   // shared index s (internal id = N_int + s)
+    std::vector<int32_t> shl_slot;   // partial-sum slot written by this chunk
+    std::vector<int32_t> sh_pstart;  // [N_sh+1] slots of shared node s, chunk order
+    std::vector<uint16_t> lidx;      // [nchunks][Np][B] chunk-local node index
+    std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)
+    std::vector<uint8_t> ncolors;    // [nchunks]
+    std::vector<int32_t> int_of;     // [N] node id (numbering of mu) -> internal id
+};
+// mu: [E][Np] node ids in [0, N) (elements in their final order).
+bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkMeta &m,
+                  std::string &err);
+
+}  // namespace sem

@@ -1,0 +1,205 @@
+"""Thin ctypes binding of libsem.so (include/sem.h).  Argument marshalling only:
+every step of the path runs in the library's CUDA kernels.  There is no CPU
+fallback -- if libsem.so is missing or no B200 is present, calls raise.
+
+The names mirror the C ABI (sem_create, sem_mesh_reorder, sem_build_operators,
+sem_step_n, sem_read_field, sem_write_state, ...); ``SemContext`` wraps them
+for convenience.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsem.so")
+
+SEM_OK, SEM_E_ARG, SEM_E_STATE, SEM_E_MESH, SEM_E_UNSUPPORTED = 0, 1, 2, 3, 4
+SEM_E_CUDA, SEM_E_NCCL, SEM_E_OOM, SEM_E_NONFINITE = 5, 6, 7, 8
+STATUS_NAMES = {0: "SEM_OK", 1: "SEM_E_ARG", 2: "SEM_E_STATE", 3: "SEM_E_MESH", 4: "SEM_E_UNSUPPORTED",
+                5: "SEM_E_CUDA", 6: "SEM_E_NCCL", 7: "SEM_E_OOM", 8: "SEM_E_NONFINITE"}
+SEM_ORDER_INPUT, SEM_ORDER_HILBERT, SEM_ORDER_RANDOM = 0, 1, 2
+SEM_NODES_FIRST_TOUCH, SEM_NODES_CANONICAL = 0, 2
+SEM_NUMBERING_CANONICAL, SEM_NUMBERING_INTERNAL = 0, 1
+
+EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem_build_operators",
+            "sem_step_n", "sem_read_field", "sem_write_state", "sem_set_step", "sem_sync",
+            "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version"]
+
+
+class SemError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+        self.msg = msg
+
+
+class sem_info(C.Structure):
+    _fields_ = [("n_elements", C.c_int64), ("n_nodes", C.c_int64), ("n_nodes_global", C.c_int64),
+                ("degree", C.c_int32), ("nodes_per_elem", C.c_int32), ("n_chunks", C.c_int64),
+                ("chunk_elems", C.c_int32), ("max_chunk_nodes", C.c_int32),
+                ("n_interior_nodes", C.c_int64), ("n_shared_nodes", C.c_int64),
+                ("n_partial_slots", C.c_int64), ("max_colors", C.c_int32),
+                ("launches_per_step", C.c_int32), ("step", C.c_int64),
+                ("bytes_alg_per_step", C.c_double), ("prep_reorder_ms", C.c_double),
+                ("prep_build_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load libsem.so (raises if it has not been built: no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError("libsem.so not built (%s); run `python -m paper_2104_08416_b200.build`" % path)
+        L = C.CDLL(path)
+        P, i64, i32, u64, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_double
+        L.sem_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, P, P]
+        L.sem_free.argtypes = [P]
+        L.sem_free.restype = None
+        L.sem_last_error.argtypes = [P]
+        L.sem_last_error.restype = C.c_char_p
+        L.sem_mesh_reorder.argtypes = [P, P, i64, P, i64, C.c_int, C.c_int, C.c_int, u64, P, P, P,
+                                       C.POINTER(i64), P]
+        L.sem_build_operators.argtypes = [P, P, i64, dbl, dbl, dbl, dbl]
+        L.sem_step_n.argtypes = [P, i64]
+        L.sem_read_field.argtypes = [P, P, C.c_int, C.POINTER(i64)]
+        L.sem_write_state.argtypes = [P, P, P, C.c_int]
+        L.sem_set_step.argtypes = [P, i64]
+        L.sem_sync.argtypes = [P]
+        L.sem_get_info.argtypes = [P, C.POINTER(sem_info)]
+        L.sem_set_kernel_timing.argtypes = [P, C.c_int]
+        L.sem_kernel_times.argtypes = [P, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]
+        L.sem_version.argtypes = []
+        L.sem_version.restype = C.c_char_p
+        for n in EXPORTED:
+            if n not in ("sem_free", "sem_last_error", "sem_version"):
+                getattr(L, n).restype = C.c_int
+        _lib = L
+        return L
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class SemContext:
+    """One libsem context (one GPU / rank)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None,
+                 stream: int | None = None):
+        self.L = load()
+        h = C.c_void_p()
+        idbuf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
+        st = self.L.sem_create(C.byref(h), device, rank, world_size, idbuf,
+                               None if stream is None else C.c_void_p(stream))
+        self.h = h
+        if st != SEM_OK:
+            msg = self.L.sem_last_error(h).decode() if h.value else ""
+            if h.value:
+                self.L.sem_free(h)
+                self.h = C.c_void_p()
+            raise SemError(st, msg or "sem_create failed")
+        self.N = None
+        self.E = None
+
+    # -- helpers --
+    def _check(self, st):
+        if st != SEM_OK:
+            raise SemError(st, self.L.sem_last_error(self.h).decode())
+
+    def close(self):
+        if self.h and self.h.value:
+            self.L.sem_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- API --
+    def sem_mesh_reorder(self, vxy, tri, degree: int, elem_order=SEM_ORDER_HILBERT,
+                         node_order=SEM_NODES_FIRST_TOUCH, seed: int = 0):
+        """Returns dict(keys, elem_perm, node_perm, n_nodes, grid)."""
+        vxy = np.ascontiguousarray(vxy, np.float64)
+        tri = np.ascontiguousarray(tri, np.int32)
+        E, nv = tri.shape[0], vxy.shape[0]
+        keys = np.empty(E, np.uint32)
+        eperm = np.empty(E, np.int32)
+        nI = (degree - 1) * (degree - 2) // 2 if degree >= 1 else 0
+        nmax = nv + 3 * E * max(degree - 1, 0) + E * nI
+        nperm = np.empty(max(nmax, 1), np.int32)
+        nn = C.c_int64(0)
+        grid = np.zeros(2, np.int32)
+        self._check(self.L.sem_mesh_reorder(self.h, _ptr(vxy), nv, _ptr(tri), E, degree, elem_order,
+                                            node_order, seed, _ptr(keys), _ptr(eperm), _ptr(nperm),
+                                            C.byref(nn), _ptr(grid)))
+        self.N = nn.value
+        self.E = E
+        return {"keys": keys, "elem_perm": eperm, "node_perm": nperm[: nn.value].copy(),
+                "n_nodes": nn.value, "grid": (int(grid[0]), int(grid[1]))}
+
+    def sem_build_operators(self, c_elem, src_vertex: int, f0: float, t0: float, amplitude: float, dt: float):
+        c_elem = np.ascontiguousarray(c_elem, np.float64)
+        self._check(self.L.sem_build_operators(self.h, _ptr(c_elem), int(src_vertex), float(f0), float(t0),
+                                               float(amplitude), float(dt)))
+
+    def sem_step_n(self, n: int):
+        self._check(self.L.sem_step_n(self.h, int(n)))
+
+    def sem_read_field(self, numbering=SEM_NUMBERING_CANONICAL, out=None):
+        out = np.empty(self.N, np.float64) if out is None else out
+        step = C.c_int64(0)
+        self._check(self.L.sem_read_field(self.h, _ptr(out), numbering, C.byref(step)))
+        return out, step.value
+
+    def sem_write_state(self, u_curr, u_prev, numbering=SEM_NUMBERING_CANONICAL):
+        a = None if u_curr is None else np.ascontiguousarray(u_curr, np.float64)
+        b = None if u_prev is None else np.ascontiguousarray(u_prev, np.float64)
+        self._check(self.L.sem_write_state(self.h, _ptr(a), _ptr(b), numbering))
+
+    def sem_set_step(self, step: int):
+        self._check(self.L.sem_set_step(self.h, int(step)))
+
+    def sem_sync(self):
+        self._check(self.L.sem_sync(self.h))
+
+    def sem_get_info(self) -> dict:
+        info = sem_info()
+        self._check(self.L.sem_get_info(self.h, C.byref(info)))
+        return info.as_dict()
+
+    def sem_set_kernel_timing(self, enable: bool):
+        self._check(self.L.sem_set_kernel_timing(self.h, int(bool(enable))))
+
+    def sem_kernel_times(self):
+        a, b = C.c_double(), C.c_double()
+        na, nb = C.c_int64(), C.c_int64()
+        self._check(self.L.sem_kernel_times(self.h, C.byref(a), C.byref(na), C.byref(b), C.byref(nb)))
+        return {"k7_ms": a.value, "k7_launches": na.value, "k8_ms": b.value, "k8_launches": nb.value}
+
+
+def version() -> str:
+    return load().sem_version().decode()

@@ -1,0 +1,57 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol that
+include/sem.h declares; without a GPU it fails loudly (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2104_08416_b200 import build, sem
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "sem.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sem_[a-z_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return sem.load()
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_symbols()
+    for n in ("sem_mesh_reorder", "sem_build_operators", "sem_step_n", "sem_read_field"):
+        assert n in names
+
+
+def test_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", build.LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (sem_[a-z_]+)\b", out))
+    missing = [n for n in declared_symbols() if n not in exported]
+    assert not missing, missing
+    assert set(sem.EXPORTED) <= exported
+    # no POSIX-semaphore names are interposed by this library
+    for posix in ("sem_destroy", "sem_init", "sem_open", "sem_close", "sem_post", "sem_wait"):
+        assert posix not in exported
+
+
+def test_sm100a_cubin_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_version(lib):
+    assert "sm_100a" in sem.version()
+
+
+@pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="only meaningful without a GPU")
+def test_no_gpu_fails_loudly(lib):
+    with pytest.raises(sem.SemError) as e:
+        sem.SemContext(0)
+    assert e.value.status == sem.SEM_E_CUDA

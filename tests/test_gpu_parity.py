@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): keys, permutations and renumbering bit-exact;
+fp64 field within relative L2 <= 1e-10 (tolerance stated per test).  Inputs are
+the seeded recipe of paper_2104_08416_b200/meshgen.py; nothing the oracle sees
+comes from the GPU.
+"""
+import numpy as np
+import pytest
+
+from oracle import core
+from oracle.core import OracleSEM
+from paper_2104_08416_b200 import meshgen as mg
+from paper_2104_08416_b200 import sem as S
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-10
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = S.SemContext(0)
+    yield c
+    c.close()
+
+
+def oracle_reorder(m, P, elem_order=S.SEM_ORDER_HILBERT, node_order=S.SEM_NODES_FIRST_TOUCH, seed=0):
+    o_tri = core.orient(m.vxy, m.tri)
+    mu_can, N = core.canonical_nodes(o_tri, m.nv, P)
+    if elem_order == S.SEM_ORDER_HILBERT:
+        key, perm, grid = core.hilbert_order(m.vxy, m.tri)
+    elif elem_order == S.SEM_ORDER_RANDOM:
+        perm = core.random_order(m.ne, seed)
+        key, grid = np.zeros(m.ne, np.uint32), (0, 0)
+    else:
+        perm = np.arange(m.ne, dtype=np.int32)
+        key, grid = np.zeros(m.ne, np.uint32), (0, 0)
+    if node_order == S.SEM_NODES_FIRST_TOUCH:
+        node_perm, _ = core.first_touch(mu_can[perm], N)
+    else:
+        node_perm = np.arange(N, dtype=np.int32)
+    return key, perm, node_perm, N, grid
+
+
+CASES = [("C1", 1), ("C2", 8), ("C3", 20), ("C4", 32), ("C5", 128), ("C2", 1)]
+
+
+@pytest.mark.parametrize("name,scale", CASES)
+def test_reorder_bit_exact(ctx, name, scale):
+    pb = mg.config(name, scale)
+    m = pb.mesh
+    r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
+    key, perm, node_perm, N, grid = oracle_reorder(m, pb.P)
+    assert r["grid"] == grid
+    assert r["n_nodes"] == N
+    assert np.array_equal(r["keys"], key)
+    assert np.array_equal(r["elem_perm"], perm)
+    assert np.array_equal(r["node_perm"], node_perm)
+
+
+@pytest.mark.parametrize("elem_order,node_order", [(S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
+                                                   (S.SEM_ORDER_RANDOM, S.SEM_NODES_FIRST_TOUCH),
+                                                   (S.SEM_ORDER_HILBERT, S.SEM_NODES_CANONICAL),
+                                                   (S.SEM_ORDER_INPUT, S.SEM_NODES_FIRST_TOUCH)])
+def test_reorder_variants_bit_exact(ctx, elem_order, node_order):
+    pb = mg.config("C2", 16)
+    m = pb.mesh
+    r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, elem_order, node_order, seed=1234)
+    key, perm, node_perm, N, grid = oracle_reorder(m, pb.P, elem_order, node_order, seed=1234)
+    assert np.array_equal(r["elem_perm"], perm)
+    assert np.array_equal(r["node_perm"], node_perm)
+
+
+def run_gpu(ctx, pb, steps, elem_order=S.SEM_ORDER_HILBERT, node_order=S.SEM_NODES_FIRST_TOUCH,
+            mesh=None, c=None, src=None, state=None, step0=0):
+    m = pb.mesh if mesh is None else mesh
+    ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, elem_order, node_order, seed=7)
+    ctx.sem_build_operators(pb.c if c is None else c, pb.src_vertex if src is None else src,
+                            pb.f0, pb.t0, pb.amplitude, pb.dt)
+    if state is not None:
+        ctx.sem_write_state(state[0], state[1])
+        ctx.sem_set_step(step0)
+    ctx.sem_step_n(steps)
+    U, n = ctx.sem_read_field()
+    assert n == step0 + steps
+    return U
+
+
+def test_c1_full_run_parity(ctx):
+    pb = mg.config("C1")
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    Uo, _ = o.leapfrog(pb.dt, pb.n_steps, src=pb.src_vertex, A=pb.amplitude, f0=pb.f0, t0=pb.t0)
+    Ug = run_gpu(ctx, pb, pb.n_steps)
+    assert np.abs(Uo).max() > 0
+    assert rel_l2(Ug, Uo) <= REL_L2
+
+
+@pytest.mark.parametrize("elem_order,node_order", [(S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
+                                                   (S.SEM_ORDER_RANDOM, S.SEM_NODES_FIRST_TOUCH),
+                                                   (S.SEM_ORDER_HILBERT, S.SEM_NODES_CANONICAL)])
+def test_c1_orderings_same_field(ctx, elem_order, node_order):
+    pb = mg.config("C1")
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    Uo, _ = o.leapfrog(pb.dt, 120, src=pb.src_vertex, A=pb.amplitude, f0=pb.f0, t0=0.05)
+    pb2 = mg.Problem(**{**pb.__dict__, "t0": 0.05})
+    Ug = run_gpu(ctx, pb2, 120, elem_order, node_order)
+    assert rel_l2(Ug, Uo) <= REL_L2
+
+
+@pytest.mark.parametrize("name,scale,steps", [("C2", 4, 300), ("C3", 10, 200), ("C4", 16, 200), ("C5", 64, 150)])
+def test_reduced_configs_run_parity(ctx, name, scale, steps):
+    # shifted source peak (t0 = 10 dt) so the short run carries a real wavefield
+    pb = mg.config(name, scale)
+    pb = mg.Problem(**{**pb.__dict__, "t0": 10 * pb.dt, "f0": 1.0 / (8 * pb.dt)})
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    Uo, _ = o.leapfrog(pb.dt, steps, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
+    Ug = run_gpu(ctx, pb, steps)
+    assert np.count_nonzero(Uo) > 0.05 * Uo.size
+    assert rel_l2(Ug, Uo) <= REL_L2
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 1), ("C2", 1), ("C3", 4), ("C4", 4), ("C5", 32)])
+def test_random_state_steps_parity(ctx, name, scale):
+    """P-12: one and ten steps from seeded random full-mesh states."""
+    pb = mg.config(name, scale)
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    rng = np.random.default_rng(42)
+    U0 = rng.standard_normal(o.N)
+    Up = U0 + 0.1 * rng.standard_normal(o.N)
+    for steps in (1, 10):
+        Uo, _ = o.leapfrog(pb.dt, steps, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0,
+                           U=U0, Uprev=Up, step0=37)
+        Ug = run_gpu(ctx, pb, steps, state=(U0, Up), step0=37)
+        assert rel_l2(Ug, Uo) <= 1e-13 * steps, (name, steps, rel_l2(Ug, Uo))
+        assert np.abs(Ug - Uo).max() <= 1e-12 * np.abs(Uo).max()
+
+
+def test_read_internal_numbering(ctx):
+    pb = mg.config("C1")
+    r = ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, pb.P)
+    ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+    rng = np.random.default_rng(0)
+    U = rng.standard_normal(r["n_nodes"])
+    ctx.sem_write_state(U, None)
+    Ui, _ = ctx.sem_read_field(S.SEM_NUMBERING_INTERNAL)
+    assert np.array_equal(Ui, U[r["node_perm"]])
+    Uc, _ = ctx.sem_read_field(S.SEM_NUMBERING_CANONICAL)
+    assert np.array_equal(Uc, U)
+
+
+def test_bitwise_deterministic(ctx):
+    pb = mg.config("C2", 4)
+    a = run_gpu(ctx, pb, 50)
+    b = run_gpu(ctx, pb, 50)
+    assert np.array_equal(a, b)
+
+
+def test_errors(ctx):
+    pb = mg.config("C1", 4)
+    m = pb.mesh
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_mesh_reorder(m.vxy, m.tri, 4)
+    assert e.value.status == S.SEM_E_UNSUPPORTED
+    bad = m.vxy.copy()
+    t = m.tri[5]
+    bad[t[2]] = bad[t[0]] + 0.5 * (bad[t[1]] - bad[t[0]])  # collinear
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_mesh_reorder(bad, m.tri, 2)
+    assert e.value.status == S.SEM_E_MESH and "element" in e.value.msg
+    ctx.sem_mesh_reorder(m.vxy, m.tri, 2)
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_step_n(1)
+    assert e.value.status == S.SEM_E_STATE
+    c = pb.c.copy()
+    c[3] = -1.0
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_build_operators(c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+    assert e.value.status == S.SEM_E_ARG and "element 3" in e.value.msg
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, -1.0)
+    assert e.value.status == S.SEM_E_ARG
+
+
+def test_nonfinite_reported(ctx):
+    pb = mg.config("C1", 4)
+    ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, 2)
+    ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt * 50)  # unstable dt
+    ctx.sem_step_n(3000)
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_read_field()
+    assert e.value.status == S.SEM_E_NONFINITE and "step 3000" in e.value.msg
+
+
+def test_single_element_and_tiny(ctx):
+    vxy = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+    tri = np.array([[0, 2, 1]], np.int32)  # clockwise: fixed by the library
+    for P in (2, 3):
+        r = ctx.sem_mesh_reorder(vxy, tri, P)
+        assert r["n_nodes"] == (6 if P == 2 else 10)
+        o = OracleSEM(vxy, tri, P)
+        ctx.sem_build_operators(np.ones(1), 0, 5.0, 0.0, 1.0, 0.01)
+        U0 = np.random.default_rng(P).standard_normal(o.N)
+        ctx.sem_write_state(U0, U0)
+        ctx.sem_step_n(5)
+        Ug, _ = ctx.sem_read_field()
+        Uo, _ = o.leapfrog(0.01, 5, src=0, A=1.0, f0=5.0, t0=0.0, U=U0, Uprev=U0)
+        assert rel_l2(Ug, Uo) <= 1e-13
