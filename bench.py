@@ -123,7 +123,9 @@ def run_ours(args):
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream shared by libsem and the torch events
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     peak, peak_src, peaks = load_peak()
 
     pb = problem_for(args.config, 1)  # replicas: every rank runs the per-GPU workload
@@ -228,6 +230,7 @@ def orderings(ctx, pb, args, S):
         ("random", pb.mesh, pb.c, S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
     ]
     stream = torch.cuda.current_stream()
+    assert stream.cuda_stream != 0
     for name, m, c, eo, no in variants:
         ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, eo, no)
         src = pb.src_vertex if m is pb.mesh else int(pb.mesh.vert_perm[pb.src_vertex])

@@ -40,15 +40,17 @@ struct sem_ctx {
     double *d_vxy = nullptr;
     int32_t *d_tri_or = nullptr;  // oriented triangles, INPUT order
     int32_t *d_perm = nullptr;    // new -> input
-    int32_t *d_int_to_can = nullptr, *d_int_to_ft = nullptr;
+    int32_t *d_node_int = nullptr;   // [N] reordered node id -> internal (device layout) id
+    int32_t *d_node_perm = nullptr;  // [N] reordered node id -> canonical id
     std::vector<int32_t> can_to_int;
     DevChunks dch{};
+    int k7_grid = 0;
     ChunkMeta meta_info;  // counts only (vectors released after upload)
 
     // operators / state
     double *d_Grr = nullptr, *d_Gss = nullptr, *d_Grs = nullptr, *d_dt2M = nullptr;
     double *d_U[2] = {nullptr, nullptr};
-    double *d_partial = nullptr;
+    double *d_slot = nullptr;
     int cur = 0;
     int32_t src_int = -1;
     double amp = 0, f0 = 1, t0 = 0, dt = 0;
@@ -100,7 +102,7 @@ void reset_ops(sem_ctx *ctx) {
     free_list(ctx->ops_allocs);
     ctx->d_Grr = ctx->d_Gss = ctx->d_Grs = ctx->d_dt2M = nullptr;
     ctx->d_U[0] = ctx->d_U[1] = nullptr;
-    ctx->d_partial = nullptr;
+    ctx->d_slot = nullptr;
     ctx->have_ops = false;
     ctx->step = 0;
     ctx->cur = 0;
@@ -372,33 +374,31 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         std::vector<int32_t>().swap(mu_h);
         DevChunks &d = ctx->dch;
         d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
-        d.N_int = m.N_int; d.N_sh = m.N_sh; d.n_slots = m.n_slots; d.max_local = m.max_local;
+        d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots;
+        d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr;
         auto &L = ctx->mesh_allocs;
-        CK(upload(L, &d.int_start, m.int_start, s));
-        CK(upload(L, &d.shl_start, m.shl_start, s));
-        CK(upload(L, &d.shl_node, m.shl_node, s));
-        CK(upload(L, &d.shl_slot, m.shl_slot, s));
-        CK(upload(L, &d.sh_pstart, m.sh_pstart, s));
-        CK(upload(L, &d.lidx, m.lidx, s));
-        CK(upload(L, &d.color, m.color, s));
-        CK(upload(L, &d.ncolors, m.ncolors, s));
+        int32_t *p_cmeta, *p_pstart, *p_slots;
+        uint16_t *p_lent, *p_lptr, *p_lidx;
+        CK(upload(L, &p_cmeta, m.cmeta, s));
+        CK(upload(L, &p_lidx, m.lidx, s));
+        CK(upload(L, &p_lent, m.lent, s));
+        CK(upload(L, &p_lptr, m.lptr, s));
+        CK(upload(L, &p_pstart, m.sh_pstart, s));
+        CK(upload(L, &p_slots, m.sh_slots, s));
+        d.cmeta = p_cmeta; d.lidx = p_lidx; d.lent = p_lent; d.lptr = p_lptr; d.sh_pstart = p_pstart; d.sh_slots = p_slots;
         {
-            std::vector<int32_t> i2ft(N), i2can(N);
             ctx->can_to_int.assign(N, -1);
-            for (int64_t g = 0; g < N; g++) {
-                const int32_t i = m.int_of[g];
-                i2ft[i] = (int32_t)g;
-                i2can[i] = node_perm[g];
-                ctx->can_to_int[node_perm[g]] = i;
-            }
-            CK(upload(L, &ctx->d_int_to_ft, i2ft, s));
-            CK(upload(L, &ctx->d_int_to_can, i2can, s));
+            for (int64_t g = 0; g < N; g++) ctx->can_to_int[node_perm[g]] = m.int_of[g];
+            CK(upload(L, &ctx->d_node_int, m.int_of, s));
+            CK(upload(L, &ctx->d_node_perm, node_perm, s));
             CK(cudaStreamSynchronize(s));
         }
+        ctx->k7_grid = k7_grid(d);
         ctx->meta_info = ChunkMeta();
         ctx->meta_info.B = m.B; ctx->meta_info.Np = m.Np; ctx->meta_info.E = m.E; ctx->meta_info.N = m.N;
         ctx->meta_info.nchunks = m.nchunks; ctx->meta_info.N_int = m.N_int; ctx->meta_info.N_sh = m.N_sh;
-        ctx->meta_info.n_slots = m.n_slots; ctx->meta_info.max_local = m.max_local;
+        ctx->meta_info.N_tot = m.N_tot; ctx->meta_info.n_slots = m.n_slots; ctx->meta_info.max_local = m.max_local;
+        ctx->meta_info.max_win = m.max_win;
         ctx->meta_info.max_colors = m.max_colors;
         ctx->have_mesh = true;
         ctx->prep_reorder_ms = now_ms() - t_start;
@@ -440,19 +440,21 @@ sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t 
         CK(dalloc(L, &ctx->d_Grr, Epad));
         CK(dalloc(L, &ctx->d_Gss, Epad));
         CK(dalloc(L, &ctx->d_Grs, Epad));
-        CK(dalloc(L, &ctx->d_dt2M, ctx->N));
-        CK(dalloc(L, &ctx->d_U[0], ctx->N));
-        CK(dalloc(L, &ctx->d_U[1], ctx->N));
-        CK(dalloc(L, &ctx->d_partial, d.n_slots));
+        const int64_t Nt = d.N_tot + 2;
+        CK(dalloc(L, &ctx->d_dt2M, Nt));
+        CK(dalloc(L, &ctx->d_U[0], Nt));
+        CK(dalloc(L, &ctx->d_U[1], Nt));
+        CK(dalloc(L, &ctx->d_slot, d.n_slots + 2));
         CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
         CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm, d_c, ctx->E, Epad, ctx->d_Grr,
                            ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
         g_const_P = 0;
         sem_status st = ensure_tables(ctx);
         if (st != SEM_OK) return st;
-        CK(assemble_mass(d, d_detJ, dt, ctx->d_partial, ctx->d_dt2M, s));
-        CK(cudaMemsetAsync(ctx->d_U[0], 0, sizeof(double) * ctx->N, s));
-        CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * ctx->N, s));
+        CK(assemble_mass(d, d_detJ, dt, ctx->d_slot, ctx->d_dt2M, s));
+        CK(cudaMemsetAsync(ctx->d_U[0], 0, sizeof(double) * Nt, s));
+        CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * Nt, s));
+        CK(cudaMemsetAsync(ctx->d_slot, 0, sizeof(double) * (d.n_slots + 2), s));  // halo of U^0 = 0
         int32_t bad = 0;
         CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -482,14 +484,14 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
     if (st != SEM_OK) return st;
     StepParams p;
     p.Grr = ctx->d_Grr; p.Gss = ctx->d_Gss; p.Grs = ctx->d_Grs; p.dt2M = ctx->d_dt2M;
-    p.partial = ctx->d_partial;
+    p.slot = ctx->d_slot;
     p.src = ctx->src_int; p.amp = ctx->amp; p.f0 = ctx->f0; p.t0 = ctx->t0; p.dt = ctx->dt;
     for (int64_t k = 0; k < n_steps; k++) {
         p.U = ctx->d_U[ctx->cur];
         p.Uprev = ctx->d_U[1 - ctx->cur];
         p.n = ctx->step;
         if (ctx->timing) { st = record(ctx, ctx->ev7, true); if (st) return st; }
-        CK(launch_k7(ctx->dch, p, ctx->stream));
+        CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream));
         if (ctx->timing) { st = record(ctx, ctx->ev7, false); if (st) return st; }
         if (ctx->dch.N_sh > 0) {
             if (ctx->timing) { st = record(ctx, ctx->ev8, true); if (st) return st; }
@@ -518,8 +520,8 @@ sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t
     int32_t *d_flag = nullptr;
     CK(dalloc(tmp, &d_out, ctx->N));
     CK(dalloc(tmp, &d_flag, 1));
-    const int32_t *map = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_int_to_can : ctx->d_int_to_ft;
-    CK(launch_scatter_f64(ctx->d_U[ctx->cur], map, ctx->N, d_out, s));
+    CK(launch_permute_f64(ctx->d_U[ctx->cur], ctx->d_node_int,
+                          numbering == SEM_NUMBERING_CANONICAL ? ctx->d_node_perm : nullptr, ctx->N, d_out, s));
     CK(launch_fill_i32(d_flag, 1, INT_MAX, s));
     CK(launch_nonfinite(d_out, ctx->N, d_flag, s));
     int32_t flag = 0;
@@ -546,14 +548,16 @@ sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double
     struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
     double *d_in = nullptr;
     CK(dalloc(tmp, &d_in, ctx->N));
-    const int32_t *map = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_int_to_can : ctx->d_int_to_ft;
+    const int32_t *imap = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_node_perm : nullptr;
     const double *src[2] = {u_curr_host, u_prev_host};
     double *dst[2] = {ctx->d_U[ctx->cur], ctx->d_U[1 - ctx->cur]};
     for (int k = 0; k < 2; k++) {
-        if (!src[k]) { CK(cudaMemsetAsync(dst[k], 0, sizeof(double) * ctx->N, s)); continue; }
+        CK(cudaMemsetAsync(dst[k], 0, sizeof(double) * (ctx->dch.N_tot + 2), s));
+        if (!src[k]) continue;
         CK(cudaMemcpyAsync(d_in, src[k], sizeof(double) * ctx->N, cudaMemcpyHostToDevice, s));
-        CK(launch_gather_f64(d_in, map, ctx->N, dst[k], s));
+        CK(launch_permute_f64(d_in, imap, ctx->d_node_int, ctx->N, dst[k], s));
     }
+    CK(launch_halo_fill(ctx->dch, ctx->d_U[ctx->cur], ctx->d_slot, s));
     CK(cudaStreamSynchronize(s));
     return SEM_OK;
 }
@@ -588,7 +592,7 @@ sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
     o->n_chunks = m.nchunks;
     o->chunk_elems = m.B;
     o->max_chunk_nodes = m.max_local;
-    o->n_interior_nodes = m.N_int;
+    o->n_interior_nodes = ctx->N - m.N_sh;
     o->n_shared_nodes = m.N_sh;
     o->n_partial_slots = m.n_slots;
     o->max_colors = m.max_colors;
@@ -625,3 +629,34 @@ sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches, d
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host-only diagnostics of the chunk builder (no GPU needed): used by the CPU
+// test-suite to check the metadata invariants and by DESIGN.md's sizing table.
+// stats_out[16] = {nchunks, N_int(padded), N_sh, n_slots, max_local, max_win,
+//                  max_lptr, max_colors, sum_nint, sum_nsh, max_nsh, 0...}
+// ---------------------------------------------------------------------------
+extern "C" sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
+                                            int64_t *stats_out, int32_t *int_of_out,
+                                            int32_t *cmeta_out) {
+    if (!mu || !stats_out || E <= 0 || N <= 0) return SEM_E_ARG;
+    try {
+        ChunkMeta m;
+        std::string err;
+        if (!build_chunks(mu, E, Np, N, B, m, err)) return SEM_E_MESH;
+        int64_t sum_nint = 0, sum_nsh = 0, max_nsh = 0;
+        for (int64_t c = 0; c < m.nchunks; c++) {
+            sum_nint += m.cmeta[8 * c + 1];
+            sum_nsh += m.cmeta[8 * c + 3];
+            if (m.cmeta[8 * c + 3] > max_nsh) max_nsh = m.cmeta[8 * c + 3];
+        }
+        const int64_t st[16] = {m.nchunks, m.N_int, m.N_sh, m.n_slots, m.max_local, m.max_win,
+                                m.max_lptr, m.max_colors, sum_nint, sum_nsh, max_nsh, 0, 0, 0, 0, 0};
+        std::memcpy(stats_out, st, sizeof(st));
+        if (int_of_out) std::memcpy(int_of_out, m.int_of.data(), sizeof(int32_t) * N);
+        if (cmeta_out) std::memcpy(cmeta_out, m.cmeta.data(), sizeof(int32_t) * m.cmeta.size());
+        return SEM_OK;
+    } catch (const std::bad_alloc &) {
+        return SEM_E_OOM;
+    }
+}

@@ -3,20 +3,22 @@
 //
 // The paper avoids the scatter race of Algorithm 2 by
 // colouring the whole mesh and running colours one after another.  On the GPU
-// we keep the colouring idea but at CTA scale: elements are cut into chunks of
-// B consecutive elements (consecutive along the Hilbert order, so a chunk is a
-// compact patch of the domain), each chunk is one CTA, and
+// we keep the colouring idea at CTA scale: elements are cut into chunks of B
+// consecutive elements (consecutive along the Hilbert order, so a chunk is a
+// compact patch of the domain) and each chunk is processed by one CTA:
 //   * nodes touched by a single chunk ("interior") are summed in shared memory
 //     in a fixed colour order and finalised by that CTA;
-//   * nodes touched by several chunks ("shared") receive one partial sum per
-//     chunk in a slot of their own; a fix-up kernel adds the slots in
-//     ascending chunk order.
-// Both orders are fixed, so results are bitwise reproducible run to run.
+//   * nodes touched by several chunks ("shared") get one SLOT per touching
+//     chunk.  A chunk's slots are contiguous.  Before the step a slot holds the
+//     node's U^n (a halo copy, so the step kernel only streams contiguous
+//     blocks); the step kernel overwrites it with the chunk's partial K U sum;
+//     the fix-up kernel adds a node's slots in ascending chunk order, updates
+//     the node and writes U^{n+1} back into its slots.
+// Both summation orders are fixed, so results are bitwise reproducible.
 //
-// Internal node numbering: interior nodes of chunk c occupy the contiguous id
-// range [int_start[c], int_start[c+1]) (ordered by their incoming id); shared
-// nodes follow at [N_int, N) in ascending incoming id.  With first-touch input
-// numbering this is a small perturbation of that order.
+// Internal node numbering: interior nodes of chunk c occupy [i0_c, i0_c+nint_c),
+// i0_c even (16-byte aligned for TMA bulk copies, one hole at most per chunk),
+// in ascending incoming id; shared nodes follow at [N_int, N_int+N_sh).
 #include <algorithm>
 #include <cstring>
 
@@ -24,13 +26,15 @@
 
 namespace sem {
 
+static inline int64_t align2(int64_t v) { return (v + 1) & ~int64_t(1); }
+
 bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkMeta &m,
                   std::string &err) {
-    if (E <= 0 || N <= 0 || B <= 0 || B > 1024 || Np > kMaxNp) {
+    if (E <= 0 || N <= 0 || B <= 0 || B > 1024 || (B % 16) != 0 || Np > kMaxNp) {
         err = "build_chunks: bad arguments";
         return false;
     }
-    if ((int64_t)B * Np > 65535) {
+    if ((int64_t)B * Np > 32767) {
         err = "build_chunks: chunk too large for 16-bit local indices";
         return false;
     }
@@ -65,20 +69,22 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
             return false;
         }
 
-    // Internal numbering.
-    m.int_start.assign(nch + 1, 0);
+    // Interior windows (even-aligned starts).
+    std::vector<int64_t> nint(nch, 0);
     int64_t nsh = 0;
     for (int64_t g = 0; g < N; g++) {
-        if (nref[g] == 1) m.int_start[firstc[g] + 1]++;
+        if (nref[g] == 1) nint[firstc[g]]++;
         else nsh++;
     }
-    for (int64_t c = 0; c < nch; c++) m.int_start[c + 1] += m.int_start[c];
-    m.N_int = m.int_start[nch];
+    m.i0.assign(nch + 1, 0);
+    for (int64_t c = 0; c < nch; c++) m.i0[c + 1] = (int32_t)align2(m.i0[c] + nint[c]);
+    m.N_int = m.i0[nch];
     m.N_sh = nsh;
+    m.N_tot = m.N_int + nsh;
     m.int_of.assign(N, -1);
     std::vector<int32_t> sh_index(N, -1);
     {
-        std::vector<int32_t> cur(m.int_start.begin(), m.int_start.end() - 1);
+        std::vector<int32_t> cur(m.i0.begin(), m.i0.end() - 1);
         int64_t s = 0;
         for (int64_t g = 0; g < N; g++) {
             if (nref[g] == 1) m.int_of[g] = cur[firstc[g]]++;
@@ -86,14 +92,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         }
     }
 
-    // Shared slots: node s owns [sh_pstart[s], sh_pstart[s+1]), one per chunk.
-    m.sh_pstart.assign(nsh + 1, 0);
-    for (int64_t g = 0; g < N; g++)
-        if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref[g];
-    for (int64_t s = 0; s < nsh; s++) m.sh_pstart[s + 1] += m.sh_pstart[s];
-    m.n_slots = nsh ? m.sh_pstart[nsh] : 0;
-
-    // Per-chunk shared lists (sorted, unique) -- independent per chunk.
+    // Per-chunk shared lists (sorted, unique).
     std::vector<std::vector<int32_t>> lists(nch);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t c = 0; c < nch; c++) {
@@ -107,36 +106,47 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         std::sort(L.begin(), L.end());
         L.erase(std::unique(L.begin(), L.end()), L.end());
     }
-    m.shl_start.assign(nch + 1, 0);
-    for (int64_t c = 0; c < nch; c++) m.shl_start[c + 1] = m.shl_start[c] + (int32_t)lists[c].size();
-    m.shl_node.resize(m.shl_start[nch]);
-    m.shl_slot.resize(m.shl_start[nch]);
+    // Chunk-contiguous slot blocks (even-aligned starts).
+    m.s0.assign(nch + 1, 0);
+    for (int64_t c = 0; c < nch; c++) m.s0[c + 1] = (int32_t)align2(m.s0[c] + (int64_t)lists[c].size());
+    m.n_slots = m.s0[nch];
+    // Slots of each shared node, in ascending chunk order (for the fix-up).
+    m.sh_pstart.assign(nsh + 1, 0);
+    for (int64_t g = 0; g < N; g++)
+        if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref[g];
+    for (int64_t s = 0; s < nsh; s++) m.sh_pstart[s + 1] += m.sh_pstart[s];
+    m.sh_slots.assign(nsh ? m.sh_pstart[nsh] : 0, -1);
     {
         std::vector<int32_t> cursor(nsh, 0);
-        for (int64_t c = 0; c < nch; c++) {  // ascending chunk order -> slot order
-            int64_t k = m.shl_start[c];
-            for (int32_t s : lists[c]) {
-                m.shl_node[k] = s;
-                m.shl_slot[k] = m.sh_pstart[s] + cursor[s]++;
-                k++;
-            }
+        for (int64_t c = 0; c < nch; c++) {
+            int32_t k = m.s0[c];
+            for (int32_t s : lists[c]) m.sh_slots[m.sh_pstart[s] + cursor[s]++] = k++;
         }
     }
 
-    // Local indices and per-chunk greedy colouring (first fit in element order).
+    // Local indices, the per-chunk node CSR (local node -> entries p*B + t in
+    // ascending order; this fixes the summation order), a per-chunk greedy
+    // colouring (first fit in element order; used by diagnostics only), and
+    // the per-chunk descriptor.
     m.lidx.assign((size_t)nch * Np * B, 0);
     m.color.assign((size_t)nch * B, 255);
-    m.ncolors.assign(nch, 0);
-    int max_local = 0, max_col = 0;
+    m.cmeta.assign((size_t)nch * 8, 0);
+    m.lp0.assign(nch + 1, 0);
+    std::vector<int32_t> nlocal(nch, 0);
+    int max_local = 0, max_win = 0, max_col = 0;
     bool bad_color = false;
-#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_local, max_col)
+#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_local, max_win, max_col)
     for (int64_t c = 0; c < nch; c++) {
         const int64_t e0 = c * B, e1 = std::min<int64_t>(E, e0 + B);
-        const int32_t i0 = m.int_start[c];
-        const int32_t nint = m.int_start[c + 1] - i0;
+        const int32_t i0 = m.i0[c];
+        const int32_t ni = (int32_t)nint[c];
+        const int32_t ni_al = (int32_t)align2(ni);
         const std::vector<int32_t> &L = lists[c];
-        const int nl = nint + (int)L.size();
+        const int32_t ns = (int32_t)L.size();
+        const int nl = ni_al + (int)align2(ns);  // u-buffer length (TMA sizes are even)
+        nlocal[c] = ni_al + ns;
         if (nl > max_local) max_local = nl;
+        if (ni_al > max_win) max_win = ni_al;
         std::vector<uint32_t> used(nl, 0u);
         int ncol = 0;
         for (int64_t e = e0; e < e1; e++) {
@@ -147,7 +157,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
                 const int32_t g = mu[e * Np + p];
                 int loc;
                 if (sh_index[g] < 0) loc = m.int_of[g] - i0;
-                else loc = nint + (int)(std::lower_bound(L.begin(), L.end(), sh_index[g]) - L.begin());
+                else loc = ni_al + (int)(std::lower_bound(L.begin(), L.end(), sh_index[g]) - L.begin());
                 li[p] = (uint16_t)loc;
                 m.lidx[(size_t)c * Np * B + (size_t)p * B + t] = (uint16_t)loc;
                 forb |= used[loc];
@@ -162,14 +172,48 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
             for (int p = 0; p < Np; p++) used[li[p]] |= (1u << col);
             if (col + 1 > ncol) ncol = col + 1;
         }
-        m.ncolors[c] = (uint8_t)ncol;
+        int32_t *cm = &m.cmeta[(size_t)c * 8];
+        cm[0] = i0;
+        cm[1] = ni;
+        cm[2] = m.s0[c];
+        cm[3] = ns;
+        cm[4] = ncol;
+        cm[5] = (int32_t)(e1 - e0);
+        cm[6] = ni_al;
         if (ncol > max_col) max_col = ncol;
     }
     if (bad_color) {
         err = "build_chunks: more than 32 colours needed inside a chunk";
         return false;
     }
+    // CSR blocks: chunk c owns lptr[lp0[c] .. lp0[c] + nlocal+1) (start aligned
+    // to 8 entries = 16 bytes for TMA) and lent[c*Np*B .. (c+1)*Np*B).
+    for (int64_t c = 0; c < nch; c++) m.lp0[c + 1] = (int32_t)((m.lp0[c] + nlocal[c] + 1 + 7) & ~7);
+    m.lptr.assign((size_t)m.lp0[nch] + 8, 0);
+    m.lent.assign((size_t)nch * Np * B, 0);
+    int max_lp = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_lp)
+    for (int64_t c = 0; c < nch; c++) {
+        const int nl = nlocal[c];
+        const int ne = (int)(std::min<int64_t>(E, (c + 1) * B) - c * B);
+        std::vector<int> cnt(nl + 1, 0);
+        const uint16_t *li = &m.lidx[(size_t)c * Np * B];
+        for (int p = 0; p < Np; p++)
+            for (int t = 0; t < ne; t++) cnt[li[p * B + t] + 1]++;
+        for (int i = 0; i < nl; i++) cnt[i + 1] += cnt[i];
+        uint16_t *lp = &m.lptr[m.lp0[c]];
+        for (int i = 0; i <= nl; i++) lp[i] = (uint16_t)cnt[i];
+        uint16_t *le = &m.lent[(size_t)c * Np * B];
+        // entries visited in ascending e = p*B + t order -> each list ascending
+        for (int p = 0; p < Np; p++)
+            for (int t = 0; t < ne; t++) le[cnt[li[p * B + t]]++] = (uint16_t)(p * B + t);
+        m.cmeta[(size_t)c * 8 + 7] = m.lp0[c];
+        const int w = (nl + 1 + 7) & ~7;
+        if (w > max_lp) max_lp = w;
+    }
+    m.max_lptr = max_lp;
     m.max_local = max_local;
+    m.max_win = max_win;
     m.max_colors = max_col;
     return true;
 }

@@ -40,13 +40,16 @@ cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t
                         int32_t *mu_out, int64_t *n_labels, cudaStream_t s);
 
 // ------------------------------- step.cu -----------------------------------
-struct DevChunks {  // device copy of ChunkMeta
+struct DevChunks {  // device view of ChunkMeta
     int B, Np;
-    int64_t E, N, nchunks, N_int, N_sh, n_slots;
-    int max_local;
-    int32_t *int_start, *shl_start, *shl_node, *shl_slot, *sh_pstart;
-    uint16_t *lidx;
-    uint8_t *color, *ncolors;
+    int64_t E, N, nchunks, N_int, N_sh, N_tot, n_slots;
+    int max_local, max_win, max_lptr;
+    const int32_t *cmeta;      // [nchunks][8]
+    const uint16_t *lidx;      // [nchunks][Np][B] chunk-local node of (p, t)
+    const uint16_t *lent;      // [nchunks][Np*B] node CSR entries p*B + t
+    const uint16_t *lptr;      // per-chunk CSR row pointers (block at cmeta[7])
+    const int32_t *sh_pstart;  // [N_sh+1]
+    const int32_t *sh_slots;   // [n_slots used]
 };
 
 cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s);
@@ -55,8 +58,9 @@ cudaError_t launch_geometry(const double *vxy, const int32_t *tri_or_in, const i
                             const double *c_in, int64_t E, int64_t Epad, double *Grr,
                             double *Gss, double *Grs, double *detJ, int32_t *bad,
                             cudaStream_t s);
-// Lumped mass, assembled with the chunk machinery; writes dt2M = dt^2 / Mbar.
-cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *partial,
+// Lumped mass, assembled with the chunk machinery; writes dt2M = dt^2 / Mbar
+// (0 in the alignment holes).  Uses `slot` as scratch.
+cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *slot,
                           double *dt2M, cudaStream_t s);
 
 struct StepParams {
@@ -64,19 +68,19 @@ struct StepParams {
     const double *dt2M;
     const double *U;   // U^n
     double *Uprev;     // U^{n-1} in, U^{n+1} out
-    double *partial;
+    double *slot;      // halo copies of U^n in, partial sums out (K7); reversed in K8
     int32_t src;       // internal node id of the source (-1 none)
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
 };
-cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, cudaStream_t s);
+int k7_grid(const DevChunks &ch);
+cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s);
 cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s);
-
-// Node-array permutations for I/O: out[map[i]] = in[i] / out[i] = in[map[i]].
-cudaError_t launch_scatter_f64(const double *in, const int32_t *map, int64_t n, double *out,
-                               cudaStream_t s);
-cudaError_t launch_gather_f64(const double *in, const int32_t *map, int64_t n, double *out,
-                              cudaStream_t s);
+// slot[j] = U[shared node of j] for every slot (after the state is set externally)
+cudaError_t launch_halo_fill(const DevChunks &ch, const double *U, double *slot, cudaStream_t s);
+// out[omap ? omap[i] : i] = in[imap ? imap[i] : i], i < n
+cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,
+                               double *out, cudaStream_t s);
 cudaError_t launch_nonfinite(const double *a, int64_t n, int32_t *flag, cudaStream_t s);
 
 }  // namespace sem

@@ -1,20 +1,26 @@
 // step.cu -- sm_100a kernels of the leapfrog step (product path).
 //
-//  K6  launch_geometry   G_e = c_e^2 detJ J^-1 J^-T (3 fp64), detJ
-//      assemble_mass     M-bar_nu = sum detJ w^M_q, dt^2 / M-bar
-//  K7  launch_k7         per chunk (one CTA): gather U^n into shared memory,
-//                        y_e = K^e u_e, colour-ordered shared-memory scatter,
-//                        fused leapfrog update of the chunk's interior nodes,
-//                        partial sums for shared nodes                   (Alg. 1+2+3)
-//  K8  launch_k8         shared nodes: add the per-chunk partials in chunk
-//                        order, then the same fused update
+//  K6  launch_geometry  G_e = c_e^2 detJ J^-1 J^-T (3 fp64), detJ
+//      assemble_mass    M-bar_nu = sum detJ w^M_q, then dt^2 / M-bar
+//  K7  launch_k7        persistent, warp-specialised: a producer warp streams
+//                       each chunk's contiguous blocks into shared memory with
+//                       TMA bulk copies (cp.async.bulk + mbarrier, 2 stages);
+//                       8 consumer warps: (E) u_e gathered through the chunk's
+//                       local index table, y_e = K^e u_e (one element per
+//                       thread, written to [p][t] slots), (B) node-centric gather of
+//                       y in fixed CSR order fused with the leapfrog update of
+//                       the chunk's interior nodes, partial sums of its shared
+//                       nodes into the chunk's slot block  (Alg. 1+2+3)
+//  K8  launch_k8        shared nodes: add the slots in ascending chunk order,
+//                       same fused update, write U^{n+1} back into the slots
+//                       (halo copies for the next step)
 //
 // Element stiffness (readings R2, R5): K^e = Grr*Srr + Gss*Sss + Grs*Srs, with
-// S_ab = D_a^T W D_b (+ transpose for rs) from the reference tables.  It is
-// the composition of Algorithm 1's gradient and Algorithm
-// 2's weighted divergence with F = c^2 I, B = -I, and the
-// FK/BK precalculation pushed one step further
-// into the reference matrices, as PAPER.md:1568 suggests.
+// S_ab = D_a^T W D_b (+ transpose for rs) from the reference tables: the
+// composition of Algorithm 1's gradient and Algorithm 2's
+// weighted divergence with F = c^2 I, B = -I; the FK/BK
+// precalculation is pushed into the reference
+// matrices, as PAPER.md:1568 suggests.
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -24,6 +30,9 @@ namespace sem {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kStages = 2;
+constexpr int kD = 6;    // list depth handled without a loop (mesh vertex degree)
+constexpr int kPre = 5;  // interior nodes per thread prefetched in registers
 
 __constant__ double c_Srr[kMaxNp][kMaxNp];
 __constant__ double c_Sss[kMaxNp][kMaxNp];
@@ -42,6 +51,61 @@ __device__ __forceinline__ double ricker_dev(double t, double f0, double t0) {
     a = a * a;
     return (1.0 - 2.0 * a) * exp(-a);
 }
+
+// ---- PTX helpers: mbarrier + TMA bulk copy -----------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0,
+// both addresses 16-byte aligned).
+__device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+}
+
+// Shared-memory layout of one pipeline stage (all offsets 16-byte aligned).
+struct StageLayout {
+    int lidx, lent, lptr, g, meta, u, size;
+    __host__ __device__ StageLayout(int np, int L, int Lp) {
+        lidx = 0;
+        lent = np * kThreads * 2;
+        lptr = lent + np * kThreads * 2;
+        g = lptr + Lp * 2;
+        meta = g + 3 * kThreads * 8;
+        u = meta + 32;
+        size = (u + L * 8 + 127) & ~127;
+    }
+};
 
 __global__ void k_geometry(const double *__restrict__ vxy, const int32_t *__restrict__ tri,
                            const int32_t *__restrict__ perm, const double *__restrict__ c_in,
@@ -65,127 +129,212 @@ __global__ void k_geometry(const double *__restrict__ vxy, const int32_t *__rest
     detJ[k] = det;
 }
 
-// ---- lumped mass with the chunk machinery ------------------------------------
+// ---- lumped mass with the chunk machinery (one-time, not pipelined) -----------
 template <int NP>
 __global__ void __launch_bounds__(kThreads) k_mass_chunk(const DevChunks ch, const double *__restrict__ detJ,
-                                                         double dt2, double *__restrict__ partial,
+                                                         double dt2, double *__restrict__ slot,
                                                          double *__restrict__ dt2M) {
-    extern __shared__ double smem[];
-    const int c = blockIdx.x, t = threadIdx.x, B = ch.B;
-    const int i0 = ch.int_start[c], nint = ch.int_start[c + 1] - i0;
-    const int s0 = ch.shl_start[c], nsh = ch.shl_start[c + 1] - s0;
-    double *y_s = smem;
-    for (int i = t; i < nint + nsh; i += B) y_s[i] = 0.0;
-    const int64_t e = (int64_t)c * B + t;
-    uint16_t li[NP];
+    __shared__ double ybuf[NP * kThreads];
+    const int c = blockIdx.x, t = threadIdx.x;
+    const int *cm = ch.cmeta + 8 * (int64_t)c;
+    const int i0 = cm[0], nint = cm[1], s0 = cm[2], nsh = cm[3], ne = cm[5], ni_al = cm[6], lp0 = cm[7];
+    const int64_t e = (int64_t)c * kThreads + t;
+    const double dj = (t < ne) ? detJ[e] : 0.0;
 #pragma unroll
-    for (int p = 0; p < NP; p++) li[p] = ch.lidx[(int64_t)c * NP * B + p * B + t];
-    const int col = ch.color[e];
-    const double dj = detJ[e];
+    for (int p = 0; p < NP; p++) ybuf[p * kThreads + t] = 1.0 * dj * c_wM[p];
     __syncthreads();
-    const int ncol = ch.ncolors[c];
-    for (int k = 0; k < ncol; k++) {
-        if (col == k) {
-#pragma unroll
-            for (int p = 0; p < NP; p++) y_s[li[p]] += 1.0 * dj * c_wM[p];
-        }
-        __syncthreads();
+    const uint16_t *lp = ch.lptr + lp0;
+    const uint16_t *le = ch.lent + (int64_t)c * NP * kThreads;
+    for (int i = t; i < ni_al + nsh; i += kThreads) {
+        double m = 0.0;
+        for (int j = lp[i]; j < lp[i + 1]; j++) m += ybuf[le[j]];
+        if (i < nint) dt2M[i0 + i] = dt2 / m;
+        else if (i >= ni_al) slot[s0 + i - ni_al] = m;
     }
-    for (int i = t; i < nint; i += B) dt2M[i0 + i] = dt2 / y_s[i];
-    for (int k = t; k < nsh; k += B) partial[ch.shl_slot[s0 + k]] = y_s[nint + k];
 }
 
-__global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ partial, double dt2,
+__global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ slot, double dt2,
                            double *__restrict__ dt2M) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh) return;
     double m = 0.0;
-    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) m += partial[j];
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) m += slot[ch.sh_slots[j]];
     dt2M[ch.N_int + s] = dt2 / m;
 }
 
-// ---- K7: stiffness apply + fused leapfrog for one chunk ----------------------
-template <int NP>
-__global__ void __launch_bounds__(kThreads) k7_step(const DevChunks ch, const StepParams a) {
-    extern __shared__ double smem[];
-    const int c = blockIdx.x, t = threadIdx.x, B = ch.B;
-    const int i0 = ch.int_start[c], nint = ch.int_start[c + 1] - i0;
-    const int s0 = ch.shl_start[c], nsh = ch.shl_start[c + 1] - s0;
-    double *u_s = smem;
-    double *y_s = smem + ch.max_local;
-
-    // element data of this thread (coalesced: [chunk][p][t] and SoA G)
-    const int64_t e = (int64_t)c * B + t;
-    uint16_t li[NP];
+// Sum of a local node's element contributions in CSR order (fixed order; the
+// first kD entries are loaded together, absent ones contribute an exact +0).
+__device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *le, const uint16_t *lp, int i) {
+    const int j0 = lp[i], j1 = lp[i + 1];
+    double part[kD];
 #pragma unroll
-    for (int p = 0; p < NP; p++) li[p] = ch.lidx[(int64_t)c * NP * B + p * B + t];
-    const double grr = a.Grr[e], gss = a.Gss[e], grs = a.Grs[e];
-    const int col = ch.color[e];
+    for (int d = 0; d < kD; d++) part[d] = (j0 + d < j1) ? ebuf[le[j0 + d]] : 0.0;
+    double y = 0.0;
+#pragma unroll
+    for (int d = 0; d < kD; d++) y += part[d];
+    for (int j = j0 + kD; j < j1; j++) y += ebuf[le[j]];
+    return y;
+}
 
-    // gather U^n: the chunk's interior window is contiguous, shared nodes listed
-    for (int i = t; i < nint; i += B) { u_s[i] = a.U[i0 + i]; y_s[i] = 0.0; }
-    for (int k = t; k < nsh; k += B) {
-        u_s[nint + k] = a.U[ch.N_int + ch.shl_node[s0 + k]];
-        y_s[nint + k] = 0.0;
+// ---- K7 ---------------------------------------------------------------------------
+template <int NP>
+__global__ void __launch_bounds__(kThreads + 32, 2)
+    k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const StageLayout lay(NP, L, Lp);
+    double *ebuf = reinterpret_cast<double *>(sm + kStages * lay.size);  // [NP][B] element slots
+    uint64_t *full = reinterpret_cast<uint64_t *>(ebuf + NP * kThreads);
+    uint64_t *empty = full + kStages;
+    const int t = threadIdx.x;
+    const int64_t nch = ch.nchunks;
+
+    if (t == 0) {
+        for (int s = 0; s < kStages; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        fence_mbar_init();
     }
     __syncthreads();
 
-    double u[NP], y[NP];
-#pragma unroll
-    for (int p = 0; p < NP; p++) { u[p] = u_s[li[p]]; y[p] = 0.0; }
-    // y = K^e u with K^e symmetric: build each K_pq once (p <= q)
-#pragma unroll
-    for (int p = 0; p < NP; p++) {
-#pragma unroll
-        for (int q = p; q < NP; q++) {
-            const double k = fma(grr, c_Srr[p][q], fma(gss, c_Sss[p][q], grs * c_Srs[p][q]));
-            if (q == p) {
-                y[p] = fma(k, u[p], y[p]);
-            } else {
-                y[p] = fma(k, u[q], y[p]);
-                y[q] = fma(k, u[p], y[q]);
+    if (t >= kThreads) {
+        // ===== producer warp: one lane streams chunk blocks with TMA =====
+        if (t == kThreads) {
+            int k = 0;
+            for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+                const int s = k % kStages;
+                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) & 1) ^ 1);
+                unsigned char *st = sm + s * lay.size;
+                const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+                const int4 m1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
+                reinterpret_cast<int4 *>(st + lay.meta)[0] = m0;
+                reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
+                const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z, lp0 = m1.w;
+                const int nsh_al = (nsh + 1) & ~1;
+                const int nlp = (ni_al + nsh + 1 + 7) & ~7;
+                const uint32_t bytes = 2 * NP * kThreads * 2 + nlp * 2 + 3 * kThreads * 8 +
+                                       (uint32_t)(ni_al + nsh_al) * 8;
+                mbar_arrive_expect_tx(&full[s], bytes);
+                const int64_t e0 = c * kThreads;
+                tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * kThreads * 2, &full[s]);
+                tma_load(st + lay.lent, ch.lent + e0 * NP, NP * kThreads * 2, &full[s]);
+                tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
+                tma_load(st + lay.g, a.Grr + e0, kThreads * 8, &full[s]);
+                tma_load(st + lay.g + kThreads * 8, a.Gss + e0, kThreads * 8, &full[s]);
+                tma_load(st + lay.g + 2 * kThreads * 8, a.Grs + e0, kThreads * 8, &full[s]);
+                if (ni_al > 0) tma_load(st + lay.u, a.U + i0, ni_al * 8, &full[s]);
+                if (nsh_al > 0) tma_load(st + lay.u + ni_al * 8, a.slot + s0, nsh_al * 8, &full[s]);
             }
         }
+        return;
     }
-    // conflict-free, deterministic scatter: one colour at a time
-    const int ncol = ch.ncolors[c];
-    for (int k = 0; k < ncol; k++) {
-        if (col == k) {
+
+    // ===== consumer warps =====
+    int k = 0;
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+        const int s = k % kStages;
+        mbar_wait(&full[s], (k / kStages) & 1);
+        const unsigned char *st = sm + s * lay.size;
+        const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
+        const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
+        const int i0 = m0.x, nint = m0.y, s0 = m0.z, nsh = m0.w, ne = m1.y, ni_al = m1.z;
+        const int nl = ni_al + nsh;
+        const double *u_s = reinterpret_cast<const double *>(st + lay.u);
+        const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
+        const uint16_t *le = reinterpret_cast<const uint16_t *>(st + lay.lent);
+        const uint16_t *lp = reinterpret_cast<const uint16_t *>(st + lay.lptr);
+        const double *g_s = reinterpret_cast<const double *>(st + lay.g);
+
+        // (E) y = K^e u, K^e symmetric: each K_pq (p <= q) built once
+        double y[NP];
 #pragma unroll
-            for (int p = 0; p < NP; p++) y_s[li[p]] += y[p];
+        for (int p = 0; p < NP; p++) y[p] = 0.0;
+        if (t < ne) {
+            const double grr = g_s[t], gss = g_s[kThreads + t], grs = g_s[2 * kThreads + t];
+            double u[NP];
+#pragma unroll
+            for (int p = 0; p < NP; p++) u[p] = u_s[li_s[p * kThreads + t]];
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+#pragma unroll
+                for (int q = p; q < NP; q++) {
+                    const double kk = fma(grr, c_Srr[p][q], fma(gss, c_Sss[p][q], grs * c_Srs[p][q]));
+                    if (q == p) {
+                        y[p] = fma(kk, u[p], y[p]);
+                    } else {
+                        y[p] = fma(kk, u[q], y[p]);
+                        y[q] = fma(kk, u[p], y[q]);
+                    }
+                }
+            }
         }
-        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < NP; p++) ebuf[p * kThreads + t] = y[p];
+        // prefetch U^{n-1} and dt^2/M of this thread's interior nodes (coalesced;
+        // the loads overlap the barrier and the reduction below)
+        double upr[kPre], mr[kPre];
+#pragma unroll
+        for (int q = 0; q < kPre; q++) {
+            const int i = t + q * kThreads;
+            upr[q] = 0.0;
+            mr[q] = 0.0;
+            if (i < nint) { upr[q] = a.Uprev[i0 + i]; mr[q] = a.dt2M[i0 + i]; }
+        }
+        consumer_sync();
+        // (B) node-centric gather of K U^n in fixed order + fused update
+        double *Unew = a.Uprev;
+#pragma unroll
+        for (int q = 0; q < kPre; q++) {
+            const int i = t + q * kThreads;
+            if (i < nl) {
+                const double yi = csr_sum(ebuf, le, lp, i);
+                if (i < nint) {
+                    const int id = i0 + i;
+                    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+                    Unew[id] = 2.0 * u_s[i] - upr[q] + mr[q] * (f - yi);
+                } else if (i >= ni_al) {
+                    a.slot[s0 + (i - ni_al)] = yi;
+                }
+            }
+        }
+        for (int i = t + kPre * kThreads; i < nl; i += kThreads) {  // chunks larger than kPre*B nodes
+            const double yi = csr_sum(ebuf, le, lp, i);
+            if (i < nint) {
+                const int id = i0 + i;
+                const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+                Unew[id] = 2.0 * u_s[i] - Unew[id] + a.dt2M[id] * (f - yi);
+            } else if (i >= ni_al) {
+                a.slot[s0 + (i - ni_al)] = yi;
+            }
+        }
+        consumer_sync();
+        if (t == 0) mbar_arrive(&empty[s]);
     }
-    // fused update of interior nodes: U^{n+1} = 2U^n - U^{n-1} + dt^2/M (f - K U^n)
-    for (int i = t; i < nint; i += B) {
-        const int id = i0 + i;
-        const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-        a.Uprev[id] = 2.0 * u_s[i] - a.Uprev[id] + a.dt2M[id] * (f - y_s[i]);
-    }
-    for (int k = t; k < nsh; k += B) a.partial[ch.shl_slot[s0 + k]] = y_s[nint + k];
 }
 
 // ---- K8: shared-node fix-up --------------------------------------------------
 __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh) return;
+    const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
     double y = 0.0;
-    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) y += a.partial[j];
+    for (int j = j0; j < j1; j++) y += a.slot[ch.sh_slots[j]];
     const int64_t id = ch.N_int + s;
     const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-    a.Uprev[id] = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
+    const double un = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
+    a.Uprev[id] = un;
+    for (int j = j0; j < j1; j++) a.slot[ch.sh_slots[j]] = un;
 }
 
-__global__ void k_scatter_f64(const double *__restrict__ in, const int32_t *__restrict__ map,
-                              int64_t n, double *__restrict__ out) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) out[map[i]] = in[i];
+__global__ void k_halo_fill(const DevChunks ch, const double *__restrict__ U, double *__restrict__ slot) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= ch.N_sh) return;
+    const double v = U[ch.N_int + s];
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) slot[ch.sh_slots[j]] = v;
 }
 
-__global__ void k_gather_f64(const double *__restrict__ in, const int32_t *__restrict__ map,
-                             int64_t n, double *__restrict__ out) {
+__global__ void k_permute_f64(const double *__restrict__ in, const int32_t *__restrict__ imap,
+                              const int32_t *__restrict__ omap, int64_t n, double *__restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[map[i]];
+    if (i >= n) return;
+    out[omap ? omap[i] : i] = in[imap ? imap[i] : i];
 }
 
 __global__ void k_nonfinite(const double *__restrict__ a, int64_t n, int32_t *flag) {
@@ -195,8 +344,13 @@ __global__ void k_nonfinite(const double *__restrict__ a, int64_t n, int32_t *fl
 
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
-    if (bytes <= 48 * 1024) return cudaSuccess;
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+size_t k7_smem_bytes(int np, int L, int W, int Lp) {
+    (void)W;
+    const StageLayout lay(np, L, Lp);
+    return (size_t)kStages * lay.size + (size_t)np * kThreads * 8 + 2 * kStages * 8;
 }
 
 }  // namespace
@@ -218,32 +372,47 @@ cudaError_t launch_geometry(const double *vxy, const int32_t *tri_or_in, const i
     return cudaGetLastError();
 }
 
-cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *partial,
+cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *slot,
                           double *dt2M, cudaStream_t s) {
-    const size_t smem = sizeof(double) * ch.max_local;
     const double dt2 = dt * dt;
     cudaError_t e;
-    if (ch.Np == 6) {
-        if ((e = set_smem(k_mass_chunk<6>, smem))) return e;
-        k_mass_chunk<6><<<(unsigned)ch.nchunks, ch.B, smem, s>>>(ch, detJ, dt2, partial, dt2M);
-    } else {
-        if ((e = set_smem(k_mass_chunk<10>, smem))) return e;
-        k_mass_chunk<10><<<(unsigned)ch.nchunks, ch.B, smem, s>>>(ch, detJ, dt2, partial, dt2M);
-    }
-    if (ch.N_sh > 0) k_mass_fix<<<blocks_for(ch.N_sh), kThreads, 0, s>>>(ch, partial, dt2, dt2M);
+    if ((e = cudaMemsetAsync(dt2M, 0, sizeof(double) * (ch.N_tot + 2), s))) return e;
+    if (ch.Np == 6)
+        k_mass_chunk<6><<<(unsigned)ch.nchunks, kThreads, 0, s>>>(ch, detJ, dt2, slot, dt2M);
+    else
+        k_mass_chunk<10><<<(unsigned)ch.nchunks, kThreads, 0, s>>>(ch, detJ, dt2, slot, dt2M);
+    if (ch.N_sh > 0) k_mass_fix<<<blocks_for(ch.N_sh), kThreads, 0, s>>>(ch, slot, dt2, dt2M);
     return cudaGetLastError();
 }
 
-cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, cudaStream_t s) {
-    const size_t smem = 2 * sizeof(double) * ch.max_local;
-    cudaError_t e;
-    if (ch.Np == 6) {
-        if ((e = set_smem(k7_step<6>, smem))) return e;
-        k7_step<6><<<(unsigned)ch.nchunks, ch.B, smem, s>>>(ch, p);
-    } else {
-        if ((e = set_smem(k7_step<10>, smem))) return e;
-        k7_step<10><<<(unsigned)ch.nchunks, ch.B, smem, s>>>(ch, p);
+int k7_grid(const DevChunks &ch) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
+    const size_t smem = k7_smem_bytes(ch.Np, ch.max_local, ch.max_win, ch.max_lptr);
+    int occ = 0;
+    if (ch.Np == 6) {
+        set_smem(k7_step<6>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k7_step<6>, kThreads + 32, smem);
+    } else {
+        set_smem(k7_step<10>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k7_step<10>, kThreads + 32, smem);
+    }
+    if (occ < 1) occ = 1;
+    int64_t g = (int64_t)occ * nsm;
+    if (g > ch.nchunks) g = ch.nchunks;
+    return (int)g;
+}
+
+cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s) {
+    const size_t smem = k7_smem_bytes(ch.Np, ch.max_local, ch.max_win, ch.max_lptr);
+    if (ch.Np == 6)
+        k7_step<6><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr);
+    else
+        k7_step<10><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr);
     return cudaGetLastError();
 }
 
@@ -253,15 +422,15 @@ cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s) 
     return cudaGetLastError();
 }
 
-cudaError_t launch_scatter_f64(const double *in, const int32_t *map, int64_t n, double *out,
-                               cudaStream_t s) {
-    k_scatter_f64<<<blocks_for(n), kThreads, 0, s>>>(in, map, n, out);
+cudaError_t launch_halo_fill(const DevChunks &ch, const double *U, double *slot, cudaStream_t s) {
+    if (ch.N_sh == 0) return cudaSuccess;
+    k_halo_fill<<<blocks_for(ch.N_sh), kThreads, 0, s>>>(ch, U, slot);
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather_f64(const double *in, const int32_t *map, int64_t n, double *out,
-                              cudaStream_t s) {
-    k_gather_f64<<<blocks_for(n), kThreads, 0, s>>>(in, map, n, out);
+cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,
+                               double *out, cudaStream_t s) {
+    k_permute_f64<<<blocks_for(n), kThreads, 0, s>>>(in, imap, omap, n, out);
     return cudaGetLastError();
 }
 

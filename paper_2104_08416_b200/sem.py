@@ -27,7 +27,8 @@ SEM_NUMBERING_CANONICAL, SEM_NUMBERING_INTERNAL = 0, 1
 
 EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem_build_operators",
             "sem_step_n", "sem_read_field", "sem_write_state", "sem_set_step", "sem_sync",
-            "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version"]
+            "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version",
+            "sem_debug_chunk_stats"]
 
 
 class SemError(RuntimeError):
@@ -81,6 +82,7 @@ def load(path: str = LIB_PATH):
         L.sem_get_info.argtypes = [P, C.POINTER(sem_info)]
         L.sem_set_kernel_timing.argtypes = [P, C.c_int]
         L.sem_kernel_times.argtypes = [P, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]
+        L.sem_debug_chunk_stats.argtypes = [P, i64, C.c_int, i64, C.c_int, P, P, P]
         L.sem_version.argtypes = []
         L.sem_version.restype = C.c_char_p
         for n in EXPORTED:
@@ -203,3 +205,26 @@ class SemContext:
 
 def version() -> str:
     return load().sem_version().decode()
+
+
+CHUNK_STAT_KEYS = ["nchunks", "N_int", "N_sh", "n_slots", "max_local", "max_win", "max_lptr",
+                   "max_colors", "sum_nint", "sum_nsh", "max_nsh"]
+
+
+def sem_debug_chunk_stats(mu, N: int, B: int = 256, want_maps: bool = False):
+    """Host-only chunk-builder diagnostics (see include/sem.h)."""
+    L = load()
+    mu = np.ascontiguousarray(mu, np.int32)
+    E, Np = mu.shape
+    st = np.zeros(16, np.int64)
+    int_of = np.empty(N, np.int32) if want_maps else None
+    nch = (E + B - 1) // B
+    cmeta = np.empty(nch * 8, np.int32) if want_maps else None
+    rc = L.sem_debug_chunk_stats(_ptr(mu), E, Np, N, B, _ptr(st), _ptr(int_of), _ptr(cmeta))
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_debug_chunk_stats failed")
+    d = {k: int(v) for k, v in zip(CHUNK_STAT_KEYS, st)}
+    if want_maps:
+        d["int_of"] = int_of
+        d["cmeta"] = cmeta.reshape(nch, 8)
+    return d
