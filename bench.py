@@ -314,21 +314,30 @@ def _cpu_model():
 
 def run_reference(args):
     """--impl reference: the oracle (the reference arm of this tier), timed as it
-    stands on the host cores, on a bounded sample of the same workload."""
+    stands on the host cores, on a bounded sample of the same workload recipe.
+
+    The sample is the same recipe at a reduced cell count per axis, chosen from
+    a short calibration so that the W + K oracle steps take about a minute."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import core
     from oracle.core import OracleSEM
     from paper_2104_08416_b200 import meshgen as mg
-    # sample: the same recipe at reduced size so W + K oracle steps take ~1-2 min
-    budget_s = 90.0
-    scale = 1
+    budget_s = 60.0
     nthr = core.num_threads()
-    per_elem_s = 1.2e-6 / max(nthr, 1)  # rough oracle cost per element-update
-    while (2048 // scale) ** 2 * 2 * per_elem_s * (args.steps + args.warmup) > budget_s and scale < 256:
+    # calibrate the oracle's element-update rate on a small sample of the recipe
+    cal = mg.config(args.config, 16)
+    oc = OracleSEM(cal.mesh.vxy, cal.mesh.tri, cal.P, cal.c)
+    oc.leapfrog(cal.dt, 1, src=cal.src_vertex, A=1.0, f0=cal.f0, t0=cal.t0)
+    t0 = time.perf_counter()
+    oc.leapfrog(cal.dt, 3, src=cal.src_vertex, A=1.0, f0=cal.f0, t0=cal.t0)
+    rate = 3 * cal.mesh.ne / (time.perf_counter() - t0)
+    full_e = problem_elems(args.config)
+    scale = 1
+    while full_e / (scale * scale) * (args.steps + args.warmup) / rate > budget_s and scale < 64:
         scale *= 2
-    pb = mg.config(args.config, scale) if args.config != "C4" else mg.config("C4", scale)
+    pb = mg.config(args.config, scale)
     m = pb.mesh
     o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
     U, Up = o.leapfrog(pb.dt, args.warmup, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
@@ -337,7 +346,8 @@ def run_reference(args):
                step0=args.warmup)
     dt = time.perf_counter() - t0
     value = m.ne * args.steps / dt
-    sample = "%s recipe at 1/%d cell count per axis (%d elements), %d steps" % (args.config, scale, m.ne, args.steps)
+    sample = ("%s recipe at 1/%d cells per axis (%d elements of %d), %d steps on %d host threads"
+              % (args.config, scale, m.ne, full_e, args.steps, nthr))
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -346,6 +356,10 @@ def run_reference(args):
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthr, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def problem_elems(name):
+    return {"C1": 2048, "C2": 524288, "C3": 4000000, "C4": 8388608, "C5": 268435456}[name]
 
 
 def main():
