@@ -108,19 +108,34 @@ def k7_bytes(info):
     return float(k7), float(k8)
 
 
+def _make_ctx(S, local, rank, world, stream, dist):
+    nccl_id = None
+    if world > 1:
+        obj = [S.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    return S.SemContext(local, rank, world, nccl_id=nccl_id, stream=stream.cuda_stream)
+
+
+def _max_over_ranks(dist, x):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import torch
     from paper_2104_08416_b200 import sem as S
-    from paper_2104_08416_b200 import meshgen as mg
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        world = args.gpus if world == 1 else world
     torch.cuda.set_device(local)
     dist = None
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # a real (non-default) stream shared by libsem and the torch events
@@ -128,13 +143,14 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     peak, peak_src, peaks = load_peak()
 
-    pb = problem_for(args.config, 1)  # replicas: every rank runs the per-GPU workload
+    # weak scaling: the global C4 mesh grows with the GPU count (2048^2 cells per GPU)
+    pb = problem_for(args.config, world)
     m = pb.mesh
-    ctx = S.SemContext(local, stream=stream.cuda_stream)
-    r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
+    ctx = _make_ctx(S, local, rank, world, stream, dist)
+    ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
     ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt)
     info = ctx.sem_get_info()
-    E = info["n_elements"]
+    E_glob = info["n_elements_global"]
 
     # warm-up (untimed)
     ctx.sem_step_n(args.warmup)
@@ -159,15 +175,12 @@ def run_ours(args):
     kt = ctx.sem_kernel_times()
     ctx.sem_set_kernel_timing(False)
     clk = clocks.stop()
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(dist, ms)
     U, nstep = ctx.sem_read_field()
-    finite = bool(np.isfinite(U).all())
+    finite = bool(np.isfinite(U[~np.isnan(U)]).all()) if world > 1 else bool(np.isfinite(U).all())
 
     ms_step = ms / args.steps
-    value = E * world * args.steps / (ms / 1e3)
+    value = E_glob * args.steps / (ms / 1e3)
     b7, b8 = k7_bytes(info)
     k7_avg = kt["k7_ms"] / max(kt["k7_launches"], 1)
     k8_avg = kt["k8_ms"] / max(kt["k8_launches"], 1)
@@ -175,14 +188,19 @@ def run_ours(args):
     step_gbs = info["bytes_alg_per_step"] / (ms_step * 1e-3) / 1e9
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if args.config == "C4" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded meshgen recipe, DESIGN.md)",
         "config": {"workload": "%s: %s" % (args.config, WORKLOADS.get(args.config, "")),
-                   "elements_per_gpu": E, "nodes_per_gpu": info["n_nodes"], "degree": pb.P,
-                   "ordering": "hilbert elements + first-touch nodes", "parallelism": "replicas" if world > 1 else "1 GPU",
-                   "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (info["bytes_alg_per_step"] / 1e9),
+                   "elements_global": E_glob, "elements_per_gpu": info["n_elements"],
+                   "nodes_global": info["n_nodes_global"], "nodes_rank0": info["n_nodes"], "degree": pb.P,
+                   "ordering": "hilbert elements + first-touch nodes",
+                   "parallelism": ("contiguous Hilbert-range partition, NCCL interface exchange (%d ranks)" % world
+                                   if world > 1 else "1 GPU"),
+                   "interface_nodes_rank0": info["n_interface_nodes"], "neighbors_rank0": info["n_neighbors"],
+                   "l2": "no flush: per-step working set %.2f GB per GPU > 126 MB L2" % (info["bytes_alg_per_step"] / 1e9),
                    "chunk_elems": info["chunk_elems"], "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
-                   "max_colors": info["max_colors"], "dt": pb.dt},
+                   "dt": pb.dt},
         "roofline": {"bound": "hbm", "kernel": "k7_step (stiffness apply + fused leapfrog)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src, "traffic": None,
@@ -191,21 +209,22 @@ def run_ours(args):
                      "k8_avg_launch_ms": k8_avg, "k8_bytes_per_launch": b8},
         "step_alg_gbs": step_gbs, "step_alg_frac": step_gbs / peak,
         "step_alg_frac_of_8tbs": step_gbs / 8000.0,
-        "gpu_launches": int(kt["k7_launches"] + kt["k8_launches"]),
+        "gpu_launches": int(args.steps * info["launches_per_step"]),
         "clocks": clk,
         "prep_ms": {"mesh_reorder": info["prep_reorder_ms"], "build_operators": info["prep_build_ms"]},
         "field_finite": finite,
     }
     if rank == 0 and args.orderings and world == 1:
         out["orderings"] = orderings(ctx, pb, args, S)
-    if rank == 0 and args.e2e:
-        out["e2e"] = e2e(pb, args, S, local, stream)
     ctx.close()
+    if args.e2e:
+        out["e2e"] = e2e(pb, args, S, local, rank, world, stream, dist)
     if rank == 0 and world == 1 and args.cpu:
         out["cpu_baseline"] = cpu_baseline(pb)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -256,29 +275,32 @@ def orderings(ctx, pb, args, S):
     return res
 
 
-def e2e(pb, args, S, device, stream):
+def e2e(pb, args, S, device, rank, world, stream, dist):
     """The whole job through the public C ABI from pinned host buffers:
     mesh H2D + reorder + operators + K steps + field D2H, timed on the host
-    around synchronising calls (inputs start in host memory)."""
+    around synchronising calls (inputs start in host memory); max over ranks."""
     import torch
     m = pb.mesh
     vxy = torch.from_numpy(m.vxy).pin_memory()
     tri = torch.from_numpy(m.tri).pin_memory()
     c = torch.from_numpy(pb.c).pin_memory()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
-    ctx = S.SemContext(device, stream=stream.cuda_stream)
+    ctx = _make_ctx(S, device, rank, world, stream, dist)
     r = ctx.sem_mesh_reorder(vxy.numpy(), tri.numpy(), pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
     ctx.sem_build_operators(c.numpy(), pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt)
-    out = torch.empty(r["n_nodes"], dtype=torch.float64).pin_memory()
+    out = torch.zeros(r["n_nodes"], dtype=torch.float64).pin_memory()
     ctx.sem_step_n(args.steps)
     ctx.sem_read_field(out=out.numpy())
     t1 = time.perf_counter()
     ctx.close()
+    secs = _max_over_ranks(dist, t1 - t0)
     E = m.ne
-    h2d = m.vxy.nbytes + m.tri.nbytes + pb.c.nbytes
+    h2d = m.vxy.nbytes + m.tri.nbytes + pb.c.nbytes + (out.numel() * 8 if world > 1 else 0)
     d2h = out.numel() * 8 + E * 8 + r["n_nodes"] * 4
-    return {"value": E * args.steps / (t1 - t0), "unit": UNIT, "seconds": t1 - t0,
+    return {"value": E * args.steps / secs, "unit": UNIT, "seconds": secs,
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
             "includes": "sem_mesh_reorder + sem_build_operators + sem_step_n(K) + sem_read_field"}
 

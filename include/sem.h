@@ -66,15 +66,27 @@ enum { SEM_NUMBERING_CANONICAL = 0, SEM_NUMBERING_INTERNAL = 1 };
 /*
  * Create a context on CUDA device `device`.
  *  rank, world_size : this process's place in a multi-GPU run (world_size = 1
- *                     for one GPU).  world_size > 1 requires nccl_unique_id.
- *  nccl_unique_id   : 128-byte ncclUniqueId from rank 0 (NULL iff world_size==1).
+ *                     for one GPU; at most 32).  Rank r owns the contiguous
+ *                     range [floor(rE/G), floor((r+1)E/G)) of the reordered
+ *                     elements; nodes touched by several ranks
+ *                     are exchanged every step (NCCL send/recv).
+ *  nccl_unique_id   : 128-byte ncclUniqueId from rank 0 (sem_nccl_unique_id).
+ *                     NULL with world_size > 1 creates an in-process LOOPBACK
+ *                     partition: all G contexts live in one process (possibly
+ *                     on one GPU) and are built/stepped together with
+ *                     sem_group_build_operators / sem_group_step_n.
  *  cuda_stream      : cudaStream_t to enqueue on (e.g. torch's current stream),
  *                     or NULL for a stream owned by the context.
  * Errors: SEM_E_ARG (bad rank/world/device), SEM_E_CUDA (no sm_100 device),
- *         SEM_E_UNSUPPORTED (world_size > 1 in a build without NCCL).
+ *         SEM_E_NCCL (libnccl.so.2 not loadable / ncclCommInitRank failed).
+ * On error *out may still hold a context carrying the message; free it.
  */
 sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
                       const void *nccl_unique_id, void *cuda_stream);
+
+/* 128-byte NCCL unique id for sem_create (call on rank 0, broadcast the bytes).
+ * NCCL is loaded with dlopen("libnccl.so.2").  Errors: SEM_E_ARG, SEM_E_NCCL. */
+sem_status sem_nccl_unique_id(void *out128);
 
 /* Release every device buffer and the context.  NULL is a no-op. */
 void sem_free(sem_ctx *ctx);
@@ -152,15 +164,30 @@ sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t 
 sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps);
 
 /*
- * Copy U^n to out_host[N] (fp64) in the requested numbering and return the
- * step index n.  Synchronises.  Errors: SEM_E_STATE, SEM_E_ARG, SEM_E_CUDA,
- * SEM_E_NONFINITE ("non-finite field at step n").
+ * Loopback partitions (contexts created with world_size > 1 and no NCCL id):
+ * the same builds and steps as sem_build_operators / sem_step_n, run for all n
+ * contexts of the group together; the interface exchange is a device-to-device
+ * copy ordered with CUDA events.  The kernels are the multi-GPU ones.
+ */
+sem_status sem_group_build_operators(sem_ctx **ctxs, int n, const double *c_elem_host, int64_t src_vertex,
+                                     double f0, double t0, double amplitude, double dt);
+sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps);
+
+/*
+ * Copy U^n to out_host[N] (fp64, N = global node count) in the requested
+ * numbering and return the step index n.  With several ranks only the nodes
+ * this rank owns (an interface node belongs to the lowest rank touching it) are
+ * written; other entries of out_host are left as they were, so a caller merges
+ * ranks by giving each the same array in turn.  Synchronises.
+ * Errors: SEM_E_STATE, SEM_E_ARG, SEM_E_CUDA, SEM_E_NONFINITE ("non-finite
+ * field at step n").
  */
 sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t *step_out);
 
 /*
- * Test/checkpoint hook: overwrite (U^n, U^{n-1}) from host arrays [N] in the
- * given numbering; the step index is left unchanged.  Either pointer may be
+ * Test/checkpoint hook: overwrite (U^n, U^{n-1}) from host arrays [N] (global
+ * node count) in the given numbering; each rank takes its local nodes.  The
+ * step index is left unchanged.  Either pointer may be
  * NULL to set that array to zero.  Errors: SEM_E_STATE, SEM_E_ARG, SEM_E_CUDA.
  */
 sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double *u_prev_host,
@@ -191,6 +218,11 @@ typedef struct {
     double bytes_alg_per_step;/* E (4 Np + 24) + 32 N */
     double prep_reorder_ms;   /* last sem_mesh_reorder wall time */
     double prep_build_ms;     /* last sem_build_operators wall time */
+    int64_t n_interface_nodes;/* nodes exchanged with other ranks */
+    int32_t n_neighbors;      /* ranks this rank exchanges with */
+    int32_t rank, world_size;
+    int64_t n_elements_global;
+    int64_t first_element;    /* global index of this rank's first element */
 } sem_info;
 
 sem_status sem_get_info(sem_ctx *ctx, sem_info *out);
@@ -217,6 +249,20 @@ sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches,
  */
 sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
                                  int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out);
+
+/*
+ * Host-only diagnostic of the multi-GPU partition (no GPU, no context): rank's
+ * part of a reordered connectivity mu [E][Np] (global node ids in [0, N)).
+ * sizes_out[8] = {e0, e1, n_local_nodes, n_neighbors, n_send, n_interface,
+ * n_sum_src, n_owned}; optional arrays (caller-sized from a first call with
+ * NULLs): loc2glob [n_local], nbr [n_neighbors], nbr_off [n_neighbors+1],
+ * send_glob [n_send] (global id sent at each position), if_glob [n_interface],
+ * sum_start [n_interface+1], sum_src [n_sum_src].  Errors: SEM_E_ARG, SEM_E_OOM.
+ */
+sem_status sem_debug_partition(const int32_t *mu, int64_t E, int Np, int64_t N, int rank, int world,
+                               int64_t *sizes_out, int32_t *loc2glob_out, int32_t *nbr_out, int32_t *nbr_off_out,
+                               int32_t *send_glob_out, int32_t *if_glob_out, int32_t *sum_start_out,
+                               int32_t *sum_src_out);
 
 /* Library version string. */
 const char *sem_version(void);

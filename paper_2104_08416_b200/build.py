@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsem.so")
-SOURCES = ["api.cu", "reorder.cu", "step.cu", "chunks.cpp", "refelem.cpp"]
+SOURCES = ["api.cu", "reorder.cu", "step.cu", "chunks.cpp", "partition.cpp", "refelem.cpp"]
 HEADERS = ["kernels.h", "sem_internal.h"]
 
 NVCC_FLAGS = [
@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB + ".tmp", "-lgomp"]
+           *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB + ".tmp", "-lgomp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr
     with open(os.path.join(CSRC, "build.log"), "w") as f:

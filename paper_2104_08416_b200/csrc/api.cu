@@ -1,6 +1,10 @@
 // api.cu -- the C ABI of libsem.so (include/sem.h).  Orchestrates the kernels
-// of reorder.cu / step.cu and owns all device memory of a context.
+// of reorder.cu / step.cu, the multi-GPU interface exchange (NCCL, loaded with
+// dlopen, or an in-process loopback for one-GPU testing), and owns all device
+// memory of a context.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <chrono>
 #include <climits>
@@ -21,10 +25,53 @@ using namespace sem;
 namespace {
 int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 constexpr int kChunkElems = 256;
+
+// ---- NCCL through dlopen (no link-time dependency; torch's copy is reused) ----
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        api.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+        return api;
+    }
+#define SYM(field, name)                                                  \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));    \
+    if (!api.field) { api.err = std::string("missing NCCL symbol ") + name; return api; }
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(Send, "ncclSend");
+    SYM(Recv, "ncclRecv");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    api.ok = true;
+    return api;
+}
 }  // namespace
 
 struct sem_ctx {
     int device = 0, rank = 0, world = 1;
+    bool loopback = false;  // world > 1 without NCCL: only the sem_group_* calls may step it
+    ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::string err;
@@ -33,19 +80,27 @@ struct sem_ctx {
     // mesh
     bool have_mesh = false, have_ops = false;
     int P = 0, Np = 0;
-    int64_t nv = 0, E = 0, N = 0;
+    int64_t nv = 0, E = 0, N = 0;  // E, N: this rank's elements / nodes
+    int64_t E_glob = 0, N_glob = 0, e0 = 0;
     int32_t grid[2] = {0, 0};
     RefTables T;
     std::vector<void *> mesh_allocs, ops_allocs;
     double *d_vxy = nullptr;
     int32_t *d_tri_or = nullptr;  // oriented triangles, INPUT order
-    int32_t *d_perm = nullptr;    // new -> input
-    int32_t *d_node_int = nullptr;   // [N] reordered node id -> internal (device layout) id
-    int32_t *d_node_perm = nullptr;  // [N] reordered node id -> canonical id
-    std::vector<int32_t> can_to_int;
+    int32_t *d_perm = nullptr;    // new -> input (global order)
+    // local node l: internal id, canonical id, reordered (first-touch) id; "own" = I/O owner subset
+    int32_t *d_loc_int = nullptr, *d_loc_can = nullptr, *d_loc_ft = nullptr;
+    int32_t *d_own_int = nullptr, *d_own_can = nullptr, *d_own_ft = nullptr;
+    int64_t n_own = 0;
+    std::vector<int32_t> can_to_int;  // canonical id -> internal id (-1 if not local)
     DevChunks dch{};
+    ChunkMeta meta_info;  // counts only
     int k7_grid = 0;
-    ChunkMeta meta_info;  // counts only (vectors released after upload)
+    // interface exchange
+    int64_t n_if = 0, n_send = 0;
+    std::vector<int32_t> nbr, nbr_off;
+    int32_t *d_send_if = nullptr, *d_sum_start = nullptr, *d_sum_src = nullptr;
+    double *d_xbuf = nullptr, *d_sendbuf = nullptr;  // xbuf = [own partials | received]
 
     // operators / state
     double *d_Grr = nullptr, *d_Gss = nullptr, *d_Grs = nullptr, *d_dt2M = nullptr;
@@ -55,6 +110,7 @@ struct sem_ctx {
     int32_t src_int = -1;
     double amp = 0, f0 = 1, t0 = 0, dt = 0;
     int64_t step = 0;
+    cudaEvent_t xev = nullptr;  // loopback: phase-1 done on this rank
 
     // timing
     bool timing = false;
@@ -81,6 +137,12 @@ sem_status cuda_fail(sem_ctx *c, cudaError_t e, const char *where) {
     do {                                                                \
         cudaError_t _e = (call);                                        \
         if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call);        \
+    } while (0)
+
+#define ST(call)                        \
+    do {                                \
+        sem_status _s = (call);         \
+        if (_s != SEM_OK) return _s;    \
     } while (0)
 
 template <typename T>
@@ -114,6 +176,9 @@ void reset_mesh(sem_ctx *ctx) {
     ctx->have_mesh = false;
     ctx->can_to_int.clear();
     ctx->dch = DevChunks{};
+    ctx->n_if = ctx->n_send = 0;
+    ctx->nbr.clear();
+    ctx->nbr_off.clear();
 }
 
 double now_ms() {
@@ -168,52 +233,247 @@ sem_status drain_events(sem_ctx *ctx) {
     return SEM_OK;
 }
 
+sem_status check_usable(sem_ctx *ctx) {
+    if (!ctx) return SEM_E_ARG;
+    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    return SEM_OK;
+}
+
+// ---- interface exchange ------------------------------------------------------------
+// NCCL: grouped send/recv of the packed partials with every neighbour rank.
+sem_status exchange_nccl(sem_ctx *ctx) {
+    if (ctx->nbr.empty()) return SEM_OK;
+    NcclApi &N = nccl();
+    ncclResult_t r = N.GroupStart();
+    for (size_t k = 0; r == ncclSuccess && k < ctx->nbr.size(); k++) {
+        const size_t off = ctx->nbr_off[k], cnt = ctx->nbr_off[k + 1] - off;
+        r = N.Send(ctx->d_sendbuf + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, ctx->stream);
+        if (r == ncclSuccess)
+            r = N.Recv(ctx->d_xbuf + ctx->n_if + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, ctx->stream);
+    }
+    ncclResult_t r2 = N.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(ctx, SEM_E_NCCL, std::string("NCCL exchange failed: ") +
+                                         N.GetErrorString(r != ncclSuccess ? r : r2));
+    return SEM_OK;
+}
+
+// Loopback: contexts of one process; rank r copies what rank q packed for it.
+sem_status exchange_loopback(sem_ctx **ctxs, int n) {
+    for (int r = 0; r < n; r++) {
+        sem_ctx *ctx = ctxs[r];
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaEventRecord(ctx->xev, ctx->stream));
+    }
+    for (int r = 0; r < n; r++) {
+        sem_ctx *ctx = ctxs[r];
+        CK(cudaSetDevice(ctx->device));
+        for (size_t k = 0; k < ctx->nbr.size(); k++) {
+            const int q = ctx->nbr[k];
+            sem_ctx *src = nullptr;
+            for (int j = 0; j < n; j++)
+                if (ctxs[j]->rank == q) src = ctxs[j];
+            if (!src) return fail(ctx, SEM_E_ARG, "loopback group lacks rank " + std::to_string(q));
+            size_t kq = 0;
+            while (kq < src->nbr.size() && src->nbr[kq] != ctx->rank) kq++;
+            if (kq == src->nbr.size()) return fail(ctx, SEM_E_MESH, "asymmetric neighbour lists");
+            const size_t cnt = ctx->nbr_off[k + 1] - ctx->nbr_off[k];
+            if ((size_t)(src->nbr_off[kq + 1] - src->nbr_off[kq]) != cnt)
+                return fail(ctx, SEM_E_MESH, "interface sizes differ between ranks");
+            CK(cudaStreamWaitEvent(ctx->stream, src->xev, 0));
+            CK(cudaMemcpyAsync(ctx->d_xbuf + ctx->n_if + ctx->nbr_off[k], src->d_sendbuf + src->nbr_off[kq],
+                               cnt * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    }
+    // a rank's send buffer must not be overwritten before its neighbours copied it
+    for (int r = 0; r < n; r++) {
+        sem_ctx *ctx = ctxs[r];
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaEventRecord(ctx->xev, ctx->stream));
+    }
+    for (int r = 0; r < n; r++) {
+        sem_ctx *ctx = ctxs[r];
+        CK(cudaSetDevice(ctx->device));
+        for (size_t k = 0; k < ctx->nbr.size(); k++)
+            for (int j = 0; j < n; j++)
+                if (ctxs[j]->rank == ctx->nbr[k]) CK(cudaStreamWaitEvent(ctx->stream, ctxs[j]->xev, 0));
+    }
+    return SEM_OK;
+}
+
+StepParams step_params(sem_ctx *ctx) {
+    StepParams p;
+    p.Grr = ctx->d_Grr; p.Gss = ctx->d_Gss; p.Grs = ctx->d_Grs; p.dt2M = ctx->d_dt2M;
+    p.slot = ctx->d_slot;
+    p.src = ctx->src_int; p.amp = ctx->amp; p.f0 = ctx->f0; p.t0 = ctx->t0; p.dt = ctx->dt;
+    p.U = ctx->d_U[ctx->cur];
+    p.Uprev = ctx->d_U[1 - ctx->cur];
+    p.n = ctx->step;
+    return p;
+}
+
+// Step phase 1: stiffness + update of everything local; pack interface partials.
+sem_status step_phase1(sem_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    ST(ensure_tables(ctx));
+    const StepParams p = step_params(ctx);
+    if (ctx->timing) ST(record(ctx, ctx->ev7, true));
+    CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream));
+    if (ctx->timing) ST(record(ctx, ctx->ev7, false));
+    if (ctx->timing) ST(record(ctx, ctx->ev8, true));
+    CK(launch_k8(ctx->dch, p, ctx->stream));
+    CK(launch_if_partial(ctx->dch, ctx->d_slot, ctx->d_xbuf, ctx->d_send_if, ctx->n_send, ctx->d_sendbuf,
+                         ctx->stream));
+    if (ctx->timing && ctx->n_if == 0) ST(record(ctx, ctx->ev8, false));
+    return SEM_OK;
+}
+
+// Step phase 2: rank-ordered interface sums + update; advance the step.
+sem_status step_phase2(sem_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->n_if > 0) {
+        const StepParams p = step_params(ctx);
+        CK(launch_k8_if(ctx->dch, p, ctx->d_xbuf, ctx->d_sum_start, ctx->d_sum_src, ctx->stream));
+        if (ctx->timing) ST(record(ctx, ctx->ev8, false));
+    }
+    ctx->cur = 1 - ctx->cur;
+    ctx->step++;
+    if (ctx->timing && ctx->ev7.size() >= 4096) ST(drain_events(ctx));
+    return SEM_OK;
+}
+
+sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_vertex, double f0, double t0,
+                        double amplitude, double dt) {
+    if (!ctx->have_mesh) return fail(ctx, SEM_E_STATE, "sem_build_operators before sem_mesh_reorder");
+    if (!c_elem_host) return fail(ctx, SEM_E_ARG, "c_elem is NULL");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(ctx, SEM_E_ARG, "dt must be > 0");
+    if (!(f0 > 0.0) && src_vertex >= 0) return fail(ctx, SEM_E_ARG, "f0 must be > 0");
+    if (src_vertex < -1 || src_vertex >= ctx->nv)
+        return fail(ctx, SEM_E_ARG, "source vertex " + std::to_string(src_vertex) + " out of range");
+    for (int64_t e = 0; e < ctx->E_glob; e++)
+        if (!(c_elem_host[e] > 0.0) || !std::isfinite(c_elem_host[e]))
+            return fail(ctx, SEM_E_ARG, "element " + std::to_string(e) + " has wave speed c <= 0");
+    CK(cudaSetDevice(ctx->device));
+    reset_ops(ctx);
+    ctx->prep_build_ms = -now_ms();
+    cudaStream_t s = ctx->stream;
+    const DevChunks &d = ctx->dch;
+    const int64_t Epad = d.nchunks * d.B;
+    auto &L = ctx->ops_allocs;
+    std::vector<void *> tmp;
+    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    double *d_c = nullptr, *d_detJ = nullptr;
+    int32_t *d_bad = nullptr;
+    CK(dalloc(tmp, &d_c, ctx->E_glob));
+    CK(dalloc(tmp, &d_detJ, Epad));
+    CK(dalloc(tmp, &d_bad, 1));
+    CK(cudaMemcpyAsync(d_c, c_elem_host, sizeof(double) * ctx->E_glob, cudaMemcpyHostToDevice, s));
+    CK(dalloc(L, &ctx->d_Grr, Epad));
+    CK(dalloc(L, &ctx->d_Gss, Epad));
+    CK(dalloc(L, &ctx->d_Grs, Epad));
+    const int64_t Nt = d.N_tot + 2;
+    CK(dalloc(L, &ctx->d_dt2M, Nt));
+    CK(dalloc(L, &ctx->d_U[0], Nt));
+    CK(dalloc(L, &ctx->d_U[1], Nt));
+    CK(dalloc(L, &ctx->d_slot, d.n_slots + 2));
+    CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
+    CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm + ctx->e0, d_c, ctx->E, Epad, ctx->d_Grr,
+                       ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
+    g_const_P = 0;
+    ST(ensure_tables(ctx));
+    CK(assemble_mass(d, d_detJ, dt, ctx->d_slot, ctx->d_dt2M, s));
+    CK(launch_if_partial(d, ctx->d_slot, ctx->d_xbuf, ctx->d_send_if, ctx->n_send, ctx->d_sendbuf, s));
+    CK(cudaMemsetAsync(ctx->d_U[0], 0, sizeof(double) * Nt, s));
+    CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * Nt, s));
+    int32_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has detJ <= 0");
+    ctx->src_int = src_vertex >= 0 ? ctx->can_to_int[src_vertex] : -1;
+    ctx->amp = amplitude;
+    ctx->f0 = f0;
+    ctx->t0 = t0;
+    ctx->dt = dt;
+    ctx->prep_build_ms += now_ms();
+    return SEM_OK;
+}
+
+sem_status build_phase2(sem_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const double t = now_ms();
+    CK(launch_mass_if(ctx->dch, ctx->d_xbuf, ctx->d_sum_start, ctx->d_sum_src, ctx->dt, ctx->d_dt2M, s));
+    CK(cudaMemsetAsync(ctx->d_slot, 0, sizeof(double) * (ctx->dch.n_slots + 2), s));  // halo of U^0 = 0
+    CK(cudaStreamSynchronize(s));
+    ctx->step = 0;
+    ctx->cur = 0;
+    ctx->have_ops = true;
+    ctx->prep_build_ms += now_ms() - t;
+    return SEM_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-const char *sem_version(void) { return "sem-hilbert-b200 0.1 (sm_100a)"; }
+const char *sem_version(void) { return "sem-hilbert-b200 0.2 (sm_100a)"; }
+
+sem_status sem_nccl_unique_id(void *out128) {
+    if (!out128) return SEM_E_ARG;
+    NcclApi &N = nccl();
+    if (!N.ok) return SEM_E_NCCL;
+    ncclUniqueId id;
+    if (N.GetUniqueId(&id) != ncclSuccess) return SEM_E_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, 128);
+    return SEM_OK;
+}
 
 sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
                       const void *nccl_unique_id, void *cuda_stream) {
     if (!out) return SEM_E_ARG;
     *out = nullptr;
-    if (world_size < 1 || rank < 0 || rank >= world_size || device < 0) return SEM_E_ARG;
-    if (world_size > 1) return SEM_E_UNSUPPORTED;  // multi-GPU halo: not in this build yet
-    (void)nccl_unique_id;
+    if (world_size < 1 || world_size > 32 || rank < 0 || rank >= world_size || device < 0) return SEM_E_ARG;
     sem_ctx *ctx = new (std::nothrow) sem_ctx();
     if (!ctx) return SEM_E_OOM;
+    *out = ctx;
     ctx->device = device;
     ctx->rank = rank;
     ctx->world = world_size;
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || device >= ndev) {
-        *out = ctx;
         ctx->dead = true;
         ctx->err = "no CUDA device available (libsem has no CPU fallback)";
         return SEM_E_CUDA;
     }
     cudaDeviceProp prop;
     if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess || prop.major != 10) {
-        *out = ctx;
         ctx->dead = true;
         ctx->err = "device is not sm_100 (B200); this library is built for sm_100a only";
         return SEM_E_CUDA;
     }
-    if ((e = cudaSetDevice(device)) != cudaSuccess) {
-        *out = ctx;
-        return cuda_fail(ctx, e, "cudaSetDevice");
-    }
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
     if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
     else {
-        if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) {
-            *out = ctx;
+        if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(ctx, e, "cudaStreamCreate");
-        }
         ctx->own_stream = true;
     }
-    *out = ctx;
+    if ((e = cudaEventCreateWithFlags(&ctx->xev, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(ctx, e, "cudaEventCreate");
+    if (world_size > 1) {
+        if (!nccl_unique_id) {
+            ctx->loopback = true;  // in-process partitions: step only through sem_group_*
+        } else {
+            NcclApi &N = nccl();
+            if (!N.ok) return fail(ctx, SEM_E_NCCL, N.err);
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_unique_id, sizeof(id));
+            ncclResult_t r = N.CommInitRank(&ctx->comm, world_size, id, rank);
+            if (r != ncclSuccess) return fail(ctx, SEM_E_NCCL, std::string("ncclCommInitRank: ") + N.GetErrorString(r));
+        }
+    }
     return SEM_OK;
 }
 
@@ -226,6 +486,8 @@ void sem_free(sem_ctx *ctx) {
     reset_mesh(ctx);
     for (auto *lst : {&ctx->ev7, &ctx->ev8, &ctx->pool})
         for (auto &ev : *lst) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    if (ctx->xev) cudaEventDestroy(ctx->xev);
+    if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -238,8 +500,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
                             uint32_t *hilbert_key_out, int32_t *elem_perm_out,
                             int32_t *node_perm_out, int64_t *n_nodes_out,
                             int32_t grid_wh_out[2]) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    ST(check_usable(ctx));
     if (degree != 2 && degree != 3)
         return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) + " (2 or 3)");
     if (elem_order < 0 || elem_order > 2)
@@ -251,6 +512,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
     const int Np = (degree + 1) * (degree + 2) / 2;
     if (n_elements * Np >= (int64_t)INT_MAX || n_vertices >= INT_MAX)
         return fail(ctx, SEM_E_ARG, "mesh too large for 32-bit indices");
+    if (n_elements < ctx->world) return fail(ctx, SEM_E_ARG, "fewer elements than ranks");
     for (int64_t i = 0; i < 3 * n_elements; i++)
         if (tri_host[i] < 0 || tri_host[i] >= n_vertices)
             return fail(ctx, SEM_E_MESH, "element " + std::to_string(i / 3) + " has a vertex id out of range");
@@ -262,7 +524,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         ctx->P = degree;
         ctx->Np = Np;
         ctx->nv = n_vertices;
-        ctx->E = n_elements;
+        ctx->E_glob = n_elements;
         if (!build_ref_tables(degree, ctx->T)) return fail(ctx, SEM_E_UNSUPPORTED, "reference tables");
         const int64_t E = n_elements, nv = n_vertices;
         std::vector<void *> tmp;  // freed at the end of this call
@@ -340,7 +602,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         const int nI = (degree - 1) * (degree - 2) / 2;
         const int64_t N = nv + nedges * (degree - 1) + E * nI;
         if (N >= INT_MAX) return fail(ctx, SEM_E_ARG, "too many nodes for 32-bit indices");
-        ctx->N = N;
+        ctx->N_glob = N;
         CK(dalloc(tmp, &d_mu_new, E * Np));
         CK(launch_permute_rows(d_mu_can, ctx->d_perm, E, Np, d_mu_new, s));
         CK(dalloc(tmp, &d_node_perm, N));
@@ -367,14 +629,24 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         if (n_nodes_out) *n_nodes_out = N;
         if (grid_wh_out) { grid_wh_out[0] = ctx->grid[0]; grid_wh_out[1] = ctx->grid[1]; }
 
+        // ---- this rank's part: contiguous range of the global order ----
+        Partition part;
+        std::string err;
+        if (!build_partition(mu_h.data(), E, Np, N, ctx->rank, ctx->world, part, err))
+            return fail(ctx, SEM_E_MESH, err);
+        std::vector<int32_t>().swap(mu_h);
+        ctx->e0 = part.e0;
+        ctx->E = part.e1 - part.e0;
+        ctx->N = (int64_t)part.loc2glob.size();
+
         // ---- chunk metadata for the step kernel ----
         ChunkMeta m;
-        std::string err;
-        if (!build_chunks(mu_h.data(), E, Np, N, kChunkElems, m, err)) return fail(ctx, SEM_E_MESH, err);
-        std::vector<int32_t>().swap(mu_h);
+        if (!build_chunks(part.mu_local.data(), ctx->E, Np, ctx->N, kChunkElems, m, err,
+                          ctx->world > 1 ? part.remote.data() : nullptr))
+            return fail(ctx, SEM_E_MESH, err);
         DevChunks &d = ctx->dch;
         d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
-        d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots;
+        d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
         d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr;
         auto &L = ctx->mesh_allocs;
         int32_t *p_cmeta, *p_pstart, *p_slots;
@@ -385,21 +657,50 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(upload(L, &p_lptr, m.lptr, s));
         CK(upload(L, &p_pstart, m.sh_pstart, s));
         CK(upload(L, &p_slots, m.sh_slots, s));
-        d.cmeta = p_cmeta; d.lidx = p_lidx; d.lent = p_lent; d.lptr = p_lptr; d.sh_pstart = p_pstart; d.sh_slots = p_slots;
+        d.cmeta = p_cmeta; d.lidx = p_lidx; d.lent = p_lent; d.lptr = p_lptr; d.sh_pstart = p_pstart;
+        d.sh_slots = p_slots;
+        // node maps for I/O
         {
+            std::vector<int32_t> loc_int(ctx->N), loc_can(ctx->N), own_int, own_can, own_ft;
             ctx->can_to_int.assign(N, -1);
-            for (int64_t g = 0; g < N; g++) ctx->can_to_int[node_perm[g]] = m.int_of[g];
-            CK(upload(L, &ctx->d_node_int, m.int_of, s));
-            CK(upload(L, &ctx->d_node_perm, node_perm, s));
-            CK(cudaStreamSynchronize(s));
+            for (int64_t l = 0; l < ctx->N; l++) {
+                const int32_t g = part.loc2glob[l];
+                loc_int[l] = m.int_of[l];
+                loc_can[l] = node_perm[g];
+                ctx->can_to_int[node_perm[g]] = m.int_of[l];
+                if (part.owned[l]) {
+                    own_int.push_back(m.int_of[l]);
+                    own_can.push_back(node_perm[g]);
+                    own_ft.push_back(g);
+                }
+            }
+            ctx->n_own = (int64_t)own_int.size();
+            CK(upload(L, &ctx->d_loc_int, loc_int, s));
+            CK(upload(L, &ctx->d_loc_can, loc_can, s));
+            CK(upload(L, &ctx->d_loc_ft, part.loc2glob, s));
+            CK(upload(L, &ctx->d_own_int, own_int, s));
+            CK(upload(L, &ctx->d_own_can, own_can, s));
+            CK(upload(L, &ctx->d_own_ft, own_ft, s));
         }
+        // interface exchange buffers
+        ctx->n_if = m.N_if;
+        if ((int64_t)part.if_local.size() != m.N_if)
+            return fail(ctx, SEM_E_MESH, "interface node count mismatch between partition and chunks");
+        ctx->n_send = (int64_t)part.send_if.size();
+        ctx->nbr = part.nbr;
+        ctx->nbr_off = part.nbr_off;
+        CK(upload(L, &ctx->d_send_if, part.send_if, s));
+        CK(upload(L, &ctx->d_sum_start, part.sum_start, s));
+        CK(upload(L, &ctx->d_sum_src, part.sum_src, s));
+        CK(dalloc(L, &ctx->d_xbuf, ctx->n_if + ctx->n_send + 2));
+        CK(dalloc(L, &ctx->d_sendbuf, ctx->n_send + 2));
+        CK(cudaStreamSynchronize(s));
         ctx->k7_grid = k7_grid(d);
         ctx->meta_info = ChunkMeta();
-        ctx->meta_info.B = m.B; ctx->meta_info.Np = m.Np; ctx->meta_info.E = m.E; ctx->meta_info.N = m.N;
-        ctx->meta_info.nchunks = m.nchunks; ctx->meta_info.N_int = m.N_int; ctx->meta_info.N_sh = m.N_sh;
-        ctx->meta_info.N_tot = m.N_tot; ctx->meta_info.n_slots = m.n_slots; ctx->meta_info.max_local = m.max_local;
-        ctx->meta_info.max_win = m.max_win;
-        ctx->meta_info.max_colors = m.max_colors;
+        ChunkMeta &mi = ctx->meta_info;
+        mi.B = m.B; mi.Np = m.Np; mi.E = m.E; mi.N = m.N; mi.nchunks = m.nchunks; mi.N_int = m.N_int;
+        mi.N_sh = m.N_sh; mi.N_if = m.N_if; mi.N_tot = m.N_tot; mi.n_slots = m.n_slots;
+        mi.max_local = m.max_local; mi.max_win = m.max_win; mi.max_colors = m.max_colors;
         ctx->have_mesh = true;
         ctx->prep_reorder_ms = now_ms() - t_start;
         return SEM_OK;
@@ -410,104 +711,63 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
 
 sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t src_vertex,
                                double f0, double t0, double amplitude, double dt) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
-    if (!ctx->have_mesh) return fail(ctx, SEM_E_STATE, "sem_build_operators before sem_mesh_reorder");
-    if (!c_elem_host) return fail(ctx, SEM_E_ARG, "c_elem is NULL");
-    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(ctx, SEM_E_ARG, "dt must be > 0");
-    if (!(f0 > 0.0) && src_vertex >= 0) return fail(ctx, SEM_E_ARG, "f0 must be > 0");
-    if (src_vertex < -1 || src_vertex >= ctx->nv)
-        return fail(ctx, SEM_E_ARG, "source vertex " + std::to_string(src_vertex) + " out of range");
-    for (int64_t e = 0; e < ctx->E; e++)
-        if (!(c_elem_host[e] > 0.0) || !std::isfinite(c_elem_host[e]))
-            return fail(ctx, SEM_E_ARG, "element " + std::to_string(e) + " has wave speed c <= 0");
+    ST(check_usable(ctx));
+    if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions are built with sem_group_build_operators");
     try {
-        CK(cudaSetDevice(ctx->device));
-        reset_ops(ctx);
-        const double t_start = now_ms();
-        cudaStream_t s = ctx->stream;
-        const DevChunks &d = ctx->dch;
-        const int64_t Epad = d.nchunks * d.B;
-        auto &L = ctx->ops_allocs;
-        std::vector<void *> tmp;
-        struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
-        double *d_c = nullptr, *d_detJ = nullptr;
-        int32_t *d_bad = nullptr;
-        CK(dalloc(tmp, &d_c, ctx->E));
-        CK(dalloc(tmp, &d_detJ, Epad));
-        CK(dalloc(tmp, &d_bad, 1));
-        CK(cudaMemcpyAsync(d_c, c_elem_host, sizeof(double) * ctx->E, cudaMemcpyHostToDevice, s));
-        CK(dalloc(L, &ctx->d_Grr, Epad));
-        CK(dalloc(L, &ctx->d_Gss, Epad));
-        CK(dalloc(L, &ctx->d_Grs, Epad));
-        const int64_t Nt = d.N_tot + 2;
-        CK(dalloc(L, &ctx->d_dt2M, Nt));
-        CK(dalloc(L, &ctx->d_U[0], Nt));
-        CK(dalloc(L, &ctx->d_U[1], Nt));
-        CK(dalloc(L, &ctx->d_slot, d.n_slots + 2));
-        CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
-        CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm, d_c, ctx->E, Epad, ctx->d_Grr,
-                           ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
-        g_const_P = 0;
-        sem_status st = ensure_tables(ctx);
-        if (st != SEM_OK) return st;
-        CK(assemble_mass(d, d_detJ, dt, ctx->d_slot, ctx->d_dt2M, s));
-        CK(cudaMemsetAsync(ctx->d_U[0], 0, sizeof(double) * Nt, s));
-        CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * Nt, s));
-        CK(cudaMemsetAsync(ctx->d_slot, 0, sizeof(double) * (d.n_slots + 2), s));  // halo of U^0 = 0
-        int32_t bad = 0;
-        CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has detJ <= 0");
-        ctx->src_int = src_vertex >= 0 ? ctx->can_to_int[src_vertex] : -1;
-        ctx->amp = amplitude;
-        ctx->f0 = f0;
-        ctx->t0 = t0;
-        ctx->dt = dt;
-        ctx->step = 0;
-        ctx->cur = 0;
-        ctx->have_ops = true;
-        ctx->prep_build_ms = now_ms() - t_start;
-        return SEM_OK;
+        ST(build_phase1(ctx, c_elem_host, src_vertex, f0, t0, amplitude, dt));
+        if (ctx->world > 1) ST(exchange_nccl(ctx));
+        return build_phase2(ctx);
     } catch (const std::bad_alloc &) {
         return fail(ctx, SEM_E_OOM, "host allocation failed in sem_build_operators");
     }
 }
 
 sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    ST(check_usable(ctx));
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_step_n before sem_build_operators");
+    if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions step with sem_group_step_n");
     if (n_steps < 0) return fail(ctx, SEM_E_ARG, "n_steps < 0");
-    CK(cudaSetDevice(ctx->device));
-    sem_status st = ensure_tables(ctx);
-    if (st != SEM_OK) return st;
-    StepParams p;
-    p.Grr = ctx->d_Grr; p.Gss = ctx->d_Gss; p.Grs = ctx->d_Grs; p.dt2M = ctx->d_dt2M;
-    p.slot = ctx->d_slot;
-    p.src = ctx->src_int; p.amp = ctx->amp; p.f0 = ctx->f0; p.t0 = ctx->t0; p.dt = ctx->dt;
     for (int64_t k = 0; k < n_steps; k++) {
-        p.U = ctx->d_U[ctx->cur];
-        p.Uprev = ctx->d_U[1 - ctx->cur];
-        p.n = ctx->step;
-        if (ctx->timing) { st = record(ctx, ctx->ev7, true); if (st) return st; }
-        CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream));
-        if (ctx->timing) { st = record(ctx, ctx->ev7, false); if (st) return st; }
-        if (ctx->dch.N_sh > 0) {
-            if (ctx->timing) { st = record(ctx, ctx->ev8, true); if (st) return st; }
-            CK(launch_k8(ctx->dch, p, ctx->stream));
-            if (ctx->timing) { st = record(ctx, ctx->ev8, false); if (st) return st; }
-        }
-        ctx->cur = 1 - ctx->cur;
-        ctx->step++;
-        if (ctx->timing && ctx->ev7.size() >= 4096) { st = drain_events(ctx); if (st) return st; }
+        ST(step_phase1(ctx));
+        if (ctx->world > 1) ST(exchange_nccl(ctx));
+        ST(step_phase2(ctx));
+    }
+    return SEM_OK;
+}
+
+sem_status sem_group_build_operators(sem_ctx **ctxs, int n, const double *c_elem_host, int64_t src_vertex,
+                                     double f0, double t0, double amplitude, double dt) {
+    if (!ctxs || n < 1) return SEM_E_ARG;
+    for (int r = 0; r < n; r++) {
+        ST(check_usable(ctxs[r]));
+        if (!ctxs[r]->loopback && ctxs[r]->world > 1) return fail(ctxs[r], SEM_E_STATE, "not a loopback context");
+    }
+    try {
+        for (int r = 0; r < n; r++) ST(build_phase1(ctxs[r], c_elem_host, src_vertex, f0, t0, amplitude, dt));
+        ST(exchange_loopback(ctxs, n));
+        for (int r = 0; r < n; r++) ST(build_phase2(ctxs[r]));
+        return SEM_OK;
+    } catch (const std::bad_alloc &) {
+        return SEM_E_OOM;
+    }
+}
+
+sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps) {
+    if (!ctxs || n < 1 || n_steps < 0) return SEM_E_ARG;
+    for (int r = 0; r < n; r++) {
+        ST(check_usable(ctxs[r]));
+        if (!ctxs[r]->have_ops) return fail(ctxs[r], SEM_E_STATE, "sem_group_step_n before build");
+    }
+    for (int64_t k = 0; k < n_steps; k++) {
+        for (int r = 0; r < n; r++) ST(step_phase1(ctxs[r]));
+        ST(exchange_loopback(ctxs, n));
+        for (int r = 0; r < n; r++) ST(step_phase2(ctxs[r]));
     }
     return SEM_OK;
 }
 
 sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t *step_out) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    ST(check_usable(ctx));
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_read_field before sem_build_operators");
     if (!out_host) return fail(ctx, SEM_E_ARG, "out is NULL");
     if (numbering != SEM_NUMBERING_CANONICAL && numbering != SEM_NUMBERING_INTERNAL)
@@ -518,27 +778,30 @@ sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t
     struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
     double *d_out = nullptr;
     int32_t *d_flag = nullptr;
-    CK(dalloc(tmp, &d_out, ctx->N));
+    const int64_t NG = ctx->N_glob;
+    CK(dalloc(tmp, &d_out, NG));
     CK(dalloc(tmp, &d_flag, 1));
-    CK(launch_permute_f64(ctx->d_U[ctx->cur], ctx->d_node_int,
-                          numbering == SEM_NUMBERING_CANONICAL ? ctx->d_node_perm : nullptr, ctx->N, d_out, s));
+    const bool full = ctx->n_own == NG;  // one rank: every global node
+    if (!full) CK(cudaMemcpyAsync(d_out, out_host, sizeof(double) * NG, cudaMemcpyHostToDevice, s));
+    CK(launch_permute_f64(ctx->d_U[ctx->cur], ctx->d_own_int,
+                          numbering == SEM_NUMBERING_CANONICAL ? ctx->d_own_can : ctx->d_own_ft, ctx->n_own,
+                          d_out, s));
     CK(launch_fill_i32(d_flag, 1, INT_MAX, s));
-    CK(launch_nonfinite(d_out, ctx->N, d_flag, s));
+    CK(launch_nonfinite(ctx->d_U[ctx->cur], ctx->dch.N_tot, d_flag, s));
     int32_t flag = 0;
-    CK(cudaMemcpyAsync(out_host, d_out, sizeof(double) * ctx->N, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_host, d_out, sizeof(double) * NG, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&flag, d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (step_out) *step_out = ctx->step;
     if (flag != INT_MAX)
         return fail(ctx, SEM_E_NONFINITE, "non-finite field at step " + std::to_string(ctx->step) +
-                                              " (node " + std::to_string(flag) + ")");
+                                              " (internal node " + std::to_string(flag) + ")");
     return SEM_OK;
 }
 
 sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double *u_prev_host,
                            int numbering) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    ST(check_usable(ctx));
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_write_state before sem_build_operators");
     if (numbering != SEM_NUMBERING_CANONICAL && numbering != SEM_NUMBERING_INTERNAL)
         return fail(ctx, SEM_E_ARG, "unknown numbering");
@@ -547,15 +810,15 @@ sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double
     std::vector<void *> tmp;
     struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
     double *d_in = nullptr;
-    CK(dalloc(tmp, &d_in, ctx->N));
-    const int32_t *imap = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_node_perm : nullptr;
+    CK(dalloc(tmp, &d_in, ctx->N_glob));
+    const int32_t *imap = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_loc_can : ctx->d_loc_ft;
     const double *src[2] = {u_curr_host, u_prev_host};
     double *dst[2] = {ctx->d_U[ctx->cur], ctx->d_U[1 - ctx->cur]};
     for (int k = 0; k < 2; k++) {
         CK(cudaMemsetAsync(dst[k], 0, sizeof(double) * (ctx->dch.N_tot + 2), s));
         if (!src[k]) continue;
-        CK(cudaMemcpyAsync(d_in, src[k], sizeof(double) * ctx->N, cudaMemcpyHostToDevice, s));
-        CK(launch_permute_f64(d_in, imap, ctx->d_node_int, ctx->N, dst[k], s));
+        CK(cudaMemcpyAsync(d_in, src[k], sizeof(double) * ctx->N_glob, cudaMemcpyHostToDevice, s));
+        CK(launch_permute_f64(d_in, imap, ctx->d_loc_int, ctx->N, dst[k], s));
     }
     CK(launch_halo_fill(ctx->dch, ctx->d_U[ctx->cur], ctx->d_slot, s));
     CK(cudaStreamSynchronize(s));
@@ -571,8 +834,7 @@ sem_status sem_set_step(sem_ctx *ctx, int64_t step) {
 }
 
 sem_status sem_sync(sem_ctx *ctx) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
+    ST(check_usable(ctx));
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
@@ -586,7 +848,7 @@ sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
     const ChunkMeta &m = ctx->meta_info;
     o->n_elements = ctx->E;
     o->n_nodes = ctx->N;
-    o->n_nodes_global = ctx->N;
+    o->n_nodes_global = ctx->N_glob;
     o->degree = ctx->P;
     o->nodes_per_elem = ctx->Np;
     o->n_chunks = m.nchunks;
@@ -596,19 +858,23 @@ sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
     o->n_shared_nodes = m.N_sh;
     o->n_partial_slots = m.n_slots;
     o->max_colors = m.max_colors;
-    o->launches_per_step = 1 + (m.N_sh > 0 ? 1 : 0);
+    o->launches_per_step = 1 + ((m.N_sh - m.N_if) > 0 ? 1 : 0) + (m.N_if > 0 ? 3 : 0);
     o->step = ctx->step;
     o->bytes_alg_per_step = (double)ctx->E * (4.0 * ctx->Np + 24.0) + 32.0 * (double)ctx->N;
     o->prep_reorder_ms = ctx->prep_reorder_ms;
     o->prep_build_ms = ctx->prep_build_ms;
+    o->n_interface_nodes = m.N_if;
+    o->n_neighbors = (int32_t)ctx->nbr.size();
+    o->rank = ctx->rank;
+    o->world_size = ctx->world;
+    o->n_elements_global = ctx->E_glob;
+    o->first_element = ctx->e0;
     return SEM_OK;
 }
 
 sem_status sem_set_kernel_timing(sem_ctx *ctx, int enable) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
-    sem_status st = drain_events(ctx);
-    if (st) return st;
+    ST(check_usable(ctx));
+    ST(drain_events(ctx));
     ctx->timing = enable != 0;
     ctx->t7 = ctx->t8 = 0;
     ctx->n7 = ctx->n8 = 0;
@@ -617,10 +883,8 @@ sem_status sem_set_kernel_timing(sem_ctx *ctx, int enable) {
 
 sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches, double *k8_ms,
                             int64_t *k8_launches) {
-    if (!ctx) return SEM_E_ARG;
-    if (ctx->dead) return fail(ctx, SEM_E_CUDA, "context unusable after a CUDA error: " + ctx->err);
-    sem_status st = drain_events(ctx);
-    if (st) return st;
+    ST(check_usable(ctx));
+    ST(drain_events(ctx));
     if (k7_ms) *k7_ms = ctx->t7;
     if (k7_launches) *k7_launches = ctx->n7;
     if (k8_ms) *k8_ms = ctx->t8;
@@ -628,17 +892,11 @@ sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches, d
     return SEM_OK;
 }
 
-}  // extern "C"
-
 // ---------------------------------------------------------------------------
-// Host-only diagnostics of the chunk builder (no GPU needed): used by the CPU
-// test-suite to check the metadata invariants and by DESIGN.md's sizing table.
-// stats_out[16] = {nchunks, N_int(padded), N_sh, n_slots, max_local, max_win,
-//                  max_lptr, max_colors, sum_nint, sum_nsh, max_nsh, 0...}
+// Host-only diagnostics (no GPU needed), used by the CPU test-suite.
 // ---------------------------------------------------------------------------
-extern "C" sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
-                                            int64_t *stats_out, int32_t *int_of_out,
-                                            int32_t *cmeta_out) {
+sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
+                                 int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out) {
     if (!mu || !stats_out || E <= 0 || N <= 0) return SEM_E_ARG;
     try {
         ChunkMeta m;
@@ -660,3 +918,40 @@ extern "C" sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np
         return SEM_E_OOM;
     }
 }
+
+sem_status sem_debug_partition(const int32_t *mu, int64_t E, int Np, int64_t N, int rank, int world,
+                               int64_t *sizes_out, int32_t *loc2glob_out, int32_t *nbr_out, int32_t *nbr_off_out,
+                               int32_t *send_glob_out, int32_t *if_glob_out, int32_t *sum_start_out,
+                               int32_t *sum_src_out) {
+    if (!mu || !sizes_out) return SEM_E_ARG;
+    try {
+        Partition P;
+        std::string err;
+        if (!build_partition(mu, E, Np, N, rank, world, P, err)) return SEM_E_ARG;
+        const int64_t nif = (int64_t)P.if_local.size();
+        sizes_out[0] = P.e0;
+        sizes_out[1] = P.e1;
+        sizes_out[2] = (int64_t)P.loc2glob.size();
+        sizes_out[3] = (int64_t)P.nbr.size();
+        sizes_out[4] = (int64_t)P.send_if.size();
+        sizes_out[5] = nif;
+        sizes_out[6] = (int64_t)P.sum_src.size();
+        int64_t nown = 0;
+        for (uint8_t o : P.owned) nown += o;
+        sizes_out[7] = nown;
+        if (loc2glob_out) std::memcpy(loc2glob_out, P.loc2glob.data(), sizeof(int32_t) * P.loc2glob.size());
+        if (nbr_out) std::memcpy(nbr_out, P.nbr.data(), sizeof(int32_t) * P.nbr.size());
+        if (nbr_off_out) std::memcpy(nbr_off_out, P.nbr_off.data(), sizeof(int32_t) * P.nbr_off.size());
+        if (send_glob_out)
+            for (size_t k = 0; k < P.send_if.size(); k++) send_glob_out[k] = P.loc2glob[P.if_local[P.send_if[k]]];
+        if (if_glob_out)
+            for (int64_t i = 0; i < nif; i++) if_glob_out[i] = P.loc2glob[P.if_local[i]];
+        if (sum_start_out) std::memcpy(sum_start_out, P.sum_start.data(), sizeof(int32_t) * P.sum_start.size());
+        if (sum_src_out) std::memcpy(sum_src_out, P.sum_src.data(), sizeof(int32_t) * P.sum_src.size());
+        return SEM_OK;
+    } catch (const std::bad_alloc &) {
+        return SEM_E_OOM;
+    }
+}
+
+}  // extern "C"

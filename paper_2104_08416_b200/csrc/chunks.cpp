@@ -29,7 +29,7 @@ namespace sem {
 static inline int64_t align2(int64_t v) { return (v + 1) & ~int64_t(1); }
 
 bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkMeta &m,
-                  std::string &err) {
+                  std::string &err, const uint8_t *force_shared) {
     if (E <= 0 || N <= 0 || B <= 0 || B > 1024 || (B % 16) != 0 || Np > kMaxNp) {
         err = "build_chunks: bad arguments";
         return false;
@@ -69,26 +69,37 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
             return false;
         }
 
+    // Nodes touched by another rank (multi-GPU interface) are shared even when a
+    // single local chunk touches them; they go last in the shared range.
+    if (force_shared)
+        for (int64_t g = 0; g < N; g++)
+            if (force_shared[g] && nref[g] == 1) nref[g] = -1;  // marker: 1 local chunk, forced
+    auto is_interior = [&](int64_t g) { return nref[g] == 1; };
+    auto forced = [&](int64_t g) { return force_shared && force_shared[g]; };
+    auto nref_local = [&](int64_t g) { return nref[g] < 0 ? 1 : nref[g]; };
+
     // Interior windows (even-aligned starts).
     std::vector<int64_t> nint(nch, 0);
-    int64_t nsh = 0;
+    int64_t nsh = 0, nif = 0;
     for (int64_t g = 0; g < N; g++) {
-        if (nref[g] == 1) nint[firstc[g]]++;
-        else nsh++;
+        if (is_interior(g)) nint[firstc[g]]++;
+        else { nsh++; if (forced(g)) nif++; }
     }
     m.i0.assign(nch + 1, 0);
     for (int64_t c = 0; c < nch; c++) m.i0[c + 1] = (int32_t)align2(m.i0[c] + nint[c]);
     m.N_int = m.i0[nch];
     m.N_sh = nsh;
+    m.N_if = nif;
     m.N_tot = m.N_int + nsh;
     m.int_of.assign(N, -1);
     std::vector<int32_t> sh_index(N, -1);
     {
         std::vector<int32_t> cur(m.i0.begin(), m.i0.end() - 1);
-        int64_t s = 0;
+        int64_t s = 0, sf = nsh - nif;
         for (int64_t g = 0; g < N; g++) {
-            if (nref[g] == 1) m.int_of[g] = cur[firstc[g]]++;
-            else { sh_index[g] = (int32_t)s; m.int_of[g] = (int32_t)(m.N_int + s); s++; }
+            if (is_interior(g)) m.int_of[g] = cur[firstc[g]]++;
+            else if (!forced(g)) { sh_index[g] = (int32_t)s; m.int_of[g] = (int32_t)(m.N_int + s); s++; }
+            else { sh_index[g] = (int32_t)sf; m.int_of[g] = (int32_t)(m.N_int + sf); sf++; }
         }
     }
 
@@ -113,7 +124,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     // Slots of each shared node, in ascending chunk order (for the fix-up).
     m.sh_pstart.assign(nsh + 1, 0);
     for (int64_t g = 0; g < N; g++)
-        if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref[g];
+        if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref_local(g);
     for (int64_t s = 0; s < nsh; s++) m.sh_pstart[s + 1] += m.sh_pstart[s];
     m.sh_slots.assign(nsh ? m.sh_pstart[nsh] : 0, -1);
     {

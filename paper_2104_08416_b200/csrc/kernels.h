@@ -43,6 +43,7 @@ cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t
 struct DevChunks {  // device view of ChunkMeta
     int B, Np;
     int64_t E, N, nchunks, N_int, N_sh, N_tot, n_slots;
+    int64_t N_if;              // interface nodes: the last N_if of the shared range
     int max_local, max_win, max_lptr;
     const int32_t *cmeta;      // [nchunks][8]
     const uint16_t *lidx;      // [nchunks][Np][B] chunk-local node of (p, t)
@@ -76,6 +77,14 @@ struct StepParams {
 int k7_grid(const DevChunks &ch);
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s);
 cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s);
+// Multi-GPU interface: local partials (+ pack per neighbour), then the
+// rank-ordered sum and update (step) or dt^2/M (mass).
+cudaError_t launch_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
+                              int64_t n_send, double *sendbuf, cudaStream_t s);
+cudaError_t launch_k8_if(const DevChunks &ch, const StepParams &p, const double *xbuf, const int32_t *sum_start,
+                         const int32_t *sum_src, cudaStream_t s);
+cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_t *sum_start, const int32_t *sum_src,
+                           double dt, double *dt2M, cudaStream_t s);
 // slot[j] = U[shared node of j] for every slot (after the state is set externally)
 cudaError_t launch_halo_fill(const DevChunks &ch, const double *U, double *slot, cudaStream_t s);
 // out[omap ? omap[i] : i] = in[imap ? imap[i] : i], i < n

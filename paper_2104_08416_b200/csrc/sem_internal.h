@@ -47,6 +47,7 @@ struct ChunkMeta {
     int B = 0, Np = 0;
     int64_t E = 0, N = 0, nchunks = 0;
     int64_t N_int = 0, N_sh = 0, N_tot = 0, n_slots = 0;
+    int64_t N_if = 0;                // forced-shared (rank-interface) nodes, last N_if of the shared range
     int max_local = 0, max_win = 0, max_colors = 0, max_lptr = 0;
     std::vector<int32_t> i0;         // [nchunks+1] interior window starts (even)
     std::vector<int32_t> s0;         // [nchunks+1] slot block starts (even)
@@ -60,8 +61,37 @@ struct ChunkMeta {
     std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)
     std::vector<int32_t> int_of;     // [N] node id (numbering of mu) -> internal id
 };
-// mu: [E][Np] node ids in [0, N) (elements in their final order).
+// mu: [E][Np] node ids in [0, N) (elements in their final order).  Nodes with
+// force_shared[g] != 0 (touched by another rank) are always shared; they take
+// the last N_if ids of the shared range, in ascending g.
 bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkMeta &m,
-                  std::string &err);
+                  std::string &err, const uint8_t *force_shared = nullptr);
+
+// ---------------------------------------------------------------------------
+// Multi-GPU partition (partition.cpp).  Rank r owns the global
+// elements [e0, e1) = [floor(rE/G), floor((r+1)E/G)) of the reordered mesh.
+// Local nodes are the global nodes its elements touch, in ascending global id.
+// Interface nodes (touched by >= 2 ranks) are exchanged every step: the rank
+// sends its local partial to every other rank touching the node (one buffer
+// per neighbour, nodes in ascending global id) and sums all ranks' partials
+// in ascending rank order, so every replica computes the same bits.
+// ---------------------------------------------------------------------------
+struct Partition {
+    int rank = 0, world = 1;
+    int64_t e0 = 0, e1 = 0;
+    std::vector<int32_t> loc2glob;      // [N_loc] ascending global node id
+    std::vector<int32_t> mu_local;      // [(e1-e0)][Np] local node ids
+    std::vector<uint8_t> remote;        // [N_loc] touched by another rank
+    std::vector<uint8_t> owned;         // [N_loc] this rank is the lowest toucher (I/O owner)
+    std::vector<int32_t> if_local;      // [n_if] local id of interface node i (ascending global)
+    std::vector<int32_t> nbr;           // neighbour ranks, ascending
+    std::vector<int32_t> nbr_off;       // [nnbr+1] blocks of the send / recv arrays
+    std::vector<int32_t> send_if;       // [n_send] interface index sent at each send position
+    std::vector<int32_t> sum_start;     // [n_if+1]
+    std::vector<int32_t> sum_src;       // parts index in ascending rank order: own = i (< n_if),
+                                        // received = n_if + recv position
+};
+bool build_partition(const int32_t *mu_global, int64_t E, int Np, int64_t N, int rank, int world,
+                     Partition &P, std::string &err);
 
 }  // namespace sem

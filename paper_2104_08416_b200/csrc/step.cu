@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads) k_mass_chunk(const DevChunks ch, con
 __global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ slot, double dt2,
                            double *__restrict__ dt2M) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= ch.N_sh) return;
+    if (s >= ch.N_sh - ch.N_if) return;
     double m = 0.0;
     for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) m += slot[ch.sh_slots[j]];
     dt2M[ch.N_int + s] = dt2 / m;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 // ---- K8: shared-node fix-up --------------------------------------------------
 __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= ch.N_sh) return;
+    if (s >= ch.N_sh - ch.N_if) return;  // interface nodes: k_if_partial / k8_if
     const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
     double y = 0.0;
     for (int j = j0; j < j1; j++) y += a.slot[ch.sh_slots[j]];
@@ -321,6 +321,48 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     const double un = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
     a.Uprev[id] = un;
     for (int j = j0; j < j1; j++) a.slot[ch.sh_slots[j]] = un;
+}
+
+// ---- multi-GPU interface -----------------------------------------
+// This rank's partial of interface node i = its slots summed in chunk order.
+__global__ void k_if_partial(const DevChunks ch, const double *__restrict__ slot, double *__restrict__ xbuf) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ch.N_if) return;
+    const int64_t s = ch.N_sh - ch.N_if + i;
+    double y = 0.0;
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) y += slot[ch.sh_slots[j]];
+    xbuf[i] = y;
+}
+
+__global__ void k_pack(const double *__restrict__ xbuf, const int32_t *__restrict__ send_if, int64_t n,
+                       double *__restrict__ sendbuf) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) sendbuf[k] = xbuf[send_if[k]];
+}
+
+// All ranks' partials of interface node i, added in ascending rank order, then
+// the fused update (identical bits on every rank holding the node).
+__global__ void k8_if(const DevChunks ch, const StepParams a, const double *__restrict__ xbuf,
+                      const int32_t *__restrict__ sum_start, const int32_t *__restrict__ sum_src) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ch.N_if) return;
+    double y = 0.0;
+    for (int j = sum_start[i]; j < sum_start[i + 1]; j++) y += xbuf[sum_src[j]];
+    const int64_t s = ch.N_sh - ch.N_if + i;
+    const int64_t id = ch.N_int + s;
+    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    const double un = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
+    a.Uprev[id] = un;
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) a.slot[ch.sh_slots[j]] = un;
+}
+
+__global__ void k_mass_if(const DevChunks ch, const double *__restrict__ xbuf, const int32_t *__restrict__ sum_start,
+                          const int32_t *__restrict__ sum_src, double dt2, double *__restrict__ dt2M) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ch.N_if) return;
+    double m = 0.0;
+    for (int j = sum_start[i]; j < sum_start[i + 1]; j++) m += xbuf[sum_src[j]];
+    dt2M[ch.N_int + ch.N_sh - ch.N_if + i] = dt2 / m;
 }
 
 __global__ void k_halo_fill(const DevChunks ch, const double *__restrict__ U, double *__restrict__ slot) {
@@ -381,7 +423,7 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, do
         k_mass_chunk<6><<<(unsigned)ch.nchunks, kThreads, 0, s>>>(ch, detJ, dt2, slot, dt2M);
     else
         k_mass_chunk<10><<<(unsigned)ch.nchunks, kThreads, 0, s>>>(ch, detJ, dt2, slot, dt2M);
-    if (ch.N_sh > 0) k_mass_fix<<<blocks_for(ch.N_sh), kThreads, 0, s>>>(ch, slot, dt2, dt2M);
+    if (ch.N_sh - ch.N_if > 0) k_mass_fix<<<blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s>>>(ch, slot, dt2, dt2M);
     return cudaGetLastError();
 }
 
@@ -417,8 +459,30 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
 }
 
 cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s) {
-    if (ch.N_sh == 0) return cudaSuccess;
-    k8_fix<<<blocks_for(ch.N_sh), kThreads, 0, s>>>(ch, p);
+    if (ch.N_sh - ch.N_if == 0) return cudaSuccess;
+    k8_fix<<<blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s>>>(ch, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
+                              int64_t n_send, double *sendbuf, cudaStream_t s) {
+    if (ch.N_if == 0) return cudaSuccess;
+    k_if_partial<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, slot, xbuf);
+    if (n_send > 0) k_pack<<<blocks_for(n_send), kThreads, 0, s>>>(xbuf, send_if, n_send, sendbuf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k8_if(const DevChunks &ch, const StepParams &p, const double *xbuf, const int32_t *sum_start,
+                         const int32_t *sum_src, cudaStream_t s) {
+    if (ch.N_if == 0) return cudaSuccess;
+    k8_if<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, p, xbuf, sum_start, sum_src);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_t *sum_start, const int32_t *sum_src,
+                           double dt, double *dt2M, cudaStream_t s) {
+    if (ch.N_if == 0) return cudaSuccess;
+    k_mass_if<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, xbuf, sum_start, sum_src, dt * dt, dt2M);
     return cudaGetLastError();
 }
 

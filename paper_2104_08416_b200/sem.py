@@ -28,7 +28,8 @@ SEM_NUMBERING_CANONICAL, SEM_NUMBERING_INTERNAL = 0, 1
 EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem_build_operators",
             "sem_step_n", "sem_read_field", "sem_write_state", "sem_set_step", "sem_sync",
             "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version",
-            "sem_debug_chunk_stats"]
+            "sem_debug_chunk_stats", "sem_debug_partition", "sem_nccl_unique_id",
+            "sem_group_build_operators", "sem_group_step_n"]
 
 
 class SemError(RuntimeError):
@@ -46,7 +47,9 @@ class sem_info(C.Structure):
                 ("n_partial_slots", C.c_int64), ("max_colors", C.c_int32),
                 ("launches_per_step", C.c_int32), ("step", C.c_int64),
                 ("bytes_alg_per_step", C.c_double), ("prep_reorder_ms", C.c_double),
-                ("prep_build_ms", C.c_double)]
+                ("prep_build_ms", C.c_double), ("n_interface_nodes", C.c_int64),
+                ("n_neighbors", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
+                ("n_elements_global", C.c_int64), ("first_element", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -83,6 +86,10 @@ def load(path: str = LIB_PATH):
         L.sem_set_kernel_timing.argtypes = [P, C.c_int]
         L.sem_kernel_times.argtypes = [P, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]
         L.sem_debug_chunk_stats.argtypes = [P, i64, C.c_int, i64, C.c_int, P, P, P]
+        L.sem_debug_partition.argtypes = [P, i64, C.c_int, i64, C.c_int, C.c_int, P, P, P, P, P, P, P, P]
+        L.sem_nccl_unique_id.argtypes = [P]
+        L.sem_group_build_operators.argtypes = [P, C.c_int, P, i64, dbl, dbl, dbl, dbl]
+        L.sem_group_step_n.argtypes = [P, C.c_int, i64]
         L.sem_version.argtypes = []
         L.sem_version.restype = C.c_char_p
         for n in EXPORTED:
@@ -172,7 +179,9 @@ class SemContext:
         self._check(self.L.sem_step_n(self.h, int(n)))
 
     def sem_read_field(self, numbering=SEM_NUMBERING_CANONICAL, out=None):
-        out = np.empty(self.N, np.float64) if out is None else out
+        """U^n as a global array [N]; with several ranks only this rank's owned
+        entries are written into `out` (merge ranks by passing the same array)."""
+        out = np.full(self.N, np.nan) if out is None else out
         step = C.c_int64(0)
         self._check(self.L.sem_read_field(self.h, _ptr(out), numbering, C.byref(step)))
         return out, step.value
@@ -228,3 +237,80 @@ def sem_debug_chunk_stats(mu, N: int, B: int = 256, want_maps: bool = False):
         d["int_of"] = int_of
         d["cmeta"] = cmeta.reshape(nch, 8)
     return d
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast the bytes)."""
+    L = load()
+    buf = C.create_string_buffer(128)
+    rc = L.sem_nccl_unique_id(buf)
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+class LoopbackGroup:
+    """G in-process partitions (loopback exchange, SURVEY §8e test transport)."""
+
+    def __init__(self, world: int, device: int = 0):
+        self.ctxs = [SemContext(device, r, world) for r in range(world)]
+        self.world = world
+        self._arr = (C.c_void_p * world)(*[c.h.value for c in self.ctxs])
+
+    def sem_mesh_reorder(self, *a, **k):
+        return [c.sem_mesh_reorder(*a, **k) for c in self.ctxs][0]
+
+    def sem_build_operators(self, c_elem, src_vertex, f0, t0, amplitude, dt):
+        c_elem = np.ascontiguousarray(c_elem, np.float64)
+        rc = load().sem_group_build_operators(self._arr, self.world, _ptr(c_elem), int(src_vertex), float(f0),
+                                              float(t0), float(amplitude), float(dt))
+        self._check(rc)
+
+    def sem_step_n(self, n):
+        self._check(load().sem_group_step_n(self._arr, self.world, int(n)))
+
+    def _check(self, rc):
+        if rc != SEM_OK:
+            msgs = "; ".join(c.L.sem_last_error(c.h).decode() for c in self.ctxs)
+            raise SemError(rc, msgs)
+
+    def sem_write_state(self, u, up, numbering=SEM_NUMBERING_CANONICAL):
+        for c in self.ctxs:
+            c.sem_write_state(u, up, numbering)
+
+    def sem_set_step(self, n):
+        for c in self.ctxs:
+            c.sem_set_step(n)
+
+    def sem_read_field(self, numbering=SEM_NUMBERING_CANONICAL):
+        out = np.full(self.ctxs[0].N, np.nan)
+        step = None
+        for c in self.ctxs:
+            _, step = c.sem_read_field(numbering, out=out)
+        return out, step
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+
+
+def sem_debug_partition(mu, N: int, rank: int, world: int) -> dict:
+    """Host-only partition diagnostics (see include/sem.h)."""
+    L = load()
+    mu = np.ascontiguousarray(mu, np.int32)
+    E, Np = mu.shape
+    sz = np.zeros(8, np.int64)
+    rc = L.sem_debug_partition(_ptr(mu), E, Np, N, rank, world, _ptr(sz), None, None, None, None, None, None, None)
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_debug_partition failed")
+    e0, e1, nl, nn, ns, nif, nsum, nown = (int(x) for x in sz)
+    out = {"e0": e0, "e1": e1, "loc2glob": np.empty(nl, np.int32), "nbr": np.empty(nn, np.int32),
+           "nbr_off": np.empty(nn + 1, np.int32), "send_glob": np.empty(ns, np.int32),
+           "if_glob": np.empty(nif, np.int32), "sum_start": np.empty(nif + 1, np.int32),
+           "sum_src": np.empty(nsum, np.int32), "n_owned": nown}
+    rc = L.sem_debug_partition(_ptr(mu), E, Np, N, rank, world, _ptr(sz), _ptr(out["loc2glob"]), _ptr(out["nbr"]),
+                               _ptr(out["nbr_off"]), _ptr(out["send_glob"]), _ptr(out["if_glob"]),
+                               _ptr(out["sum_start"]), _ptr(out["sum_src"]))
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_debug_partition failed")
+    return out

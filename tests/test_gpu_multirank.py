@@ -1,0 +1,92 @@
+"""Multi-GPU path on one B200: G in-process partitions (loopback transport).
+
+The partitions run the multi-GPU kernels (interface partials, pack, rank-ordered
+sums) with a device-to-device copy in place of NCCL send/recv; the host
+sequences the ranks with events, so no kernel ever waits on another rank.
+Results must match the oracle (rel L2 <= 1e-10) and the one-rank GPU run
+(rounding-level: only the summation order of interface nodes differs).
+"""
+import numpy as np
+import pytest
+
+from oracle.core import OracleSEM
+from paper_2104_08416_b200 import meshgen as mg
+from paper_2104_08416_b200 import sem as S
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def shifted(pb):
+    return mg.Problem(**{**pb.__dict__, "t0": 10 * pb.dt, "f0": 1.0 / (8 * pb.dt)})
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_loopback_matches_oracle_and_single_rank(world):
+    pb = shifted(mg.config("C2", 4))  # 128 x 128 cells, P3
+    m = pb.mesh
+    steps = 150
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    Uo, _ = o.leapfrog(pb.dt, steps, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
+    with S.SemContext(0) as one:
+        one.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        one.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        one.sem_step_n(steps)
+        U1, _ = one.sem_read_field()
+    g = S.LoopbackGroup(world)
+    try:
+        g.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        infos = [c.sem_get_info() for c in g.ctxs]
+        assert sum(i["n_elements"] for i in infos) == m.ne
+        assert all(i["n_interface_nodes"] > 0 for i in infos)
+        g.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        g.sem_step_n(steps)
+        Ug, n = g.sem_read_field()
+    finally:
+        g.close()
+    assert n == steps
+    assert not np.isnan(Ug).any()  # every node written by exactly its owner
+    assert rel_l2(Ug, Uo) <= 1e-10
+    assert rel_l2(Ug, U1) <= 1e-13
+
+
+@pytest.mark.parametrize("name,scale,world", [("C3", 20, 4), ("C5", 128, 8), ("C1", 1, 3)])
+def test_loopback_random_state_steps(name, scale, world):
+    pb = mg.config(name, scale)
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    rng = np.random.default_rng(5)
+    U0 = rng.standard_normal(o.N)
+    Up = U0 + 0.1 * rng.standard_normal(o.N)
+    Uo, _ = o.leapfrog(pb.dt, 10, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0, U=U0, Uprev=Up, step0=3)
+    g = S.LoopbackGroup(world)
+    try:
+        g.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        g.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        g.sem_write_state(U0, Up)
+        g.sem_set_step(3)
+        g.sem_step_n(10)
+        Ug, n = g.sem_read_field()
+    finally:
+        g.close()
+    assert n == 13
+    assert rel_l2(Ug, Uo) <= 1e-12
+
+
+def test_loopback_bitwise_deterministic():
+    pb = shifted(mg.config("C2", 8))
+    m = pb.mesh
+    outs = []
+    for _ in range(2):
+        g = S.LoopbackGroup(4)
+        try:
+            g.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+            g.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+            g.sem_step_n(60)
+            outs.append(g.sem_read_field()[0])
+        finally:
+            g.close()
+    assert np.array_equal(outs[0], outs[1])
