@@ -28,6 +28,16 @@ bool build_partition(const int32_t *mu, int64_t E, int Np, int64_t N, int rank, 
         err = "build_partition: rank " + std::to_string(rank) + " has no elements";
         return false;
     }
+    if (world == 1) {  // one rank: everything is local, nothing is exchanged
+        P.loc2glob.resize(N);
+        for (int64_t g = 0; g < N; g++) P.loc2glob[g] = (int32_t)g;
+        P.mu_local.assign(mu, mu + E * Np);
+        P.remote.assign(N, 0);
+        P.owned.assign(N, 1);
+        P.nbr_off.assign(1, 0);
+        P.sum_start.assign(1, 0);
+        return true;
+    }
     // Which ranks touch each node (bit mask; world <= 32).
     std::vector<uint32_t> mask(N, 0u);
     for (int q = 0; q < world; q++) {

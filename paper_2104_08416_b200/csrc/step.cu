@@ -384,9 +384,16 @@ __global__ void k_nonfinite(const double *__restrict__ a, int64_t n, int32_t *fl
     if (i < n && !isfinite(a[i])) atomicMin(flag, (int32_t)i);
 }
 
+// The max-dynamic-smem attribute is per function (process-wide), and several
+// contexts may launch the same kernel with different sizes: only ever raise it.
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    static size_t cur[2] = {0, 0};
+    size_t &c = cur[(void *)kernel == (void *)k7_step<6> ? 0 : 1];
+    if (bytes <= c) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c = bytes;
+    return e;
 }
 
 size_t k7_smem_bytes(int np, int L, int W, int Lp) {
@@ -451,6 +458,8 @@ int k7_grid(const DevChunks &ch) {
 
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s) {
     const size_t smem = k7_smem_bytes(ch.Np, ch.max_local, ch.max_win, ch.max_lptr);
+    cudaError_t e = ch.Np == 6 ? set_smem(k7_step<6>, smem) : set_smem(k7_step<10>, smem);
+    if (e != cudaSuccess) return e;
     if (ch.Np == 6)
         k7_step<6><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr);
     else
