@@ -111,6 +111,10 @@ struct sem_ctx {
     double amp = 0, f0 = 1, t0 = 0, dt = 0;
     int64_t step = 0;
     cudaEvent_t xev = nullptr;  // loopback: phase-1 done on this rank
+    cudaStream_t comm_stream = nullptr;           // NCCL exchange, overlapped with interior chunks
+    cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
+    int32_t *d_bnd = nullptr, *d_intc = nullptr;  // boundary / interior chunk lists
+    int64_t n_bnd = 0, n_intc = 0;
 
     // timing
     bool timing = false;
@@ -241,15 +245,15 @@ sem_status check_usable(sem_ctx *ctx) {
 
 // ---- interface exchange ------------------------------------------------------------
 // NCCL: grouped send/recv of the packed partials with every neighbour rank.
-sem_status exchange_nccl(sem_ctx *ctx) {
+sem_status exchange_nccl(sem_ctx *ctx, cudaStream_t st) {
     if (ctx->nbr.empty()) return SEM_OK;
     NcclApi &N = nccl();
     ncclResult_t r = N.GroupStart();
     for (size_t k = 0; r == ncclSuccess && k < ctx->nbr.size(); k++) {
         const size_t off = ctx->nbr_off[k], cnt = ctx->nbr_off[k + 1] - off;
-        r = N.Send(ctx->d_sendbuf + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, ctx->stream);
+        r = N.Send(ctx->d_sendbuf + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, st);
         if (r == ncclSuccess)
-            r = N.Recv(ctx->d_xbuf + ctx->n_if + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, ctx->stream);
+            r = N.Recv(ctx->d_xbuf + ctx->n_if + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, st);
     }
     ncclResult_t r2 = N.GroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
@@ -313,17 +317,31 @@ StepParams step_params(sem_ctx *ctx) {
 }
 
 // Step phase 1: stiffness + update of everything local; pack interface partials.
-sem_status step_phase1(sem_ctx *ctx) {
+// With NCCL (use_nccl) the exchange is issued on the comm stream right after
+// the boundary chunks are done and overlaps the interior chunks.
+sem_status step_phase1(sem_ctx *ctx, bool use_nccl) {
     CK(cudaSetDevice(ctx->device));
     ST(ensure_tables(ctx));
     const StepParams p = step_params(ctx);
     if (ctx->timing) ST(record(ctx, ctx->ev7, true));
-    CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream));
+    if (ctx->n_if == 0) {
+        CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream));
+    } else {
+        CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream, ctx->d_bnd, ctx->n_bnd));
+        CK(launch_if_partial(ctx->dch, ctx->d_slot, ctx->d_xbuf, ctx->d_send_if, ctx->n_send, ctx->d_sendbuf,
+                             ctx->stream));
+        if (use_nccl) {
+            CK(cudaEventRecord(ctx->ev_packed, ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+            ST(exchange_nccl(ctx, ctx->comm_stream));
+            CK(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
+        }
+        CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream, ctx->d_intc, ctx->n_intc));
+    }
     if (ctx->timing) ST(record(ctx, ctx->ev7, false));
     if (ctx->timing) ST(record(ctx, ctx->ev8, true));
     CK(launch_k8(ctx->dch, p, ctx->stream));
-    CK(launch_if_partial(ctx->dch, ctx->d_slot, ctx->d_xbuf, ctx->d_send_if, ctx->n_send, ctx->d_sendbuf,
-                         ctx->stream));
+    if (use_nccl && ctx->n_if > 0) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
     if (ctx->timing && ctx->n_if == 0) ST(record(ctx, ctx->ev8, false));
     return SEM_OK;
 }
@@ -460,8 +478,12 @@ sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
             return cuda_fail(ctx, e, "cudaStreamCreate");
         ctx->own_stream = true;
     }
-    if ((e = cudaEventCreateWithFlags(&ctx->xev, cudaEventDisableTiming)) != cudaSuccess)
+    if ((e = cudaEventCreateWithFlags(&ctx->xev, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming)) != cudaSuccess)
         return cuda_fail(ctx, e, "cudaEventCreate");
+    if (world_size > 1 && (e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(ctx, e, "cudaStreamCreate(comm)");
     if (world_size > 1) {
         if (!nccl_unique_id) {
             ctx->loopback = true;  // in-process partitions: step only through sem_group_*
@@ -487,6 +509,9 @@ void sem_free(sem_ctx *ctx) {
     for (auto *lst : {&ctx->ev7, &ctx->ev8, &ctx->pool})
         for (auto &ev : *lst) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
     if (ctx->xev) cudaEventDestroy(ctx->xev);
+    if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
+    if (ctx->ev_exchanged) cudaEventDestroy(ctx->ev_exchanged);
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
     if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -689,6 +714,10 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         ctx->n_send = (int64_t)part.send_if.size();
         ctx->nbr = part.nbr;
         ctx->nbr_off = part.nbr_off;
+        ctx->n_bnd = (int64_t)m.bnd_chunks.size();
+        ctx->n_intc = (int64_t)m.int_chunks.size();
+        CK(upload(L, &ctx->d_bnd, m.bnd_chunks, s));
+        CK(upload(L, &ctx->d_intc, m.int_chunks, s));
         CK(upload(L, &ctx->d_send_if, part.send_if, s));
         CK(upload(L, &ctx->d_sum_start, part.sum_start, s));
         CK(upload(L, &ctx->d_sum_src, part.sum_src, s));
@@ -715,7 +744,7 @@ sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t 
     if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions are built with sem_group_build_operators");
     try {
         ST(build_phase1(ctx, c_elem_host, src_vertex, f0, t0, amplitude, dt));
-        if (ctx->world > 1) ST(exchange_nccl(ctx));
+        if (ctx->world > 1) ST(exchange_nccl(ctx, ctx->stream));
         return build_phase2(ctx);
     } catch (const std::bad_alloc &) {
         return fail(ctx, SEM_E_OOM, "host allocation failed in sem_build_operators");
@@ -728,8 +757,7 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
     if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions step with sem_group_step_n");
     if (n_steps < 0) return fail(ctx, SEM_E_ARG, "n_steps < 0");
     for (int64_t k = 0; k < n_steps; k++) {
-        ST(step_phase1(ctx));
-        if (ctx->world > 1) ST(exchange_nccl(ctx));
+        ST(step_phase1(ctx, ctx->world > 1));
         ST(step_phase2(ctx));
     }
     return SEM_OK;
@@ -759,7 +787,7 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps) {
         if (!ctxs[r]->have_ops) return fail(ctxs[r], SEM_E_STATE, "sem_group_step_n before build");
     }
     for (int64_t k = 0; k < n_steps; k++) {
-        for (int r = 0; r < n; r++) ST(step_phase1(ctxs[r]));
+        for (int r = 0; r < n; r++) ST(step_phase1(ctxs[r], false));
         ST(exchange_loopback(ctxs, n));
         for (int r = 0; r < n; r++) ST(step_phase2(ctxs[r]));
     }

@@ -117,6 +117,13 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         std::sort(L.begin(), L.end());
         L.erase(std::unique(L.begin(), L.end()), L.end());
     }
+    // Boundary chunks (touching a rank-interface node) run first so that the
+    // interface exchange overlaps the interior chunks.
+    for (int64_t c = 0; c < nch; c++) {
+        bool bnd = false;
+        for (int32_t sidx : lists[c]) bnd |= sidx >= nsh - nif;
+        (bnd ? m.bnd_chunks : m.int_chunks).push_back((int32_t)c);
+    }
     // Chunk-contiguous slot blocks (even-aligned starts).
     m.s0.assign(nch + 1, 0);
     for (int64_t c = 0; c < nch; c++) m.s0[c + 1] = (int32_t)align2(m.s0[c] + (int64_t)lists[c].size());

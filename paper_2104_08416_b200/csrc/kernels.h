@@ -75,7 +75,9 @@ struct StepParams {
     int64_t n;         // step index of U
 };
 int k7_grid(const DevChunks &ch);
-cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s);
+// K7 over all chunks (list == nullptr) or over the chunk ids list[0..nlist).
+cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
+                      const int32_t *list = nullptr, int64_t nlist = 0);
 cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s);
 // Multi-GPU interface: local partials (+ pack per neighbour), then the
 // rank-ordered sum and update (step) or dt^2/M (mass).

@@ -60,6 +60,8 @@ struct ChunkMeta {
     std::vector<uint16_t> lidx;      // [nchunks][Np][B] chunk-local node index
     std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)
     std::vector<int32_t> int_of;     // [N] node id (numbering of mu) -> internal id
+    std::vector<int32_t> bnd_chunks; // chunks touching a rank-interface node (ascending)
+    std::vector<int32_t> int_chunks; // all other chunks (ascending)
 };
 // mu: [E][Np] node ids in [0, N) (elements in their final order).  Nodes with
 // force_shared[g] != 0 (touched by another rank) are always shared; they take

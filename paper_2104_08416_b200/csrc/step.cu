@@ -179,14 +179,15 @@ __device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *le
 // ---- K7 ---------------------------------------------------------------------------
 template <int NP>
 __global__ void __launch_bounds__(kThreads + 32, 2)
-    k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp) {
+    k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, const int32_t *__restrict__ list,
+            int64_t nlist) {
     extern __shared__ __align__(128) unsigned char sm[];
     const StageLayout lay(NP, L, Lp);
     double *ebuf = reinterpret_cast<double *>(sm + kStages * lay.size);  // [NP][B] element slots
     uint64_t *full = reinterpret_cast<uint64_t *>(ebuf + NP * kThreads);
     uint64_t *empty = full + kStages;
     const int t = threadIdx.x;
-    const int64_t nch = ch.nchunks;
+    const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
     if (t == 0) {
         for (int s = 0; s < kStages; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -198,7 +199,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
         // ===== producer warp: one lane streams chunk blocks with TMA =====
         if (t == kThreads) {
             int k = 0;
-            for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+            for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
+                const int64_t c = list ? list[pos] : pos;
                 const int s = k % kStages;
                 if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) & 1) ^ 1);
                 unsigned char *st = sm + s * lay.size;
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 
     // ===== consumer warps =====
     int k = 0;
-    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+    for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
         const int s = k % kStages;
         mbar_wait(&full[s], (k / kStages) & 1);
         const unsigned char *st = sm + s * lay.size;
@@ -456,14 +458,18 @@ int k7_grid(const DevChunks &ch) {
     return (int)g;
 }
 
-cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s) {
+cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
+                      const int32_t *list, int64_t nlist) {
+    const int64_t n = list ? nlist : ch.nchunks;
+    if (n == 0) return cudaSuccess;
+    if (grid > n) grid = (int)n;
     const size_t smem = k7_smem_bytes(ch.Np, ch.max_local, ch.max_win, ch.max_lptr);
     cudaError_t e = ch.Np == 6 ? set_smem(k7_step<6>, smem) : set_smem(k7_step<10>, smem);
     if (e != cudaSuccess) return e;
     if (ch.Np == 6)
-        k7_step<6><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr);
+        k7_step<6><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, list, nlist);
     else
-        k7_step<10><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr);
+        k7_step<10><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, list, nlist);
     return cudaGetLastError();
 }
 
