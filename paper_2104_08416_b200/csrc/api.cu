@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -24,7 +25,14 @@ using namespace sem;
 
 namespace {
 int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
-constexpr int kChunkElems = 256;
+
+// Elements per chunk (one CTA iteration of K7): 256 by default; SEM_CHUNK=128|512
+// selects the other compiled variants (design experiments).
+int chunk_elems() {
+    const char *v = getenv("SEM_CHUNK");
+    const int b = v ? atoi(v) : 256;
+    return (b == 128 || b == 512) ? b : 256;
+}
 
 // ---- NCCL through dlopen (no link-time dependency; torch's copy is reused) ----
 struct NcclApi {
@@ -421,7 +429,6 @@ sem_status build_phase2(sem_ctx *ctx) {
     cudaStream_t s = ctx->stream;
     const double t = now_ms();
     CK(launch_mass_if(ctx->dch, ctx->d_xbuf, ctx->d_sum_start, ctx->d_sum_src, ctx->dt, ctx->d_dt2M, s));
-    CK(cudaMemsetAsync(ctx->d_slot, 0, sizeof(double) * (ctx->dch.n_slots + 2), s));  // halo of U^0 = 0
     CK(cudaStreamSynchronize(s));
     ctx->step = 0;
     ctx->cur = 0;
@@ -666,24 +673,26 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
 
         // ---- chunk metadata for the step kernel ----
         ChunkMeta m;
-        if (!build_chunks(part.mu_local.data(), ctx->E, Np, ctx->N, kChunkElems, m, err,
+        if (!build_chunks(part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(), m, err,
                           ctx->world > 1 ? part.remote.data() : nullptr))
             return fail(ctx, SEM_E_MESH, err);
         DevChunks &d = ctx->dch;
         d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
         d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
-        d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr;
+        d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
         auto &L = ctx->mesh_allocs;
-        int32_t *p_cmeta, *p_pstart, *p_slots;
+        int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
         uint16_t *p_lent, *p_lptr, *p_lidx;
         CK(upload(L, &p_cmeta, m.cmeta, s));
         CK(upload(L, &p_lidx, m.lidx, s));
         CK(upload(L, &p_lent, m.lent, s));
         CK(upload(L, &p_lptr, m.lptr, s));
         CK(upload(L, &p_pstart, m.sh_pstart, s));
-        CK(upload(L, &p_slots, m.sh_slots, s));
+        CK(upload(L, &p_shn, m.shl_node, s));
+        CK(upload(L, &p_shs, m.shl_slot, s));
         d.cmeta = p_cmeta; d.lidx = p_lidx; d.lent = p_lent; d.lptr = p_lptr; d.sh_pstart = p_pstart;
-        d.sh_slots = p_slots;
+        d.shl_node = p_shn;
+        d.shl_slot = p_shs;
         // node maps for I/O
         {
             std::vector<int32_t> loc_int(ctx->N), loc_can(ctx->N), own_int, own_can, own_ft;
@@ -848,7 +857,6 @@ sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double
         CK(cudaMemcpyAsync(d_in, src[k], sizeof(double) * ctx->N_glob, cudaMemcpyHostToDevice, s));
         CK(launch_permute_f64(d_in, imap, ctx->d_loc_int, ctx->N, dst[k], s));
     }
-    CK(launch_halo_fill(ctx->dch, ctx->d_U[ctx->cur], ctx->d_slot, s));
     CK(cudaStreamSynchronize(s));
     return SEM_OK;
 }

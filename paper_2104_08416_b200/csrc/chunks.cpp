@@ -9,12 +9,12 @@
 //   * nodes touched by a single chunk ("interior") are summed in shared memory
 //     in a fixed colour order and finalised by that CTA;
 //   * nodes touched by several chunks ("shared") get one SLOT per touching
-//     chunk.  A chunk's slots are contiguous.  Before the step a slot holds the
-//     node's U^n (a halo copy, so the step kernel only streams contiguous
-//     blocks); the step kernel overwrites it with the chunk's partial K U sum;
-//     the fix-up kernel adds a node's slots in ascending chunk order, updates
-//     the node and writes U^{n+1} back into its slots.
+//     chunk, node-major.  The step kernel's producer warp gathers the U^n of
+//     a chunk's shared nodes with cp.async; its consumers write the chunk's
+//     partial K U sums into the slots; the fix-up kernel adds a node's slots
+//     (a contiguous run, ascending chunk order) and updates the node.
 // Both summation orders are fixed, so results are bitwise reproducible.
+// (Slot layout: node-major -- see below.)
 //
 // Internal node numbering: interior nodes of chunk c occupy [i0_c, i0_c+nint_c),
 // i0_c even (16-byte aligned for TMA bulk copies, one hole at most per chunk),
@@ -124,21 +124,29 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         for (int32_t sidx : lists[c]) bnd |= sidx >= nsh - nif;
         (bnd ? m.bnd_chunks : m.int_chunks).push_back((int32_t)c);
     }
-    // Chunk-contiguous slot blocks (even-aligned starts).
-    m.s0.assign(nch + 1, 0);
-    for (int64_t c = 0; c < nch; c++) m.s0[c + 1] = (int32_t)align2(m.s0[c] + (int64_t)lists[c].size());
-    m.n_slots = m.s0[nch];
-    // Slots of each shared node, in ascending chunk order (for the fix-up).
+    // Slots are node-major: shared node s owns [sh_pstart[s], sh_pstart[s+1]),
+    // one per touching chunk in ascending chunk order (so the fix-up sums a
+    // contiguous run).  Each chunk lists, contiguously, the shared index and the
+    // slot of every shared node it touches (block start 16-byte aligned).
     m.sh_pstart.assign(nsh + 1, 0);
     for (int64_t g = 0; g < N; g++)
         if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref_local(g);
     for (int64_t s = 0; s < nsh; s++) m.sh_pstart[s + 1] += m.sh_pstart[s];
-    m.sh_slots.assign(nsh ? m.sh_pstart[nsh] : 0, -1);
+    m.n_slots = nsh ? m.sh_pstart[nsh] : 0;
+    m.s0.assign(nch + 1, 0);
+    for (int64_t c = 0; c < nch; c++) m.s0[c + 1] = (int32_t)((m.s0[c] + (int64_t)lists[c].size() + 3) & ~int64_t(3));
+    for (int64_t c = 0; c < nch; c++) m.max_nsh = std::max(m.max_nsh, (int)((lists[c].size() + 3) & ~size_t(3)));
+    m.shl_node.assign((size_t)m.s0[nch] + 4, 0);
+    m.shl_slot.assign((size_t)m.s0[nch] + 4, 0);
     {
         std::vector<int32_t> cursor(nsh, 0);
-        for (int64_t c = 0; c < nch; c++) {
+        for (int64_t c = 0; c < nch; c++) {  // ascending chunk order -> slot order within a node
             int32_t k = m.s0[c];
-            for (int32_t s : lists[c]) m.sh_slots[m.sh_pstart[s] + cursor[s]++] = k++;
+            for (int32_t sidx : lists[c]) {
+                m.shl_node[k] = sidx;
+                m.shl_slot[k] = m.sh_pstart[sidx] + cursor[sidx]++;
+                k++;
+            }
         }
     }
 

@@ -44,13 +44,14 @@ struct DevChunks {  // device view of ChunkMeta
     int B, Np;
     int64_t E, N, nchunks, N_int, N_sh, N_tot, n_slots;
     int64_t N_if;              // interface nodes: the last N_if of the shared range
-    int max_local, max_win, max_lptr;
+    int max_local, max_win, max_lptr, max_nsh;
     const int32_t *cmeta;      // [nchunks][8]
     const uint16_t *lidx;      // [nchunks][Np][B] chunk-local node of (p, t)
     const uint16_t *lent;      // [nchunks][Np*B] node CSR entries p*B + t
     const uint16_t *lptr;      // per-chunk CSR row pointers (block at cmeta[7])
-    const int32_t *sh_pstart;  // [N_sh+1]
-    const int32_t *sh_slots;   // [n_slots used]
+    const int32_t *sh_pstart;  // [N_sh+1] node-major slots of shared node s
+    const int32_t *shl_node;   // per chunk (block at cmeta[2]): shared index of each local shared node
+    const int32_t *shl_slot;   // per chunk: the slot it writes
 };
 
 cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s);
@@ -69,7 +70,7 @@ struct StepParams {
     const double *dt2M;
     const double *U;   // U^n
     double *Uprev;     // U^{n-1} in, U^{n+1} out
-    double *slot;      // halo copies of U^n in, partial sums out (K7); reversed in K8
+    double *slot;      // node-major partial sums of shared nodes (K7 writes, K8 reads)
     int32_t src;       // internal node id of the source (-1 none)
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
@@ -87,8 +88,6 @@ cudaError_t launch_k8_if(const DevChunks &ch, const StepParams &p, const double 
                          const int32_t *sum_src, cudaStream_t s);
 cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_t *sum_start, const int32_t *sum_src,
                            double dt, double *dt2M, cudaStream_t s);
-// slot[j] = U[shared node of j] for every slot (after the state is set externally)
-cudaError_t launch_halo_fill(const DevChunks &ch, const double *U, double *slot, cudaStream_t s);
 // out[omap ? omap[i] : i] = in[imap ? imap[i] : i], i < n
 cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,
                                double *out, cudaStream_t s);

@@ -41,22 +41,23 @@ const LocalNode *local_nodes(int P);
 // each).  Nodes touched by exactly one chunk are "interior": contiguous
 // internal ids per chunk, window start even.  All other nodes are "shared":
 // internal ids [N_int, N_int+N_sh); every (chunk, shared node) pair owns one
-// slot, and a chunk's slots are contiguous (halo copy in, partial sum out).
+// slot (node-major: a shared node's slots are contiguous, in chunk order).
 // ---------------------------------------------------------------------------
 struct ChunkMeta {
     int B = 0, Np = 0;
     int64_t E = 0, N = 0, nchunks = 0;
     int64_t N_int = 0, N_sh = 0, N_tot = 0, n_slots = 0;
     int64_t N_if = 0;                // forced-shared (rank-interface) nodes, last N_if of the shared range
-    int max_local = 0, max_win = 0, max_colors = 0, max_lptr = 0;
+    int max_local = 0, max_win = 0, max_colors = 0, max_lptr = 0, max_nsh = 0;  // max_nsh: multiple of 4
     std::vector<int32_t> i0;         // [nchunks+1] interior window starts (even)
-    std::vector<int32_t> s0;         // [nchunks+1] slot block starts (even)
+    std::vector<int32_t> s0;         // [nchunks+1] chunk blocks in shl_node / shl_slot (multiple of 4)
+    std::vector<int32_t> shl_node;   // shared index s of each chunk-local shared node
+    std::vector<int32_t> shl_slot;   // node-major slot written by that chunk
     std::vector<int32_t> cmeta;      // [nchunks][8] {i0, nint, s0, nsh, ncol, ne, nint_al, lp0}
     std::vector<int32_t> lp0;        // [nchunks+1] start of chunk c's block in lptr (multiple of 8)
     std::vector<uint16_t> lptr;      // per chunk: CSR row pointers over local nodes (nlocal+1)
     std::vector<uint16_t> lent;      // [nchunks][Np*B] CSR entries p*B + t, ascending per node
-    std::vector<int32_t> sh_pstart;  // [N_sh+1] range in sh_slots of shared node s
-    std::vector<int32_t> sh_slots;   // slots of shared node s, ascending chunk order
+    std::vector<int32_t> sh_pstart;  // [N_sh+1] slots of shared node s (node-major, chunk order)
     std::vector<uint16_t> lidx;      // [nchunks][Np][B] chunk-local node index
     std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)
     std::vector<int32_t> int_of;     // [N] node id (numbering of mu) -> internal id

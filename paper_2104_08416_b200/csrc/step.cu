@@ -23,6 +23,8 @@
 // matrices, as PAPER.md:1568 suggests.
 #include <cuda_runtime.h>
 
+#include <map>
+
 #include "kernels.h"
 
 namespace sem {
@@ -89,19 +91,29 @@ __device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// 8-byte asynchronous global -> shared copy (LDGSTS) and the per-thread
+// mbarrier arrive that fires when all of this thread's cp.async have landed.
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int B>
 __device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(B) : "memory");
 }
 
 // Shared-memory layout of one pipeline stage (all offsets 16-byte aligned).
 struct StageLayout {
-    int lidx, lent, lptr, g, meta, u, size;
-    __host__ __device__ StageLayout(int np, int L, int Lp) {
+    int lidx, lent, lptr, shs, g, meta, u, size;
+    __host__ __device__ StageLayout(int np, int B, int L, int Lp, int Ls) {
         lidx = 0;
-        lent = np * kThreads * 2;
-        lptr = lent + np * kThreads * 2;
-        g = lptr + Lp * 2;
-        meta = g + 3 * kThreads * 8;
+        lent = np * B * 2;
+        lptr = lent + np * B * 2;
+        shs = lptr + Lp * 2;
+        g = shs + Ls * 4;
+        meta = g + 3 * B * 8;
         u = meta + 32;
         size = (u + L * 8 + 127) & ~127;
     }
@@ -130,26 +142,26 @@ __global__ void k_geometry(const double *__restrict__ vxy, const int32_t *__rest
 }
 
 // ---- lumped mass with the chunk machinery (one-time, not pipelined) -----------
-template <int NP>
-__global__ void __launch_bounds__(kThreads) k_mass_chunk(const DevChunks ch, const double *__restrict__ detJ,
+template <int NP, int B>
+__global__ void __launch_bounds__(B) k_mass_chunk(const DevChunks ch, const double *__restrict__ detJ,
                                                          double dt2, double *__restrict__ slot,
                                                          double *__restrict__ dt2M) {
-    __shared__ double ybuf[NP * kThreads];
+    __shared__ double ybuf[NP * B];
     const int c = blockIdx.x, t = threadIdx.x;
     const int *cm = ch.cmeta + 8 * (int64_t)c;
     const int i0 = cm[0], nint = cm[1], s0 = cm[2], nsh = cm[3], ne = cm[5], ni_al = cm[6], lp0 = cm[7];
-    const int64_t e = (int64_t)c * kThreads + t;
+    const int64_t e = (int64_t)c * B + t;
     const double dj = (t < ne) ? detJ[e] : 0.0;
 #pragma unroll
-    for (int p = 0; p < NP; p++) ybuf[p * kThreads + t] = 1.0 * dj * c_wM[p];
+    for (int p = 0; p < NP; p++) ybuf[p * B + t] = 1.0 * dj * c_wM[p];
     __syncthreads();
     const uint16_t *lp = ch.lptr + lp0;
-    const uint16_t *le = ch.lent + (int64_t)c * NP * kThreads;
-    for (int i = t; i < ni_al + nsh; i += kThreads) {
+    const uint16_t *le = ch.lent + (int64_t)c * NP * B;
+    for (int i = t; i < ni_al + nsh; i += B) {
         double m = 0.0;
         for (int j = lp[i]; j < lp[i + 1]; j++) m += ybuf[le[j]];
         if (i < nint) dt2M[i0 + i] = dt2 / m;
-        else if (i >= ni_al) slot[s0 + i - ni_al] = m;
+        else if (i >= ni_al) slot[ch.shl_slot[s0 + i - ni_al]] = m;
     }
 }
 
@@ -158,7 +170,7 @@ __global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ slot, 
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh - ch.N_if) return;
     double m = 0.0;
-    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) m += slot[ch.sh_slots[j]];
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) m += slot[j];
     dt2M[ch.N_int + s] = dt2 / m;
 }
 
@@ -177,52 +189,79 @@ __device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *le
 }
 
 // ---- K7 ---------------------------------------------------------------------------
-template <int NP>
-__global__ void __launch_bounds__(kThreads + 32, 2)
-    k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, const int32_t *__restrict__ list,
-            int64_t nlist) {
+template <int NP, int B>
+__global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 256 ? 2 : 1))
+    k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
+            const int32_t *__restrict__ list, int64_t nlist) {
     extern __shared__ __align__(128) unsigned char sm[];
-    const StageLayout lay(NP, L, Lp);
+    const StageLayout lay(NP, B, L, Lp, Ls);
     double *ebuf = reinterpret_cast<double *>(sm + kStages * lay.size);  // [NP][B] element slots
-    uint64_t *full = reinterpret_cast<uint64_t *>(ebuf + NP * kThreads);
-    uint64_t *empty = full + kStages;
+    double *up_s = ebuf + NP * B;                                       // U^{n-1} window (single buffer)
+    double *m_s = up_s + W;                                             // dt^2/M window (single buffer)
+    uint64_t *full = reinterpret_cast<uint64_t *>(m_s + W);            // TMA blocks landed
+    uint64_t *gath = full + kStages;                                    // shared-node gathers landed
+    uint64_t *empty = gath + kStages;                                   // consumers done with stage
+    uint64_t *wfull = empty + kStages;                                  // U^{n-1}, dt^2/M windows landed
+    uint64_t *wempty = wfull + 1;                                       // ... consumed
     const int t = threadIdx.x;
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
     if (t == 0) {
-        for (int s = 0; s < kStages; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < kStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&gath[s], 32);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(wfull, 1);
+        mbar_init(wempty, 1);
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (t >= kThreads) {
-        // ===== producer warp: one lane streams chunk blocks with TMA =====
-        if (t == kThreads) {
-            int k = 0;
-            for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
-                const int64_t c = list ? list[pos] : pos;
-                const int s = k % kStages;
-                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) & 1) ^ 1);
-                unsigned char *st = sm + s * lay.size;
-                const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
-                const int4 m1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
+    if (t >= B) {
+        // ===== producer warp =====
+        // lane 0 streams the chunk's contiguous blocks with TMA bulk copies; all
+        // 32 lanes gather U^n of the chunk's shared nodes with cp.async.
+        const int lane = t - B;
+        int k = 0;
+        for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
+            const int64_t c = list ? list[pos] : pos;
+            const int s = k % kStages;
+            if (k >= kStages && lane == 0) mbar_wait(&empty[s], ((k / kStages) & 1) ^ 1);
+            __syncwarp();
+            unsigned char *st = sm + s * lay.size;
+            const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+            const int4 m1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
+            const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z, lp0 = m1.w;
+            if (lane == 0) {
                 reinterpret_cast<int4 *>(st + lay.meta)[0] = m0;
                 reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
-                const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z, lp0 = m1.w;
-                const int nsh_al = (nsh + 1) & ~1;
                 const int nlp = (ni_al + nsh + 1 + 7) & ~7;
-                const uint32_t bytes = 2 * NP * kThreads * 2 + nlp * 2 + 3 * kThreads * 8 +
-                                       (uint32_t)(ni_al + nsh_al) * 8;
+                const int nsh4 = (nsh + 3) & ~3;
+                const uint32_t bytes = 2 * NP * B * 2 + nlp * 2 + nsh4 * 4 + 3 * B * 8 + (uint32_t)ni_al * 8;
                 mbar_arrive_expect_tx(&full[s], bytes);
-                const int64_t e0 = c * kThreads;
-                tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * kThreads * 2, &full[s]);
-                tma_load(st + lay.lent, ch.lent + e0 * NP, NP * kThreads * 2, &full[s]);
+                const int64_t e0 = c * B;
+                tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
+                tma_load(st + lay.lent, ch.lent + e0 * NP, NP * B * 2, &full[s]);
                 tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
-                tma_load(st + lay.g, a.Grr + e0, kThreads * 8, &full[s]);
-                tma_load(st + lay.g + kThreads * 8, a.Gss + e0, kThreads * 8, &full[s]);
-                tma_load(st + lay.g + 2 * kThreads * 8, a.Grs + e0, kThreads * 8, &full[s]);
+                if (nsh4 > 0) tma_load(st + lay.shs, ch.shl_slot + s0, nsh4 * 4, &full[s]);
+                tma_load(st + lay.g, a.Grr + e0, B * 8, &full[s]);
+                tma_load(st + lay.g + B * 8, a.Gss + e0, B * 8, &full[s]);
+                tma_load(st + lay.g + 2 * B * 8, a.Grs + e0, B * 8, &full[s]);
                 if (ni_al > 0) tma_load(st + lay.u, a.U + i0, ni_al * 8, &full[s]);
-                if (nsh_al > 0) tma_load(st + lay.u + ni_al * 8, a.slot + s0, nsh_al * 8, &full[s]);
+            }
+            double *u_sh = reinterpret_cast<double *>(st + lay.u) + ni_al;
+            for (int j = lane; j < nsh; j += 32) cp_async8(u_sh + j, a.U + ch.N_int + ch.shl_node[s0 + j]);
+            cp_async_arrive_noinc(&gath[s]);
+            // the single U^{n-1} / dt^2/M window buffer: free once the previous
+            // chunk's update is done; lands while this chunk's element phase runs
+            if (lane == 0) {
+                if (k >= 1) mbar_wait(wempty, (k - 1) & 1);
+                mbar_arrive_expect_tx(wfull, (uint32_t)ni_al * 16);
+                if (ni_al > 0) {
+                    tma_load(up_s, a.Uprev + i0, ni_al * 8, wfull);
+                    tma_load(m_s, a.dt2M + i0, ni_al * 8, wfull);
+                }
             }
         }
         return;
@@ -233,15 +272,17 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
     for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
         const int s = k % kStages;
         mbar_wait(&full[s], (k / kStages) & 1);
+        mbar_wait(&gath[s], (k / kStages) & 1);
         const unsigned char *st = sm + s * lay.size;
         const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
         const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
-        const int i0 = m0.x, nint = m0.y, s0 = m0.z, nsh = m0.w, ne = m1.y, ni_al = m1.z;
+        const int i0 = m0.x, nint = m0.y, nsh = m0.w, ne = m1.y, ni_al = m1.z;
         const int nl = ni_al + nsh;
         const double *u_s = reinterpret_cast<const double *>(st + lay.u);
         const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
         const uint16_t *le = reinterpret_cast<const uint16_t *>(st + lay.lent);
         const uint16_t *lp = reinterpret_cast<const uint16_t *>(st + lay.lptr);
+        const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
         const double *g_s = reinterpret_cast<const double *>(st + lay.g);
 
         // (E) y = K^e u, K^e symmetric: each K_pq (p <= q) built once
@@ -249,10 +290,10 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 #pragma unroll
         for (int p = 0; p < NP; p++) y[p] = 0.0;
         if (t < ne) {
-            const double grr = g_s[t], gss = g_s[kThreads + t], grs = g_s[2 * kThreads + t];
+            const double grr = g_s[t], gss = g_s[B + t], grs = g_s[2 * B + t];
             double u[NP];
 #pragma unroll
-            for (int p = 0; p < NP; p++) u[p] = u_s[li_s[p * kThreads + t]];
+            for (int p = 0; p < NP; p++) u[p] = u_s[li_s[p * B + t]];
 #pragma unroll
             for (int p = 0; p < NP; p++) {
 #pragma unroll
@@ -268,46 +309,27 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
             }
         }
 #pragma unroll
-        for (int p = 0; p < NP; p++) ebuf[p * kThreads + t] = y[p];
-        // prefetch U^{n-1} and dt^2/M of this thread's interior nodes (coalesced;
-        // the loads overlap the barrier and the reduction below)
-        double upr[kPre], mr[kPre];
-#pragma unroll
-        for (int q = 0; q < kPre; q++) {
-            const int i = t + q * kThreads;
-            upr[q] = 0.0;
-            mr[q] = 0.0;
-            if (i < nint) { upr[q] = a.Uprev[i0 + i]; mr[q] = a.dt2M[i0 + i]; }
-        }
-        consumer_sync();
-        // (B) node-centric gather of K U^n in fixed order + fused update
+        for (int p = 0; p < NP; p++) ebuf[p * B + t] = y[p];
+        consumer_sync<B>();
+        mbar_wait(wfull, k & 1);
+        // (B) node-centric gather of K U^n in fixed order + fused update;
+        //     shared nodes: this chunk's partial into the node's slot
         double *Unew = a.Uprev;
-#pragma unroll
-        for (int q = 0; q < kPre; q++) {
-            const int i = t + q * kThreads;
-            if (i < nl) {
-                const double yi = csr_sum(ebuf, le, lp, i);
-                if (i < nint) {
-                    const int id = i0 + i;
-                    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-                    Unew[id] = 2.0 * u_s[i] - upr[q] + mr[q] * (f - yi);
-                } else if (i >= ni_al) {
-                    a.slot[s0 + (i - ni_al)] = yi;
-                }
-            }
-        }
-        for (int i = t + kPre * kThreads; i < nl; i += kThreads) {  // chunks larger than kPre*B nodes
+        for (int i = t; i < nl; i += B) {
             const double yi = csr_sum(ebuf, le, lp, i);
             if (i < nint) {
                 const int id = i0 + i;
                 const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-                Unew[id] = 2.0 * u_s[i] - Unew[id] + a.dt2M[id] * (f - yi);
+                Unew[id] = 2.0 * u_s[i] - up_s[i] + m_s[i] * (f - yi);
             } else if (i >= ni_al) {
-                a.slot[s0 + (i - ni_al)] = yi;
+                a.slot[shs[i - ni_al]] = yi;
             }
         }
-        consumer_sync();
-        if (t == 0) mbar_arrive(&empty[s]);
+        consumer_sync<B>();
+        if (t == 0) {
+            mbar_arrive(&empty[s]);
+            mbar_arrive(wempty);
+        }
     }
 }
 
@@ -317,12 +339,10 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     if (s >= ch.N_sh - ch.N_if) return;  // interface nodes: k_if_partial / k8_if
     const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
     double y = 0.0;
-    for (int j = j0; j < j1; j++) y += a.slot[ch.sh_slots[j]];
+    for (int j = j0; j < j1; j++) y += a.slot[j];  // contiguous, ascending chunk order
     const int64_t id = ch.N_int + s;
     const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-    const double un = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
-    a.Uprev[id] = un;
-    for (int j = j0; j < j1; j++) a.slot[ch.sh_slots[j]] = un;
+    a.Uprev[id] = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
 }
 
 // ---- multi-GPU interface -----------------------------------------
@@ -332,7 +352,7 @@ __global__ void k_if_partial(const DevChunks ch, const double *__restrict__ slot
     if (i >= ch.N_if) return;
     const int64_t s = ch.N_sh - ch.N_if + i;
     double y = 0.0;
-    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) y += slot[ch.sh_slots[j]];
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) y += slot[j];
     xbuf[i] = y;
 }
 
@@ -353,9 +373,7 @@ __global__ void k8_if(const DevChunks ch, const StepParams a, const double *__re
     const int64_t s = ch.N_sh - ch.N_if + i;
     const int64_t id = ch.N_int + s;
     const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-    const double un = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
-    a.Uprev[id] = un;
-    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) a.slot[ch.sh_slots[j]] = un;
+    a.Uprev[id] = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
 }
 
 __global__ void k_mass_if(const DevChunks ch, const double *__restrict__ xbuf, const int32_t *__restrict__ sum_start,
@@ -365,13 +383,6 @@ __global__ void k_mass_if(const DevChunks ch, const double *__restrict__ xbuf, c
     double m = 0.0;
     for (int j = sum_start[i]; j < sum_start[i + 1]; j++) m += xbuf[sum_src[j]];
     dt2M[ch.N_int + ch.N_sh - ch.N_if + i] = dt2 / m;
-}
-
-__global__ void k_halo_fill(const DevChunks ch, const double *__restrict__ U, double *__restrict__ slot) {
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= ch.N_sh) return;
-    const double v = U[ch.N_int + s];
-    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) slot[ch.sh_slots[j]] = v;
 }
 
 __global__ void k_permute_f64(const double *__restrict__ in, const int32_t *__restrict__ imap,
@@ -390,18 +401,23 @@ __global__ void k_nonfinite(const double *__restrict__ a, int64_t n, int32_t *fl
 // contexts may launch the same kernel with different sizes: only ever raise it.
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
-    static size_t cur[2] = {0, 0};
-    size_t &c = cur[(void *)kernel == (void *)k7_step<6> ? 0 : 1];
+    static std::map<const void *, size_t> cur;
+    size_t &c = cur[(const void *)kernel];
     if (bytes <= c) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess) c = bytes;
     return e;
 }
 
-size_t k7_smem_bytes(int np, int L, int W, int Lp) {
-    (void)W;
-    const StageLayout lay(np, L, Lp);
-    return (size_t)kStages * lay.size + (size_t)np * kThreads * 8 + 2 * kStages * 8;
+size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls) {
+    const StageLayout lay(np, B, L, Lp, Ls);
+    return (size_t)kStages * lay.size + (size_t)np * B * 8 + 2 * (size_t)W * 8 + (3 * kStages + 2) * 8;
+}
+
+using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
+K7Fn k7_fn(int np, int B) {
+    if (np == 6) return B == 128 ? k7_step<6, 128> : B == 512 ? k7_step<6, 512> : k7_step<6, 256>;
+    return B == 128 ? k7_step<10, 128> : B == 512 ? k7_step<10, 512> : k7_step<10, 256>;
 }
 
 }  // namespace
@@ -428,10 +444,13 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, do
     const double dt2 = dt * dt;
     cudaError_t e;
     if ((e = cudaMemsetAsync(dt2M, 0, sizeof(double) * (ch.N_tot + 2), s))) return e;
-    if (ch.Np == 6)
-        k_mass_chunk<6><<<(unsigned)ch.nchunks, kThreads, 0, s>>>(ch, detJ, dt2, slot, dt2M);
-    else
-        k_mass_chunk<10><<<(unsigned)ch.nchunks, kThreads, 0, s>>>(ch, detJ, dt2, slot, dt2M);
+#define MASS(NP_, B_) k_mass_chunk<NP_, B_><<<(unsigned)ch.nchunks, B_, 0, s>>>(ch, detJ, dt2, slot, dt2M)
+    if (ch.Np == 6) {
+        if (ch.B == 128) MASS(6, 128); else if (ch.B == 512) MASS(6, 512); else MASS(6, 256);
+    } else {
+        if (ch.B == 128) MASS(10, 128); else if (ch.B == 512) MASS(10, 512); else MASS(10, 256);
+    }
+#undef MASS
     if (ch.N_sh - ch.N_if > 0) k_mass_fix<<<blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s>>>(ch, slot, dt2, dt2M);
     return cudaGetLastError();
 }
@@ -443,15 +462,11 @@ int k7_grid(const DevChunks &ch) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = k7_smem_bytes(ch.Np, ch.max_local, ch.max_win, ch.max_lptr);
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh);
+    const K7Fn fn = k7_fn(ch.Np, ch.B);
+    set_smem(fn, smem);
     int occ = 0;
-    if (ch.Np == 6) {
-        set_smem(k7_step<6>, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k7_step<6>, kThreads + 32, smem);
-    } else {
-        set_smem(k7_step<10>, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k7_step<10>, kThreads + 32, smem);
-    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B + 32, smem);
     if (occ < 1) occ = 1;
     int64_t g = (int64_t)occ * nsm;
     if (g > ch.nchunks) g = ch.nchunks;
@@ -463,13 +478,11 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
     if (grid > n) grid = (int)n;
-    const size_t smem = k7_smem_bytes(ch.Np, ch.max_local, ch.max_win, ch.max_lptr);
-    cudaError_t e = ch.Np == 6 ? set_smem(k7_step<6>, smem) : set_smem(k7_step<10>, smem);
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh);
+    const K7Fn fn = k7_fn(ch.Np, ch.B);
+    cudaError_t e = set_smem(fn, smem);
     if (e != cudaSuccess) return e;
-    if (ch.Np == 6)
-        k7_step<6><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, list, nlist);
-    else
-        k7_step<10><<<grid, kThreads + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, list, nlist);
+    fn<<<grid, ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, list, nlist);
     return cudaGetLastError();
 }
 
@@ -498,12 +511,6 @@ cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_
                            double dt, double *dt2M, cudaStream_t s) {
     if (ch.N_if == 0) return cudaSuccess;
     k_mass_if<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, xbuf, sum_start, sum_src, dt * dt, dt2M);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_halo_fill(const DevChunks &ch, const double *U, double *slot, cudaStream_t s) {
-    if (ch.N_sh == 0) return cudaSuccess;
-    k_halo_fill<<<blocks_for(ch.N_sh), kThreads, 0, s>>>(ch, U, slot);
     return cudaGetLastError();
 }
 
