@@ -682,15 +682,15 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
         auto &L = ctx->mesh_allocs;
         int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
-        uint16_t *p_lent, *p_lptr, *p_lidx;
+        uint16_t *p_lpos, *p_lptr, *p_lidx;
         CK(upload(L, &p_cmeta, m.cmeta, s));
         CK(upload(L, &p_lidx, m.lidx, s));
-        CK(upload(L, &p_lent, m.lent, s));
+        CK(upload(L, &p_lpos, m.lpos, s));
         CK(upload(L, &p_lptr, m.lptr, s));
         CK(upload(L, &p_pstart, m.sh_pstart, s));
         CK(upload(L, &p_shn, m.shl_node, s));
         CK(upload(L, &p_shs, m.shl_slot, s));
-        d.cmeta = p_cmeta; d.lidx = p_lidx; d.lent = p_lent; d.lptr = p_lptr; d.sh_pstart = p_pstart;
+        d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.lptr = p_lptr; d.sh_pstart = p_pstart;
         d.shl_node = p_shn;
         d.shl_slot = p_shs;
         // node maps for I/O

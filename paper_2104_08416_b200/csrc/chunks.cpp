@@ -48,6 +48,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
 
     // Pass 1: first chunk and number of distinct chunks touching each node.
     std::vector<int32_t> firstc(N, -1), lastc(N, -1), nref(N, 0);
+    std::vector<uint8_t> refcnt(N, 0);  // element entries per node (saturating)
     for (int64_t e = 0; e < E; e++) {
         const int32_t c = (int32_t)(e / B);
         for (int p = 0; p < Np; p++) {
@@ -56,6 +57,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
                 err = "build_chunks: node id out of range in element " + std::to_string(e);
                 return false;
             }
+            if (refcnt[g] < 255) refcnt[g]++;
             if (lastc[g] != c) {  // chunks are visited in increasing order
                 if (firstc[g] < 0) firstc[g] = c;
                 lastc[g] = c;
@@ -94,12 +96,20 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     m.int_of.assign(N, -1);
     std::vector<int32_t> sh_index(N, -1);
     {
-        std::vector<int32_t> cur(m.i0.begin(), m.i0.end() - 1);
+        // interior nodes of a chunk: descending entry count, then ascending id
+        // (warps of the reduction then see nodes of equal degree)
+        std::vector<int32_t> cur(m.i0.begin(), m.i0.end() - 1), order(m.N_int > 0 ? m.N_int : 1);
         int64_t s = 0, sf = nsh - nif;
         for (int64_t g = 0; g < N; g++) {
-            if (is_interior(g)) m.int_of[g] = cur[firstc[g]]++;
+            if (is_interior(g)) order[cur[firstc[g]]++] = (int32_t)g;
             else if (!forced(g)) { sh_index[g] = (int32_t)s; m.int_of[g] = (int32_t)(m.N_int + s); s++; }
             else { sh_index[g] = (int32_t)sf; m.int_of[g] = (int32_t)(m.N_int + sf); sf++; }
+        }
+#pragma omp parallel for schedule(dynamic, 256)
+        for (int64_t c = 0; c < nch; c++) {
+            std::stable_sort(order.begin() + m.i0[c], order.begin() + m.i0[c] + nint[c],
+                             [&](int32_t a, int32_t b) { return refcnt[a] > refcnt[b]; });
+            for (int64_t k = m.i0[c]; k < m.i0[c] + nint[c]; k++) m.int_of[order[k]] = (int32_t)k;
         }
     }
 
@@ -114,8 +124,18 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
                 const int32_t s = sh_index[mu[e * Np + p]];
                 if (s >= 0) L.push_back(s);
             }
+        // by descending local entry count, then ascending shared index
         std::sort(L.begin(), L.end());
-        L.erase(std::unique(L.begin(), L.end()), L.end());
+        std::vector<std::pair<int32_t, int32_t>> cnt;  // (-count, s)
+        for (size_t k = 0; k < L.size();) {
+            size_t j = k;
+            while (j < L.size() && L[j] == L[k]) j++;
+            cnt.push_back({-(int32_t)(j - k), L[k]});
+            k = j;
+        }
+        std::sort(cnt.begin(), cnt.end());
+        L.clear();
+        for (auto &pr : cnt) L.push_back(pr.second);
     }
     // Boundary chunks (touching a rank-interface node) run first so that the
     // interface exchange overlaps the interior chunks.
@@ -174,6 +194,10 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         if (nl > max_local) max_local = nl;
         if (ni_al > max_win) max_win = ni_al;
         std::vector<uint32_t> used(nl, 0u);
+        std::vector<std::pair<int32_t, int32_t>> pos_of;  // (shared index, local position)
+        pos_of.reserve(L.size());
+        for (int32_t k = 0; k < ns; k++) pos_of.push_back({L[k], k});
+        std::sort(pos_of.begin(), pos_of.end());
         int ncol = 0;
         for (int64_t e = e0; e < e1; e++) {
             const int t = (int)(e - e0);
@@ -183,7 +207,8 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
                 const int32_t g = mu[e * Np + p];
                 int loc;
                 if (sh_index[g] < 0) loc = m.int_of[g] - i0;
-                else loc = ni_al + (int)(std::lower_bound(L.begin(), L.end(), sh_index[g]) - L.begin());
+                else loc = ni_al + std::lower_bound(pos_of.begin(), pos_of.end(),
+                                                    std::make_pair(sh_index[g], (int32_t)-1))->second;
                 li[p] = (uint16_t)loc;
                 m.lidx[(size_t)c * Np * B + (size_t)p * B + t] = (uint16_t)loc;
                 forb |= used[loc];
@@ -213,10 +238,10 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         return false;
     }
     // CSR blocks: chunk c owns lptr[lp0[c] .. lp0[c] + nlocal+1) (start aligned
-    // to 8 entries = 16 bytes for TMA) and lent[c*Np*B .. (c+1)*Np*B).
+    // to 8 entries = 16 bytes for TMA) and lpos[c*Np*B .. (c+1)*Np*B).
     for (int64_t c = 0; c < nch; c++) m.lp0[c + 1] = (int32_t)((m.lp0[c] + nlocal[c] + 1 + 7) & ~7);
     m.lptr.assign((size_t)m.lp0[nch] + 8, 0);
-    m.lent.assign((size_t)nch * Np * B, 0);
+    m.lpos.assign((size_t)nch * Np * B, 0);
     int max_lp = 0;
 #pragma omp parallel for schedule(dynamic, 64) reduction(max : max_lp)
     for (int64_t c = 0; c < nch; c++) {
@@ -229,10 +254,11 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         for (int i = 0; i < nl; i++) cnt[i + 1] += cnt[i];
         uint16_t *lp = &m.lptr[m.lp0[c]];
         for (int i = 0; i <= nl; i++) lp[i] = (uint16_t)cnt[i];
-        uint16_t *le = &m.lent[(size_t)c * Np * B];
-        // entries visited in ascending e = p*B + t order -> each list ascending
+        // entries visited in ascending e = p*B + t order -> each node's run is
+        // ascending; lpos[e] = CSR position of entry e (where y_e[p] goes)
+        uint16_t *lpo = &m.lpos[(size_t)c * Np * B];
         for (int p = 0; p < Np; p++)
-            for (int t = 0; t < ne; t++) le[cnt[li[p * B + t]]++] = (uint16_t)(p * B + t);
+            for (int t = 0; t < ne; t++) lpo[p * B + t] = (uint16_t)(cnt[li[p * B + t]]++);
         m.cmeta[(size_t)c * 8 + 7] = m.lp0[c];
         const int w = (nl + 1 + 7) & ~7;
         if (w > max_lp) max_lp = w;

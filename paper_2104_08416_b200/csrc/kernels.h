@@ -47,7 +47,7 @@ struct DevChunks {  // device view of ChunkMeta
     int max_local, max_win, max_lptr, max_nsh;
     const int32_t *cmeta;      // [nchunks][8]
     const uint16_t *lidx;      // [nchunks][Np][B] chunk-local node of (p, t)
-    const uint16_t *lent;      // [nchunks][Np*B] node CSR entries p*B + t
+    const uint16_t *lpos;      // [nchunks][Np*B] CSR position of entry p*B + t
     const uint16_t *lptr;      // per-chunk CSR row pointers (block at cmeta[7])
     const int32_t *sh_pstart;  // [N_sh+1] node-major slots of shared node s
     const int32_t *shl_node;   // per chunk (block at cmeta[2]): shared index of each local shared node

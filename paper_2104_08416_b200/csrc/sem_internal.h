@@ -56,7 +56,7 @@ struct ChunkMeta {
     std::vector<int32_t> cmeta;      // [nchunks][8] {i0, nint, s0, nsh, ncol, ne, nint_al, lp0}
     std::vector<int32_t> lp0;        // [nchunks+1] start of chunk c's block in lptr (multiple of 8)
     std::vector<uint16_t> lptr;      // per chunk: CSR row pointers over local nodes (nlocal+1)
-    std::vector<uint16_t> lent;      // [nchunks][Np*B] CSR entries p*B + t, ascending per node
+    std::vector<uint16_t> lpos;      // [nchunks][Np*B] CSR position of entry p*B + t (runs ascending in e)
     std::vector<int32_t> sh_pstart;  // [N_sh+1] slots of shared node s (node-major, chunk order)
     std::vector<uint16_t> lidx;      // [nchunks][Np][B] chunk-local node index
     std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)

@@ -33,8 +33,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kStages = 2;
-constexpr int kD = 6;    // list depth handled without a loop (mesh vertex degree)
-constexpr int kPre = 5;  // interior nodes per thread prefetched in registers
+constexpr int kD = 8;    // entries per node loaded together (mesh vertex degree <= 8 typical)
 
 __constant__ double c_Srr[kMaxNp][kMaxNp];
 __constant__ double c_Sss[kMaxNp][kMaxNp];
@@ -106,11 +105,11 @@ __device__ __forceinline__ void consumer_sync() {
 
 // Shared-memory layout of one pipeline stage (all offsets 16-byte aligned).
 struct StageLayout {
-    int lidx, lent, lptr, shs, g, meta, u, size;
+    int lidx, lpos, lptr, shs, g, meta, u, size;
     __host__ __device__ StageLayout(int np, int B, int L, int Lp, int Ls) {
         lidx = 0;
-        lent = np * B * 2;
-        lptr = lent + np * B * 2;
+        lpos = np * B * 2;
+        lptr = lpos + np * B * 2;
         shs = lptr + Lp * 2;
         g = shs + Ls * 4;
         meta = g + 3 * B * 8;
@@ -151,15 +150,17 @@ __global__ void __launch_bounds__(B) k_mass_chunk(const DevChunks ch, const doub
     const int *cm = ch.cmeta + 8 * (int64_t)c;
     const int i0 = cm[0], nint = cm[1], s0 = cm[2], nsh = cm[3], ne = cm[5], ni_al = cm[6], lp0 = cm[7];
     const int64_t e = (int64_t)c * B + t;
-    const double dj = (t < ne) ? detJ[e] : 0.0;
+    if (t < ne) {
+        const double dj = detJ[e];
+        const uint16_t *lpo = ch.lpos + (int64_t)c * NP * B;
 #pragma unroll
-    for (int p = 0; p < NP; p++) ybuf[p * B + t] = 1.0 * dj * c_wM[p];
+        for (int p = 0; p < NP; p++) ybuf[lpo[p * B + t]] = 1.0 * dj * c_wM[p];
+    }
     __syncthreads();
     const uint16_t *lp = ch.lptr + lp0;
-    const uint16_t *le = ch.lent + (int64_t)c * NP * B;
     for (int i = t; i < ni_al + nsh; i += B) {
         double m = 0.0;
-        for (int j = lp[i]; j < lp[i + 1]; j++) m += ybuf[le[j]];
+        for (int j = lp[i]; j < lp[i + 1]; j++) m += ybuf[j];
         if (i < nint) dt2M[i0 + i] = dt2 / m;
         else if (i >= ni_al) slot[ch.shl_slot[s0 + i - ni_al]] = m;
     }
@@ -174,17 +175,19 @@ __global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ slot, 
     dt2M[ch.N_int + s] = dt2 / m;
 }
 
-// Sum of a local node's element contributions in CSR order (fixed order; the
-// first kD entries are loaded together, absent ones contribute an exact +0).
-__device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *le, const uint16_t *lp, int i) {
+// Sum of a local node's element contributions, stored contiguously in CSR
+// order (ascending e = p*B + t: a fixed order).  Up to kD entries are loaded
+// together (predicated); absent ones contribute an exact +0.  Local nodes are
+// sorted by degree, so a warp's lanes take the same path.
+__device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *lp, int i) {
     const int j0 = lp[i], j1 = lp[i + 1];
     double part[kD];
 #pragma unroll
-    for (int d = 0; d < kD; d++) part[d] = (j0 + d < j1) ? ebuf[le[j0 + d]] : 0.0;
-    double y = 0.0;
+    for (int d = 0; d < kD; d++) part[d] = (j0 + d < j1) ? ebuf[j0 + d] : 0.0;
+    double y = part[0];
 #pragma unroll
-    for (int d = 0; d < kD; d++) y += part[d];
-    for (int j = j0 + kD; j < j1; j++) y += ebuf[le[j]];
+    for (int d = 1; d < kD; d++) y += part[d];
+    for (int j = j0 + kD; j < j1; j++) y += ebuf[j];
     return y;
 }
 
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 256 ? 2 : 1))
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
                 tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
-                tma_load(st + lay.lent, ch.lent + e0 * NP, NP * B * 2, &full[s]);
+                tma_load(st + lay.lpos, ch.lpos + e0 * NP, NP * B * 2, &full[s]);
                 tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
                 if (nsh4 > 0) tma_load(st + lay.shs, ch.shl_slot + s0, nsh4 * 4, &full[s]);
                 tma_load(st + lay.g, a.Grr + e0, B * 8, &full[s]);
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 256 ? 2 : 1))
         const int nl = ni_al + nsh;
         const double *u_s = reinterpret_cast<const double *>(st + lay.u);
         const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
-        const uint16_t *le = reinterpret_cast<const uint16_t *>(st + lay.lent);
+        const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
         const uint16_t *lp = reinterpret_cast<const uint16_t *>(st + lay.lptr);
         const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
         const double *g_s = reinterpret_cast<const double *>(st + lay.g);
@@ -308,15 +311,17 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 256 ? 2 : 1))
                 }
             }
         }
+        if (t < ne) {
 #pragma unroll
-        for (int p = 0; p < NP; p++) ebuf[p * B + t] = y[p];
+            for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = y[p];  // straight to the node's CSR run
+        }
         consumer_sync<B>();
         mbar_wait(wfull, k & 1);
         // (B) node-centric gather of K U^n in fixed order + fused update;
         //     shared nodes: this chunk's partial into the node's slot
         double *Unew = a.Uprev;
         for (int i = t; i < nl; i += B) {
-            const double yi = csr_sum(ebuf, le, lp, i);
+            const double yi = csr_sum(ebuf, lp, i);
             if (i < nint) {
                 const int id = i0 + i;
                 const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
