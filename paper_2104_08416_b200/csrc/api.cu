@@ -26,12 +26,12 @@ using namespace sem;
 namespace {
 int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 
-// Elements per chunk (one CTA iteration of K7): 256 by default; SEM_CHUNK=128|512
+// Elements per chunk (one CTA iteration of K7): 256 by default; SEM_CHUNK=128|192|512
 // selects the other compiled variants (design experiments).
 int chunk_elems() {
     const char *v = getenv("SEM_CHUNK");
     const int b = v ? atoi(v) : 256;
-    return (b == 128 || b == 512) ? b : 256;
+    return (b == 128 || b == 192 || b == 512) ? b : 256;
 }
 
 // ---- NCCL through dlopen (no link-time dependency; torch's copy is reused) ----

@@ -193,7 +193,7 @@ __device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *lp
 
 // ---- K7 ---------------------------------------------------------------------------
 template <int NP, int B>
-__global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -343,11 +343,17 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh - ch.N_if) return;  // interface nodes: k_if_partial / k8_if
     const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
-    double y = 0.0;
-    for (int j = j0; j < j1; j++) y += a.slot[j];  // contiguous, ascending chunk order
     const int64_t id = ch.N_int + s;
+    const double u = a.U[id], up = a.Uprev[id], m = a.dt2M[id];  // independent of the slots
+    double part[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) part[d] = (j0 + d < j1) ? a.slot[j0 + d] : 0.0;
+    double y = part[0];  // contiguous slots, ascending chunk order
+#pragma unroll
+    for (int d = 1; d < 4; d++) y += part[d];
+    for (int j = j0 + 4; j < j1; j++) y += a.slot[j];
     const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
-    a.Uprev[id] = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
+    a.Uprev[id] = 2.0 * u - up + m * (f - y);
 }
 
 // ---- multi-GPU interface -----------------------------------------
@@ -421,8 +427,9 @@ size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls) {
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
 K7Fn k7_fn(int np, int B) {
-    if (np == 6) return B == 128 ? k7_step<6, 128> : B == 512 ? k7_step<6, 512> : k7_step<6, 256>;
-    return B == 128 ? k7_step<10, 128> : B == 512 ? k7_step<10, 512> : k7_step<10, 256>;
+    if (np == 6)
+        return B == 128 ? k7_step<6, 128> : B == 192 ? k7_step<6, 192> : B == 512 ? k7_step<6, 512> : k7_step<6, 256>;
+    return B == 128 ? k7_step<10, 128> : B == 192 ? k7_step<10, 192> : B == 512 ? k7_step<10, 512> : k7_step<10, 256>;
 }
 
 }  // namespace
@@ -451,9 +458,9 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, do
     if ((e = cudaMemsetAsync(dt2M, 0, sizeof(double) * (ch.N_tot + 2), s))) return e;
 #define MASS(NP_, B_) k_mass_chunk<NP_, B_><<<(unsigned)ch.nchunks, B_, 0, s>>>(ch, detJ, dt2, slot, dt2M)
     if (ch.Np == 6) {
-        if (ch.B == 128) MASS(6, 128); else if (ch.B == 512) MASS(6, 512); else MASS(6, 256);
+        if (ch.B == 128) MASS(6, 128); else if (ch.B == 192) MASS(6, 192); else if (ch.B == 512) MASS(6, 512); else MASS(6, 256);
     } else {
-        if (ch.B == 128) MASS(10, 128); else if (ch.B == 512) MASS(10, 512); else MASS(10, 256);
+        if (ch.B == 128) MASS(10, 128); else if (ch.B == 192) MASS(10, 192); else if (ch.B == 512) MASS(10, 512); else MASS(10, 256);
     }
 #undef MASS
     if (ch.N_sh - ch.N_if > 0) k_mass_fix<<<blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s>>>(ch, slot, dt2, dt2M);
