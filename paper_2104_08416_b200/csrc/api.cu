@@ -100,7 +100,8 @@ struct sem_ctx {
     int32_t *d_loc_int = nullptr, *d_loc_can = nullptr, *d_loc_ft = nullptr;
     int32_t *d_own_int = nullptr, *d_own_can = nullptr, *d_own_ft = nullptr;
     int64_t n_own = 0;
-    std::vector<int32_t> can_to_int;  // canonical id -> internal id (-1 if not local)
+    std::vector<int32_t> src_lookup;  // local node -> canonical id (source lookup)
+    std::vector<int32_t> src_int_of;  // local node -> internal id
     DevChunks dch{};
     ChunkMeta meta_info;  // counts only
     int k7_grid = 0;
@@ -186,7 +187,8 @@ void reset_mesh(sem_ctx *ctx) {
     reset_ops(ctx);
     free_list(ctx->mesh_allocs);
     ctx->have_mesh = false;
-    ctx->can_to_int.clear();
+    ctx->src_lookup.clear();
+    ctx->src_int_of.clear();
     ctx->dch = DevChunks{};
     ctx->n_if = ctx->n_send = 0;
     ctx->nbr.clear();
@@ -197,6 +199,18 @@ double now_ms() {
     using namespace std::chrono;
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
+
+struct PhaseTrace {  // SEM_TRACE=1: wall time of each preparation phase on stderr
+    bool on = getenv("SEM_TRACE") != nullptr;
+    double t = now_ms();
+    void mark(cudaStream_t s, const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const double n = now_ms();
+        fprintf(stderr, "[sem mesh_reorder] %-30s %8.1f ms\n", what, n - t);
+        t = n;
+    }
+};
 
 template <typename T>
 cudaError_t upload(std::vector<void *> &list, T **dst, const std::vector<T> &src, cudaStream_t s) {
@@ -415,7 +429,10 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has detJ <= 0");
-    ctx->src_int = src_vertex >= 0 ? ctx->can_to_int[src_vertex] : -1;
+    ctx->src_int = -1;
+    if (src_vertex >= 0)  // vertex node: canonical id == input vertex id (R13)
+        for (size_t l = 0; l < ctx->src_lookup.size(); l++)
+            if (ctx->src_lookup[l] == (int32_t)src_vertex) { ctx->src_int = ctx->src_int_of[l]; break; }
     ctx->amp = amplitude;
     ctx->f0 = f0;
     ctx->t0 = t0;
@@ -553,6 +570,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         reset_mesh(ctx);
         const double t_start = now_ms();
         cudaStream_t s = ctx->stream;
+        PhaseTrace tr;
         ctx->P = degree;
         ctx->Np = Np;
         ctx->nv = n_vertices;
@@ -575,6 +593,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has zero area");
+        tr.mark(s, "H2D + orientation");
 
         // ---- element order (list L) ----
         CK(dalloc(ctx->mesh_allocs, &ctx->d_perm, E));
@@ -623,6 +642,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             if (hilbert_key_out) std::memset(hilbert_key_out, 0, sizeof(uint32_t) * E);
         }
 
+        tr.mark(s, "SFC keys + sort");
         // ---- canonical SEM nodes, relabel ----
         int32_t *d_mu_can = nullptr, *d_mu_new = nullptr, *d_mu_ft = nullptr, *d_node_perm = nullptr;
         CK(dalloc(tmp, &d_mu_can, E * Np));
@@ -649,6 +669,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             d_mu_ft = d_mu_new;
         }
 
+        tr.mark(s, "canonical nodes + first touch");
         // ---- host outputs ----
         std::vector<int32_t> node_perm(N), mu_h((size_t)E * Np);
         CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
@@ -656,26 +677,38 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         if (elem_perm_out)
             CK(cudaMemcpyAsync(elem_perm_out, ctx->d_perm, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        free_list(tmp);
         if (node_perm_out) std::memcpy(node_perm_out, node_perm.data(), sizeof(int32_t) * N);
         if (n_nodes_out) *n_nodes_out = N;
         if (grid_wh_out) { grid_wh_out[0] = ctx->grid[0]; grid_wh_out[1] = ctx->grid[1]; }
 
+        tr.mark(s, "D2H outputs");
         // ---- this rank's part: contiguous range of the global order ----
         Partition part;
         std::string err;
-        if (!build_partition(mu_h.data(), E, Np, N, ctx->rank, ctx->world, part, err))
-            return fail(ctx, SEM_E_MESH, err);
-        std::vector<int32_t>().swap(mu_h);
-        ctx->e0 = part.e0;
-        ctx->E = part.e1 - part.e0;
-        ctx->N = (int64_t)part.loc2glob.size();
+        const bool one = ctx->world == 1;  // fast path: every node local, identity maps
+        if (!one) {
+            if (!build_partition(mu_h.data(), E, Np, N, ctx->rank, ctx->world, part, err))
+                return fail(ctx, SEM_E_MESH, err);
+            std::vector<int32_t>().swap(mu_h);
+            ctx->e0 = part.e0;
+            ctx->E = part.e1 - part.e0;
+            ctx->N = (int64_t)part.loc2glob.size();
+        } else {
+            part.nbr_off.assign(1, 0);
+            part.sum_start.assign(1, 0);
+            ctx->e0 = 0;
+            ctx->E = E;
+            ctx->N = N;
+        }
+        tr.mark(s, "partition");
 
         // ---- chunk metadata for the step kernel ----
         ChunkMeta m;
-        if (!build_chunks(part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(), m, err,
-                          ctx->world > 1 ? part.remote.data() : nullptr))
+        if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(), m, err,
+                          one ? nullptr : part.remote.data()))
             return fail(ctx, SEM_E_MESH, err);
+        std::vector<int32_t>().swap(mu_h);
+        tr.mark(s, "chunk builder (host)");
         DevChunks &d = ctx->dch;
         d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
         d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
@@ -693,15 +726,27 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.lptr = p_lptr; d.sh_pstart = p_pstart;
         d.shl_node = p_shn;
         d.shl_slot = p_shs;
-        // node maps for I/O
-        {
+        // node maps for I/O (local node l -> internal / canonical / reordered id)
+        if (one) {
+            // reordered id == local id; the device node_perm (reordered -> canonical) is kept
+            CK(upload(L, &ctx->d_loc_int, m.int_of, s));
+            ctx->d_loc_can = d_node_perm;
+            for (auto it = tmp.begin(); it != tmp.end(); ++it)
+                if (*it == (void *)d_node_perm) { L.push_back(*it); tmp.erase(it); break; }
+            ctx->d_loc_ft = nullptr;
+            ctx->d_own_int = ctx->d_loc_int;
+            ctx->d_own_can = ctx->d_loc_can;
+            ctx->d_own_ft = nullptr;
+            ctx->n_own = N;
+            ctx->src_lookup.swap(node_perm);   // for the source vertex lookup
+            ctx->src_int_of.swap(m.int_of);
+        } else {
             std::vector<int32_t> loc_int(ctx->N), loc_can(ctx->N), own_int, own_can, own_ft;
-            ctx->can_to_int.assign(N, -1);
+            ctx->src_lookup.assign(ctx->N, -1);
             for (int64_t l = 0; l < ctx->N; l++) {
                 const int32_t g = part.loc2glob[l];
                 loc_int[l] = m.int_of[l];
                 loc_can[l] = node_perm[g];
-                ctx->can_to_int[node_perm[g]] = m.int_of[l];
                 if (part.owned[l]) {
                     own_int.push_back(m.int_of[l]);
                     own_can.push_back(node_perm[g]);
@@ -715,6 +760,8 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             CK(upload(L, &ctx->d_own_int, own_int, s));
             CK(upload(L, &ctx->d_own_can, own_can, s));
             CK(upload(L, &ctx->d_own_ft, own_ft, s));
+            ctx->src_lookup.swap(loc_can);
+            ctx->src_int_of.swap(loc_int);
         }
         // interface exchange buffers
         ctx->n_if = m.N_if;
@@ -733,7 +780,9 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(dalloc(L, &ctx->d_xbuf, ctx->n_if + ctx->n_send + 2));
         CK(dalloc(L, &ctx->d_sendbuf, ctx->n_send + 2));
         CK(cudaStreamSynchronize(s));
+        tr.mark(s, "uploads + maps");
         ctx->k7_grid = k7_grid(d);
+        tr.mark(s, "k7 occupancy");
         ctx->meta_info = ChunkMeta();
         ChunkMeta &mi = ctx->meta_info;
         mi.B = m.B; mi.Np = m.Np; mi.E = m.E; mi.N = m.N; mi.nchunks = m.nchunks; mi.N_int = m.N_int;

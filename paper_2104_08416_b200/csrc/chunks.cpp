@@ -3,30 +3,60 @@
 //
 // The paper avoids the scatter race of Algorithm 2 by
 // colouring the whole mesh and running colours one after another.  On the GPU
-// we keep the colouring idea at CTA scale: elements are cut into chunks of B
+// the race is removed at CTA scale instead: elements are cut into chunks of B
 // consecutive elements (consecutive along the Hilbert order, so a chunk is a
 // compact patch of the domain) and each chunk is processed by one CTA:
-//   * nodes touched by a single chunk ("interior") are summed in shared memory
-//     in a fixed colour order and finalised by that CTA;
+//   * nodes touched by a single chunk ("interior") are reduced in shared memory
+//     through a per-chunk node CSR (each node's element contributions form a
+//     contiguous run, summed in ascending entry order) and finalised there;
 //   * nodes touched by several chunks ("shared") get one SLOT per touching
 //     chunk, node-major.  The step kernel's producer warp gathers the U^n of
 //     a chunk's shared nodes with cp.async; its consumers write the chunk's
 //     partial K U sums into the slots; the fix-up kernel adds a node's slots
 //     (a contiguous run, ascending chunk order) and updates the node.
-// Both summation orders are fixed, so results are bitwise reproducible.
-// (Slot layout: node-major -- see below.)
+// Every summation order is fixed, so results are bitwise reproducible.
 //
 // Internal node numbering: interior nodes of chunk c occupy [i0_c, i0_c+nint_c),
-// i0_c even (16-byte aligned for TMA bulk copies, one hole at most per chunk),
-// in ascending incoming id; shared nodes follow at [N_int, N_int+N_sh).
+// i0_c even (16-byte aligned for TMA bulk copies, at most one hole per chunk),
+// ordered by descending entry count then ascending incoming id (so warps of
+// the reduction see nodes of equal degree); shared nodes follow at
+// [N_int, N_int+N_sh): non-interface ones in ascending id, then the
+// rank-interface ones (multi-GPU) in ascending id.
+//
+// Parallel structure: one pass sorts every chunk's node ids (OpenMP over
+// chunks); the per-node facts (first chunk, number of touching chunks) come
+// from atomics on those per-chunk unique lists; everything per chunk after that
+// is again independent.  Only cheap loops over nodes/slots are serial.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sem_internal.h"
 
 namespace sem {
 
-static inline int64_t align2(int64_t v) { return (v + 1) & ~int64_t(1); }
+namespace {
+struct Trace {  // SEM_TRACE=1: phase timings of the builder on stderr
+    bool on = getenv("SEM_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[sem build_chunks] %-28s %8.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
+inline int64_t align2(int64_t v) { return (v + 1) & ~int64_t(1); }
+
+struct Uniq {  // unique node of a chunk
+    int32_t g;    // incoming node id
+    int32_t cnt;  // entries of the chunk that reference it
+};
+}  // namespace
 
 bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkMeta &m,
                   std::string &err, const uint8_t *force_shared) {
@@ -45,97 +75,114 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     m.N = N;
     const int64_t nch = (E + B - 1) / B;
     m.nchunks = nch;
+    Trace tr;
 
-    // Pass 1: first chunk and number of distinct chunks touching each node.
-    std::vector<int32_t> firstc(N, -1), lastc(N, -1), nref(N, 0);
-    std::vector<uint8_t> refcnt(N, 0);  // element entries per node (saturating)
-    for (int64_t e = 0; e < E; e++) {
-        const int32_t c = (int32_t)(e / B);
-        for (int p = 0; p < Np; p++) {
-            const int32_t g = mu[e * Np + p];
-            if (g < 0 || g >= N) {
-                err = "build_chunks: node id out of range in element " + std::to_string(e);
-                return false;
-            }
-            if (refcnt[g] < 255) refcnt[g]++;
-            if (lastc[g] != c) {  // chunks are visited in increasing order
-                if (firstc[g] < 0) firstc[g] = c;
-                lastc[g] = c;
-                nref[g]++;
+    // ---- per chunk: sorted unique node ids with entry counts; per node: first
+    //      touching chunk and number of touching chunks (atomics, order-free) ----
+    std::vector<std::vector<Uniq>> uq(nch);
+    std::vector<int32_t> firstc(N, INT32_MAX), nref(N, 0);
+    bool bad_id = false;
+#pragma omp parallel
+    {
+    std::vector<int32_t> ids;
+    ids.reserve((size_t)B * Np);
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t c = 0; c < nch; c++) {
+        const int64_t e0 = c * B, e1 = std::min<int64_t>(E, e0 + B);
+        ids.assign(mu + e0 * Np, mu + e1 * Np);
+        std::sort(ids.begin(), ids.end());
+        std::vector<Uniq> &U = uq[c];
+        U.reserve(ids.size() / 2 + 16);
+        for (size_t k = 0; k < ids.size();) {
+            size_t j = k;
+            while (j < ids.size() && ids[j] == ids[k]) j++;
+            U.push_back({ids[k], (int32_t)(j - k)});
+            k = j;
+        }
+        if (U.front().g < 0 || U.back().g >= N) {
+            bad_id = true;
+            continue;
+        }
+        for (const Uniq &u : U) {
+            __atomic_fetch_add(&nref[u.g], 1, __ATOMIC_RELAXED);
+            int32_t cur = __atomic_load_n(&firstc[u.g], __ATOMIC_RELAXED);
+            while ((int32_t)c < cur &&
+                   !__atomic_compare_exchange_n(&firstc[u.g], &cur, (int32_t)c, true, __ATOMIC_RELAXED,
+                                                __ATOMIC_RELAXED)) {
             }
         }
+        U.shrink_to_fit();
+    }
+    }
+    if (bad_id) {
+        err = "build_chunks: node id out of range";
+        return false;
     }
     for (int64_t g = 0; g < N; g++)
-        if (firstc[g] < 0) {
+        if (nref[g] == 0) {
             err = "node " + std::to_string(g) + " is not used by any element";
             return false;
         }
+    tr.mark("chunk sort + node facts");
 
-    // Nodes touched by another rank (multi-GPU interface) are shared even when a
-    // single local chunk touches them; they go last in the shared range.
-    if (force_shared)
-        for (int64_t g = 0; g < N; g++)
-            if (force_shared[g] && nref[g] == 1) nref[g] = -1;  // marker: 1 local chunk, forced
-    auto is_interior = [&](int64_t g) { return nref[g] == 1; };
+    // ---- classification: nodes touched by another rank are always shared ----
     auto forced = [&](int64_t g) { return force_shared && force_shared[g]; };
-    auto nref_local = [&](int64_t g) { return nref[g] < 0 ? 1 : nref[g]; };
+    auto interior = [&](int64_t g) { return nref[g] == 1 && !forced(g); };
 
-    // Interior windows (even-aligned starts).
     std::vector<int64_t> nint(nch, 0);
-    int64_t nsh = 0, nif = 0;
-    for (int64_t g = 0; g < N; g++) {
-        if (is_interior(g)) nint[firstc[g]]++;
-        else { nsh++; if (forced(g)) nif++; }
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t c = 0; c < nch; c++) {
+        int64_t n = 0;
+        for (const Uniq &u : uq[c]) n += interior(u.g);
+        nint[c] = n;
     }
     m.i0.assign(nch + 1, 0);
     for (int64_t c = 0; c < nch; c++) m.i0[c + 1] = (int32_t)align2(m.i0[c] + nint[c]);
     m.N_int = m.i0[nch];
+
+    // shared indices: non-interface in ascending id, then interface in ascending id
+    m.int_of.assign(N, -1);
+    std::vector<int32_t> sh_index(N, -1);
+    int64_t nsh = 0, nif = 0;
+    for (int64_t g = 0; g < N; g++)
+        if (!interior(g)) { nsh++; nif += forced(g); }
+    {
+        int64_t s = 0, sf = nsh - nif;
+        for (int64_t g = 0; g < N; g++) {
+            if (interior(g)) continue;
+            const int64_t k = forced(g) ? sf++ : s++;
+            sh_index[g] = (int32_t)k;
+            m.int_of[g] = (int32_t)(m.N_int + k);
+        }
+    }
     m.N_sh = nsh;
     m.N_if = nif;
     m.N_tot = m.N_int + nsh;
-    m.int_of.assign(N, -1);
-    std::vector<int32_t> sh_index(N, -1);
-    {
-        // interior nodes of a chunk: descending entry count, then ascending id
-        // (warps of the reduction then see nodes of equal degree)
-        std::vector<int32_t> cur(m.i0.begin(), m.i0.end() - 1), order(m.N_int > 0 ? m.N_int : 1);
-        int64_t s = 0, sf = nsh - nif;
-        for (int64_t g = 0; g < N; g++) {
-            if (is_interior(g)) order[cur[firstc[g]]++] = (int32_t)g;
-            else if (!forced(g)) { sh_index[g] = (int32_t)s; m.int_of[g] = (int32_t)(m.N_int + s); s++; }
-            else { sh_index[g] = (int32_t)sf; m.int_of[g] = (int32_t)(m.N_int + sf); sf++; }
-        }
-#pragma omp parallel for schedule(dynamic, 256)
-        for (int64_t c = 0; c < nch; c++) {
-            std::stable_sort(order.begin() + m.i0[c], order.begin() + m.i0[c] + nint[c],
-                             [&](int32_t a, int32_t b) { return refcnt[a] > refcnt[b]; });
-            for (int64_t k = m.i0[c]; k < m.i0[c] + nint[c]; k++) m.int_of[order[k]] = (int32_t)k;
-        }
-    }
 
-    // Per-chunk shared lists (sorted, unique).
+    // interior ids: per chunk, descending entry count then ascending id
+    // (stable counting sort; the unique list is ascending in id)
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t c = 0; c < nch; c++) {
+        int off[256] = {0};
+        for (const Uniq &u : uq[c])
+            if (interior(u.g)) off[255 - std::min(u.cnt, 255)]++;
+        int acc = 0;
+        for (int b = 0; b < 256; b++) { const int h = off[b]; off[b] = acc; acc += h; }
+        for (const Uniq &u : uq[c])
+            if (interior(u.g)) m.int_of[u.g] = (int32_t)(m.i0[c] + off[255 - std::min(u.cnt, 255)]++);
+    }
+    tr.mark("internal numbering");
+
+    // ---- per-chunk shared lists: descending local count, then ascending index ----
     std::vector<std::vector<int32_t>> lists(nch);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t c = 0; c < nch; c++) {
-        std::vector<int32_t> &L = lists[c];
-        const int64_t e0 = c * B, e1 = std::min<int64_t>(E, e0 + B);
-        for (int64_t e = e0; e < e1; e++)
-            for (int p = 0; p < Np; p++) {
-                const int32_t s = sh_index[mu[e * Np + p]];
-                if (s >= 0) L.push_back(s);
-            }
-        // by descending local entry count, then ascending shared index
-        std::sort(L.begin(), L.end());
-        std::vector<std::pair<int32_t, int32_t>> cnt;  // (-count, s)
-        for (size_t k = 0; k < L.size();) {
-            size_t j = k;
-            while (j < L.size() && L[j] == L[k]) j++;
-            cnt.push_back({-(int32_t)(j - k), L[k]});
-            k = j;
-        }
-        std::sort(cnt.begin(), cnt.end());
-        L.clear();
-        for (auto &pr : cnt) L.push_back(pr.second);
+        std::vector<std::pair<int32_t, int32_t>> key;  // (-count, s)
+        for (const Uniq &u : uq[c])
+            if (!interior(u.g)) key.push_back({-u.cnt, sh_index[u.g]});
+        std::sort(key.begin(), key.end());
+        lists[c].reserve(key.size());
+        for (auto &pr : key) lists[c].push_back(pr.second);
     }
     // Boundary chunks (touching a rank-interface node) run first so that the
     // interface exchange overlaps the interior chunks.
@@ -144,13 +191,13 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         for (int32_t sidx : lists[c]) bnd |= sidx >= nsh - nif;
         (bnd ? m.bnd_chunks : m.int_chunks).push_back((int32_t)c);
     }
-    // Slots are node-major: shared node s owns [sh_pstart[s], sh_pstart[s+1]),
-    // one per touching chunk in ascending chunk order (so the fix-up sums a
-    // contiguous run).  Each chunk lists, contiguously, the shared index and the
-    // slot of every shared node it touches (block start 16-byte aligned).
+    tr.mark("shared lists");
+
+    // ---- node-major slots: shared node s owns [sh_pstart[s], sh_pstart[s+1]),
+    //      one per touching chunk in ascending chunk order ----
     m.sh_pstart.assign(nsh + 1, 0);
     for (int64_t g = 0; g < N; g++)
-        if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref_local(g);
+        if (sh_index[g] >= 0) m.sh_pstart[sh_index[g] + 1] = nref[g];
     for (int64_t s = 0; s < nsh; s++) m.sh_pstart[s + 1] += m.sh_pstart[s];
     m.n_slots = nsh ? m.sh_pstart[nsh] : 0;
     m.s0.assign(nch + 1, 0);
@@ -169,19 +216,16 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
             }
         }
     }
+    tr.mark("slots");
 
-    // Local indices, the per-chunk node CSR (local node -> entries p*B + t in
-    // ascending order; this fixes the summation order), a per-chunk greedy
-    // colouring (first fit in element order; used by diagnostics only), and
-    // the per-chunk descriptor.
+    // ---- local indices, the per-chunk node CSR and the chunk descriptor ----
     m.lidx.assign((size_t)nch * Np * B, 0);
-    m.color.assign((size_t)nch * B, 255);
+    m.lpos.assign((size_t)nch * Np * B, 0);
     m.cmeta.assign((size_t)nch * 8, 0);
     m.lp0.assign(nch + 1, 0);
     std::vector<int32_t> nlocal(nch, 0);
-    int max_local = 0, max_win = 0, max_col = 0;
-    bool bad_color = false;
-#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_local, max_win, max_col)
+    int max_local = 0, max_win = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_local, max_win)
     for (int64_t c = 0; c < nch; c++) {
         const int64_t e0 = c * B, e1 = std::min<int64_t>(E, e0 + B);
         const int32_t i0 = m.i0[c];
@@ -193,55 +237,35 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         nlocal[c] = ni_al + ns;
         if (nl > max_local) max_local = nl;
         if (ni_al > max_win) max_win = ni_al;
-        std::vector<uint32_t> used(nl, 0u);
         std::vector<std::pair<int32_t, int32_t>> pos_of;  // (shared index, local position)
         pos_of.reserve(L.size());
         for (int32_t k = 0; k < ns; k++) pos_of.push_back({L[k], k});
         std::sort(pos_of.begin(), pos_of.end());
-        int ncol = 0;
         for (int64_t e = e0; e < e1; e++) {
             const int t = (int)(e - e0);
-            uint32_t forb = 0;
-            uint16_t li[kMaxNp];
             for (int p = 0; p < Np; p++) {
                 const int32_t g = mu[e * Np + p];
                 int loc;
-                if (sh_index[g] < 0) loc = m.int_of[g] - i0;
+                if (interior(g)) loc = m.int_of[g] - i0;
                 else loc = ni_al + std::lower_bound(pos_of.begin(), pos_of.end(),
                                                     std::make_pair(sh_index[g], (int32_t)-1))->second;
-                li[p] = (uint16_t)loc;
                 m.lidx[(size_t)c * Np * B + (size_t)p * B + t] = (uint16_t)loc;
-                forb |= used[loc];
             }
-            if (forb == 0xFFFFFFFFu) {
-                bad_color = true;
-                continue;
-            }
-            int col = 0;
-            while (forb & (1u << col)) col++;
-            m.color[(size_t)c * B + t] = (uint8_t)col;
-            for (int p = 0; p < Np; p++) used[li[p]] |= (1u << col);
-            if (col + 1 > ncol) ncol = col + 1;
         }
         int32_t *cm = &m.cmeta[(size_t)c * 8];
         cm[0] = i0;
         cm[1] = ni;
         cm[2] = m.s0[c];
         cm[3] = ns;
-        cm[4] = ncol;
+        cm[4] = 0;
         cm[5] = (int32_t)(e1 - e0);
         cm[6] = ni_al;
-        if (ncol > max_col) max_col = ncol;
     }
-    if (bad_color) {
-        err = "build_chunks: more than 32 colours needed inside a chunk";
-        return false;
-    }
+    tr.mark("local indices");
     // CSR blocks: chunk c owns lptr[lp0[c] .. lp0[c] + nlocal+1) (start aligned
     // to 8 entries = 16 bytes for TMA) and lpos[c*Np*B .. (c+1)*Np*B).
     for (int64_t c = 0; c < nch; c++) m.lp0[c + 1] = (int32_t)((m.lp0[c] + nlocal[c] + 1 + 7) & ~7);
     m.lptr.assign((size_t)m.lp0[nch] + 8, 0);
-    m.lpos.assign((size_t)nch * Np * B, 0);
     int max_lp = 0;
 #pragma omp parallel for schedule(dynamic, 64) reduction(max : max_lp)
     for (int64_t c = 0; c < nch; c++) {
@@ -263,10 +287,11 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         const int w = (nl + 1 + 7) & ~7;
         if (w > max_lp) max_lp = w;
     }
-    m.max_lptr = max_lp;
     m.max_local = max_local;
     m.max_win = max_win;
-    m.max_colors = max_col;
+    m.max_lptr = max_lp;
+    m.max_colors = 0;
+    tr.mark("CSR");
     return true;
 }
 
