@@ -62,6 +62,13 @@ def lib():
             L.orc_leapfrog.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P,
                                        i64, dbl, dbl, dbl, dbl, i64, i64, P, P]
             L.orc_leapfrog.restype = C.c_int
+            L.orc_vdot.argtypes = [P, i64, C.c_int, P, P, P, P, P, P]
+            L.orc_vdot.restype = None
+            L.orc_rv.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P, P]
+            L.orc_rv.restype = None
+            L.orc_heun.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P,
+                                   i64, dbl, dbl, dbl, dbl, i64, i64, P, P]
+            L.orc_heun.restype = C.c_int
             L.orc_num_threads.argtypes = []
             L.orc_num_threads.restype = C.c_int
             _lib = L
@@ -208,6 +215,37 @@ class OracleSEM:
         if rc != 0:
             raise OracleError("leapfrog rc=%d" % rc)
         return U, Up
+
+    # ---- the paper's Heun scheme on (U, V) (NEXT-1) ----
+    def vdot(self, U):
+        """Algorithm 1 (E = 0): Vdot [E, Np, 2]."""
+        U = np.ascontiguousarray(U, np.float64)
+        Vd = np.empty((self.ne, self.Np, 2))
+        lib().orc_vdot(_p(self.mu), self.ne, self.Np, _p(self.Jinv), _p(self.c), _p(self.Dr), _p(self.Ds),
+                       _p(U), _p(Vd))
+        return Vd
+
+    def rv(self, V):
+        """Algorithm 2 first term (D = 0, B = -I) applied to V [E, Np, 2]."""
+        V = np.ascontiguousarray(V, np.float64)
+        R = np.empty(self.N)
+        if self._ebuf is None:
+            self._ebuf = np.empty(self.ne * self.Np)
+        lib().orc_rv(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.Jinv), _p(self.Dr),
+                     _p(self.Ds), _p(self.wK), _p(V), _p(R), _p(self._ebuf))
+        return R
+
+    def heun(self, h: float, n_steps: int, src: int = -1, A: float = 1.0, f0: float = 1.0, t0: float = 0.0,
+             U=None, V=None, step0: int = 0):
+        """n_steps Heun steps from (U^n, V^n) (zeros by default)."""
+        U = np.zeros(self.N) if U is None else np.array(U, np.float64, copy=True)
+        V = np.zeros((self.ne, self.Np, 2)) if V is None else np.array(V, np.float64, copy=True)
+        rc = lib().orc_heun(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.Jinv), _p(self.c),
+                            _p(self.Dr), _p(self.Ds), _p(self.wK), _p(self.Mbar), int(src), float(A), float(f0),
+                            float(t0), float(h), int(step0), int(n_steps), _p(U), _p(V))
+        if rc != 0:
+            raise OracleError("heun rc=%d" % rc)
+        return U, V
 
     def node_xy(self) -> np.ndarray:
         """Coordinates of every canonical node, x_mu(p,e) = F^(e)(x^_p)."""

@@ -453,6 +453,107 @@ int orc_leapfrog(const int32_t *mu, int64_t ne, int Np, int64_t nn,
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* The paper's own integrator: Heun predictor-corrector on (U, V)           */
+/* (§4.2.1) with Algorithms 1-3.       */
+/* NEXT-1 of SURVEY §8f.  V[e][p][k] is stored element-major with the two   */
+/* components of a local node adjacent (Fig. mem_layout). */
+/* ------------------------------------------------------------------------ */
+
+/* Algorithm 1 with E = 0: Vdot_kp = sum_q,j,jh F_kj K_jjh N_q,jh(x_p) U_mu(q,e),
+ * F = c^2 I (R2), K_jjh = (J^-1)_{jh j} (R5). */
+void orc_vdot(const int32_t *mu, int64_t ne, int Np, const double *Jinv, const double *c,
+              const double *Dr, const double *Ds, const double *U, double *Vd) {
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < ne; e++) {
+        double U2[16];
+        const double *Ki = Jinv + 4 * e;
+        const double c2 = c[e] * c[e];
+        for (int q = 0; q < Np; q++) U2[q] = U[mu[e * Np + q]];
+        for (int k = 0; k < 2; k++)
+            for (int p = 0; p < Np; p++) {
+                double acc = 0.0;
+                for (int q = 0; q < Np; q++) {
+                    double FK1 = c2 * Ki[0 * 2 + k];
+                    double FK2 = c2 * Ki[1 * 2 + k];
+                    acc += FK1 * Dr[p * Np + q] * U2[q] + FK2 * Ds[p * Np + q] * U2[q];
+                }
+                Vd[(e * Np + p) * 2 + k] = acc;
+            }
+    }
+}
+
+/* Algorithm 2, first term (D = 0, B = -I): R_nu = sum over (e,p) with
+ * mu(p,e) = nu of sum_k sum_q detJ w_q B_kk V_kq sum_jh K_k,jh N_p,jh(x_q). */
+void orc_rv(const int32_t *mu, int64_t ne, int Np, int64_t nn, const double *detJ, const double *Jinv,
+            const double *Dr, const double *Ds, const double *wK, const double *V, double *R, double *ebuf) {
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < ne; e++) {
+        const double *Ki = Jinv + 4 * e;
+        for (int p = 0; p < Np; p++) {
+            double val = 0.0;
+            for (int k = 0; k < 2; k++) {
+                double BK1 = -1.0 * Ki[0 * 2 + k];
+                double BK2 = -1.0 * Ki[1 * 2 + k];
+                for (int q = 0; q < Np; q++) {
+                    double aux2 = detJ[e] * wK[q] * V[(e * Np + q) * 2 + k];
+                    val += BK1 * aux2 * Dr[q * Np + p] + BK2 * aux2 * Ds[q * Np + p];
+                }
+            }
+            ebuf[e * Np + p] = val;
+        }
+    }
+    for (int64_t g = 0; g < nn; g++) R[g] = 0.0;
+    for (int64_t e = 0; e < ne; e++)
+        for (int p = 0; p < Np; p++) R[mu[e * Np + p]] += ebuf[e * Np + p];
+}
+
+/*
+ * n_steps Heun steps:
+ *   predictor  U~ = U + h Udot(V, t_n),       V~ = V + h Vdot(U)
+ *   corrector  U+ = U + h/2 (Udot(V, t_n) + Udot(V~, t_{n+1})),
+ *              V+ = V + h/2 (Vdot(U) + Vdot(U~))
+ * with Udot(V, t) = Mbar^-1 (R(V) + y(t)) (eq. u_change, Algorithm 3 adds the
+ * source) and Vdot = Algorithm 1.  Reading R18: the corrector's rates are
+ * evaluated at t_{n+1} = t_n + h.  U [nn] and V [ne*Np*2] are updated in place.
+ */
+int orc_heun(const int32_t *mu, int64_t ne, int Np, int64_t nn,
+             const double *detJ, const double *Jinv, const double *c,
+             const double *Dr, const double *Ds, const double *wK, const double *Mbar,
+             int64_t src, double A, double f0, double t0, double h,
+             int64_t step0, int64_t n_steps, double *U, double *V) {
+    const int64_t nv = ne * Np * 2;
+    double *R = (double *)malloc(sizeof(double) * nn);
+    double *Ud1 = (double *)malloc(sizeof(double) * nn);
+    double *Ut = (double *)malloc(sizeof(double) * nn);
+    double *Vd1 = (double *)malloc(sizeof(double) * nv);
+    double *Vd2 = (double *)malloc(sizeof(double) * nv);
+    double *Vt = (double *)malloc(sizeof(double) * nv);
+    double *ebuf = (double *)malloc(sizeof(double) * ne * Np);
+    if (!R || !Ud1 || !Ut || !Vd1 || !Vd2 || !Vt || !ebuf) {
+        free(R); free(Ud1); free(Ut); free(Vd1); free(Vd2); free(Vt); free(ebuf);
+        return ORC_E_OOM;
+    }
+    for (int64_t s = 0; s < n_steps; s++) {
+        const int64_t n = step0 + s;
+        const double tn = (double)n * h, tn1 = (double)(n + 1) * h;
+        /* predictor */
+        orc_rv(mu, ne, Np, nn, detJ, Jinv, Dr, Ds, wK, V, R, ebuf);
+        if (src >= 0) R[src] += A * orc_ricker(tn, f0, t0);
+        for (int64_t g = 0; g < nn; g++) { Ud1[g] = R[g] / Mbar[g]; Ut[g] = U[g] + h * Ud1[g]; }
+        orc_vdot(mu, ne, Np, Jinv, c, Dr, Ds, U, Vd1);
+        for (int64_t i = 0; i < nv; i++) Vt[i] = V[i] + h * Vd1[i];
+        /* corrector */
+        orc_rv(mu, ne, Np, nn, detJ, Jinv, Dr, Ds, wK, Vt, R, ebuf);
+        if (src >= 0) R[src] += A * orc_ricker(tn1, f0, t0);
+        orc_vdot(mu, ne, Np, Jinv, c, Dr, Ds, Ut, Vd2);
+        for (int64_t g = 0; g < nn; g++) U[g] = U[g] + h / 2.0 * (Ud1[g] + R[g] / Mbar[g]);
+        for (int64_t i = 0; i < nv; i++) V[i] = V[i] + h / 2.0 * (Vd1[i] + Vd2[i]);
+    }
+    free(R); free(Ud1); free(Ut); free(Vd1); free(Vd2); free(Vt); free(ebuf);
+    return ORC_OK;
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
