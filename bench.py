@@ -99,6 +99,18 @@ def problem_for(name: str, world: int):
     return mg.config(name, 1, gpus=world) if name == "C4" else mg.config(name, 1)
 
 
+def ncu_traffic(config, kernel):
+    """DRAM bytes (read + write) of one launch of `kernel` on `config`, from the
+    committed `ncu --set full` capture summarised in profiles/traffic_<config>.json
+    (None if there is none).  Not measured in this run: ncu perturbs timing."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_%s.json" % config)) as f:
+            d = json.load(f)[kernel]
+        return float(d["traffic_bytes"]) / 1e9
+    except Exception:
+        return None
+
+
 def k7_bytes(info):
     """Algorithmic bytes per launch of K7 / K8."""
     E, Np, N = info["n_elements"], info["nodes_per_elem"], info["n_nodes"]
@@ -203,7 +215,8 @@ def run_ours(args):
                    "dt": pb.dt},
         "roofline": {"bound": "hbm", "kernel": "k7_step (stiffness apply + fused leapfrog)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_source": peak_src, "traffic": None,
+                     "peak_source": peak_src, "traffic": ncu_traffic(args.config, "k7_step"),
+                     "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/)",
                      "bytes_per_launch": b7, "avg_launch_ms": k7_avg,
                      "k7_share_of_step": kt["k7_ms"] / max(ms, 1e-9),
                      "k8_avg_launch_ms": k8_avg, "k8_bytes_per_launch": b8},
