@@ -229,6 +229,8 @@ def run_ours(args):
     }
     if rank == 0 and args.orderings and world == 1:
         out["orderings"] = orderings(ctx, pb, args, S)
+    if rank == 0 and args.heun and world == 1:
+        out["heun"] = heun_leg(ctx, pb, args, S, peak)
     ctx.close()
     if args.e2e:
         out["e2e"] = e2e(pb, args, S, local, rank, world, stream, dist)
@@ -286,6 +288,54 @@ def orderings(ctx, pb, args, S):
                      "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
                      "max_chunk_nodes": info["max_chunk_nodes"], "steps": K}
     return res
+
+
+def heun_bytes(info):
+    """Algorithmic bytes per launch of the Heun element pass KH7 / fix-up KH8
+    (DESIGN.md "Heun"): per element mu (4 Np) + F, sd (40) + V read and write
+    (32 Np); per node U, W read (16) in KH7, and (h/2)/M read + U, W write (24)
+    where the node is finalised (KH7 interior, KH8 shared)."""
+    E, Np, N = info["n_elements"], info["nodes_per_elem"], info["n_nodes"]
+    Nint, Nsh = info["n_interior_nodes"], info["n_shared_nodes"]
+    return float(E * (36 * Np + 40) + 16 * N + 24 * Nint), float(24 * Nsh)
+
+
+def heun_leg(ctx, pb, args, S, peak):
+    """The paper's own integrator (Heun on (U, V), NEXT-1) on the same mesh:
+    one step = both RHS evaluations of PAPER.md:269-291, fused in one pass."""
+    import torch
+    m = pb.mesh
+    K = max(50, min(args.steps, 500))
+    ctx.sem_set_integrator(S.SEM_INTEGRATOR_HEUN)
+    ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
+    h = pb.dt * 0.2  # reading R19 (meshgen.heun_h)
+    ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, pb.amplitude, h)
+    ctx.sem_step_n(5)
+    stream = torch.cuda.current_stream()
+    ctx.sem_set_kernel_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    ctx.sem_step_n(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    kt = ctx.sem_kernel_times()
+    ctx.sem_set_kernel_timing(False)
+    info = ctx.sem_get_info()
+    U, _ = ctx.sem_read_field()
+    ctx.sem_set_integrator(S.SEM_INTEGRATOR_LEAPFROG)
+    b7, b8 = heun_bytes(info)
+    k7 = kt["k7_ms"] / max(kt["k7_launches"], 1)
+    achieved = b7 / (k7 * 1e-3) / 1e9
+    return {"element_updates_per_s": info["n_elements"] / (ms * 1e-3), "ms_per_step": ms, "steps": K, "h": h,
+            "alg_bytes_per_step": info["bytes_alg_per_step"],
+            "alg_gbs": info["bytes_alg_per_step"] / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "k_heun (lagged V update + Alg. 2 + K u + fused Heun update)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "bytes_per_launch": b7, "avg_launch_ms": k7,
+                         "fix_avg_launch_ms": kt["k8_ms"] / max(kt["k8_launches"], 1), "fix_bytes_per_launch": b8},
+            "field_finite": bool(np.isfinite(U).all())}
 
 
 def e2e(pb, args, S, device, rank, world, stream, dist):
@@ -407,6 +457,7 @@ def main():
     ap.add_argument("--no-orderings", dest="orderings", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-heun", dest="heun", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -63,6 +63,11 @@ enum { SEM_NODES_FIRST_TOUCH = 0, SEM_NODES_CANONICAL = 2 };
  * chosen by sem_mesh_reorder (node_perm_out maps them to CANONICAL). */
 enum { SEM_NUMBERING_CANONICAL = 0, SEM_NUMBERING_INTERNAL = 1 };
 
+/* Time integrators.  LEAPFROG = the north_star step on M U'' = -K U + f
+ * (reading R1); HEUN = the paper's own predictor-corrector on the
+ * first-order (U, V) system with Algorithms 1-3. */
+enum { SEM_INTEGRATOR_LEAPFROG = 0, SEM_INTEGRATOR_HEUN = 1 };
+
 /*
  * Create a context on CUDA device `device`.
  *  rank, world_size : this process's place in a multi-GPU run (world_size = 1
@@ -174,6 +179,33 @@ sem_status sem_group_build_operators(sem_ctx **ctxs, int n, const double *c_elem
 sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps);
 
 /*
+ * Select the time integrator used by the next sem_build_operators (default
+ * LEAPFROG).  With SEM_INTEGRATOR_HEUN (§4.2.1):
+ *   predictor  U~ = U + h Udot(V, t_n),  V~ = V + h Vdot(U)
+ *   corrector  U+ = U + h/2 (Udot(V, t_n) + Udot(V~, t_n+1)),
+ *              V+ = V + h/2 (Vdot(U) + Vdot(U~))
+ * with Vdot = Algorithm 1 (F = c^2 I), Udot = M-bar^-1 (R(V) +
+ * y(t)) with R = Algorithm 2 (B = -I) and y = Algorithm 3;
+ * t_n = n h, the corrector's source at t_{n+1} (reading R18).  The state is
+ * (U [N], V [E][Np][2]), zero after sem_build_operators; `dt` is h.  Heun runs
+ * with world_size 1 and chunks of 128 or 256 elements.
+ * Errors: SEM_E_UNSUPPORTED (unknown integrator).
+ */
+sem_status sem_set_integrator(sem_ctx *ctx, int integrator);
+
+/*
+ * Heun only: copy V^n to out_host[E][Np][2] (fp64; INPUT element order, local
+ * node p in the lattice order of reading R3 after the orientation fix, then the
+ * x and y components) and return the step index.  Synchronises.
+ * Errors: SEM_E_STATE (no Heun operators), SEM_E_ARG, SEM_E_CUDA, SEM_E_NONFINITE.
+ */
+sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out);
+
+/* Heun only: overwrite V from v_host[E][Np][2] (layout of sem_read_velocity);
+ * NULL sets V = 0.  U is set with sem_write_state(ctx, U, NULL, numbering). */
+sem_status sem_write_velocity(sem_ctx *ctx, const double *v_host);
+
+/*
  * Copy U^n to out_host[N] (fp64, N = global node count) in the requested
  * numbering and return the step index n.  With several ranks only the nodes
  * this rank owns (an interface node belongs to the lowest rank touching it) are
@@ -215,7 +247,8 @@ typedef struct {
     int32_t max_colors;       /* largest per-chunk colour count */
     int32_t launches_per_step;/* kernels launched per leapfrog step */
     int64_t step;             /* current step index n */
-    double bytes_alg_per_step;/* E (4 Np + 24) + 32 N */
+    double bytes_alg_per_step;/* leapfrog: E (4 Np + 24) + 32 N;
+                                 Heun: E (4 Np + 40 + 32 Np) + 40 N */
     double prep_reorder_ms;   /* last sem_mesh_reorder wall time */
     double prep_build_ms;     /* last sem_build_operators wall time */
     int64_t n_interface_nodes;/* nodes exchanged with other ranks */
@@ -223,6 +256,8 @@ typedef struct {
     int32_t rank, world_size;
     int64_t n_elements_global;
     int64_t first_element;    /* global index of this rank's first element */
+    int32_t integrator;       /* SEM_INTEGRATOR_* of the built operators (else the selected one) */
+    int32_t reserved0;
 } sem_info;
 
 sem_status sem_get_info(sem_ctx *ctx, sem_info *out);

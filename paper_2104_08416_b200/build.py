@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsem.so")
-SOURCES = ["api.cu", "reorder.cu", "step.cu", "chunks.cpp", "partition.cpp", "refelem.cpp"]
-HEADERS = ["kernels.h", "sem_internal.h"]
+SOURCES = ["api.cu", "reorder.cu", "step.cu", "heun.cu", "chunks.cpp", "partition.cpp", "refelem.cpp"]
+HEADERS = ["kernels.h", "sem_internal.h", "dev_common.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -116,6 +116,12 @@ struct sem_ctx {
     double *d_U[2] = {nullptr, nullptr};
     double *d_slot = nullptr;
     int cur = 0;
+    // Heun (NEXT-1): U = d_U[0], hM = (h/2)/M-bar in d_dt2M, double2 slots in d_slot
+    int integrator = SEM_INTEGRATOR_LEAPFROG;
+    int ops_integrator = SEM_INTEGRATOR_LEAPFROG;  // integrator the built operators belong to
+    double *d_geo[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    double *d_W = nullptr, *d_V = nullptr;
+    bool v_lag = false;  // V holds V^{n-1}; V^n = V + h Vdot(W)
     int32_t src_int = -1;
     double amp = 0, f0 = 1, t0 = 0, dt = 0;
     int64_t step = 0;
@@ -178,6 +184,9 @@ void reset_ops(sem_ctx *ctx) {
     ctx->d_Grr = ctx->d_Gss = ctx->d_Grs = ctx->d_dt2M = nullptr;
     ctx->d_U[0] = ctx->d_U[1] = nullptr;
     ctx->d_slot = nullptr;
+    for (auto &g : ctx->d_geo) g = nullptr;
+    ctx->d_W = ctx->d_V = nullptr;
+    ctx->v_lag = false;
     ctx->have_ops = false;
     ctx->step = 0;
     ctx->cur = 0;
@@ -223,6 +232,7 @@ cudaError_t upload(std::vector<void *> &list, T **dst, const std::vector<T> &src
 sem_status ensure_tables(sem_ctx *ctx) {
     if (g_const_P != ctx->P) {
         CK(upload_ref_tables(ctx->T, ctx->stream));
+        CK(upload_heun_tables(ctx->T, ctx->stream));
         g_const_P = ctx->P;
     }
     return SEM_OK;
@@ -368,6 +378,47 @@ sem_status step_phase1(sem_ctx *ctx, bool use_nccl) {
     return SEM_OK;
 }
 
+HeunParams heun_params(sem_ctx *ctx) {
+    HeunParams p;
+    for (int g = 0; g < 5; g++) p.geo[g] = ctx->d_geo[g];
+    p.hM = ctx->d_dt2M;
+    p.U = ctx->d_U[0];
+    p.W = ctx->d_W;
+    p.V = ctx->d_V;
+    p.slot = ctx->d_slot;
+    p.src = ctx->src_int; p.amp = ctx->amp; p.f0 = ctx->f0; p.t0 = ctx->t0; p.h = ctx->dt;
+    p.n = ctx->step;
+    return p;
+}
+
+// One Heun step (heun.cu): element pass with the lagged V update, then the
+// shared-node fix-up.  Leaves V lagged by one W update.
+sem_status heun_step(sem_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    ST(ensure_tables(ctx));
+    const HeunParams p = heun_params(ctx);
+    if (ctx->timing) ST(record(ctx, ctx->ev7, true));
+    CK(launch_heun(ctx->dch, p, ctx->v_lag ? 1 : 0, ctx->stream));
+    if (ctx->timing) ST(record(ctx, ctx->ev7, false));
+    if (ctx->timing) ST(record(ctx, ctx->ev8, true));
+    CK(launch_heun_fix(ctx->dch, p, ctx->stream));
+    if (ctx->timing) ST(record(ctx, ctx->ev8, false));
+    ctx->v_lag = true;
+    ctx->step++;
+    if (ctx->timing && ctx->ev7.size() >= 4096) ST(drain_events(ctx));
+    return SEM_OK;
+}
+
+// Apply a pending lagged V update (before V is read or overwritten in part).
+sem_status heun_finalize(sem_ctx *ctx) {
+    if (!ctx->v_lag) return SEM_OK;
+    CK(cudaSetDevice(ctx->device));
+    ST(ensure_tables(ctx));
+    CK(launch_heun(ctx->dch, heun_params(ctx), 2, ctx->stream));
+    ctx->v_lag = false;
+    return SEM_OK;
+}
+
 // Step phase 2: rank-ordered interface sums + update; advance the step.
 sem_status step_phase2(sem_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
@@ -393,6 +444,12 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     for (int64_t e = 0; e < ctx->E_glob; e++)
         if (!(c_elem_host[e] > 0.0) || !std::isfinite(c_elem_host[e]))
             return fail(ctx, SEM_E_ARG, "element " + std::to_string(e) + " has wave speed c <= 0");
+    if (ctx->integrator == SEM_INTEGRATOR_HEUN) {
+        if (ctx->world > 1)
+            return fail(ctx, SEM_E_UNSUPPORTED, "the Heun integrator runs on one rank (world_size 1)");
+        if (!heun_supported(ctx->Np, ctx->dch.B))
+            return fail(ctx, SEM_E_UNSUPPORTED, "Heun kernels are built for chunks of 128 or 256 elements");
+    }
     CK(cudaSetDevice(ctx->device));
     reset_ops(ctx);
     ctx->prep_build_ms = -now_ms();
@@ -408,23 +465,38 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     CK(dalloc(tmp, &d_detJ, Epad));
     CK(dalloc(tmp, &d_bad, 1));
     CK(cudaMemcpyAsync(d_c, c_elem_host, sizeof(double) * ctx->E_glob, cudaMemcpyHostToDevice, s));
-    CK(dalloc(L, &ctx->d_Grr, Epad));
-    CK(dalloc(L, &ctx->d_Gss, Epad));
-    CK(dalloc(L, &ctx->d_Grs, Epad));
+    const bool heun = ctx->integrator == SEM_INTEGRATOR_HEUN;
     const int64_t Nt = d.N_tot + 2;
     CK(dalloc(L, &ctx->d_dt2M, Nt));
     CK(dalloc(L, &ctx->d_U[0], Nt));
-    CK(dalloc(L, &ctx->d_U[1], Nt));
-    CK(dalloc(L, &ctx->d_slot, d.n_slots + 2));
     CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
-    CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm + ctx->e0, d_c, ctx->E, Epad, ctx->d_Grr,
-                       ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
+    if (!heun) {
+        CK(dalloc(L, &ctx->d_Grr, Epad));
+        CK(dalloc(L, &ctx->d_Gss, Epad));
+        CK(dalloc(L, &ctx->d_Grs, Epad));
+        CK(dalloc(L, &ctx->d_U[1], Nt));
+        CK(dalloc(L, &ctx->d_slot, d.n_slots + 2));
+        CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm + ctx->e0, d_c, ctx->E, Epad, ctx->d_Grr,
+                           ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
+    } else {
+        for (auto &g : ctx->d_geo) CK(dalloc(L, &g, Epad));
+        CK(dalloc(L, &ctx->d_W, Nt));
+        CK(dalloc(L, &ctx->d_V, Epad * 2 * ctx->Np));
+        CK(dalloc(L, &ctx->d_slot, 2 * d.n_slots + 4));
+        CK(launch_geometry_heun(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm + ctx->e0, d_c, ctx->E, Epad, ctx->d_geo,
+                                d_detJ, d_bad, s));
+        CK(cudaMemsetAsync(ctx->d_W, 0, sizeof(double) * Nt, s));
+        CK(cudaMemsetAsync(ctx->d_V, 0, sizeof(double) * Epad * 2 * ctx->Np, s));
+        ctx->v_lag = false;
+    }
+    ctx->ops_integrator = ctx->integrator;
     g_const_P = 0;
     ST(ensure_tables(ctx));
-    CK(assemble_mass(d, d_detJ, dt, ctx->d_slot, ctx->d_dt2M, s));
+    // lumped mass -> dt^2 / M-bar (leapfrog) or (h/2) / M-bar (Heun)
+    CK(assemble_mass(d, d_detJ, heun ? 0.5 * dt : dt * dt, ctx->d_slot, ctx->d_dt2M, s));
     CK(launch_if_partial(d, ctx->d_slot, ctx->d_xbuf, ctx->d_send_if, ctx->n_send, ctx->d_sendbuf, s));
     CK(cudaMemsetAsync(ctx->d_U[0], 0, sizeof(double) * Nt, s));
-    CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * Nt, s));
+    if (!heun) CK(cudaMemsetAsync(ctx->d_U[1], 0, sizeof(double) * Nt, s));
     int32_t bad = 0;
     CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -814,6 +886,10 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_step_n before sem_build_operators");
     if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions step with sem_group_step_n");
     if (n_steps < 0) return fail(ctx, SEM_E_ARG, "n_steps < 0");
+    if (ctx->ops_integrator == SEM_INTEGRATOR_HEUN) {
+        for (int64_t k = 0; k < n_steps; k++) ST(heun_step(ctx));
+        return SEM_OK;
+    }
     for (int64_t k = 0; k < n_steps; k++) {
         ST(step_phase1(ctx, ctx->world > 1));
         ST(step_phase2(ctx));
@@ -843,12 +919,66 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps) {
     for (int r = 0; r < n; r++) {
         ST(check_usable(ctxs[r]));
         if (!ctxs[r]->have_ops) return fail(ctxs[r], SEM_E_STATE, "sem_group_step_n before build");
+        if (ctxs[r]->ops_integrator != SEM_INTEGRATOR_LEAPFROG)
+            return fail(ctxs[r], SEM_E_UNSUPPORTED, "loopback groups step the leapfrog only");
     }
     for (int64_t k = 0; k < n_steps; k++) {
         for (int r = 0; r < n; r++) ST(step_phase1(ctxs[r], false));
         ST(exchange_loopback(ctxs, n));
         for (int r = 0; r < n; r++) ST(step_phase2(ctxs[r]));
     }
+    return SEM_OK;
+}
+
+sem_status sem_set_integrator(sem_ctx *ctx, int integrator) {
+    ST(check_usable(ctx));
+    if (integrator != SEM_INTEGRATOR_LEAPFROG && integrator != SEM_INTEGRATOR_HEUN)
+        return fail(ctx, SEM_E_UNSUPPORTED, "unknown integrator " + std::to_string(integrator));
+    ctx->integrator = integrator;
+    return SEM_OK;
+}
+
+sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out) {
+    ST(check_usable(ctx));
+    if (!ctx->have_ops || ctx->ops_integrator != SEM_INTEGRATOR_HEUN)
+        return fail(ctx, SEM_E_STATE, "sem_read_velocity needs operators built for the Heun integrator");
+    if (!out_host) return fail(ctx, SEM_E_ARG, "out is NULL");
+    ST(heun_finalize(ctx));
+    cudaStream_t s = ctx->stream;
+    std::vector<void *> tmp;
+    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    double *d_out = nullptr;
+    const int64_t n = ctx->E * ctx->Np * 2;
+    CK(dalloc(tmp, &d_out, n));
+    CK(launch_v_out(ctx->d_V, ctx->d_perm, ctx->E, ctx->Np, ctx->dch.B, d_out, s));
+    CK(cudaMemcpyAsync(out_host, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (step_out) *step_out = ctx->step;
+    for (int64_t i = 0; i < n; i++)
+        if (!std::isfinite(out_host[i]))
+            return fail(ctx, SEM_E_NONFINITE, "non-finite velocity at step " + std::to_string(ctx->step) +
+                                                  " (element " + std::to_string(i / (2 * ctx->Np)) + ")");
+    return SEM_OK;
+}
+
+sem_status sem_write_velocity(sem_ctx *ctx, const double *v_host) {
+    ST(check_usable(ctx));
+    if (!ctx->have_ops || ctx->ops_integrator != SEM_INTEGRATOR_HEUN)
+        return fail(ctx, SEM_E_STATE, "sem_write_velocity needs operators built for the Heun integrator");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::vector<void *> tmp;
+    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    double *d_in = nullptr;
+    const int64_t n = ctx->E * ctx->Np * 2;
+    if (v_host) {
+        CK(dalloc(tmp, &d_in, n));
+        CK(cudaMemcpyAsync(d_in, v_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemsetAsync(ctx->d_V, 0, sizeof(double) * ctx->dch.nchunks * ctx->dch.B * 2 * ctx->Np, s));
+    CK(launch_v_in(d_in, ctx->d_perm, ctx->E, ctx->Np, ctx->dch.B, ctx->d_V, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->v_lag = false;
     return SEM_OK;
 }
 
@@ -900,7 +1030,10 @@ sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double
     const int32_t *imap = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_loc_can : ctx->d_loc_ft;
     const double *src[2] = {u_curr_host, u_prev_host};
     double *dst[2] = {ctx->d_U[ctx->cur], ctx->d_U[1 - ctx->cur]};
-    for (int k = 0; k < 2; k++) {
+    const bool heun = ctx->ops_integrator == SEM_INTEGRATOR_HEUN;
+    if (heun && u_prev_host) return fail(ctx, SEM_E_ARG, "the Heun state has no U^{n-1} (pass NULL)");
+    if (heun) ST(heun_finalize(ctx));  // the pending V update uses the old W
+    for (int k = 0; k < (heun ? 1 : 2); k++) {
         CK(cudaMemsetAsync(dst[k], 0, sizeof(double) * (ctx->dch.N_tot + 2), s));
         if (!src[k]) continue;
         CK(cudaMemcpyAsync(d_in, src[k], sizeof(double) * ctx->N_glob, cudaMemcpyHostToDevice, s));
@@ -946,6 +1079,12 @@ sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
     o->launches_per_step = 1 + ((m.N_sh - m.N_if) > 0 ? 1 : 0) + (m.N_if > 0 ? 3 : 0);
     o->step = ctx->step;
     o->bytes_alg_per_step = (double)ctx->E * (4.0 * ctx->Np + 24.0) + 32.0 * (double)ctx->N;
+    o->integrator = ctx->have_ops ? ctx->ops_integrator : ctx->integrator;
+    if (o->integrator == SEM_INTEGRATOR_HEUN) {
+        // mu, F (4) + sd, V read + write per element; U r/w, W r/w, (h/2)/M per node
+        o->bytes_alg_per_step = (double)ctx->E * (4.0 * ctx->Np + 40.0 + 32.0 * ctx->Np) + 40.0 * (double)ctx->N;
+        o->launches_per_step = 1 + ((m.N_sh - m.N_if) > 0 ? 1 : 0);
+    }
     o->prep_reorder_ms = ctx->prep_reorder_ms;
     o->prep_build_ms = ctx->prep_build_ms;
     o->n_interface_nodes = m.N_if;

@@ -1,0 +1,441 @@
+// heun.cu -- sm_100a kernels of the paper's own integrator (NEXT-1 of SURVEY §8f):
+// Heun's predictor-corrector on the first-order velocity-pressure system
+// (§4.2.1) with Algorithm 1 (V-dot = F grad U,
+// per element and node), Algorithm 2 (R = weighted divergence
+// of V, scattered to the global nodes), Algorithm 3 (point
+// source).  Acoustic coefficients B = -I, F = c_e^2 I, M = 1
+// (reading R2).  Product path; the oracle's orc_heun is the CPU definition.
+//
+// One Heun step, exactly rearranged (linearity of Algorithms 1 and 2):
+//   a   = R(V^n)                       (Algorithm 2 on the stored V)
+//   b   = K U^n                        (= -R(Vdot(U^n)): Alg. 2 o Alg. 1)
+//   Ud1 = (a + y(t_n)) / M
+//   U^{n+1} = U^n + (h/2)/M (2a - h b + y(t_n) + y(t_{n+1}))
+//   W^n     = U^n + (h/2) Ud1
+//   V^{n+1} = V^n + h Vdot(W^n)        (= V + h/2 (Vdot(U) + Vdot(U + h Ud1)))
+// The V update needs W^n at all nodes of an element, i.e. after the step's
+// node reduction, so it is LAGGED into the next step's element pass: kernel
+// mode LAG first finalises V^n = V^{n-1}+h Vdot(W^{n-1}) from the gathered W,
+// then runs the step.  Mode FIN only finalises V (before read-out).  One pass
+// over the mesh per Heun step, where the paper runs two RHS evaluations.
+//
+//  KH7 k_heun<NP,B,MODE>  persistent, warp-specialised like K7 (step.cu): TMA
+//                         bulk copies of the chunk's blocks + cp.async gathers of
+//                         shared-node U, W; per element (one thread): V lagged
+//                         update, r = Alg. 2 element contribution of V, k = K^e u;
+//                         (r, k) pairs reduced per node in CSR order, interior
+//                         nodes updated in place, shared nodes -> double2 slots
+//  KH8 k_heun_fix         shared nodes: slots summed in chunk order, same update
+#include <cuda_runtime.h>
+
+#include <map>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace sem {
+
+namespace {
+
+constexpr int kStagesH = 2;
+constexpr int kDH = 8;  // CSR entries per node loaded together
+
+__constant__ double h_Dr[kMaxNp][kMaxNp];  // h_Dr[p][q] = dN_q/dr at node p
+__constant__ double h_Ds[kMaxNp][kMaxNp];
+__constant__ double h_Srr[kMaxNp][kMaxNp];
+__constant__ double h_Sss[kMaxNp][kMaxNp];
+__constant__ double h_Srs[kMaxNp][kMaxNp];
+__constant__ double h_wK[kMaxNp];
+
+// Shared-memory layout of one stage (offsets 16-byte aligned).
+struct HeunLayout {
+    int lidx, lpos, lptr, shs, g, meta, u, w, size;
+    __host__ __device__ HeunLayout(int np, int B, int L, int Lp, int Ls) {
+        lidx = 0;
+        lpos = np * B * 2;
+        lptr = lpos + np * B * 2;
+        shs = lptr + Lp * 2;
+        g = shs + Ls * 4;
+        meta = g + 5 * B * 8;
+        u = meta + 32;
+        w = u + L * 8;
+        size = (w + L * 8 + 127) & ~127;
+    }
+};
+
+__device__ __forceinline__ double2 csr_sum2(const double2 *ebuf, const uint16_t *lp, int i) {
+    const int j0 = lp[i], j1 = lp[i + 1];
+    double2 part[kDH];
+#pragma unroll
+    for (int d = 0; d < kDH; d++) part[d] = (j0 + d < j1) ? ebuf[j0 + d] : make_double2(0.0, 0.0);
+    double2 y = part[0];
+#pragma unroll
+    for (int d = 1; d < kDH; d++) { y.x += part[d].x; y.y += part[d].y; }
+    for (int j = j0 + kDH; j < j1; j++) { const double2 e = ebuf[j]; y.x += e.x; y.y += e.y; }
+    return y;
+}
+
+__device__ __forceinline__ double src_term(const HeunParams &a, int64_t id, int64_t n) {
+    return (id == a.src) ? a.amp * ricker_dev((double)n * a.h, a.f0, a.t0) : 0.0;
+}
+
+// MODE 0: step with V^n stored (no lag); 1: step with V lagged by one W
+// update; 2: finalise V only.
+template <int NP, int B, int MODE>
+__global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
+    k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls) {
+    constexpr bool kLag = MODE >= 1, kStep = MODE <= 1, kFin = MODE == 2;
+    extern __shared__ __align__(128) unsigned char sm[];
+    const HeunLayout lay(NP, B, L, Lp, Ls);
+    double2 *ebuf = reinterpret_cast<double2 *>(sm + kStagesH * lay.size);  // [NP*B] (r, k) per entry
+    double *m_s = reinterpret_cast<double *>(ebuf + (kStep ? NP * B : 0));  // (h/2)/M window
+    uint64_t *full = reinterpret_cast<uint64_t *>(m_s + (kStep ? W : 0));
+    uint64_t *gath = full + kStagesH;
+    uint64_t *empty = gath + kStagesH;
+    uint64_t *wfull = empty + kStagesH;
+    uint64_t *wempty = wfull + 1;
+    const int t = threadIdx.x;
+    const int64_t nch = ch.nchunks;
+
+    if (t == 0) {
+        for (int s = 0; s < kStagesH; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&gath[s], 32);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(wfull, 1);
+        mbar_init(wempty, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (t >= B) {
+        // ===== producer warp =====
+        const int lane = t - B;
+        int k = 0;
+        for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+            const int s = k % kStagesH;
+            if (k >= kStagesH && lane == 0) mbar_wait(&empty[s], ((k / kStagesH) & 1) ^ 1);
+            __syncwarp();
+            unsigned char *st = sm + s * lay.size;
+            const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+            const int4 m1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
+            const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z, lp0 = m1.w;
+            if (lane == 0) {
+                reinterpret_cast<int4 *>(st + lay.meta)[0] = m0;
+                reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
+                const int nlp = (ni_al + nsh + 1 + 7) & ~7;
+                const int nsh4 = (nsh + 3) & ~3;
+                uint32_t bytes = NP * B * 2 + 5 * B * 8;
+                if (kStep) bytes += NP * B * 2 + nlp * 2 + nsh4 * 4 + (uint32_t)ni_al * 8;
+                if (kLag) bytes += (uint32_t)ni_al * 8;
+                mbar_arrive_expect_tx(&full[s], bytes);
+                const int64_t e0 = c * B;
+                tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
+                for (int g = 0; g < 5; g++) tma_load(st + lay.g + g * B * 8, a.geo[g] + e0, B * 8, &full[s]);
+                if (kStep) {
+                    tma_load(st + lay.lpos, ch.lpos + e0 * NP, NP * B * 2, &full[s]);
+                    tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
+                    if (nsh4 > 0) tma_load(st + lay.shs, ch.shl_slot + s0, nsh4 * 4, &full[s]);
+                    if (ni_al > 0) tma_load(st + lay.u, a.U + i0, ni_al * 8, &full[s]);
+                }
+                if (kLag && ni_al > 0) tma_load(st + lay.w, a.W + i0, ni_al * 8, &full[s]);
+            }
+            double *u_sh = reinterpret_cast<double *>(st + lay.u) + ni_al;
+            double *w_sh = reinterpret_cast<double *>(st + lay.w) + ni_al;
+            for (int j = lane; j < nsh; j += 32) {
+                const int64_t g = ch.N_int + ch.shl_node[s0 + j];
+                if (kStep) cp_async8(u_sh + j, a.U + g);
+                if (kLag) cp_async8(w_sh + j, a.W + g);
+            }
+            cp_async_arrive_noinc(&gath[s]);
+            if (kStep && lane == 0) {
+                if (k >= 1) mbar_wait(wempty, (k - 1) & 1);
+                mbar_arrive_expect_tx(wfull, (uint32_t)ni_al * 8);
+                if (ni_al > 0) tma_load(m_s, a.hM + i0, ni_al * 8, wfull);
+            }
+        }
+        return;
+    }
+
+    // ===== consumer warps =====
+    int k = 0;
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+        const int s = k % kStagesH;
+        // this element's V (layout [chunk][2 NP][B]): issued before the stage wait
+        double *vg = a.V + (c * 2 * NP) * B + t;
+        double v[2 * NP];
+#pragma unroll
+        for (int j = 0; j < 2 * NP; j++) v[j] = vg[j * B];
+        mbar_wait(&full[s], (k / kStagesH) & 1);
+        mbar_wait(&gath[s], (k / kStagesH) & 1);
+        const unsigned char *st = sm + s * lay.size;
+        const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
+        const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
+        const int i0 = m0.x, nint = m0.y, nsh = m0.w, ne = m1.y, ni_al = m1.z;
+        const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
+        const double *g_s = reinterpret_cast<const double *>(st + lay.g);
+        const double F00 = g_s[t], F01 = g_s[B + t], F10 = g_s[2 * B + t], F11 = g_s[3 * B + t];
+        const double sd = g_s[4 * B + t];
+
+        // (1) lagged V update: V^n = V^{n-1} + h Vdot(W^{n-1})  (Algorithm 1, E = 0)
+        if (kLag && t < ne) {
+            const double *w_s = reinterpret_cast<const double *>(st + lay.w);
+            double w[NP];
+#pragma unroll
+            for (int p = 0; p < NP; p++) w[p] = w_s[li_s[p * B + t]];
+            const double hF00 = a.h * F00, hF01 = a.h * F01, hF10 = a.h * F10, hF11 = a.h * F11;
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                double gr = 0.0, gs = 0.0;
+#pragma unroll
+                for (int q = 0; q < NP; q++) {
+                    gr = fma(h_Dr[p][q], w[q], gr);
+                    gs = fma(h_Ds[p][q], w[q], gs);
+                }
+                v[p] = fma(hF00, gr, fma(hF10, gs, v[p]));
+                v[NP + p] = fma(hF01, gr, fma(hF11, gs, v[NP + p]));
+            }
+#pragma unroll
+            for (int j = 0; j < 2 * NP; j++) vg[j * B] = v[j];
+        }
+
+        if (kStep) {
+            const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
+            const uint16_t *lp = reinterpret_cast<const uint16_t *>(st + lay.lptr);
+            const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
+            const double *u_s = reinterpret_cast<const double *>(st + lay.u);
+            if (t < ne) {
+                // (2) r = Algorithm 2 element term of V: with aux = detJ w_q V_q (B = -I),
+                //     r_p = sum_q Dr[q][p] ar_q + Ds[q][p] as_q,  (ar, as)_q = -J^-1 aux_q
+                //     (F = c^2 J^-1, sd = detJ / c^2, so detJ J^-1 = sd F)
+                double ar[NP], as[NP];
+#pragma unroll
+                for (int q = 0; q < NP; q++) {
+                    const double sw = -sd * h_wK[q];
+                    ar[q] = sw * fma(F00, v[q], F01 * v[NP + q]);
+                    as[q] = sw * fma(F10, v[q], F11 * v[NP + q]);
+                }
+                double r[NP];
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NP; q++) acc = fma(h_Dr[q][p], ar[q], fma(h_Ds[q][p], as[q], acc));
+                    r[p] = acc;
+                }
+                // (3) y = K^e u, K^e = Grr Srr + Gss Sss + Grs Srs, G = sd F F^T
+                //     (= c^2 detJ J^-1 J^-T, reading R5)
+                const double grr = sd * fma(F00, F00, F01 * F01);
+                const double gss = sd * fma(F10, F10, F11 * F11);
+                const double grs = sd * fma(F00, F10, F01 * F11);
+                double u[NP], y[NP];
+#pragma unroll
+                for (int p = 0; p < NP; p++) { u[p] = u_s[li_s[p * B + t]]; y[p] = 0.0; }
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+#pragma unroll
+                    for (int q = p; q < NP; q++) {
+                        const double kk = fma(grr, h_Srr[p][q], fma(gss, h_Sss[p][q], grs * h_Srs[p][q]));
+                        if (q == p) {
+                            y[p] = fma(kk, u[p], y[p]);
+                        } else {
+                            y[p] = fma(kk, u[q], y[p]);
+                            y[q] = fma(kk, u[p], y[q]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = make_double2(r[p], y[p]);
+            }
+            consumer_sync<B>();
+            mbar_wait(wfull, k & 1);
+            // (4) node-centric reduction in fixed CSR order + fused Heun update
+            const int nl = ni_al + nsh;
+            for (int i = t; i < nl; i += B) {
+                const double2 ab = csr_sum2(ebuf, lp, i);
+                if (i < nint) {
+                    const int64_t id = i0 + i;
+                    const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
+                    const double u0 = u_s[i], hm = m_s[i];
+                    a.W[id] = u0 + hm * (ab.x + yn);
+                    a.U[id] = u0 + hm * ((2.0 * ab.x - a.h * ab.y) + (yn + yn1));
+                } else if (i >= ni_al) {
+                    reinterpret_cast<double2 *>(a.slot)[shs[i - ni_al]] = ab;
+                }
+            }
+        }
+        consumer_sync<B>();
+        if (t == 0) {
+            mbar_arrive(&empty[s]);
+            if (kStep) mbar_arrive(wempty);
+        }
+    }
+}
+
+// ---- KH8: shared-node fix-up ------------------------------------------------------
+__global__ void k_heun_fix(const DevChunks ch, const HeunParams a) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= ch.N_sh - ch.N_if) return;
+    const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
+    const int64_t id = ch.N_int + s;
+    const double u0 = a.U[id], hm = a.hM[id];
+    const double2 *sl = reinterpret_cast<const double2 *>(a.slot);
+    double2 part[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) part[d] = (j0 + d < j1) ? sl[j0 + d] : make_double2(0.0, 0.0);
+    double2 ab = part[0];
+#pragma unroll
+    for (int d = 1; d < 4; d++) { ab.x += part[d].x; ab.y += part[d].y; }
+    for (int j = j0 + 4; j < j1; j++) { ab.x += sl[j].x; ab.y += sl[j].y; }
+    const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
+    a.W[id] = u0 + hm * (ab.x + yn);
+    a.U[id] = u0 + hm * ((2.0 * ab.x - a.h * ab.y) + (yn + yn1));
+}
+
+// Per element (new order, padded): F = c^2 J^-1 (F[jh][j] = c^2 (J^-1)_{jh j}),
+// sd = detJ / c^2, and detJ for the mass.  J columns are v1 - v0, v2 - v0.
+__global__ void k_geometry_heun(const double *__restrict__ vxy, const int32_t *__restrict__ tri,
+                                const int32_t *__restrict__ perm, const double *__restrict__ c_in, int64_t E,
+                                int64_t Epad, double *F00, double *F01, double *F10, double *F11, double *sd,
+                                double *__restrict__ detJ, int32_t *bad) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= Epad) return;
+    if (k >= E) { F00[k] = F01[k] = F10[k] = F11[k] = sd[k] = detJ[k] = 0.0; return; }
+    const int64_t e = perm[k];
+    const int32_t v0 = tri[3 * e], v1 = tri[3 * e + 1], v2 = tri[3 * e + 2];
+    const double j00 = vxy[2 * v1] - vxy[2 * v0], j01 = vxy[2 * v2] - vxy[2 * v0];
+    const double j10 = vxy[2 * v1 + 1] - vxy[2 * v0 + 1], j11 = vxy[2 * v2 + 1] - vxy[2 * v0 + 1];
+    const double det = j00 * j11 - j01 * j10;
+    const double c = c_in[e], c2 = c * c;
+    if (!(det > 0.0)) atomicMin(bad, (int32_t)e);
+    // J^-1 = [[j11, -j01], [-j10, j00]] / det, indexed [jh][j]
+    F00[k] = c2 * (j11 / det);
+    F01[k] = c2 * (-j01 / det);
+    F10[k] = c2 * (-j10 / det);
+    F11[k] = c2 * (j00 / det);
+    sd[k] = det / c2;
+    detJ[k] = det;
+}
+
+// V in the chunk layout [chunk][2 NP][B] (component j = k NP + p) <-> host layout
+// [E][NP][2] in INPUT element order (perm: new -> input).
+__global__ void k_v_out(const double *__restrict__ V, const int32_t *__restrict__ perm, int64_t E, int NP, int B,
+                        double *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= E * NP * 2) return;
+    const int64_t e = i / (2 * NP);
+    const int j = (int)(i % (2 * NP));  // host order: p * 2 + comp
+    const int p = j >> 1, comp = j & 1;
+    const int64_t c = e / B, t = e % B;
+    out[((int64_t)perm[e] * NP + p) * 2 + comp] = V[(c * 2 * NP + comp * NP + p) * B + t];
+}
+
+__global__ void k_v_in(const double *__restrict__ in, const int32_t *__restrict__ perm, int64_t E, int NP, int B,
+                       double *__restrict__ V) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= E * NP * 2) return;
+    const int64_t e = i / (2 * NP);
+    const int j = (int)(i % (2 * NP));
+    const int p = j >> 1, comp = j & 1;
+    const int64_t c = e / B, t = e % B;
+    V[(c * 2 * NP + comp * NP + p) * B + t] = in ? in[((int64_t)perm[e] * NP + p) * 2 + comp] : 0.0;
+}
+
+template <typename K>
+cudaError_t set_smem_h(K kernel, size_t bytes) {
+    static std::map<const void *, size_t> cur;
+    size_t &c = cur[(const void *)kernel];
+    if (bytes <= c) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c = bytes;
+    return e;
+}
+
+size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
+    const HeunLayout lay(np, B, L, Lp, Ls);
+    const bool step = mode <= 1;
+    return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (3 * kStagesH + 2) * 8;
+}
+
+using HFn = void (*)(const DevChunks, const HeunParams, int, int, int, int);
+template <int NP, int B>
+HFn heun_fn_b(int mode) {
+    return mode == 0 ? k_heun<NP, B, 0> : mode == 1 ? k_heun<NP, B, 1> : k_heun<NP, B, 2>;
+}
+HFn heun_fn(int np, int B, int mode) {
+    if (np == 6) return B == 128 ? heun_fn_b<6, 128>(mode) : heun_fn_b<6, 256>(mode);
+    return B == 128 ? heun_fn_b<10, 128>(mode) : heun_fn_b<10, 256>(mode);
+}
+
+inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1); }
+
+}  // namespace
+
+bool heun_supported(int np, int B) { return (np == 6 || np == 10) && (B == 128 || B == 256); }
+
+cudaError_t upload_heun_tables(const RefTables &T, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Dr, T.Dr, sizeof(T.Dr), 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Ds, T.Ds, sizeof(T.Ds), 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Srr, T.Srr, sizeof(T.Srr), 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Sss, T.Sss, sizeof(T.Sss), 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Srs, T.Srs, sizeof(T.Srs), 0, cudaMemcpyHostToDevice, s))) return e;
+    return cudaMemcpyToSymbolAsync(h_wK, T.wK, sizeof(T.wK), 0, cudaMemcpyHostToDevice, s);
+}
+
+cudaError_t launch_geometry_heun(const double *vxy, const int32_t *tri_or, const int32_t *perm, const double *c_in,
+                                 int64_t E, int64_t Epad, double *const geo[5], double *detJ, int32_t *bad,
+                                 cudaStream_t s) {
+    k_geometry_heun<<<nblk(Epad), 256, 0, s>>>(vxy, tri_or, perm, c_in, E, Epad, geo[0], geo[1], geo[2], geo[3],
+                                               geo[4], detJ, bad);
+    return cudaGetLastError();
+}
+
+int heun_grid(const DevChunks &ch, int mode) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, mode);
+    const HFn fn = heun_fn(ch.Np, ch.B, mode);
+    set_smem_h(fn, smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B + 32, smem);
+    if (occ < 1) occ = 1;
+    int64_t g = (int64_t)occ * nsm;
+    if (g > ch.nchunks) g = ch.nchunks;
+    return (int)g;
+}
+
+cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cudaStream_t s) {
+    if (ch.nchunks == 0) return cudaSuccess;
+    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, mode);
+    const HFn fn = heun_fn(ch.Np, ch.B, mode);
+    cudaError_t e = set_smem_h(fn, smem);
+    if (e != cudaSuccess) return e;
+    fn<<<heun_grid(ch, mode), ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_heun_fix(const DevChunks &ch, const HeunParams &p, cudaStream_t s) {
+    if (ch.N_sh - ch.N_if == 0) return cudaSuccess;
+    k_heun_fix<<<nblk(ch.N_sh - ch.N_if), 256, 0, s>>>(ch, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_v_out(const double *V, const int32_t *perm, int64_t E, int np, int B, double *out, cudaStream_t s) {
+    if (E == 0) return cudaSuccess;
+    k_v_out<<<nblk(E * np * 2), 256, 0, s>>>(V, perm, E, np, B, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_v_in(const double *in, const int32_t *perm, int64_t E, int np, int B, double *V, cudaStream_t s) {
+    if (E == 0) return cudaSuccess;
+    k_v_in<<<nblk(E * np * 2), 256, 0, s>>>(in, perm, E, np, B, V);
+    return cudaGetLastError();
+}
+
+}  // namespace sem

@@ -60,9 +60,10 @@ cudaError_t launch_geometry(const double *vxy, const int32_t *tri_or_in, const i
                             const double *c_in, int64_t E, int64_t Epad, double *Grr,
                             double *Gss, double *Grs, double *detJ, int32_t *bad,
                             cudaStream_t s);
-// Lumped mass, assembled with the chunk machinery; writes dt2M = dt^2 / Mbar
-// (0 in the alignment holes).  Uses `slot` as scratch.
-cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *slot,
+// Lumped mass, assembled with the chunk machinery; writes dt2M = numer / Mbar
+// (numer = dt^2 for the leapfrog, h/2 for Heun; 0 in the alignment holes).
+// Uses `slot` as scratch.
+cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer, double *slot,
                           double *dt2M, cudaStream_t s);
 
 struct StepParams {
@@ -88,6 +89,31 @@ cudaError_t launch_k8_if(const DevChunks &ch, const StepParams &p, const double 
                          const int32_t *sum_src, cudaStream_t s);
 cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_t *sum_start, const int32_t *sum_src,
                            double dt, double *dt2M, cudaStream_t s);
+// ------------------------------- heun.cu -----------------------------------
+// The paper's Heun predictor-corrector on (U, V) (NEXT-1).
+struct HeunParams {
+    const double *geo[5];  // per element (new order, padded): F00, F01, F10, F11 (F = c^2 J^-1), sd = detJ/c^2
+    const double *hM;      // (h/2) / M-bar per internal node
+    double *U;             // U^n in, U^{n+1} out (in place)
+    double *W;             // W^{n-1} in (lagged modes), W^n = U^n + (h/2) Udot1 out
+    double *V;             // [nchunks][2 Np][B] element velocities (component k*Np + p)
+    double *slot;          // double2 per slot: (R(V), K U) partials of shared nodes
+    int32_t src;
+    double amp, f0, t0, h;
+    int64_t n;             // step index of U
+};
+bool heun_supported(int np, int B);
+cudaError_t upload_heun_tables(const RefTables &T, cudaStream_t s);
+cudaError_t launch_geometry_heun(const double *vxy, const int32_t *tri_or, const int32_t *perm, const double *c_in,
+                                 int64_t E, int64_t Epad, double *const geo[5], double *detJ, int32_t *bad,
+                                 cudaStream_t s);
+// mode 0: step (V current), 1: step with the lagged V update, 2: V update only
+cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cudaStream_t s);
+cudaError_t launch_heun_fix(const DevChunks &ch, const HeunParams &p, cudaStream_t s);
+// V (chunk layout) <-> host layout [E][Np][2] in input element order; in == nullptr -> zeros
+cudaError_t launch_v_out(const double *V, const int32_t *perm, int64_t E, int np, int B, double *out, cudaStream_t s);
+cudaError_t launch_v_in(const double *in, const int32_t *perm, int64_t E, int np, int B, double *V, cudaStream_t s);
+
 // out[omap ? omap[i] : i] = in[imap ? imap[i] : i], i < n
 cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,
                                double *out, cudaStream_t s);

@@ -25,6 +25,7 @@
 
 #include <map>
 
+#include "dev_common.cuh"
 #include "kernels.h"
 
 namespace sem {
@@ -44,63 +45,6 @@ inline unsigned blocks_for(int64_t n, int threads = kThreads) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;
     return (unsigned)b;
-}
-
-__device__ __forceinline__ double ricker_dev(double t, double f0, double t0) {
-    const double tau = t - t0;
-    double a = 3.14159265358979323846 * f0 * tau;
-    a = a * a;
-    return (1.0 - 2.0 * a) * exp(-a);
-}
-
-// ---- PTX helpers: mbarrier + TMA bulk copy -----------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0,
-// both addresses 16-byte aligned).
-__device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-// 8-byte asynchronous global -> shared copy (LDGSTS) and the per-thread
-// mbarrier arrive that fires when all of this thread's cp.async have landed.
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-template <int B>
-__device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;" ::"r"(B) : "memory");
 }
 
 // Shared-memory layout of one pipeline stage (all offsets 16-byte aligned).
@@ -451,9 +395,9 @@ cudaError_t launch_geometry(const double *vxy, const int32_t *tri_or_in, const i
     return cudaGetLastError();
 }
 
-cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double dt, double *slot,
+cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer, double *slot,
                           double *dt2M, cudaStream_t s) {
-    const double dt2 = dt * dt;
+    const double dt2 = numer;
     cudaError_t e;
     if ((e = cudaMemsetAsync(dt2M, 0, sizeof(double) * (ch.N_tot + 2), s))) return e;
 #define MASS(NP_, B_) k_mass_chunk<NP_, B_><<<(unsigned)ch.nchunks, B_, 0, s>>>(ch, detJ, dt2, slot, dt2M)

@@ -250,3 +250,14 @@ def config(name: str, scale: int = 1, gpus: int = 1) -> Problem:
         c = layered_speed(nat, breaks, speeds)
         return _finish("C5", nat, 2, c, 10.0, 200, s)
     raise KeyError(name)
+
+
+# Reading R19: the Heun step amplifies a mode of frequency w
+# by (1 + (w h)^4 / 4)^(1/2) per step; every recipe dt sits below half the
+# leapfrog limit 2 / w_max (tests/test_inputs.py), so h = dt / 5 keeps
+# w_max h < 0.2 (growth < 2e-4 per step for the stiffest mode).
+HEUN_H_FRACTION = 0.2
+
+
+def heun_h(pb: Problem) -> float:
+    return pb.dt * HEUN_H_FRACTION

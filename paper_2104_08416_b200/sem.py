@@ -24,12 +24,14 @@ STATUS_NAMES = {0: "SEM_OK", 1: "SEM_E_ARG", 2: "SEM_E_STATE", 3: "SEM_E_MESH", 
 SEM_ORDER_INPUT, SEM_ORDER_HILBERT, SEM_ORDER_RANDOM = 0, 1, 2
 SEM_NODES_FIRST_TOUCH, SEM_NODES_CANONICAL = 0, 2
 SEM_NUMBERING_CANONICAL, SEM_NUMBERING_INTERNAL = 0, 1
+SEM_INTEGRATOR_LEAPFROG, SEM_INTEGRATOR_HEUN = 0, 1
 
 EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem_build_operators",
             "sem_step_n", "sem_read_field", "sem_write_state", "sem_set_step", "sem_sync",
             "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version",
             "sem_debug_chunk_stats", "sem_debug_partition", "sem_nccl_unique_id",
-            "sem_group_build_operators", "sem_group_step_n"]
+            "sem_group_build_operators", "sem_group_step_n", "sem_set_integrator", "sem_read_velocity",
+            "sem_write_velocity"]
 
 
 class SemError(RuntimeError):
@@ -49,7 +51,8 @@ class sem_info(C.Structure):
                 ("bytes_alg_per_step", C.c_double), ("prep_reorder_ms", C.c_double),
                 ("prep_build_ms", C.c_double), ("n_interface_nodes", C.c_int64),
                 ("n_neighbors", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
-                ("n_elements_global", C.c_int64), ("first_element", C.c_int64)]
+                ("n_elements_global", C.c_int64), ("first_element", C.c_int64),
+                ("integrator", C.c_int32), ("reserved0", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -90,6 +93,9 @@ def load(path: str = LIB_PATH):
         L.sem_nccl_unique_id.argtypes = [P]
         L.sem_group_build_operators.argtypes = [P, C.c_int, P, i64, dbl, dbl, dbl, dbl]
         L.sem_group_step_n.argtypes = [P, C.c_int, i64]
+        L.sem_set_integrator.argtypes = [P, C.c_int]
+        L.sem_read_velocity.argtypes = [P, P, C.POINTER(i64)]
+        L.sem_write_velocity.argtypes = [P, P]
         L.sem_version.argtypes = []
         L.sem_version.restype = C.c_char_p
         for n in EXPORTED:
@@ -190,6 +196,21 @@ class SemContext:
         a = None if u_curr is None else np.ascontiguousarray(u_curr, np.float64)
         b = None if u_prev is None else np.ascontiguousarray(u_prev, np.float64)
         self._check(self.L.sem_write_state(self.h, _ptr(a), _ptr(b), numbering))
+
+    def sem_set_integrator(self, integrator: int):
+        self._check(self.L.sem_set_integrator(self.h, int(integrator)))
+
+    def sem_read_velocity(self):
+        """Heun: V^n as [E, Np, 2] in input element order."""
+        info = self.sem_get_info()
+        out = np.empty((self.E, info["nodes_per_elem"], 2))
+        step = C.c_int64(0)
+        self._check(self.L.sem_read_velocity(self.h, _ptr(out), C.byref(step)))
+        return out, step.value
+
+    def sem_write_velocity(self, V):
+        v = None if V is None else np.ascontiguousarray(V, np.float64)
+        self._check(self.L.sem_write_velocity(self.h, _ptr(v)))
 
     def sem_set_step(self, step: int):
         self._check(self.L.sem_set_step(self.h, int(step)))
