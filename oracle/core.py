@@ -69,6 +69,14 @@ def lib():
             L.orc_heun.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P,
                                    i64, dbl, dbl, dbl, dbl, i64, i64, P, P]
             L.orc_heun.restype = C.c_int
+            L.orc_node_degree.argtypes = [P, i64, C.c_int, i64, P]
+            L.orc_node_degree.restype = C.c_int
+            L.orc_first_touch_degree.argtypes = [P, i64, C.c_int, i64, P, P]
+            L.orc_first_touch_degree.restype = C.c_int
+            L.orc_strategy_order.argtypes = [P, i64, C.c_int, i64, P, P, P]
+            L.orc_strategy_order.restype = C.c_int
+            L.orc_node_coords.argtypes = [P, P, P, i64, C.c_int, P, P]
+            L.orc_node_coords.restype = None
             L.orc_num_threads.argtypes = []
             L.orc_num_threads.restype = C.c_int
             _lib = L
@@ -151,6 +159,69 @@ def first_touch(mu: np.ndarray, N: int):
     if rc != 0:
         raise OracleError("first_touch rc=%d" % rc)
     return perm, out
+
+
+def node_degree(mu: np.ndarray, N: int) -> np.ndarray:
+    """deg[g] = distinct nodes sharing an element with g."""
+    mu = np.ascontiguousarray(mu, np.int32)
+    deg = np.empty(N, np.int32)
+    rc = lib().orc_node_degree(_p(mu), mu.shape[0], mu.shape[1], N, _p(deg))
+    if rc != 0:
+        raise OracleError("node_degree rc=%d" % rc)
+    return deg
+
+
+def first_touch_degree(mu: np.ndarray, N: int):
+    """PAPER.md:312-321 steps 1 and 2 -> (node_perm [N] new->old, mu_new)."""
+    mu = np.ascontiguousarray(mu, np.int32)
+    perm = np.empty(N, np.int32)
+    out = np.empty_like(mu)
+    rc = lib().orc_first_touch_degree(_p(mu), mu.shape[0], mu.shape[1], N, _p(perm), _p(out))
+    if rc != 0:
+        raise OracleError("first_touch_degree rc=%d" % rc)
+    return perm, out
+
+
+def strategy_order(mu_can: np.ndarray, N: int, key: np.ndarray):
+    """Conn./Dist. strategies (reading R20) on the canonical
+    connectivity (input element order) -> (elem_perm [E] new->input,
+    node_perm [N] new->canonical)."""
+    mu_can = np.ascontiguousarray(mu_can, np.int32)
+    key = np.ascontiguousarray(key, np.float64)
+    ep = np.empty(mu_can.shape[0], np.int32)
+    npm = np.empty(N, np.int32)
+    rc = lib().orc_strategy_order(_p(mu_can), mu_can.shape[0], mu_can.shape[1], N, _p(key), _p(ep), _p(npm))
+    if rc != 0:
+        raise OracleError("strategy_order rc=%d" % rc)
+    return ep, npm
+
+
+def node_coords(vxy: np.ndarray, tri_oriented: np.ndarray, mu_can: np.ndarray, P: int) -> np.ndarray:
+    """Canonical SEM node coordinates [N, 2] (reading R20)."""
+    vxy = np.ascontiguousarray(vxy, np.float64)
+    tri_oriented = np.ascontiguousarray(tri_oriented, np.int32)
+    mu_can = np.ascontiguousarray(mu_can, np.int32)
+    nodes = refelem.tables(P)["nodes"]
+    edge_t = np.ascontiguousarray([nodes[i, 0] for i in range(1, P)], np.float64)
+    N = int(mu_can.max()) + 1
+    xy = np.full((N, 2), np.nan)
+    lib().orc_node_coords(_p(vxy), _p(tri_oriented), _p(mu_can), mu_can.shape[0], P, _p(edge_t), _p(xy))
+    return xy
+
+
+def conn_key(mu_can: np.ndarray, N: int) -> np.ndarray:
+    """Node Connectivity key: the degree."""
+    return node_degree(mu_can, N).astype(np.float64)
+
+
+def dist_key(vxy: np.ndarray, tri_oriented: np.ndarray, mu_can: np.ndarray, P: int) -> np.ndarray:
+    """Node Distance key: squared distance to the lower-left corner of the
+    vertex bounding box (reading R20), dx*dx + dy*dy in fp64."""
+    xy = node_coords(vxy, tri_oriented, mu_can, P)
+    x0, y0 = vxy[:, 0].min(), vxy[:, 1].min()
+    dx = xy[:, 0] - x0
+    dy = xy[:, 1] - y0
+    return dx * dx + dy * dy
 
 
 def ricker(t: float, f0: float, t0: float) -> float:

@@ -554,6 +554,229 @@ int orc_heun(const int32_t *mu, int64_t ne, int Np, int64_t nn,
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* The paper's other memory-reordering strategies (NEXT-3 of SURVEY §8f).    */
+/* ------------------------------------------------------------------------ */
+
+/* Node graph: two SEM nodes are connected iff some element holds both
+ * ("the number of connections that the node has to other
+ * nodes").  CSR over nodes, each row the ascending list of distinct other
+ * nodes.  *ptr_out [nn+1] and *adj_out are malloc'ed here; caller frees. */
+static int build_node_graph(const int32_t *mu, int64_t ne, int Np, int64_t nn,
+                            int64_t **ptr_out, int32_t **adj_out) {
+    int64_t *inc_ptr = (int64_t *)calloc((size_t)nn + 1, sizeof(int64_t));
+    if (!inc_ptr) return ORC_E_OOM;
+    for (int64_t i = 0; i < ne * Np; i++) inc_ptr[mu[i] + 1]++;
+    for (int64_t g = 0; g < nn; g++) inc_ptr[g + 1] += inc_ptr[g];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * ((size_t)nn + 1));
+    int32_t *inc = (int32_t *)malloc(sizeof(int32_t) * ((size_t)(ne * Np) + 1));
+    int64_t *ptr = (int64_t *)calloc((size_t)nn + 1, sizeof(int64_t));
+    if (!fill || !inc || !ptr) { free(inc_ptr); free(fill); free(inc); free(ptr); return ORC_E_OOM; }
+    memcpy(fill, inc_ptr, sizeof(int64_t) * ((size_t)nn + 1));
+    for (int64_t e = 0; e < ne; e++)  /* elements touching node g, ascending e */
+        for (int p = 0; p < Np; p++) inc[fill[mu[e * Np + p]]++] = (int32_t)e;
+    /* pass 1: count distinct neighbours; pass 2: fill */
+    int32_t *buf = NULL;
+    size_t cap = 0;
+    int32_t *adj = NULL;
+    for (int pass = 0; pass < 2; pass++) {
+        for (int64_t g = 0; g < nn; g++) {
+            size_t k = (size_t)(inc_ptr[g + 1] - inc_ptr[g]) * (size_t)Np;
+            if (k > cap) {
+                free(buf);
+                cap = k;
+                buf = (int32_t *)malloc(sizeof(int32_t) * cap);
+                if (!buf) { free(inc_ptr); free(fill); free(inc); free(ptr); free(adj); return ORC_E_OOM; }
+            }
+            size_t m = 0;
+            for (int64_t j = inc_ptr[g]; j < inc_ptr[g + 1]; j++)
+                for (int q = 0; q < Np; q++) {
+                    int32_t o = mu[(int64_t)inc[j] * Np + q];
+                    if (o != g) buf[m++] = o;
+                }
+            qsort(buf, m, sizeof(int32_t), cmp_i32);
+            size_t u = 0;
+            for (size_t i = 0; i < m; i++)
+                if (i == 0 || buf[i] != buf[i - 1]) {
+                    if (pass == 1) adj[ptr[g] + (int64_t)u] = buf[i];
+                    u++;
+                }
+            if (pass == 0) ptr[g + 1] = (int64_t)u;
+        }
+        if (pass == 0) {
+            for (int64_t g = 0; g < nn; g++) ptr[g + 1] += ptr[g];
+            adj = (int32_t *)malloc(sizeof(int32_t) * ((size_t)ptr[nn] + 1));
+            if (!adj) { free(inc_ptr); free(fill); free(inc); free(ptr); free(buf); return ORC_E_OOM; }
+        }
+    }
+    free(buf); free(inc_ptr); free(fill); free(inc);
+    *ptr_out = ptr;
+    *adj_out = adj;
+    return ORC_OK;
+}
+
+/* deg[g] = number of distinct nodes sharing an element with g. */
+int orc_node_degree(const int32_t *mu, int64_t ne, int Np, int64_t nn, int32_t *deg) {
+    int64_t *ptr; int32_t *adj;
+    int rc = build_node_graph(mu, ne, Np, nn, &ptr, &adj);
+    if (rc) return rc;
+    for (int64_t g = 0; g < nn; g++) deg[g] = (int32_t)(ptr[g + 1] - ptr[g]);
+    free(ptr); free(adj);
+    return ORC_OK;
+}
+
+/* Node renumbering of PAPER.md:312-321, both steps (reading R12,
+ * SEM_NODES_FIRST_TOUCH_DEGREE): traverse the elements in their (new) order;
+ * N^(e) = the nodes of e not processed in an earlier element (step 1); sort
+ * N^(e) by ascending degree, ties by ascending old id (step 2); label in that
+ * order.  node_perm_out[new] = old, mu_out = relabelled mu. */
+int orc_first_touch_degree(const int32_t *mu, int64_t ne, int Np, int64_t nn,
+                           int32_t *node_perm_out, int32_t *mu_out) {
+    int32_t *deg = (int32_t *)malloc(sizeof(int32_t) * ((size_t)nn + 1));
+    int32_t *newid = (int32_t *)malloc(sizeof(int32_t) * ((size_t)nn + 1));
+    if (!deg || !newid) { free(deg); free(newid); return ORC_E_OOM; }
+    int rc = orc_node_degree(mu, ne, Np, nn, deg);
+    if (rc) { free(deg); free(newid); return rc; }
+    for (int64_t g = 0; g < nn; g++) newid[g] = -1;
+    int64_t next = 0;
+    for (int64_t e = 0; e < ne; e++) {
+        int32_t grp[64];
+        int ng = 0;
+        for (int p = 0; p < Np; p++) { /* step 1: N^(e), first occurrence only */
+            int32_t g = mu[e * Np + p];
+            int seen = newid[g] >= 0;
+            for (int i = 0; i < ng; i++) seen |= grp[i] == g;
+            if (!seen) grp[ng++] = g;
+        }
+        for (int i = 1; i < ng; i++) { /* step 2: insertion sort by (degree, old id) */
+            int32_t x = grp[i];
+            int j = i - 1;
+            while (j >= 0 && (deg[grp[j]] > deg[x] || (deg[grp[j]] == deg[x] && grp[j] > x))) {
+                grp[j + 1] = grp[j];
+                j--;
+            }
+            grp[j + 1] = x;
+        }
+        for (int i = 0; i < ng; i++) { newid[grp[i]] = (int32_t)next; node_perm_out[next] = grp[i]; next++; }
+    }
+    for (int64_t i = 0; i < ne * Np; i++) mu_out[i] = newid[mu[i]];
+    free(deg); free(newid);
+    return next == nn ? ORC_OK : ORC_E_MESH;
+}
+
+/* Node Connectivity / Node Distance strategies, reading
+ * R20: a Cuthill-McKee traversal of the node graph.  Start at the node with
+ * the smallest key; dequeue nodes in order and append each one's unvisited
+ * neighbours by ascending key (ties: ascending node id), marking them
+ * visited; if the queue empties first (disconnected mesh), restart at the
+ * smallest-key unvisited node.  key = degree (Conn.) or the squared distance
+ * to the reference point (Dist.), passed in by the caller.  The node list is
+ * the visit order (node_perm_out[new] = old).  Elements: at each node in
+ * visit order, the elements holding it, ascending id, each appended once
+ * (elem_perm_out[new] = input element). */
+static const double *g_key;
+static int cmp_node_key(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    if (g_key[x] < g_key[y]) return -1;
+    if (g_key[x] > g_key[y]) return 1;
+    return (x > y) - (x < y);
+}
+
+int orc_strategy_order(const int32_t *mu, int64_t ne, int Np, int64_t nn, const double *key,
+                       int32_t *elem_perm_out, int32_t *node_perm_out) {
+    int64_t *ptr; int32_t *adj;
+    int rc = build_node_graph(mu, ne, Np, nn, &ptr, &adj);
+    if (rc) return rc;
+    uint8_t *vis = (uint8_t *)calloc((size_t)nn + 1, 1);
+    int32_t *nb = (int32_t *)malloc(sizeof(int32_t) * 4096);
+    if (!vis || !nb) { free(ptr); free(adj); free(vis); free(nb); return ORC_E_OOM; }
+    g_key = key;
+    int64_t head = 0, tail = 0;
+    while (tail < nn) {
+        int64_t s = -1; /* smallest-key unvisited node */
+        for (int64_t g = 0; g < nn; g++)
+            if (!vis[g] && (s < 0 || key[g] < key[s])) s = g;
+        vis[s] = 1;
+        node_perm_out[tail++] = (int32_t)s;
+        while (head < tail) {
+            int32_t u = node_perm_out[head++];
+            int m = 0;
+            for (int64_t j = ptr[u]; j < ptr[u + 1]; j++)
+                if (!vis[adj[j]] && m < 4096) nb[m++] = adj[j];
+            if (ptr[u + 1] - ptr[u] > 4096) { free(ptr); free(adj); free(vis); free(nb); return ORC_E_MESH; }
+            qsort(nb, (size_t)m, sizeof(int32_t), cmp_node_key);
+            for (int i = 0; i < m; i++) { vis[nb[i]] = 1; node_perm_out[tail++] = nb[i]; }
+        }
+    }
+    /* element list: node -> elements incidence, ascending element id */
+    int64_t *inc_ptr = (int64_t *)calloc((size_t)nn + 1, sizeof(int64_t));
+    int32_t *inc = (int32_t *)malloc(sizeof(int32_t) * ((size_t)(ne * Np) + 1));
+    uint8_t *done = (uint8_t *)calloc((size_t)ne + 1, 1);
+    if (!inc_ptr || !inc || !done) {
+        free(ptr); free(adj); free(vis); free(nb); free(inc_ptr); free(inc); free(done);
+        return ORC_E_OOM;
+    }
+    for (int64_t i = 0; i < ne * Np; i++) inc_ptr[mu[i] + 1]++;
+    for (int64_t g = 0; g < nn; g++) inc_ptr[g + 1] += inc_ptr[g];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * ((size_t)nn + 1));
+    if (!fill) { free(ptr); free(adj); free(vis); free(nb); free(inc_ptr); free(inc); free(done); return ORC_E_OOM; }
+    memcpy(fill, inc_ptr, sizeof(int64_t) * ((size_t)nn + 1));
+    for (int64_t e = 0; e < ne; e++)
+        for (int p = 0; p < Np; p++) {
+            int32_t g = mu[e * Np + p];
+            /* an element holding g twice is listed once */
+            if (fill[g] == inc_ptr[g] || inc[fill[g] - 1] != (int32_t)e) inc[fill[g]++] = (int32_t)e;
+        }
+    int64_t k = 0;
+    for (int64_t i = 0; i < nn; i++) {
+        int32_t g = node_perm_out[i];
+        for (int64_t j = inc_ptr[g]; j < fill[g]; j++)
+            if (!done[inc[j]]) { done[inc[j]] = 1; elem_perm_out[k++] = inc[j]; }
+    }
+    free(ptr); free(adj); free(vis); free(nb); free(inc_ptr); free(inc); free(done); free(fill);
+    return k == ne ? ORC_OK : ORC_E_MESH;
+}
+
+/* Canonical coordinates of every SEM node (for the Node Distance key,
+ * reading R20): vertex nodes = the vertex; edge nodes = a + t_i (b - a) with a
+ * the lower-id end of the edge and t_i the reference position of the i-th
+ * node from that end (edge_t[i], i = 0..P-2); the P3 interior node = the
+ * centroid ((v0 + v1) + v2) / 3 of the oriented triangle.  No FMA
+ * (-ffp-contract=off).  mu is the canonical connectivity (input order). */
+void orc_node_coords(const double *vxy, const int32_t *tri, const int32_t *mu, int64_t ne, int P,
+                     const double *edge_t, double *xy) {
+    int Np = (P + 1) * (P + 2) / 2;
+    for (int64_t e = 0; e < ne; e++) {
+        int32_t v[3] = {tri[3 * e], tri[3 * e + 1], tri[3 * e + 2]};
+        /* lattice order (R3): local node (i, j), row j outer; edges v0v1 (j = 0),
+         * v0v2 (i = 0), v1v2 (i + j = P) */
+        int p = 0;
+        for (int j = 0; j <= P; j++)
+            for (int i = 0; i <= P - j; i++, p++) {
+                int32_t g = mu[e * Np + p];
+                double x, y;
+                if ((i == 0 && j == 0) || (i == P && j == 0) || (i == 0 && j == P)) {
+                    int32_t w = (j == P) ? v[2] : (i == P ? v[1] : v[0]);
+                    x = vxy[2 * w]; y = vxy[2 * w + 1];
+                } else if (j == 0 || i == 0 || i + j == P) {
+                    int32_t a, b;
+                    int m; /* position from a along a -> b, 1..P-1 */
+                    if (j == 0) { a = v[0]; b = v[1]; m = i; }
+                    else if (i == 0) { a = v[0]; b = v[2]; m = j; }
+                    else { a = v[1]; b = v[2]; m = j; }
+                    if (a > b) { int32_t t = a; a = b; b = t; m = P - m; }
+                    double t = edge_t[m - 1];
+                    x = vxy[2 * a] + t * (vxy[2 * b] - vxy[2 * a]);
+                    y = vxy[2 * a + 1] + t * (vxy[2 * b + 1] - vxy[2 * a + 1]);
+                } else {
+                    x = ((vxy[2 * v[0]] + vxy[2 * v[1]]) + vxy[2 * v[2]]) / 3.0;
+                    y = ((vxy[2 * v[0] + 1] + vxy[2 * v[1] + 1]) + vxy[2 * v[2] + 1]) / 3.0;
+                }
+                xy[2 * g] = x; xy[2 * g + 1] = y;
+            }
+    }
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
