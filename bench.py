@@ -262,6 +262,11 @@ def orderings(ctx, pb, args, S):
         ("hilbert_canonical_nodes", pb.mesh, pb.c, S.SEM_ORDER_HILBERT, S.SEM_NODES_CANONICAL),
         ("natural", pb.natural, pb.c_natural, S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
         ("random", pb.mesh, pb.c, S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
+        # the paper's other strategies (reading R20) and the
+        # degree-sorted node renumbering (reading R12)
+        ("conn", pb.mesh, pb.c, S.SEM_ORDER_CONN, S.SEM_NODES_VISIT),
+        ("dist", pb.mesh, pb.c, S.SEM_ORDER_DIST, S.SEM_NODES_VISIT),
+        ("hilbert_degree_sorted_nodes", pb.mesh, pb.c, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH_DEGREE),
     ]
     stream = torch.cuda.current_stream()
     assert stream.cuda_stream != 0
@@ -286,7 +291,8 @@ def orderings(ctx, pb, args, S):
                      "k7_ms": kt["k7_ms"] / max(kt["k7_launches"], 1),
                      "k8_ms": kt["k8_ms"] / max(kt["k8_launches"], 1),
                      "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
-                     "max_chunk_nodes": info["max_chunk_nodes"], "steps": K}
+                     "max_chunk_nodes": info["max_chunk_nodes"], "steps": K,
+                     "prep_reorder_ms": info["prep_reorder_ms"]}
     return res
 
 

@@ -50,13 +50,21 @@ typedef enum {
 /* Element orderings (§6.1).  INPUT = the paper's "None"
  * (file order); HILBERT = §4.3 steps 1-4; RANDOM = stable
  * sort of element ids by splitmix64(seed ^ id) (reading R16). */
-enum { SEM_ORDER_INPUT = 0, SEM_ORDER_HILBERT = 1, SEM_ORDER_RANDOM = 2 };
+enum { SEM_ORDER_INPUT = 0, SEM_ORDER_HILBERT = 1, SEM_ORDER_RANDOM = 2,
+       /* the paper's other strategies (reading R20):
+        * Cuthill-McKee traversal of the SEM node graph from the node with the
+        * fewest connections (CONN) or nearest the lower-left corner (DIST); the
+        * element list follows the visited nodes */
+       SEM_ORDER_CONN = 3, SEM_ORDER_DIST = 4 };
 
 /* Node numberings.  FIRST_TOUCH = PAPER.md:316 step 1 (each node gets the next
- * label the first time an element in the new order touches it); CANONICAL =
- * the input numbering of DESIGN.md reading R13 (vertex ids, then edge nodes,
- * then interior nodes). */
-enum { SEM_NODES_FIRST_TOUCH = 0, SEM_NODES_CANONICAL = 2 };
+ * label the first time an element in the new order touches it);
+ * FIRST_TOUCH_DEGREE = PAPER.md:316-318 steps 1 and 2 (each element's newly
+ * touched nodes sorted by ascending degree, ties by canonical id; reading
+ * R12); CANONICAL = the input numbering of DESIGN.md reading R13 (vertex ids,
+ * then edge nodes, then interior nodes); VISIT = the node list of the CONN /
+ * DIST traversal (only with those element orders). */
+enum { SEM_NODES_FIRST_TOUCH = 0, SEM_NODES_FIRST_TOUCH_DEGREE = 1, SEM_NODES_CANONICAL = 2, SEM_NODES_VISIT = 3 };
 
 /* Numbering of node arrays crossing the ABI (read_field / write_state).
  * CANONICAL = reading R13 input numbering; INTERNAL = the reordered labels
@@ -127,8 +135,10 @@ const char *sem_last_error(const sem_ctx *ctx);
  *  n_nodes_out          N, the number of global SEM nodes.
  *  grid_wh_out     [2]  (w_b, h_b) for HILBERT, else (0, 0).
  *
- * Errors: SEM_E_UNSUPPORTED (degree, ordering), SEM_E_MESH ("element e has zero
- * area", "vertex v is not used by any element"), SEM_E_ARG, SEM_E_CUDA, SEM_E_OOM.
+ * Errors: SEM_E_UNSUPPORTED (degree, ordering, VISIT without CONN/DIST),
+ * SEM_E_MESH ("element e has zero area", "vertex v is not used by any
+ * element", a node whose elements hold > 384 entries), SEM_E_ARG, SEM_E_CUDA,
+ * SEM_E_OOM.
  * Resets any operators/state of an earlier mesh.
  */
 sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vertices,

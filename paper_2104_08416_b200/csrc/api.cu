@@ -137,6 +137,7 @@ struct sem_ctx {
     double t7 = 0, t8 = 0;
     int64_t n7 = 0, n8 = 0;
     double prep_reorder_ms = 0, prep_build_ms = 0;
+    int64_t strategy_levels = 0;  // BFS levels of the last Conn./Dist. ordering
 };
 
 namespace {
@@ -624,10 +625,13 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
     ST(check_usable(ctx));
     if (degree != 2 && degree != 3)
         return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) + " (2 or 3)");
-    if (elem_order < 0 || elem_order > 2)
+    if (elem_order < 0 || elem_order > SEM_ORDER_DIST)
         return fail(ctx, SEM_E_UNSUPPORTED, "unknown element ordering " + std::to_string(elem_order));
-    if (node_order != SEM_NODES_FIRST_TOUCH && node_order != SEM_NODES_CANONICAL)
+    if (node_order < SEM_NODES_FIRST_TOUCH || node_order > SEM_NODES_VISIT)
         return fail(ctx, SEM_E_UNSUPPORTED, "unknown node ordering " + std::to_string(node_order));
+    const bool strategy = elem_order == SEM_ORDER_CONN || elem_order == SEM_ORDER_DIST;
+    if (node_order == SEM_NODES_VISIT && !strategy)
+        return fail(ctx, SEM_E_UNSUPPORTED, "SEM_NODES_VISIT needs SEM_ORDER_CONN or SEM_ORDER_DIST");
     if (!vxy_host || !tri_host || n_vertices < 3 || n_elements < 1)
         return fail(ctx, SEM_E_ARG, "empty or missing mesh arrays");
     const int Np = (degree + 1) * (degree + 2) / 2;
@@ -667,6 +671,30 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has zero area");
         tr.mark(s, "H2D + orientation");
 
+        // ---- canonical SEM nodes (reading R13) ----
+        int32_t *d_mu_can = nullptr, *d_node_perm = nullptr;
+        CK(dalloc(tmp, &d_mu_can, E * Np));
+        int64_t nedges = 0, nunused = 0;
+        int32_t first_unused = 0;
+        CK(canonical_nodes(ctx->d_tri_or, nv, E, degree, d_mu_can, &nedges, &nunused, &first_unused, s));
+        if (nunused)
+            return fail(ctx, SEM_E_MESH, "vertex " + std::to_string(first_unused) + " is not used by any element");
+        const int nI = (degree - 1) * (degree - 2) / 2;
+        const int64_t N = nv + nedges * (degree - 1) + E * nI;
+        if (N >= INT_MAX) return fail(ctx, SEM_E_ARG, "too many nodes for 32-bit indices");
+        ctx->N_glob = N;
+        CK(dalloc(tmp, &d_node_perm, N));
+        tr.mark(s, "canonical nodes");
+        // node graph: degrees for FIRST_TOUCH_DEGREE and the Conn. key, adjacency for Conn./Dist.
+        DevGraph graph;
+        struct GraphGuard { DevGraph &g; cudaStream_t s; ~GraphGuard() { free_node_graph(g, s); } } gguard{graph, s};
+        if (strategy || node_order == SEM_NODES_FIRST_TOUCH_DEGREE) {
+            int bad_graph = 0;
+            CK(build_node_graph(d_mu_can, E, Np, N, strategy, graph, &bad_graph, s));
+            if (bad_graph) return fail(ctx, SEM_E_MESH, "a node's elements hold more than 384 node entries");
+            tr.mark(s, "node graph");
+        }
+
         // ---- element order (list L) ----
         CK(dalloc(ctx->mesh_allocs, &ctx->d_perm, E));
         int32_t *d_ids = nullptr;
@@ -705,43 +733,56 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             CK(sort_pairs_u32(d_keys, d_ids, d_keys2, ctx->d_perm, E, bits, s));
             if (hilbert_key_out)
                 CK(cudaMemcpyAsync(hilbert_key_out, d_keys, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, s));
-        } else {
+        } else if (elem_order == SEM_ORDER_RANDOM) {
             uint64_t *d_k = nullptr, *d_k2 = nullptr;
             CK(dalloc(tmp, &d_k, E));
             CK(dalloc(tmp, &d_k2, E));
             CK(launch_random_keys(E, seed, d_k, s));
             CK(sort_pairs_u64(d_k, d_ids, d_k2, ctx->d_perm, E, 64, s));
             if (hilbert_key_out) std::memset(hilbert_key_out, 0, sizeof(uint32_t) * E);
+        } else {  // Conn. / Dist. (reading R20)
+            double x0 = 0.0, y0 = 0.0;
+            if (elem_order == SEM_ORDER_DIST) {
+                double *d_bb = nullptr;
+                CK(dalloc(tmp, &d_bb, 4));
+                CK(launch_bbox(ctx->d_vxy, nv, d_bb, s));
+                double bb[4];
+                CK(cudaMemcpyAsync(bb, d_bb, sizeof(bb), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                x0 = bb[0];
+                y0 = bb[1];
+            }
+            double edge_t[4] = {0, 0, 0, 0};
+            for (int i = 1; i < degree; i++) edge_t[i - 1] = ctx->T.node[i][0];  // lattice row j = 0
+            int64_t levels = 0;
+            CK(strategy_order(d_mu_can, ctx->d_vxy, ctx->d_tri_or, E, degree, N,
+                              elem_order == SEM_ORDER_CONN ? 0 : 1, graph, edge_t, x0, y0, ctx->d_perm,
+                              d_node_perm, &levels, s));
+            ctx->strategy_levels = levels;
+            if (hilbert_key_out) std::memset(hilbert_key_out, 0, sizeof(uint32_t) * E);
         }
 
-        tr.mark(s, "SFC keys + sort");
-        // ---- canonical SEM nodes, relabel ----
-        int32_t *d_mu_can = nullptr, *d_mu_new = nullptr, *d_mu_ft = nullptr, *d_node_perm = nullptr;
-        CK(dalloc(tmp, &d_mu_can, E * Np));
-        int64_t nedges = 0, nunused = 0;
-        int32_t first_unused = 0;
-        CK(canonical_nodes(ctx->d_tri_or, nv, E, degree, d_mu_can, &nedges, &nunused, &first_unused, s));
-        if (nunused)
-            return fail(ctx, SEM_E_MESH, "vertex " + std::to_string(first_unused) + " is not used by any element");
-        const int nI = (degree - 1) * (degree - 2) / 2;
-        const int64_t N = nv + nedges * (degree - 1) + E * nI;
-        if (N >= INT_MAX) return fail(ctx, SEM_E_ARG, "too many nodes for 32-bit indices");
-        ctx->N_glob = N;
+        tr.mark(s, "element order");
+        // ---- relabel ----
+        int32_t *d_mu_new = nullptr, *d_mu_ft = nullptr;
         CK(dalloc(tmp, &d_mu_new, E * Np));
         CK(launch_permute_rows(d_mu_can, ctx->d_perm, E, Np, d_mu_new, s));
-        CK(dalloc(tmp, &d_node_perm, N));
-        if (node_order == SEM_NODES_FIRST_TOUCH) {
+        if (node_order == SEM_NODES_FIRST_TOUCH || node_order == SEM_NODES_FIRST_TOUCH_DEGREE) {
             CK(dalloc(tmp, &d_mu_ft, E * Np));
             int64_t nl = 0;
-            CK(first_touch(d_mu_new, E, Np, N, d_node_perm, d_mu_ft, &nl, s));
+            CK(first_touch(d_mu_new, E, Np, N, d_node_perm, d_mu_ft, &nl, s,
+                           node_order == SEM_NODES_FIRST_TOUCH_DEGREE ? graph.deg : nullptr));
             if (nl != N) return fail(ctx, SEM_E_MESH, "first-touch labelled " + std::to_string(nl) +
                                                           " of " + std::to_string(N) + " nodes");
+        } else if (node_order == SEM_NODES_VISIT) {  // the strategy's node list (d_node_perm = visit order)
+            CK(dalloc(tmp, &d_mu_ft, E * Np));
+            CK(relabel_from_perm(d_mu_new, E * Np, d_node_perm, N, d_mu_ft, s));
         } else {
             CK(launch_iota(d_node_perm, N, s));
             d_mu_ft = d_mu_new;
         }
 
-        tr.mark(s, "canonical nodes + first touch");
+        tr.mark(s, "node numbering");
         // ---- host outputs ----
         std::vector<int32_t> node_perm(N), mu_h((size_t)E * Np);
         CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));

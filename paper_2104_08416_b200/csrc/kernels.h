@@ -36,8 +36,36 @@ cudaError_t launch_permute_rows(const int32_t *src, const int32_t *perm, int64_t
                                 int32_t *dst, cudaStream_t s);
 // K5: first-touch renumbering.  node_perm[new] = old;
 // mu_out = relabelled mu.  Returns number of labels via host ptr.
+// deg != nullptr: PAPER.md:318 step 2 as well (each element's group sorted by
+// (degree, old id); reading R12, SEM_NODES_FIRST_TOUCH_DEGREE).
 cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t *node_perm,
-                        int32_t *mu_out, int64_t *n_labels, cudaStream_t s);
+                        int32_t *mu_out, int64_t *n_labels, cudaStream_t s, const int32_t *deg = nullptr);
+
+// Node graph (nodes connected iff they share an element): degree [N] and,
+// with want_adj, the CSR of ascending distinct neighbours.  Device buffers
+// come from cudaMallocAsync; release with free_node_graph.  *bad = 1 if a
+// node's elements hold more than 384 entries.
+struct DevGraph {
+    int32_t *deg = nullptr;
+    int64_t *aptr = nullptr;
+    int32_t *adj = nullptr;
+    int64_t nadj = 0;
+};
+cudaError_t build_node_graph(const int32_t *mu, int64_t E, int Np, int64_t N, bool want_adj, DevGraph &g,
+                             int *bad, cudaStream_t s);
+void free_node_graph(DevGraph &g, cudaStream_t s);
+// Conn. (strategy 0, key = degree) / Dist. (strategy 1, key = squared distance
+// to (x0, y0)) traversal of reading R20 on the canonical connectivity mu_can
+// (input element order): order [N] = visit order (new -> canonical),
+// elem_perm [E] = element list (new -> input).  edge_t [P-1]: reference edge
+// node positions.  Level-synchronous: parent = smallest frontier position,
+// each level sorted by (parent, key rank) = the sequential queue order.
+cudaError_t strategy_order(const int32_t *mu_can, const double *vxy, const int32_t *tri_or, int64_t E, int P,
+                           int64_t N, int strategy, const DevGraph &g, const double *edge_t, double x0, double y0,
+                           int32_t *elem_perm, int32_t *order, int64_t *n_levels, cudaStream_t s);
+// label_of[node_perm[i]] = i, then mu_out = label_of[mu]
+cudaError_t relabel_from_perm(const int32_t *mu, int64_t n, const int32_t *node_perm, int64_t N, int32_t *mu_out,
+                              cudaStream_t s);
 
 // ------------------------------- step.cu -----------------------------------
 struct DevChunks {  // device view of ChunkMeta

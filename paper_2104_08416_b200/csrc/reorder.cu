@@ -269,6 +269,190 @@ __global__ void k_relabel(const int32_t *__restrict__ mu, const int32_t *__restr
     if (i < n) out[i] = label_of[mu[i]];
 }
 
+// ---- node graph, degrees ---------------------------------------
+constexpr int kMaxCand = 384;  // candidate neighbour entries of one node (valence x Np)
+
+__global__ void k_count_nodes(const int32_t *__restrict__ mu, int64_t n, int32_t *cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[mu[i]], 1);
+}
+
+__global__ void k_incidence(const int32_t *__restrict__ mu, int64_t n, const int32_t *__restrict__ ptr,
+                            int32_t *fill, int32_t *inc) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) inc[ptr[mu[i]] + atomicAdd(&fill[mu[i]], 1)] = (int32_t)i;  // entry index (order fixed later)
+}
+
+// Distinct other nodes of the elements holding g: count (adj == nullptr) or
+// write them ascending at adj + aptr[g].  *bad = 1 if a node has more than
+// kMaxCand candidate entries.
+__global__ void k_node_nbrs(const int32_t *__restrict__ mu, int Np, const int32_t *__restrict__ iptr,
+                            const int32_t *__restrict__ inc, int64_t N, int32_t *deg,
+                            const int64_t *__restrict__ aptr, int32_t *__restrict__ adj, int32_t *bad) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    int32_t c[kMaxCand];
+    int m = 0;
+    for (int j = iptr[g]; j < iptr[g + 1]; j++) {
+        const int64_t e = inc[j] / Np;
+        for (int q = 0; q < Np; q++) {
+            const int32_t o = mu[e * Np + q];
+            if (o == (int32_t)g) continue;
+            int k = m - 1;  // insertion into the ascending unique list
+            while (k >= 0 && c[k] > o) k--;
+            if (k >= 0 && c[k] == o) continue;
+            if (m == kMaxCand) { *bad = 1; return; }
+            for (int r = m; r > k + 1; r--) c[r] = c[r - 1];
+            c[k + 1] = o;
+            m++;
+        }
+    }
+    if (adj) {
+        for (int k = 0; k < m; k++) adj[aptr[g] + k] = c[k];
+    } else {
+        deg[g] = m;
+    }
+}
+
+// ---- degree-sorted first-touch groups (PAPER.md:318 step 2) ----------------------
+// Element e's newly touched nodes hold the labels [excl[e Np], excl[(e+1) Np]);
+// sort them by (degree, old id).
+__global__ void k_group_sort(const int32_t *__restrict__ excl, int64_t E, int Np, const int32_t *__restrict__ deg,
+                             int32_t *node_perm) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int32_t a = excl[e * Np], b = excl[(e + 1) * Np];
+    int32_t v[16];
+    const int n = b - a;
+    for (int i = 0; i < n; i++) v[i] = node_perm[a + i];
+    for (int i = 1; i < n; i++) {
+        const int32_t x = v[i];
+        int j = i - 1;
+        while (j >= 0 && (deg[v[j]] > deg[x] || (deg[v[j]] == deg[x] && v[j] > x))) { v[j + 1] = v[j]; j--; }
+        v[j + 1] = x;
+    }
+    for (int i = 0; i < n; i++) node_perm[a + i] = v[i];
+}
+
+__global__ void k_label_from_perm(const int32_t *__restrict__ node_perm, int64_t n, int32_t *label_of) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) label_of[node_perm[i]] = (int32_t)i;
+}
+
+// ---- Conn. / Dist. strategies (reading R20) -------------------
+__global__ void k_key_degree(const int32_t *__restrict__ deg, int64_t N, uint64_t *key) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g < N) key[g] = (uint64_t)(uint32_t)deg[g];
+}
+
+// Squared distance of every node to (x0, y0), from its canonical coordinates:
+// vertices exact; edge node m (1..P-1) from the lower-id end a: a + t_m (b - a);
+// P3 interior node: ((v0 + v1) + v2) / 3.  Explicit round-to-nearest, no FMA.
+// A node written by several elements gets identical bits from each.
+__constant__ double c_edge_t[4];
+__global__ void k_key_dist(const double *__restrict__ vxy, const int32_t *__restrict__ tri,
+                           const int32_t *__restrict__ mu, int64_t E, int P, double x0, double y0,
+                           uint64_t *key) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int Np = (P + 1) * (P + 2) / 2;
+    const int32_t v[3] = {tri[3 * e], tri[3 * e + 1], tri[3 * e + 2]};
+    int p = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, p++) {
+            double x, y;
+            if ((i == 0 && j == 0) || (i == P && j == 0) || (i == 0 && j == P)) {
+                const int32_t w = (j == P) ? v[2] : (i == P ? v[1] : v[0]);
+                x = vxy[2 * w];
+                y = vxy[2 * w + 1];
+            } else if (j == 0 || i == 0 || i + j == P) {
+                int32_t a, b;
+                int m;
+                if (j == 0) { a = v[0]; b = v[1]; m = i; }
+                else if (i == 0) { a = v[0]; b = v[2]; m = j; }
+                else { a = v[1]; b = v[2]; m = j; }
+                if (a > b) { const int32_t t = a; a = b; b = t; m = P - m; }
+                const double t = c_edge_t[m - 1];
+                x = __dadd_rn(vxy[2 * a], __dmul_rn(t, __dsub_rn(vxy[2 * b], vxy[2 * a])));
+                y = __dadd_rn(vxy[2 * a + 1], __dmul_rn(t, __dsub_rn(vxy[2 * b + 1], vxy[2 * a + 1])));
+            } else {
+                x = __ddiv_rn(__dadd_rn(__dadd_rn(vxy[2 * v[0]], vxy[2 * v[1]]), vxy[2 * v[2]]), 3.0);
+                y = __ddiv_rn(__dadd_rn(__dadd_rn(vxy[2 * v[0] + 1], vxy[2 * v[1] + 1]), vxy[2 * v[2] + 1]), 3.0);
+            }
+            const double dx = __dsub_rn(x, x0), dy = __dsub_rn(y, y0);
+            const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+            key[mu[e * Np + p]] = (uint64_t)__double_as_longlong(d2);  // d2 >= +0: bits are monotone
+        }
+}
+
+__global__ void k_scatter_rank(const int32_t *__restrict__ sorted_ids, int64_t N, int32_t *rank) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) rank[sorted_ids[i]] = (int32_t)i;
+}
+
+// Smallest-rank unvisited node.
+__global__ void k_min_unvisited(const int32_t *__restrict__ pos, const int32_t *__restrict__ rank, int64_t N,
+                                int32_t *best) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g < N && pos[g] < 0) atomicMin(best, rank[g]);
+}
+
+__global__ void k_bfs_start(const int32_t *__restrict__ sorted_ids, const int32_t *best, int32_t q, int32_t *pos,
+                            int32_t *order) {
+    const int32_t s = sorted_ids[*best];
+    pos[s] = q;
+    order[q] = s;
+}
+
+// Frontier positions [a, b): every unvisited neighbour w of order[q] records
+// the smallest such q (its Cuthill-McKee parent); the first claimer appends w.
+__global__ void k_bfs_expand(const int32_t *__restrict__ order, int32_t a, int32_t b,
+                             const int64_t *__restrict__ aptr, const int32_t *__restrict__ adj,
+                             const int32_t *__restrict__ pos, int32_t *par, int32_t *cand, int32_t *cnt) {
+    const int64_t q = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= b) return;
+    const int32_t u = order[q];
+    for (int64_t j = aptr[u]; j < aptr[u + 1]; j++) {
+        const int32_t w = adj[j];
+        if (pos[w] >= 0) continue;
+        if (atomicMin(&par[w], (int32_t)q) == INT_MAX) cand[atomicAdd(cnt, 1)] = w;
+    }
+}
+
+__global__ void k_bfs_keys(const int32_t *__restrict__ cand, const int32_t *cnt, const int32_t *__restrict__ par,
+                           const int32_t *__restrict__ rank, uint64_t *key) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= *cnt) return;
+    const int32_t w = cand[i];
+    key[i] = ((uint64_t)(uint32_t)par[w] << 32) | (uint32_t)rank[w];
+}
+
+__global__ void k_bfs_assign(const int32_t *__restrict__ sorted, const int32_t *cnt, int32_t b, int32_t *pos,
+                             int32_t *order) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= *cnt) return;
+    const int32_t w = sorted[i];
+    pos[w] = b + (int32_t)i;
+    order[b + i] = w;
+}
+
+// Element list: an element is appended at the first of its nodes in visit
+// order, elements of one node by ascending id -> key (min node position, e).
+__global__ void k_elem_first_pos(const int32_t *__restrict__ mu, int64_t E, int Np, const int32_t *__restrict__ pos,
+                                 uint64_t *key, int32_t *ids) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int32_t m = INT_MAX;
+    for (int p = 0; p < Np; p++) m = min(m, pos[mu[e * Np + p]]);
+    key[e] = ((uint64_t)(uint32_t)m << 32) | (uint32_t)e;
+    ids[e] = (int32_t)e;
+}
+
+__global__ void k_i32_to_i64(const int32_t *__restrict__ a, int64_t n, int64_t *out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i <= n) out[i] = (i < n) ? a[i] : 0;
+}
+
 // temporary device allocation on the stream
 struct Tmp {
     void *p = nullptr;
@@ -399,7 +583,7 @@ cudaError_t launch_permute_rows(const int32_t *src, const int32_t *perm, int64_t
 }
 
 cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t *node_perm,
-                        int32_t *mu_out, int64_t *n_labels, cudaStream_t s) {
+                        int32_t *mu_out, int64_t *n_labels, cudaStream_t s, const int32_t *deg) {
     const int64_t n = E * Np;
     Tmp firstpos(s), flags(s), excl(s), label(s), scr(s);
     RET(firstpos.alloc(sizeof(int32_t) * N));
@@ -416,11 +600,146 @@ cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t
     RET(cub::DeviceScan::ExclusiveSum(scr.p, bytes, (int32_t *)flags.p, (int32_t *)excl.p, n + 1, s));
     k_first_label<<<blocks_for(n), kThreads, 0, s>>>(mu, (int32_t *)flags.p, (int32_t *)excl.p, n,
                                                      (int32_t *)label.p, node_perm);
+    if (deg) {  // PAPER.md:318 step 2: each element's group sorted by (degree, old id)
+        k_group_sort<<<blocks_for(E), kThreads, 0, s>>>((int32_t *)excl.p, E, Np, deg, node_perm);
+        k_label_from_perm<<<blocks_for(N), kThreads, 0, s>>>(node_perm, N, (int32_t *)label.p);
+    }
     k_relabel<<<blocks_for(n), kThreads, 0, s>>>(mu, (int32_t *)label.p, n, mu_out);
     int32_t cnt = 0;
     RET(cudaMemcpyAsync(&cnt, (int32_t *)excl.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RET(cudaStreamSynchronize(s));
     *n_labels = cnt;
+    return cudaGetLastError();
+}
+
+
+cudaError_t build_node_graph(const int32_t *mu, int64_t E, int Np, int64_t N, bool want_adj, DevGraph &g,
+                             int *bad, cudaStream_t s) {
+    g = DevGraph{};
+    const int64_t n = E * Np;
+    Tmp cnt(s), iptr(s), fill(s), inc(s), scr(s), dbad(s);
+    RET(cnt.alloc(sizeof(int32_t) * (N + 1)));
+    RET(iptr.alloc(sizeof(int32_t) * (N + 1)));
+    RET(fill.alloc(sizeof(int32_t) * (N + 1)));
+    RET(inc.alloc(sizeof(int32_t) * (n + 1)));
+    RET(dbad.alloc(sizeof(int32_t)));
+    RET(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (N + 1), s));
+    RET(cudaMemsetAsync(fill.p, 0, sizeof(int32_t) * (N + 1), s));
+    RET(cudaMemsetAsync(dbad.p, 0, sizeof(int32_t), s));
+    k_count_nodes<<<blocks_for(n), kThreads, 0, s>>>(mu, n, (int32_t *)cnt.p);
+    size_t bytes = 0;
+    RET(cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int32_t *)cnt.p, (int32_t *)iptr.p, N + 1, s));
+    RET(scr.alloc(bytes));
+    RET(cub::DeviceScan::ExclusiveSum(scr.p, bytes, (int32_t *)cnt.p, (int32_t *)iptr.p, N + 1, s));
+    k_incidence<<<blocks_for(n), kThreads, 0, s>>>(mu, n, (int32_t *)iptr.p, (int32_t *)fill.p, (int32_t *)inc.p);
+    RET(cudaMallocAsync((void **)&g.deg, sizeof(int32_t) * (N + 1), s));
+    k_node_nbrs<<<blocks_for(N, 128), 128, 0, s>>>(mu, Np, (int32_t *)iptr.p, (int32_t *)inc.p, N, g.deg, nullptr,
+                                                   nullptr, (int32_t *)dbad.p);
+    if (want_adj) {
+        RET(cudaMallocAsync((void **)&g.aptr, sizeof(int64_t) * (N + 1), s));
+        Tmp deg64(s), scr2(s);
+        RET(deg64.alloc(sizeof(int64_t) * (N + 1)));
+        k_i32_to_i64<<<blocks_for(N + 1), kThreads, 0, s>>>(g.deg, N, (int64_t *)deg64.p);
+        bytes = 0;
+        RET(cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int64_t *)deg64.p, g.aptr, N + 1, s));
+        RET(scr2.alloc(bytes));
+        RET(cub::DeviceScan::ExclusiveSum(scr2.p, bytes, (int64_t *)deg64.p, g.aptr, N + 1, s));
+        RET(cudaMemcpyAsync(&g.nadj, g.aptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RET(cudaStreamSynchronize(s));
+        RET(cudaMallocAsync((void **)&g.adj, sizeof(int32_t) * (g.nadj + 1), s));
+        k_node_nbrs<<<blocks_for(N, 128), 128, 0, s>>>(mu, Np, (int32_t *)iptr.p, (int32_t *)inc.p, N, nullptr,
+                                                       g.aptr, g.adj, (int32_t *)dbad.p);
+    }
+    int32_t hb = 0;
+    RET(cudaMemcpyAsync(&hb, dbad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RET(cudaStreamSynchronize(s));
+    *bad = hb;
+    return cudaGetLastError();
+}
+
+void free_node_graph(DevGraph &g, cudaStream_t s) {
+    if (g.deg) cudaFreeAsync(g.deg, s);
+    if (g.aptr) cudaFreeAsync(g.aptr, s);
+    if (g.adj) cudaFreeAsync(g.adj, s);
+    g = DevGraph{};
+}
+
+cudaError_t strategy_order(const int32_t *mu_can, const double *vxy, const int32_t *tri_or, int64_t E, int P,
+                           int64_t N, int strategy, const DevGraph &g, const double *edge_t, double x0, double y0,
+                           int32_t *elem_perm, int32_t *order, int64_t *n_levels, cudaStream_t s) {
+    const int Np = (P + 1) * (P + 2) / 2;
+    Tmp key(s), key2(s), ids(s), ids2(s), rank(s), pos(s), par(s), cand(s), cnt(s), best(s), scr(s);
+    RET(key.alloc(sizeof(uint64_t) * (N > E ? N : E)));
+    RET(key2.alloc(sizeof(uint64_t) * (N > E ? N : E)));
+    RET(ids.alloc(sizeof(int32_t) * (N > E ? N : E)));
+    RET(ids2.alloc(sizeof(int32_t) * (N > E ? N : E)));
+    RET(rank.alloc(sizeof(int32_t) * N));
+    RET(pos.alloc(sizeof(int32_t) * N));
+    RET(par.alloc(sizeof(int32_t) * N));
+    RET(cand.alloc(sizeof(int32_t) * N));
+    RET(cnt.alloc(sizeof(int32_t)));
+    RET(best.alloc(sizeof(int32_t)));
+    // node key: degree (Conn.) or squared distance to (x0, y0) (Dist.); rank = position in (key, id) order
+    if (strategy == 0) {
+        k_key_degree<<<blocks_for(N), kThreads, 0, s>>>(g.deg, N, (uint64_t *)key.p);
+    } else {
+        RET(cudaMemcpyToSymbolAsync(c_edge_t, edge_t, sizeof(double) * (P - 1), 0, cudaMemcpyHostToDevice, s));
+        k_key_dist<<<blocks_for(E), kThreads, 0, s>>>(vxy, tri_or, mu_can, E, P, x0, y0, (uint64_t *)key.p);
+    }
+    k_iota<<<blocks_for(N), kThreads, 0, s>>>((int32_t *)ids.p, N);
+    RET(sort_pairs_u64((uint64_t *)key.p, (int32_t *)ids.p, (uint64_t *)key2.p, (int32_t *)ids2.p, N, 64, s));
+    const int32_t *sorted_ids = (const int32_t *)ids2.p;
+    k_scatter_rank<<<blocks_for(N), kThreads, 0, s>>>(sorted_ids, N, (int32_t *)rank.p);
+    k_fill_i32<<<blocks_for(N), kThreads, 0, s>>>((int32_t *)pos.p, N, -1);
+    k_fill_i32<<<blocks_for(N), kThreads, 0, s>>>((int32_t *)par.p, N, INT_MAX);
+    // one sort workspace for every level (largest case: N keys)
+    int nbits = 1;
+    while (nbits < 31 && ((int64_t)1 << nbits) < N) nbits++;
+    size_t sbytes = 0;
+    RET(cub::DeviceRadixSort::SortPairs(nullptr, sbytes, (uint64_t *)key.p, (uint64_t *)key2.p, (int32_t *)cand.p,
+                                        (int32_t *)ids.p, (int)N, 0, 32 + nbits, s));
+    RET(scr.alloc(sbytes));
+    int64_t a = 0, b = 0, levels = 0;
+    while (b < N) {
+        if (a == b) {  // (re)start at the smallest-key unvisited node
+            k_fill_i32<<<1, 32, 0, s>>>((int32_t *)best.p, 1, INT_MAX);
+            k_min_unvisited<<<blocks_for(N), kThreads, 0, s>>>((int32_t *)pos.p, (int32_t *)rank.p, N,
+                                                               (int32_t *)best.p);
+            k_bfs_start<<<1, 1, 0, s>>>(sorted_ids, (int32_t *)best.p, (int32_t)b, (int32_t *)pos.p, order);
+            b++;
+        }
+        RET(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t), s));
+        k_bfs_expand<<<blocks_for(b - a, 128), 128, 0, s>>>(order, (int32_t)a, (int32_t)b, g.aptr, g.adj,
+                                                            (int32_t *)pos.p, (int32_t *)par.p, (int32_t *)cand.p,
+                                                            (int32_t *)cnt.p);
+        int32_t c = 0;
+        RET(cudaMemcpyAsync(&c, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        RET(cudaStreamSynchronize(s));
+        a = b;
+        levels++;
+        if (c == 0) continue;
+        k_bfs_keys<<<blocks_for(c), kThreads, 0, s>>>((int32_t *)cand.p, (int32_t *)cnt.p, (int32_t *)par.p,
+                                                      (int32_t *)rank.p, (uint64_t *)key.p);
+        RET(cub::DeviceRadixSort::SortPairs(scr.p, sbytes, (uint64_t *)key.p, (uint64_t *)key2.p, (int32_t *)cand.p,
+                                            (int32_t *)ids.p, c, 0, 32 + nbits, s));
+        k_bfs_assign<<<blocks_for(c), kThreads, 0, s>>>((int32_t *)ids.p, (int32_t *)cnt.p, (int32_t)b,
+                                                        (int32_t *)pos.p, order);
+        b += c;
+    }
+    *n_levels = levels;
+    // element list (key = first visited node, then element id)
+    k_elem_first_pos<<<blocks_for(E), kThreads, 0, s>>>(mu_can, E, Np, (int32_t *)pos.p, (uint64_t *)key.p,
+                                                        (int32_t *)ids.p);
+    RET(sort_pairs_u64((uint64_t *)key.p, (int32_t *)ids.p, (uint64_t *)key2.p, elem_perm, E, 64, s));
+    return cudaGetLastError();
+}
+
+cudaError_t relabel_from_perm(const int32_t *mu, int64_t n, const int32_t *node_perm, int64_t N, int32_t *mu_out,
+                              cudaStream_t s) {
+    Tmp label(s);
+    RET(label.alloc(sizeof(int32_t) * N));
+    k_label_from_perm<<<blocks_for(N), kThreads, 0, s>>>(node_perm, N, (int32_t *)label.p);
+    k_relabel<<<blocks_for(n), kThreads, 0, s>>>(mu, (int32_t *)label.p, n, mu_out);
     return cudaGetLastError();
 }
 

@@ -21,8 +21,8 @@ SEM_OK, SEM_E_ARG, SEM_E_STATE, SEM_E_MESH, SEM_E_UNSUPPORTED = 0, 1, 2, 3, 4
 SEM_E_CUDA, SEM_E_NCCL, SEM_E_OOM, SEM_E_NONFINITE = 5, 6, 7, 8
 STATUS_NAMES = {0: "SEM_OK", 1: "SEM_E_ARG", 2: "SEM_E_STATE", 3: "SEM_E_MESH", 4: "SEM_E_UNSUPPORTED",
                 5: "SEM_E_CUDA", 6: "SEM_E_NCCL", 7: "SEM_E_OOM", 8: "SEM_E_NONFINITE"}
-SEM_ORDER_INPUT, SEM_ORDER_HILBERT, SEM_ORDER_RANDOM = 0, 1, 2
-SEM_NODES_FIRST_TOUCH, SEM_NODES_CANONICAL = 0, 2
+SEM_ORDER_INPUT, SEM_ORDER_HILBERT, SEM_ORDER_RANDOM, SEM_ORDER_CONN, SEM_ORDER_DIST = 0, 1, 2, 3, 4
+SEM_NODES_FIRST_TOUCH, SEM_NODES_FIRST_TOUCH_DEGREE, SEM_NODES_CANONICAL, SEM_NODES_VISIT = 0, 1, 2, 3
 SEM_NUMBERING_CANONICAL, SEM_NUMBERING_INTERNAL = 0, 1
 SEM_INTEGRATOR_LEAPFROG, SEM_INTEGRATOR_HEUN = 0, 1
 
