@@ -204,6 +204,23 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps);
 sem_status sem_set_integrator(sem_ctx *ctx, int integrator);
 
 /*
+ * Scatter of the element contributions for the leapfrog step (NEXT-4 ablation,
+ * SURVEY §8a "rejected as primary").  Takes effect at the next
+ * sem_mesh_reorder; world_size 1 and the leapfrog only.
+ *  SEM_SCATTER_CHUNK  the product path: chunk-owned CSR reduction in shared
+ *                     memory + ordered slots (deterministic, bitwise reproducible);
+ *  SEM_SCATTER_ATOMIC one thread per element, fp64 atomicAdd into a global K U
+ *                     (addition order not fixed: results vary in the last bits);
+ *  SEM_SCATTER_COLOR  the paper's Algorithm 2 scatter: a greedy
+ *                     global element colouring in element order, one launch per
+ *                     colour with plain read-modify-write (deterministic).
+ * Errors: SEM_E_UNSUPPORTED (unknown mode; world_size > 1 or Heun at the
+ * next reorder / build).
+ */
+enum { SEM_SCATTER_CHUNK = 0, SEM_SCATTER_ATOMIC = 1, SEM_SCATTER_COLOR = 2 };
+sem_status sem_set_scatter(sem_ctx *ctx, int mode);
+
+/*
  * Heun only: copy V^n to out_host[E][Np][2] (fp64; INPUT element order, local
  * node p in the lattice order of reading R3 after the orientation fix, then the
  * x and y components) and return the step index.  Synchronises.
@@ -267,6 +284,8 @@ typedef struct {
     int64_t n_elements_global;
     int64_t first_element;    /* global index of this rank's first element */
     int32_t integrator;       /* SEM_INTEGRATOR_* of the built operators (else the selected one) */
+    int32_t scatter;          /* SEM_SCATTER_* the mesh was prepared for */
+    int32_t n_global_colors;  /* SEM_SCATTER_COLOR: colours of the global element colouring */
     int32_t reserved0;
 } sem_info;
 

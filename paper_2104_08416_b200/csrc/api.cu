@@ -115,6 +115,8 @@ struct sem_ctx {
     double *d_Grr = nullptr, *d_Gss = nullptr, *d_Grs = nullptr, *d_dt2M = nullptr;
     double *d_U[2] = {nullptr, nullptr};
     double *d_slot = nullptr;
+    int32_t *d_cnt = nullptr;  // shared-node arrival counters (K8 fused into K7, SEM_FUSE_K8=1)
+    bool fuse_k8 = false;      // measured slower: off by default
     int cur = 0;
     // Heun (NEXT-1): U = d_U[0], hM = (h/2)/M-bar in d_dt2M, double2 slots in d_slot
     int integrator = SEM_INTEGRATOR_LEAPFROG;
@@ -122,6 +124,12 @@ struct sem_ctx {
     double *d_geo[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     double *d_W = nullptr, *d_V = nullptr;
     bool v_lag = false;  // V holds V^{n-1}; V^n = V + h Vdot(W)
+    // NEXT-4 ablation scatters (world 1, leapfrog): selected before sem_mesh_reorder
+    int scatter = SEM_SCATTER_CHUNK;       // requested
+    int mesh_scatter = SEM_SCATTER_CHUNK;  // what the current mesh was prepared for
+    int32_t *d_mu_abl = nullptr, *d_eidx_abl = nullptr;  // internal-id rows (colour order for COLOR)
+    std::vector<int64_t> color_off;                      // COLOR: element ranges per colour
+    double *d_KU = nullptr;
     int32_t src_int = -1;
     double amp = 0, f0 = 1, t0 = 0, dt = 0;
     int64_t step = 0;
@@ -185,9 +193,11 @@ void reset_ops(sem_ctx *ctx) {
     ctx->d_Grr = ctx->d_Gss = ctx->d_Grs = ctx->d_dt2M = nullptr;
     ctx->d_U[0] = ctx->d_U[1] = nullptr;
     ctx->d_slot = nullptr;
+    ctx->d_cnt = nullptr;
     for (auto &g : ctx->d_geo) g = nullptr;
     ctx->d_W = ctx->d_V = nullptr;
     ctx->v_lag = false;
+    ctx->d_KU = nullptr;
     ctx->have_ops = false;
     ctx->step = 0;
     ctx->cur = 0;
@@ -200,6 +210,9 @@ void reset_mesh(sem_ctx *ctx) {
     ctx->src_lookup.clear();
     ctx->src_int_of.clear();
     ctx->dch = DevChunks{};
+    ctx->d_mu_abl = ctx->d_eidx_abl = nullptr;
+    ctx->color_off.clear();
+    ctx->mesh_scatter = SEM_SCATTER_CHUNK;
     ctx->n_if = ctx->n_send = 0;
     ctx->nbr.clear();
     ctx->nbr_off.clear();
@@ -342,6 +355,7 @@ StepParams step_params(sem_ctx *ctx) {
     StepParams p;
     p.Grr = ctx->d_Grr; p.Gss = ctx->d_Gss; p.Grs = ctx->d_Grs; p.dt2M = ctx->d_dt2M;
     p.slot = ctx->d_slot;
+    p.cnt = ctx->d_cnt;
     p.src = ctx->src_int; p.amp = ctx->amp; p.f0 = ctx->f0; p.t0 = ctx->t0; p.dt = ctx->dt;
     p.U = ctx->d_U[ctx->cur];
     p.Uprev = ctx->d_U[1 - ctx->cur];
@@ -372,10 +386,11 @@ sem_status step_phase1(sem_ctx *ctx, bool use_nccl) {
         CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream, ctx->d_intc, ctx->n_intc));
     }
     if (ctx->timing) ST(record(ctx, ctx->ev7, false));
-    if (ctx->timing) ST(record(ctx, ctx->ev8, true));
-    CK(launch_k8(ctx->dch, p, ctx->stream));
+    const bool k8 = p.cnt == nullptr;  // fused: K7 finalised the rank-local shared nodes
+    if (ctx->timing && (k8 || ctx->n_if > 0)) ST(record(ctx, ctx->ev8, true));
+    if (k8) CK(launch_k8(ctx->dch, p, ctx->stream));
     if (use_nccl && ctx->n_if > 0) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
-    if (ctx->timing && ctx->n_if == 0) ST(record(ctx, ctx->ev8, false));
+    if (ctx->timing && ctx->n_if == 0 && k8) ST(record(ctx, ctx->ev8, false));
     return SEM_OK;
 }
 
@@ -405,6 +420,26 @@ sem_status heun_step(sem_ctx *ctx) {
     CK(launch_heun_fix(ctx->dch, p, ctx->stream));
     if (ctx->timing) ST(record(ctx, ctx->ev8, false));
     ctx->v_lag = true;
+    ctx->step++;
+    if (ctx->timing && ctx->ev7.size() >= 4096) ST(drain_events(ctx));
+    return SEM_OK;
+}
+
+// NEXT-4 ablation step: atomic or global-colour scatter of K U, then the update.
+sem_status ablation_step(sem_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    ST(ensure_tables(ctx));
+    const StepParams p = step_params(ctx);
+    const bool atomic = ctx->mesh_scatter == SEM_SCATTER_ATOMIC;
+    if (ctx->timing) ST(record(ctx, ctx->ev7, true));
+    for (size_t c = 0; c + 1 < ctx->color_off.size(); c++)
+        CK(launch_abl_elem(ctx->Np, atomic, ctx->d_mu_abl, ctx->d_eidx_abl, ctx->color_off[c], ctx->color_off[c + 1],
+                           p, ctx->d_KU, ctx->stream));
+    if (ctx->timing) ST(record(ctx, ctx->ev7, false));
+    if (ctx->timing) ST(record(ctx, ctx->ev8, true));
+    CK(launch_abl_update(ctx->dch.N_tot, p, ctx->d_KU, ctx->stream));
+    if (ctx->timing) ST(record(ctx, ctx->ev8, false));
+    ctx->cur = 1 - ctx->cur;
     ctx->step++;
     if (ctx->timing && ctx->ev7.size() >= 4096) ST(drain_events(ctx));
     return SEM_OK;
@@ -446,6 +481,8 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
         if (!(c_elem_host[e] > 0.0) || !std::isfinite(c_elem_host[e]))
             return fail(ctx, SEM_E_ARG, "element " + std::to_string(e) + " has wave speed c <= 0");
     if (ctx->integrator == SEM_INTEGRATOR_HEUN) {
+        if (ctx->mesh_scatter != SEM_SCATTER_CHUNK)
+            return fail(ctx, SEM_E_UNSUPPORTED, "the ablation scatters run the leapfrog only");
         if (ctx->world > 1)
             return fail(ctx, SEM_E_UNSUPPORTED, "the Heun integrator runs on one rank (world_size 1)");
         if (!heun_supported(ctx->Np, ctx->dch.B))
@@ -477,8 +514,17 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
         CK(dalloc(L, &ctx->d_Grs, Epad));
         CK(dalloc(L, &ctx->d_U[1], Nt));
         CK(dalloc(L, &ctx->d_slot, d.n_slots + 2));
+        ctx->fuse_k8 = getenv("SEM_FUSE_K8") != nullptr;
+        if (ctx->fuse_k8) {
+            CK(dalloc(L, &ctx->d_cnt, d.N_sh + 1));
+            CK(cudaMemsetAsync(ctx->d_cnt, 0, sizeof(int32_t) * (d.N_sh + 1), s));
+        }
         CK(launch_geometry(ctx->d_vxy, ctx->d_tri_or, ctx->d_perm + ctx->e0, d_c, ctx->E, Epad, ctx->d_Grr,
                            ctx->d_Gss, ctx->d_Grs, d_detJ, d_bad, s));
+        if (ctx->mesh_scatter != SEM_SCATTER_CHUNK) {
+            CK(dalloc(L, &ctx->d_KU, Nt));
+            CK(cudaMemsetAsync(ctx->d_KU, 0, sizeof(double) * Nt, s));
+        }
     } else {
         for (auto &g : ctx->d_geo) CK(dalloc(L, &g, Epad));
         CK(dalloc(L, &ctx->d_W, Nt));
@@ -820,6 +866,45 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(), m, err,
                           one ? nullptr : part.remote.data()))
             return fail(ctx, SEM_E_MESH, err);
+        if (ctx->scatter != SEM_SCATTER_CHUNK) {
+            if (!one) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters run with world_size 1");
+            // rows of mu in internal ids; COLOR: greedy global element colouring in
+            // element order (smallest colour absent from every node's elements,
+            // PAPER.md:516), elements grouped by colour, ascending within a colour
+            std::vector<int32_t> rows((size_t)E * Np), eidx;
+            std::vector<int32_t> color;
+            int ncol = 1;
+            if (ctx->scatter == SEM_SCATTER_COLOR) {
+                std::vector<uint64_t> used((size_t)N, 0);
+                color.assign((size_t)E, 0);
+                for (int64_t e = 0; e < E; e++) {
+                    uint64_t mask = 0;
+                    for (int p = 0; p < Np; p++) mask |= used[mu_h[e * Np + p]];
+                    if (~mask == 0) return fail(ctx, SEM_E_MESH, "global colouring needs more than 64 colours");
+                    const int c = __builtin_ctzll(~mask);
+                    color[e] = c;
+                    if (c + 1 > ncol) ncol = c + 1;
+                    for (int p = 0; p < Np; p++) used[mu_h[e * Np + p]] |= (uint64_t)1 << c;
+                }
+            }
+            ctx->color_off.assign((size_t)ncol + 1, 0);
+            if (ctx->scatter == SEM_SCATTER_COLOR) {
+                for (int64_t e = 0; e < E; e++) ctx->color_off[color[e] + 1]++;
+                for (int c = 0; c < ncol; c++) ctx->color_off[c + 1] += ctx->color_off[c];
+                std::vector<int64_t> fillc(ctx->color_off.begin(), ctx->color_off.end() - 1);
+                eidx.resize((size_t)E);
+                for (int64_t e = 0; e < E; e++) eidx[fillc[color[e]]++] = (int32_t)e;
+            } else {
+                ctx->color_off[1] = E;
+            }
+            for (int64_t k = 0; k < E; k++) {
+                const int64_t e = eidx.empty() ? k : eidx[k];
+                for (int p = 0; p < Np; p++) rows[k * Np + p] = m.int_of[mu_h[e * Np + p]];
+            }
+            CK(upload(ctx->mesh_allocs, &ctx->d_mu_abl, rows, s));
+            if (!eidx.empty()) CK(upload(ctx->mesh_allocs, &ctx->d_eidx_abl, eidx, s));
+            ctx->mesh_scatter = ctx->scatter;
+        }
         std::vector<int32_t>().swap(mu_h);
         tr.mark(s, "chunk builder (host)");
         DevChunks &d = ctx->dch;
@@ -828,7 +913,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
         auto &L = ctx->mesh_allocs;
         int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
-        uint16_t *p_lpos, *p_lptr, *p_lidx;
+        uint16_t *p_lpos, *p_lptr, *p_lidx, *p_shcr;
         CK(upload(L, &p_cmeta, m.cmeta, s));
         CK(upload(L, &p_lidx, m.lidx, s));
         CK(upload(L, &p_lpos, m.lpos, s));
@@ -836,9 +921,11 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(upload(L, &p_pstart, m.sh_pstart, s));
         CK(upload(L, &p_shn, m.shl_node, s));
         CK(upload(L, &p_shs, m.shl_slot, s));
+        CK(upload(L, &p_shcr, m.shl_cr, s));
         d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.lptr = p_lptr; d.sh_pstart = p_pstart;
         d.shl_node = p_shn;
         d.shl_slot = p_shs;
+        d.shl_cr = p_shcr;
         // node maps for I/O (local node l -> internal / canonical / reordered id)
         if (one) {
             // reordered id == local id; the device node_perm (reordered -> canonical) is kept
@@ -931,6 +1018,10 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
         for (int64_t k = 0; k < n_steps; k++) ST(heun_step(ctx));
         return SEM_OK;
     }
+    if (ctx->mesh_scatter != SEM_SCATTER_CHUNK) {
+        for (int64_t k = 0; k < n_steps; k++) ST(ablation_step(ctx));
+        return SEM_OK;
+    }
     for (int64_t k = 0; k < n_steps; k++) {
         ST(step_phase1(ctx, ctx->world > 1));
         ST(step_phase2(ctx));
@@ -968,6 +1059,14 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps) {
         ST(exchange_loopback(ctxs, n));
         for (int r = 0; r < n; r++) ST(step_phase2(ctxs[r]));
     }
+    return SEM_OK;
+}
+
+sem_status sem_set_scatter(sem_ctx *ctx, int mode) {
+    ST(check_usable(ctx));
+    if (mode != SEM_SCATTER_CHUNK && mode != SEM_SCATTER_ATOMIC && mode != SEM_SCATTER_COLOR)
+        return fail(ctx, SEM_E_UNSUPPORTED, "unknown scatter mode " + std::to_string(mode));
+    ctx->scatter = mode;
     return SEM_OK;
 }
 
@@ -1117,10 +1216,14 @@ sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
     o->n_shared_nodes = m.N_sh;
     o->n_partial_slots = m.n_slots;
     o->max_colors = m.max_colors;
-    o->launches_per_step = 1 + ((m.N_sh - m.N_if) > 0 ? 1 : 0) + (m.N_if > 0 ? 3 : 0);
+    o->launches_per_step = 1 + ((m.N_sh - m.N_if) > 0 && !(ctx->have_ops && ctx->d_cnt) ? 1 : 0) +
+                           (m.N_if > 0 ? 3 : 0);
     o->step = ctx->step;
     o->bytes_alg_per_step = (double)ctx->E * (4.0 * ctx->Np + 24.0) + 32.0 * (double)ctx->N;
     o->integrator = ctx->have_ops ? ctx->ops_integrator : ctx->integrator;
+    o->scatter = ctx->mesh_scatter;
+    o->n_global_colors = ctx->mesh_scatter == SEM_SCATTER_COLOR ? (int32_t)ctx->color_off.size() - 1 : 0;
+    if (ctx->mesh_scatter != SEM_SCATTER_CHUNK) o->launches_per_step = (int32_t)ctx->color_off.size();
     if (o->integrator == SEM_INTEGRATOR_HEUN) {
         // mu, F (4) + sd, V read + write per element; U r/w, W r/w, (h/2)/M per node
         o->bytes_alg_per_step = (double)ctx->E * (4.0 * ctx->Np + 40.0 + 32.0 * ctx->Np) + 40.0 * (double)ctx->N;

@@ -201,16 +201,25 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     for (int64_t s = 0; s < nsh; s++) m.sh_pstart[s + 1] += m.sh_pstart[s];
     m.n_slots = nsh ? m.sh_pstart[nsh] : 0;
     m.s0.assign(nch + 1, 0);
-    for (int64_t c = 0; c < nch; c++) m.s0[c + 1] = (int32_t)((m.s0[c] + (int64_t)lists[c].size() + 3) & ~int64_t(3));
-    for (int64_t c = 0; c < nch; c++) m.max_nsh = std::max(m.max_nsh, (int)((lists[c].size() + 3) & ~size_t(3)));
-    m.shl_node.assign((size_t)m.s0[nch] + 4, 0);
-    m.shl_slot.assign((size_t)m.s0[nch] + 4, 0);
+    // chunk blocks of the per-chunk lists start on multiples of 8 entries (16-byte
+    // aligned TMA copies of the u16 shl_cr block)
+    for (int64_t c = 0; c < nch; c++) m.s0[c + 1] = (int32_t)((m.s0[c] + (int64_t)lists[c].size() + 7) & ~int64_t(7));
+    for (int64_t c = 0; c < nch; c++) m.max_nsh = std::max(m.max_nsh, (int)((lists[c].size() + 7) & ~size_t(7)));
+    m.shl_node.assign((size_t)m.s0[nch] + 8, 0);
+    m.shl_slot.assign((size_t)m.s0[nch] + 8, 0);
+    m.shl_cr.assign((size_t)m.s0[nch] + 8, 0);
     {
         std::vector<int32_t> cursor(nsh, 0);
         for (int64_t c = 0; c < nch; c++) {  // ascending chunk order -> slot order within a node
             int32_t k = m.s0[c];
             for (int32_t sidx : lists[c]) {
+                const int32_t cnt = m.sh_pstart[sidx + 1] - m.sh_pstart[sidx];
+                if (cnt > 255) {
+                    err = "build_chunks: a node is shared by more than 255 chunks";
+                    return false;
+                }
                 m.shl_node[k] = sidx;
+                m.shl_cr[k] = (uint16_t)((cnt << 8) | cursor[sidx]);
                 m.shl_slot[k] = m.sh_pstart[sidx] + cursor[sidx]++;
                 k++;
             }

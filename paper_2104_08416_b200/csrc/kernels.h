@@ -80,6 +80,7 @@ struct DevChunks {  // device view of ChunkMeta
     const int32_t *sh_pstart;  // [N_sh+1] node-major slots of shared node s
     const int32_t *shl_node;   // per chunk (block at cmeta[2]): shared index of each local shared node
     const int32_t *shl_slot;   // per chunk: the slot it writes
+    const uint16_t *shl_cr;    // per chunk: (slots of the node << 8) | rank of this chunk among them
 };
 
 cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s);
@@ -100,6 +101,8 @@ struct StepParams {
     const double *U;   // U^n
     double *Uprev;     // U^{n-1} in, U^{n+1} out
     double *slot;      // node-major partial sums of shared nodes (K7 writes, K8 reads)
+    int32_t *cnt;      // [N_sh] arrival counters: K7 finalises a shared node when its last
+                       // chunk arrives (nullptr: K8 does it)
     int32_t src;       // internal node id of the source (-1 none)
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
@@ -141,6 +144,14 @@ cudaError_t launch_heun_fix(const DevChunks &ch, const HeunParams &p, cudaStream
 // V (chunk layout) <-> host layout [E][Np][2] in input element order; in == nullptr -> zeros
 cudaError_t launch_v_out(const double *V, const int32_t *perm, int64_t E, int np, int B, double *out, cudaStream_t s);
 cudaError_t launch_v_in(const double *in, const int32_t *perm, int64_t E, int np, int B, double *V, cudaStream_t s);
+
+// NEXT-4 ablation scatters: element k in [e0, e1) of mu [.][Np] (internal node
+// ids; G read at eidx[k], or k if eidx == nullptr) adds K^e u into KU with fp64
+// atomics (atomic) or plain read-modify-write (one colour of a global colouring).
+cudaError_t launch_abl_elem(int np, bool atomic, const int32_t *mu, const int32_t *eidx, int64_t e0, int64_t e1,
+                            const StepParams &p, double *KU, cudaStream_t s);
+// U^{n+1} = 2U^n - U^{n-1} + dt2M (f - KU) over n internal nodes, KU := 0.
+cudaError_t launch_abl_update(int64_t n, const StepParams &p, double *KU, cudaStream_t s);
 
 // out[omap ? omap[i] : i] = in[imap ? imap[i] : i], i < n
 cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,

@@ -48,11 +48,12 @@ struct ChunkMeta {
     int64_t E = 0, N = 0, nchunks = 0;
     int64_t N_int = 0, N_sh = 0, N_tot = 0, n_slots = 0;
     int64_t N_if = 0;                // forced-shared (rank-interface) nodes, last N_if of the shared range
-    int max_local = 0, max_win = 0, max_colors = 0, max_lptr = 0, max_nsh = 0;  // max_nsh: multiple of 4
+    int max_local = 0, max_win = 0, max_colors = 0, max_lptr = 0, max_nsh = 0;  // max_nsh: multiple of 8
     std::vector<int32_t> i0;         // [nchunks+1] interior window starts (even)
-    std::vector<int32_t> s0;         // [nchunks+1] chunk blocks in shl_node / shl_slot (multiple of 4)
+    std::vector<int32_t> s0;         // [nchunks+1] chunk blocks in shl_node / shl_slot / shl_cr (multiple of 8)
     std::vector<int32_t> shl_node;   // shared index s of each chunk-local shared node
     std::vector<int32_t> shl_slot;   // node-major slot written by that chunk
+    std::vector<uint16_t> shl_cr;    // (slots of the node << 8) | this chunk's rank among them
     std::vector<int32_t> cmeta;      // [nchunks][8] {i0, nint, s0, nsh, ncol, ne, nint_al, lp0}
     std::vector<int32_t> lp0;        // [nchunks+1] start of chunk c's block in lptr (multiple of 8)
     std::vector<uint16_t> lptr;      // per chunk: CSR row pointers over local nodes (nlocal+1)

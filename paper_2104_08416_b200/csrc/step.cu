@@ -49,13 +49,15 @@ inline unsigned blocks_for(int64_t n, int threads = kThreads) {
 
 // Shared-memory layout of one pipeline stage (all offsets 16-byte aligned).
 struct StageLayout {
-    int lidx, lpos, lptr, shs, g, meta, u, size;
+    int lidx, lpos, lptr, shs, shn, scr, g, meta, u, size;
     __host__ __device__ StageLayout(int np, int B, int L, int Lp, int Ls) {
         lidx = 0;
         lpos = np * B * 2;
         lptr = lpos + np * B * 2;
         shs = lptr + Lp * 2;
-        g = shs + Ls * 4;
+        shn = shs + Ls * 4;
+        scr = shn + Ls * 4;
+        g = scr + Ls * 2;
         meta = g + 3 * B * 8;
         u = meta + 32;
         size = (u + L * 8 + 127) & ~127;
@@ -135,6 +137,39 @@ __device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *lp
     return y;
 }
 
+// Fused K8 (shared nodes finalised by their last chunk): after writing its
+// partial into slot `sl`, a chunk counts its arrival on the node's counter with
+// an acq_rel atomic (release: the slot write is ordered before it; acquire: the
+// last arriver sees every other chunk's slot).  The last arriver sums the
+// node's slots in ascending chunk order -- the same order and association as
+// k8_fix, so the result does not depend on which chunk finishes -- applies the
+// update and resets the counter for the next step.  Rank-interface nodes stay
+// with the exchange path.
+__device__ __forceinline__ int atomic_add_acq_rel(int32_t *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepParams &a, int32_t sg, uint16_t cr,
+                                              int sl, double u) {
+    if (sg >= ch.N_sh - ch.N_if) return;
+    const int cnt = cr >> 8, rk = cr & 255;
+    if (atomic_add_acq_rel(&a.cnt[sg], 1) != cnt - 1) return;
+    const int j0 = sl - rk, j1 = j0 + cnt;
+    double part[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) part[d] = (j0 + d < j1) ? __ldcg(&a.slot[j0 + d]) : 0.0;
+    double y = part[0];
+#pragma unroll
+    for (int d = 1; d < 4; d++) y += part[d];
+    for (int j = j0 + 4; j < j1; j++) y += __ldcg(&a.slot[j]);
+    const int64_t id = ch.N_int + sg;
+    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    a.Uprev[id] = 2.0 * u - a.Uprev[id] + a.dt2M[id] * (f - y);
+    a.cnt[sg] = 0;
+}
+
 // ---- K7 ---------------------------------------------------------------------------
 template <int NP, int B>
 __global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
@@ -184,14 +219,22 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 192 ? 3 : B <= 25
                 reinterpret_cast<int4 *>(st + lay.meta)[0] = m0;
                 reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
                 const int nlp = (ni_al + nsh + 1 + 7) & ~7;
-                const int nsh4 = (nsh + 3) & ~3;
-                const uint32_t bytes = 2 * NP * B * 2 + nlp * 2 + nsh4 * 4 + 3 * B * 8 + (uint32_t)ni_al * 8;
+                const int nsh8 = (nsh + 7) & ~7;
+                const bool fuse = a.cnt != nullptr;
+                const uint32_t bytes = 2 * NP * B * 2 + nlp * 2 + nsh8 * (fuse ? 10 : 4) + 3 * B * 8 +
+                                       (uint32_t)ni_al * 8;
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
                 tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
                 tma_load(st + lay.lpos, ch.lpos + e0 * NP, NP * B * 2, &full[s]);
                 tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
-                if (nsh4 > 0) tma_load(st + lay.shs, ch.shl_slot + s0, nsh4 * 4, &full[s]);
+                if (nsh8 > 0) {
+                    tma_load(st + lay.shs, ch.shl_slot + s0, nsh8 * 4, &full[s]);
+                    if (fuse) {
+                        tma_load(st + lay.shn, ch.shl_node + s0, nsh8 * 4, &full[s]);
+                        tma_load(st + lay.scr, ch.shl_cr + s0, nsh8 * 2, &full[s]);
+                    }
+                }
                 tma_load(st + lay.g, a.Grr + e0, B * 8, &full[s]);
                 tma_load(st + lay.g + B * 8, a.Gss + e0, B * 8, &full[s]);
                 tma_load(st + lay.g + 2 * B * 8, a.Grs + e0, B * 8, &full[s]);
@@ -271,7 +314,11 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 192 ? 3 : B <= 25
                 const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
                 Unew[id] = 2.0 * u_s[i] - up_s[i] + m_s[i] * (f - yi);
             } else if (i >= ni_al) {
-                a.slot[shs[i - ni_al]] = yi;
+                const int j = i - ni_al;
+                const int sl = shs[j];
+                a.slot[sl] = yi;
+                if (a.cnt) finish_shared(ch, a, reinterpret_cast<const int32_t *>(st + lay.shn)[j],
+                                         reinterpret_cast<const uint16_t *>(st + lay.scr)[j], sl, u_s[i]);
             }
         }
         consumer_sync<B>();
@@ -350,6 +397,53 @@ __global__ void k_permute_f64(const double *__restrict__ in, const int32_t *__re
 __global__ void k_nonfinite(const double *__restrict__ a, int64_t n, int32_t *flag) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n && !isfinite(a[i])) atomicMin(flag, (int32_t)i);
+}
+
+// ---- NEXT-4 ablation scatters (the rejected alternatives of SURVEY §8a K7) -----------
+// One thread per element: u gathered straight from global U through mu (internal
+// numbering), y = K^e u as in K7, then either fp64 atomicAdd into KU (order of
+// the additions not fixed) or, for the paper's global element colouring
+// (PAPER.md:516), a plain read-modify-write: one launch per colour, elements of
+// a colour share no node.
+template <int NP, bool ATOMIC>
+__global__ void __launch_bounds__(256) k_abl_elem(const int32_t *__restrict__ mu, const int32_t *__restrict__ eidx,
+                                                  int64_t e0, int64_t e1, const StepParams a, double *KU) {
+    const int64_t k = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= e1) return;
+    const int64_t e = eidx ? eidx[k] : k;  // element (product order) for G
+    const double grr = a.Grr[e], gss = a.Gss[e], grs = a.Grs[e];
+    int32_t g[NP];
+    double u[NP], y[NP];
+#pragma unroll
+    for (int p = 0; p < NP; p++) { g[p] = mu[k * NP + p]; u[p] = a.U[g[p]]; y[p] = 0.0; }
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+#pragma unroll
+        for (int q = p; q < NP; q++) {
+            const double kk = fma(grr, c_Srr[p][q], fma(gss, c_Sss[p][q], grs * c_Srs[p][q]));
+            if (q == p) {
+                y[p] = fma(kk, u[p], y[p]);
+            } else {
+                y[p] = fma(kk, u[q], y[p]);
+                y[q] = fma(kk, u[p], y[q]);
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+        if (ATOMIC) atomicAdd(&KU[g[p]], y[p]);
+        else KU[g[p]] += y[p];
+    }
+}
+
+// Leapfrog update of every node from the assembled KU; KU reset for the next step.
+__global__ void k_abl_update(int64_t n, const StepParams a, double *KU) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double f = (i == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    const double y = KU[i];
+    KU[i] = 0.0;
+    a.Uprev[i] = 2.0 * a.U[i] - a.Uprev[i] + a.dt2M[i] * (f - y);
 }
 
 // The max-dynamic-smem attribute is per function (process-wide), and several
@@ -467,6 +561,25 @@ cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_
                            double dt, double *dt2M, cudaStream_t s) {
     if (ch.N_if == 0) return cudaSuccess;
     k_mass_if<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, xbuf, sum_start, sum_src, dt * dt, dt2M);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abl_elem(int np, bool atomic, const int32_t *mu, const int32_t *eidx, int64_t e0, int64_t e1,
+                            const StepParams &p, double *KU, cudaStream_t s) {
+    if (e1 <= e0) return cudaSuccess;
+    const unsigned nb = blocks_for(e1 - e0);
+    if (np == 6) {
+        if (atomic) k_abl_elem<6, true><<<nb, kThreads, 0, s>>>(mu, eidx, e0, e1, p, KU);
+        else k_abl_elem<6, false><<<nb, kThreads, 0, s>>>(mu, eidx, e0, e1, p, KU);
+    } else {
+        if (atomic) k_abl_elem<10, true><<<nb, kThreads, 0, s>>>(mu, eidx, e0, e1, p, KU);
+        else k_abl_elem<10, false><<<nb, kThreads, 0, s>>>(mu, eidx, e0, e1, p, KU);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abl_update(int64_t n, const StepParams &p, double *KU, cudaStream_t s) {
+    k_abl_update<<<blocks_for(n), kThreads, 0, s>>>(n, p, KU);
     return cudaGetLastError();
 }
 

@@ -25,13 +25,14 @@ SEM_ORDER_INPUT, SEM_ORDER_HILBERT, SEM_ORDER_RANDOM, SEM_ORDER_CONN, SEM_ORDER_
 SEM_NODES_FIRST_TOUCH, SEM_NODES_FIRST_TOUCH_DEGREE, SEM_NODES_CANONICAL, SEM_NODES_VISIT = 0, 1, 2, 3
 SEM_NUMBERING_CANONICAL, SEM_NUMBERING_INTERNAL = 0, 1
 SEM_INTEGRATOR_LEAPFROG, SEM_INTEGRATOR_HEUN = 0, 1
+SEM_SCATTER_CHUNK, SEM_SCATTER_ATOMIC, SEM_SCATTER_COLOR = 0, 1, 2
 
 EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem_build_operators",
             "sem_step_n", "sem_read_field", "sem_write_state", "sem_set_step", "sem_sync",
             "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version",
             "sem_debug_chunk_stats", "sem_debug_partition", "sem_nccl_unique_id",
             "sem_group_build_operators", "sem_group_step_n", "sem_set_integrator", "sem_read_velocity",
-            "sem_write_velocity"]
+            "sem_write_velocity", "sem_set_scatter"]
 
 
 class SemError(RuntimeError):
@@ -52,7 +53,8 @@ class sem_info(C.Structure):
                 ("prep_build_ms", C.c_double), ("n_interface_nodes", C.c_int64),
                 ("n_neighbors", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("n_elements_global", C.c_int64), ("first_element", C.c_int64),
-                ("integrator", C.c_int32), ("reserved0", C.c_int32)]
+                ("integrator", C.c_int32), ("scatter", C.c_int32), ("n_global_colors", C.c_int32),
+                ("reserved0", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -94,6 +96,7 @@ def load(path: str = LIB_PATH):
         L.sem_group_build_operators.argtypes = [P, C.c_int, P, i64, dbl, dbl, dbl, dbl]
         L.sem_group_step_n.argtypes = [P, C.c_int, i64]
         L.sem_set_integrator.argtypes = [P, C.c_int]
+        L.sem_set_scatter.argtypes = [P, C.c_int]
         L.sem_read_velocity.argtypes = [P, P, C.POINTER(i64)]
         L.sem_write_velocity.argtypes = [P, P]
         L.sem_version.argtypes = []
@@ -196,6 +199,9 @@ class SemContext:
         a = None if u_curr is None else np.ascontiguousarray(u_curr, np.float64)
         b = None if u_prev is None else np.ascontiguousarray(u_prev, np.float64)
         self._check(self.L.sem_write_state(self.h, _ptr(a), _ptr(b), numbering))
+
+    def sem_set_scatter(self, mode: int):
+        self._check(self.L.sem_set_scatter(self.h, int(mode)))
 
     def sem_set_integrator(self, integrator: int):
         self._check(self.L.sem_set_integrator(self.h, int(integrator)))
