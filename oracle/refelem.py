@@ -51,7 +51,7 @@ def nodes(P: int):
                 (0, a), (t, t), (1 - a, a),
                 (0, 1 - a), (a, 1 - a),
                 (0, 1))
-    raise ValueError("unsupported order %r (oracle supports P = 1, 2, 3)" % P)
+    raise ValueError("exact node set only for P <= 3; P >= 4 uses tables_hp (reading R21)")
 
 
 def monomials(P: int):
@@ -106,11 +106,13 @@ def _f64(e) -> float:
 
 @lru_cache(maxsize=None)
 def tables(P: int):
-    """fp64 tables (rounded once from exact values).
+    """fp64 tables (rounded once from exact values; P >= 4: tables_hp).
 
     Returns dict with numpy arrays:
       nodes [Np,2], wK [Np], wM [Np], Dr [Np,Np], Ds [Np,Np]  (Dr[k,p] = dN_p/dr at x_k)
     """
+    if P >= 4:
+        return tables_hp(P)
     nd = nodes(P)
     Dr, Ds = deriv_tables(P)
     out = {
@@ -121,6 +123,92 @@ def tables(P: int):
         "wM": np.array([_f64(w) for w in weights_M(P)], dtype=np.float64),
         "Dr": np.array([[_f64(v) for v in row] for row in Dr], dtype=np.float64),
         "Ds": np.array([[_f64(v) for v in row] for row in Ds], dtype=np.float64),
+    }
+    for k in ("nodes", "wK", "wM", "Dr", "Ds"):
+        out[k].setflags(write=False)
+    return out
+
+
+# --------------------------------------------------------------------------
+# P >= 4 (NEXT-2, reading R21): Blyth-Pozrikidis Lobatto grid, computed in
+# 60-digit arithmetic (mpmath) and rounded to fp64 once.  The 1D master nodes
+# v_0..v_P are the Gauss-Lobatto points on [0, 1] (0, 1 and the roots of
+# P_P'(2v - 1)); the triangle node of lattice indices (i, j), k = P - i - j, is
+#   x = (1 + 2 v_i - v_j - v_k) / 3,   y = (1 + 2 v_j - v_i - v_k) / 3
+# (Blyth & Pozrikidis 2006; for P = 2, 3 it gives the R3 node sets above).
+# The paper cites these locations without printing them:
+# parity unpinned beyond the invariants of tests/test_oracle_refelem.py.
+# --------------------------------------------------------------------------
+HP_DPS = 60
+
+
+def lobatto01_hp(P: int):
+    """Gauss-Lobatto points on [0, 1] (mpmath, HP_DPS digits), ascending."""
+    import mpmath as mp
+    mp.mp.dps = HP_DPS
+    leg = sp.legendre_poly(P, X)
+    dpoly = sp.Poly(sp.diff(leg, X), X)
+    roots = sorted(sp.Float(r, HP_DPS) for r in dpoly.nroots(n=HP_DPS, maxsteps=200))
+    v = [mp.mpf(0)] + [(mp.mpf(str(r)) + 1) / 2 for r in roots] + [mp.mpf(1)]
+    for i in range(P // 2 + 1):  # exact symmetry v_{P-i} = 1 - v_i (roots come in +- pairs)
+        v[P - i] = 1 - v[i]
+    if P % 2 == 0:
+        v[P // 2] = mp.mpf(1) / 2
+    return v
+
+
+def nodes_hp(P: int):
+    import mpmath as mp
+    v = lobatto01_hp(P)
+    out = []
+    for j in range(P + 1):
+        for i in range(P + 1 - j):
+            k = P - i - j
+            x = mp.mpf(0) if i == 0 else (1 + 2 * v[i] - v[j] - v[k]) / 3  # edges x = 0, y = 0 exact
+            y = mp.mpf(0) if j == 0 else (1 + 2 * v[j] - v[i] - v[k]) / 3
+            out.append((x, y))
+    return out
+
+
+@lru_cache(maxsize=None)
+def tables_hp(P: int):
+    """fp64 tables for any P (same keys as ``tables``) from the HP_DPS-digit
+    dual-system solve: N_p = sum_m C[m, p] x^a y^b with V C = I; w_p = int N_p
+    (closed-form monomial integrals a! b! / (a+b+2)!); Dr[k, p] = dN_p/dx (x_k)."""
+    import mpmath as mp
+    from math import factorial
+    mp.mp.dps = HP_DPS
+    nd = nodes_hp(P)
+    Np = len(nd)
+    ex = [(a, b) for a in range(P + 1) for b in range(P + 1 - a)]
+    V = mp.matrix([[x ** a * y ** b for (a, b) in ex] for (x, y) in nd])
+    C = mp.inverse(V)  # C[m, p]
+    mint = [mp.mpf(factorial(a) * factorial(b)) / factorial(a + b + 2) for (a, b) in ex]
+    w = [mp.fsum(C[m, p] * mint[m] for m in range(Np)) for p in range(Np)]
+
+    def dN(p, x, y, d):
+        acc = []
+        for m, (a, b) in enumerate(ex):
+            if d == 0 and a > 0:
+                acc.append(C[m, p] * a * x ** (a - 1) * y ** b)
+            if d == 1 and b > 0:
+                acc.append(C[m, p] * b * x ** a * y ** (b - 1))
+        return mp.fsum(acc)
+
+    Dr = [[dN(p, x, y, 0) for p in range(Np)] for (x, y) in nd]
+    Ds = [[dN(p, x, y, 1) for p in range(Np)] for (x, y) in nd]
+    def f(q):  # round once; |q| < 1e-40 is the 60-digit residue of an exact zero
+        return 0.0 if abs(q) < mp.mpf("1e-40") else float(q)
+
+    out = {
+        "P": P,
+        "Np": Np,
+        "nodes": np.array([[f(x), f(y)] for (x, y) in nd], dtype=np.float64),
+        "wK": np.array([f(q) for q in w], dtype=np.float64),
+        "wM": np.array([f(q) for q in w], dtype=np.float64),
+        "Dr": np.array([[f(q) for q in row] for row in Dr], dtype=np.float64),
+        "Ds": np.array([[f(q) for q in row] for row in Ds], dtype=np.float64),
+        "C": C, "exps": ex,  # high-precision basis (pins only)
     }
     for k in ("nodes", "wK", "wM", "Dr", "Ds"):
         out[k].setflags(write=False)

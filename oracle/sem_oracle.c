@@ -237,12 +237,35 @@ static int cmp_i32(const void *a, const void *b) {
 
 /* mu_out[e*Np + p] = canonical global node of local node p of element e.
  * tri must already be oriented. Returns the node count N (>0) or an error. */
+/* Lattice-order local node kinds for any P (R3 extended to P >= 4, R21): node
+ * (i, j) is a vertex at (0,0), (P,0), (0,P); on edge v0-v1 if j = 0 (position
+ * i - 1 from v0), v0-v2 if i = 0 (j - 1 from v0), v1-v2 if i + j = P (j - 1
+ * from v1); otherwise interior, numbered in lattice order. */
+static orc_lnode LN_GEN[64];
+static int lattice_nodes(int P) {
+    int p = 0, m = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, p++) {
+            orc_lnode n = {2, 0, 0};
+            if (i == 0 && j == 0) n = (orc_lnode){0, 0, 0};
+            else if (i == P && j == 0) n = (orc_lnode){0, 1, 0};
+            else if (i == 0 && j == P) n = (orc_lnode){0, 2, 0};
+            else if (j == 0) n = (orc_lnode){1, 0, i - 1};
+            else if (i == 0) n = (orc_lnode){1, 1, j - 1};
+            else if (i + j == P) n = (orc_lnode){1, 2, j - 1};
+            else n = (orc_lnode){2, 0, m++};
+            LN_GEN[p] = n;
+        }
+    return p;
+}
+
 int64_t orc_canonical_nodes(const int32_t *tri, int64_t nv, int64_t ne, int P, int32_t *mu_out) {
     const orc_lnode *LN;
     int Np;
     if (P == 1) { LN = LN_P1; Np = 3; }
     else if (P == 2) { LN = LN_P2; Np = 6; }
     else if (P == 3) { LN = LN_P3; Np = 10; }
+    else if (P >= 4 && P <= 9) { Np = lattice_nodes(P); LN = LN_GEN; }
     else return ORC_E_ARG;
     int nI = (P - 1) * (P - 2) / 2;
     /* Unique edges sorted by (min, max): bucket by min vertex, sort each bucket. */
@@ -376,7 +399,7 @@ void orc_apply_R(const int32_t *mu, int64_t ne, int Np, int64_t nn,
                  const double *U, double *R, double *ebuf /* [ne*Np] scratch */) {
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < ne; e++) {
-        double U2[16], Vd[2][16];
+        double U2[64], Vd[2][64];
         const double *Ki = Jinv + 4 * e; /* Ki[2*jh + j] = (J^-1)_{jh j} */
         double c2 = c[e] * c[e];
         /* Algorithm 1: gather U_2[q] = U_mu(q,e) */
@@ -466,7 +489,7 @@ void orc_vdot(const int32_t *mu, int64_t ne, int Np, const double *Jinv, const d
               const double *Dr, const double *Ds, const double *U, double *Vd) {
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < ne; e++) {
-        double U2[16];
+        double U2[64];
         const double *Ki = Jinv + 4 * e;
         const double c2 = c[e] * c[e];
         for (int q = 0; q < Np; q++) U2[q] = U[mu[e * Np + q]];

@@ -41,7 +41,7 @@ def test_node_counts_and_two_triangles():
     assert OracleSEM(vxy, two, 1).N == 4
 
 
-@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("P", [2, 3, 5, 7])
 def test_grid_node_count_and_coordinates(P):
     m = mg.shuffle(mg.grid_mesh(7, 5, 3.0, 2.0, alpha=0.2, seed=1), 2, 3)
     o = OracleSEM(m.vxy, m.tri, P)
@@ -132,7 +132,7 @@ def brute_dense_K(m, P, c):
     return K
 
 
-@pytest.mark.parametrize("P", [1, 2, 3])
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 7])
 def test_dense_K_matches_direct_quadrature(P):
     m = mg.shuffle(mg.grid_mesh(3, 2, 1.5, 1.0, alpha=0.2, seed=5), 1, 2)
     assert m.ne <= 12
@@ -143,7 +143,7 @@ def test_dense_K_matches_direct_quadrature(P):
     assert np.abs(K - Kb).max() < 1e-12 * np.abs(Kb).max()
 
 
-@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("P", [2, 3, 5, 7])
 def test_K_properties(P):
     m = mg.grid_mesh(4, 3, 1.3, 1.0, alpha=0.2, seed=2)
     o = OracleSEM(m.vxy, m.tri, P, np.linspace(0.5, 3.0, m.ne))
@@ -155,7 +155,7 @@ def test_K_properties(P):
     assert ev[1] > 1e-8 * ev[-1]  # exactly one zero mode (connected mesh, natural BC)
 
 
-@pytest.mark.parametrize("P", [1, 2, 3])
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 7])
 def test_patch_test_linear_field(P):
     m = mg.shuffle(mg.grid_mesh(9, 7, 2.0, 1.5, alpha=0.2, seed=4), 5, 6)
     o = OracleSEM(m.vxy, m.tri, P, np.full(m.ne, 1.3))
@@ -169,7 +169,7 @@ def test_patch_test_linear_field(P):
     assert np.abs(Kl[~interior]).max() > 1e-6  # the boundary flux is really there
 
 
-@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("P", [2, 3, 5, 7])
 def test_lumped_mass_area_and_positivity(P):
     m = mg.shuffle(mg.grid_mesh(11, 6, 3.0, 1.0, alpha=0.25, seed=7, grade=(10.0, 2, 1)), 8, 9)
     o = OracleSEM(m.vxy, m.tri, P)
@@ -195,3 +195,11 @@ def test_standing_mode_rayleigh_quotient_converges(P, ratio):
     errs = [_rayleigh_err(P, n) for n in (4, 8, 16)]
     assert errs[2] < 2e-3
     assert errs[0] / errs[1] > ratio and errs[1] / errs[2] > ratio
+
+
+def test_standing_mode_higher_orders_more_accurate():
+    # NEXT-2 (orders 5 and 7 of PAPER.md:746-776): on the same coarse mesh the
+    # Rayleigh-quotient error drops with the order, and P5 converges fast
+    e3, e5, e7 = (_rayleigh_err(P, 4) for P in (3, 5, 7))
+    assert e5 < e3 / 20 and e7 < e5 / 20
+    assert _rayleigh_err(5, 2) / e5 > 30

@@ -131,3 +131,69 @@ def test_fp64_tables_rounded_once(P):
         for p in range(T["Np"]):
             assert T["Dr"][k, p] == float(sp.N(Dr[k][p], 40))
             assert T["Ds"][k, p] == float(sp.N(Ds[k][p], 40))
+
+
+# ---- P >= 4 (NEXT-2, reading R21): the high-precision path ---------------------
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_hp_path_reproduces_exact_tables_bitwise(P):
+    # two independent computations (sympy exact vs 60-digit mpmath) round to
+    # the same fp64 tables
+    T, H = R.tables(P), R.tables_hp(P)
+    for k in ("nodes", "wK", "Dr", "Ds"):
+        assert np.array_equal(T[k], H[k]), k
+
+
+@pytest.mark.parametrize("P", [4, 5, 6, 7])
+def test_hp_lobatto_edges_are_legendre_derivative_roots(P):
+    import mpmath as mp
+    v = R.lobatto01_hp(P)
+    assert v[0] == 0 and v[-1] == 1 and len(v) == P + 1
+    for x in v[1:-1]:  # P_P'(2x - 1) = 0  (textbook Gauss-Lobatto)
+        assert abs(mp.diff(lambda t: mp.legendre(P, t), 2 * x - 1)) < mp.mpf("1e-40")
+    nd = R.tables(P)["nodes"]
+    Np = (P + 1) * (P + 2) // 2
+    assert nd.shape == (Np, 2)
+    # edge v0-v1 carries the 1D points, in lattice order
+    assert np.array_equal(nd[:P + 1, 0], np.array([float(x) for x in v]))
+    assert (nd[:P + 1, 1] == 0).all()
+
+
+@pytest.mark.parametrize("P", [5, 7])
+def test_hp_dual_system_and_exactness(P):
+    import mpmath as mp
+    T = R.tables_hp(P)
+    C, ex = T["C"], T["exps"]
+    nd = R.nodes_hp(P)
+    Np = len(nd)
+    for q, (x, y) in enumerate(nd):  # N_p(x_q) = delta_pq
+        for p in range(Np):
+            val = mp.fsum(C[m, p] * x ** a * y ** b for m, (a, b) in enumerate(ex))
+            assert abs(val - (1 if p == q else 0)) < mp.mpf("1e-40")
+    w = T["wK"]
+    assert abs(w.sum() - 0.5) < 1e-15
+    xy = T["nodes"]
+    for a in range(P + 1):  # nodal quadrature exact to degree P
+        for b in range(P + 1 - a):
+            q = float(np.sum(w * xy[:, 0] ** a * xy[:, 1] ** b))
+            assert abs(q - float(closed_form_monomial(a, b))) < 1e-14, (a, b)
+    for a in range(P + 1):  # D exact on monomials of degree <= P
+        for b in range(P + 1 - a):
+            f = xy[:, 0] ** a * xy[:, 1] ** b
+            dfx = a * xy[:, 0] ** max(a - 1, 0) * xy[:, 1] ** b if a else 0 * f
+            dfy = b * xy[:, 0] ** a * xy[:, 1] ** max(b - 1, 0) if b else 0 * f
+            assert np.abs(T["Dr"] @ f - dfx).max() < 1e-10
+            assert np.abs(T["Ds"] @ f - dfy).max() < 1e-10
+
+
+def test_order_5_has_21_nodes_and_positive_weights_odd_orders_only():
+    # order 5 -> 21 local nodes.  The paper's orders 5-7: int N_p
+    # is positive for P = 5 and 7 but negative at the vertices for P = 4 and 6,
+    # where the lumped mass would not be positive (why R21 keeps P in {5, 7}).
+    assert R.tables(5)["Np"] == 21 and R.tables(7)["Np"] == 36
+    for P in (5, 7):
+        assert (R.tables(P)["wK"] > 0).all()
+    for P in (4, 6):
+        w = R.tables(P)["wK"]
+        verts = [0, P, (P + 1) * (P + 2) // 2 - 1]
+        assert (w[verts] < 0).all() and (np.delete(w, verts) > 0).all()
