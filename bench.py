@@ -235,6 +235,8 @@ def run_ours(args):
         out["scatter_ablation"] = scatter_ablation(ctx, pb, args, S)
     if rank == 0 and args.heun and world == 1:
         out["heun"] = heun_leg(ctx, pb, args, S, peak)
+    if rank == 0 and args.orders and world == 1:
+        out["orders_5_7"] = orders_leg(ctx, args, S, peak, peaks)
     ctx.close()
     if args.e2e:
         out["e2e"] = e2e(pb, args, S, local, rank, world, stream, dist)
@@ -327,6 +329,51 @@ def scatter_ablation(ctx, pb, args, S):
                      "launches_per_step": info["launches_per_step"], "global_colors": info["n_global_colors"],
                      "steps": K}
     ctx.sem_set_scatter(S.SEM_SCATTER_CHUNK)
+    return res
+
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
+
+
+def orders_leg(ctx, args, S, peak, peaks):
+    """NEXT-2: the paper's Benchmark 1 shape (2000 x 1000 units, 1M elements,
+    PAPER.md:572) at its orders 5 and 7, Hilbert vs the
+    shuffled file order ("None").  P5/P7 are FP64-bound."""
+    import torch
+    from paper_2104_08416_b200 import meshgen as mg
+    res = {}
+    stream = torch.cuda.current_stream()
+    for P in (5, 7):
+        pb = mg.config("B1", 1, degree=P)
+        Np = (P + 1) * (P + 2) // 2
+        flop_elem = 2.0 * (3 * Np * (Np + 1) / 2 + Np * Np)  # K^e entries (2 FMA + MUL) + symmetric mat-vec
+        for name, eo, no in [("hilbert", S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH),
+                             ("none", S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL)]:
+            ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, P, eo, no)
+            ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt)
+            ctx.sem_step_n(5)
+            K = max(50, min(args.steps, 300))
+            ctx.sem_set_kernel_timing(True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            ctx.sem_step_n(K)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / K
+            kt = ctx.sem_kernel_times()
+            ctx.sem_set_kernel_timing(False)
+            info = ctx.sem_get_info()
+            k7 = kt["k7_ms"] / max(kt["k7_launches"], 1)
+            b7, _ = k7_bytes(info)
+            tf = info["n_elements"] * flop_elem / (k7 * 1e-3) / 1e12
+            res["P%d_%s" % (P, name)] = {
+                "elements": info["n_elements"], "element_updates_per_s": info["n_elements"] / (ms * 1e-3),
+                "ms_per_step": ms, "k7_ms": k7, "k8_ms": kt["k8_ms"] / max(kt["k8_launches"], 1),
+                "alg_gbs": info["bytes_alg_per_step"] / (ms * 1e-3) / 1e9,
+                "k7_hbm_frac": b7 / (k7 * 1e-3) / 1e9 / peak,
+                "k7_fp64_tflops": tf, "k7_fp64_frac": tf / FP64_PEAK_TFLOPS,
+                "fp64_peak_tflops": FP64_PEAK_TFLOPS, "steps": K}
     return res
 
 
@@ -498,6 +545,7 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--no-heun", dest="heun", action="store_false")
+    ap.add_argument("--no-orders", dest="orders", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

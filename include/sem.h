@@ -328,6 +328,16 @@ sem_status sem_debug_partition(const int32_t *mu, int64_t E, int Np, int64_t N, 
                                int32_t *send_glob_out, int32_t *if_glob_out, int32_t *sum_start_out,
                                int32_t *sum_src_out);
 
+/*
+ * Host-only diagnostic (no GPU, no context): the reference-triangle tables the
+ * library derives for `degree` (refelem.cpp; readings R3, R4, R21): *np_out = Np,
+ * nodes_out [Np][2], wK_out / wM_out [Np] (stiffness / mass weights), Dr_out /
+ * Ds_out [Np][Np] with Dr[k][p] = dN_p/dr at node k.  Any output may be NULL.
+ * Errors: SEM_E_UNSUPPORTED (degree not in {2, 3, 5, 7}).
+ */
+sem_status sem_debug_ref_tables(int degree, int32_t *np_out, double *nodes_out, double *wK_out, double *wM_out,
+                                double *Dr_out, double *Ds_out);
+
 /* Library version string. */
 const char *sem_version(void);
 

@@ -28,8 +28,10 @@ int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 
 // Elements per chunk (one CTA iteration of K7): 256 by default; SEM_CHUNK=128|192|512
 // selects the other compiled variants (design experiments).
-int chunk_elems() {
+int chunk_elems(int P) {
     const char *v = getenv("SEM_CHUNK");
+    if (P == 5) return 128;  // shared-memory budget of the stage at 21 nodes per element
+    if (P == 7) return 64;   // ... and at 36
     const int b = v ? atoi(v) : 256;
     return (b == 128 || b == 192 || b == 512) ? b : 256;
 }
@@ -669,8 +671,9 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
                             int32_t *node_perm_out, int64_t *n_nodes_out,
                             int32_t grid_wh_out[2]) {
     ST(check_usable(ctx));
-    if (degree != 2 && degree != 3)
-        return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) + " (2 or 3)");
+    if (!degree_supported(degree))
+        return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) +
+                                                " (2, 3, 5 or 7; 4 and 6 have negative vertex weights, reading R21)");
     if (elem_order < 0 || elem_order > SEM_ORDER_DIST)
         return fail(ctx, SEM_E_UNSUPPORTED, "unknown element ordering " + std::to_string(elem_order));
     if (node_order < SEM_NODES_FIRST_TOUCH || node_order > SEM_NODES_VISIT)
@@ -798,7 +801,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
                 x0 = bb[0];
                 y0 = bb[1];
             }
-            double edge_t[4] = {0, 0, 0, 0};
+            double edge_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int i = 1; i < degree; i++) edge_t[i - 1] = ctx->T.node[i][0];  // lattice row j = 0
             int64_t levels = 0;
             CK(strategy_order(d_mu_can, ctx->d_vxy, ctx->d_tri_or, E, degree, N,
@@ -863,11 +866,12 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
 
         // ---- chunk metadata for the step kernel ----
         ChunkMeta m;
-        if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(), m, err,
+        if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree), m, err,
                           one ? nullptr : part.remote.data()))
             return fail(ctx, SEM_E_MESH, err);
         if (ctx->scatter != SEM_SCATTER_CHUNK) {
             if (!one) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters run with world_size 1");
+            if (degree > 3) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters are built for P = 2, 3");
             // rows of mu in internal ids; COLOR: greedy global element colouring in
             // element order (smallest colour absent from every node's elements,
             // PAPER.md:516), elements grouped by colour, ascending within a colour
@@ -1285,6 +1289,25 @@ sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N
     } catch (const std::bad_alloc &) {
         return SEM_E_OOM;
     }
+}
+
+sem_status sem_debug_ref_tables(int degree, int32_t *np_out, double *nodes_out, double *wK_out, double *wM_out,
+                                double *Dr_out, double *Ds_out) {
+    if (!degree_supported(degree)) return SEM_E_UNSUPPORTED;
+    RefTables T;
+    if (!build_ref_tables(degree, T)) return SEM_E_UNSUPPORTED;
+    const int Np = T.Np;
+    if (np_out) *np_out = Np;
+    for (int p = 0; p < Np; p++) {
+        if (nodes_out) { nodes_out[2 * p] = T.node[p][0]; nodes_out[2 * p + 1] = T.node[p][1]; }
+        if (wK_out) wK_out[p] = T.wK[p];
+        if (wM_out) wM_out[p] = T.wM[p];
+        for (int q = 0; q < Np; q++) {
+            if (Dr_out) Dr_out[p * Np + q] = T.Dr[p][q];
+            if (Ds_out) Ds_out[p * Np + q] = T.Ds[p][q];
+        }
+    }
+    return SEM_OK;
 }
 
 sem_status sem_debug_partition(const int32_t *mu, int64_t E, int Np, int64_t N, int rank, int world,

@@ -39,15 +39,170 @@ long double ipow(long double x, int n) {
     return r;
 }
 
+// Lattice-order local nodes for any P (readings R3, R21): (i, j) is a vertex at
+// (0,0), (P,0), (0,P); on edge 0 (v0-v1) if j = 0, edge 1 (v0-v2) if i = 0,
+// edge 2 (v1-v2) if i + j = P; interior otherwise, numbered in lattice order.
+LocalNode kGen[2][kMaxNp];
+const LocalNode *lattice_nodes(int P, LocalNode *out) {
+    int p = 0, m = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, p++) {
+            LocalNode n;
+            if (i == 0 && j == 0) n = {0, 0, 0};
+            else if (i == P && j == 0) n = {0, 1, 0};
+            else if (i == 0 && j == P) n = {0, 2, 0};
+            else if (j == 0) n = {1, 0, i - 1};
+            else if (i == 0) n = {1, 1, j - 1};
+            else if (i + j == P) n = {1, 2, j - 1};
+            else n = {2, 0, m++};
+            out[p] = n;
+        }
+    return out;
+}
+
+// ---- orders 5 and 7 (reading R21): Blyth-Pozrikidis Lobatto grid, binary128 ----
+typedef __float128 q128;
+
+q128 qabs(q128 x) { return x < 0 ? -x : x; }
+
+// Legendre P_n and P_n' at x (three-term recurrence).
+void legendre(int n, q128 x, q128 &p, q128 &dp) {
+    q128 p0 = 1, p1 = x;
+    if (n == 0) { p = 1; dp = 0; return; }
+    for (int k = 2; k <= n; k++) {
+        const q128 p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+    }
+    p = p1;
+    dp = n * (x * p1 - p0) / (x * x - 1);  // valid for |x| < 1
+}
+
+// Gauss-Lobatto points on [0, 1]: 0, 1 and the roots of P_P'(2v - 1); Newton on
+// P_P' from the Chebyshev-Gauss-Lobatto guesses; exact symmetry v_{P-i} = 1 - v_i.
+void lobatto01(int P, q128 *v) {
+    const q128 pi = (q128)3.14159265358979323846264338327950288L;
+    v[0] = 0;
+    v[P] = 1;
+    for (int i = 1; i < P; i++) {
+        q128 x = -cosl((long double)(pi * i / P));
+        for (int it = 0; it < 100; it++) {
+            // f = P_P'(x), f' = P_P''(x) = (2x P_P' - P(P+1) P_P) / (1 - x^2)
+            q128 p, dp;
+            legendre(P, x, p, dp);
+            const q128 d2 = (2 * x * dp - (q128)P * (P + 1) * p) / (1 - x * x);
+            const q128 dx = dp / d2;
+            x -= dx;
+            if (qabs(dx) < (q128)1e-33L) break;
+        }
+        v[i] = (x + 1) / 2;
+    }
+    for (int i = 0; i <= P / 2; i++) v[P - i] = 1 - v[i];
+    if (P % 2 == 0) v[P / 2] = (q128)0.5L;
+}
+
+bool build_tables_q(int P, RefTables &T) {
+    const int Np = (P + 1) * (P + 2) / 2;
+    q128 v[kMaxNp], nx[kMaxNp], ny[kMaxNp];
+    lobatto01(P, v);
+    int p = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, p++) {
+            const int k = P - i - j;
+            nx[p] = (i == 0) ? 0 : (1 + 2 * v[i] - v[j] - v[k]) / 3;  // edges x = 0, y = 0 exact
+            ny[p] = (j == 0) ? 0 : (1 + 2 * v[j] - v[i] - v[k]) / 3;
+        }
+    int ea[kMaxNp], eb[kMaxNp], nm = 0;
+    for (int a = 0; a <= P; a++)
+        for (int b = 0; b + a <= P; b++) { ea[nm] = a; eb[nm] = b; nm++; }
+    static q128 A[kMaxNp][2 * kMaxNp];
+    auto qpow = [](q128 x, int n) { q128 r = 1; for (int i = 0; i < n; i++) r *= x; return r; };
+    for (int q = 0; q < Np; q++) {
+        for (int m = 0; m < Np; m++) A[q][m] = qpow(nx[q], ea[m]) * qpow(ny[q], eb[m]);
+        for (int m = 0; m < Np; m++) A[q][Np + m] = (q == m) ? 1 : 0;
+    }
+    for (int col = 0; col < Np; col++) {  // Gauss-Jordan, partial pivoting
+        int piv = col;
+        for (int r = col + 1; r < Np; r++)
+            if (qabs(A[r][col]) > qabs(A[piv][col])) piv = r;
+        if (qabs(A[piv][col]) < (q128)1e-30L) return false;
+        if (piv != col)
+            for (int k = 0; k < 2 * Np; k++) { const q128 t = A[col][k]; A[col][k] = A[piv][k]; A[piv][k] = t; }
+        const q128 d = A[col][col];
+        for (int k = 0; k < 2 * Np; k++) A[col][k] /= d;
+        for (int r = 0; r < Np; r++) {
+            if (r == col) continue;
+            const q128 f = A[r][col];
+            if (f == 0) continue;
+            for (int k = 0; k < 2 * Np; k++) A[r][k] -= f * A[col][k];
+        }
+    }
+    auto mono_int_q = [](int a, int b) {  // a! b! / (a+b+2)!
+        q128 f = 1;
+        for (int i = 2; i <= a; i++) f *= i;
+        for (int i = 2; i <= b; i++) f *= i;
+        for (int i = 2; i <= a + b + 2; i++) f /= i;
+        return f;
+    };
+    static q128 w[kMaxNp], Dr[kMaxNp][kMaxNp], Ds[kMaxNp][kMaxNp];
+    for (int pp = 0; pp < Np; pp++) {
+        q128 s = 0;
+        for (int m = 0; m < Np; m++) s += A[m][Np + pp] * mono_int_q(ea[m], eb[m]);
+        w[pp] = s;
+        if (!(s > 0)) return false;  // P = 4, 6: negative vertex weights (R21)
+    }
+    for (int k = 0; k < Np; k++)
+        for (int pp = 0; pp < Np; pp++) {
+            q128 dr = 0, ds = 0;
+            for (int m = 0; m < Np; m++) {
+                if (ea[m] > 0) dr += A[m][Np + pp] * ea[m] * qpow(nx[k], ea[m] - 1) * qpow(ny[k], eb[m]);
+                if (eb[m] > 0) ds += A[m][Np + pp] * eb[m] * qpow(nx[k], ea[m]) * qpow(ny[k], eb[m] - 1);
+            }
+            Dr[k][pp] = dr;
+            Ds[k][pp] = ds;
+        }
+    auto rd = [](q128 x) { return qabs(x) < (q128)1e-24L ? 0.0 : (double)x; };  // residue of exact zeros
+    T.P = P;
+    T.Np = Np;
+    for (int pp = 0; pp < Np; pp++) {
+        T.node[pp][0] = rd(nx[pp]);
+        T.node[pp][1] = rd(ny[pp]);
+        T.wK[pp] = rd(w[pp]);
+        T.wM[pp] = rd(w[pp]);
+        for (int k = 0; k < Np; k++) { T.Dr[k][pp] = rd(Dr[k][pp]); T.Ds[k][pp] = rd(Ds[k][pp]); }
+    }
+    std::memset(&T.Srr, 0, sizeof(T.Srr));
+    std::memset(&T.Sss, 0, sizeof(T.Sss));
+    std::memset(&T.Srs, 0, sizeof(T.Srs));
+    for (int a = 0; a < Np; a++)
+        for (int b = 0; b < Np; b++) {
+            q128 rr = 0, ss = 0, rs = 0;
+            for (int k = 0; k < Np; k++) {
+                rr += w[k] * Dr[k][a] * Dr[k][b];
+                ss += w[k] * Ds[k][a] * Ds[k][b];
+                rs += w[k] * (Dr[k][a] * Ds[k][b] + Ds[k][a] * Dr[k][b]);
+            }
+            T.Srr[a][b] = rd(rr);
+            T.Sss[a][b] = rd(ss);
+            T.Srs[a][b] = rd(rs);
+        }
+    return true;
+}
+
 }  // namespace
+
+bool degree_supported(int P) { return P == 2 || P == 3 || P == 5 || P == 7; }
 
 const LocalNode *local_nodes(int P) {
     if (P == 2) return kP2;
     if (P == 3) return kP3;
+    if (P == 5) return lattice_nodes(5, kGen[0]);
+    if (P == 7) return lattice_nodes(7, kGen[1]);
     return nullptr;
 }
 
 bool build_ref_tables(int P, RefTables &T) {
+    if (P == 5 || P == 7) return build_tables_q(P, T);
     if (P != 2 && P != 3) return false;
     const int Np = (P + 1) * (P + 2) / 2;
     T.P = P;
@@ -126,12 +281,15 @@ bool build_ref_tables(int P, RefTables &T) {
     std::memset(&T.Srr, 0, sizeof(T.Srr));
     std::memset(&T.Sss, 0, sizeof(T.Sss));
     std::memset(&T.Srs, 0, sizeof(T.Srs));
+    // round once; |x| < 1e-14 is the 80-bit residue of an exact zero (e.g. the P2
+    // vertex weights, derivative entries that vanish by symmetry)
+    auto rd = [](long double x) { return fabsl(x) < 1e-14L ? 0.0 : (double)x; };
     for (int p = 0; p < Np; p++) {
         T.node[p][0] = (double)nx[p];
         T.node[p][1] = (double)ny[p];
-        T.wK[p] = (double)wK[p];
-        T.wM[p] = (double)wM[p];
-        for (int k = 0; k < Np; k++) { T.Dr[k][p] = (double)Dr[k][p]; T.Ds[k][p] = (double)Ds[k][p]; }
+        T.wK[p] = rd(wK[p]);
+        T.wM[p] = rd(wM[p]);
+        for (int k = 0; k < Np; k++) { T.Dr[k][p] = rd(Dr[k][p]); T.Ds[k][p] = rd(Ds[k][p]); }
     }
     for (int p = 0; p < Np; p++)
         for (int q = 0; q < Np; q++) {

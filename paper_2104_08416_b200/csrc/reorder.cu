@@ -175,7 +175,7 @@ __global__ void k_fill_i32(int32_t *a, int64_t n, int32_t v) {
 
 // ---- K4 canonical nodes -----------------------------------------------------
 __constant__ int c_edge_v[3][2] = {{0, 1}, {0, 2}, {1, 2}};
-__constant__ int c_ln[10][3];  // local node table of the current degree (R3)
+__constant__ int c_ln[kMaxNp][3];  // local node table of the current degree (R3)
 
 __global__ void k_edge_keys(const int32_t *__restrict__ tri, int64_t E, uint64_t *keys,
                             int32_t *vals) {
@@ -322,7 +322,7 @@ __global__ void k_group_sort(const int32_t *__restrict__ excl, int64_t E, int Np
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= E) return;
     const int32_t a = excl[e * Np], b = excl[(e + 1) * Np];
-    int32_t v[16];
+    int32_t v[kMaxNp];
     const int n = b - a;
     for (int i = 0; i < n; i++) v[i] = node_perm[a + i];
     for (int i = 1; i < n; i++) {
@@ -349,7 +349,7 @@ __global__ void k_key_degree(const int32_t *__restrict__ deg, int64_t N, uint64_
 // vertices exact; edge node m (1..P-1) from the lower-id end a: a + t_m (b - a);
 // P3 interior node: ((v0 + v1) + v2) / 3.  Explicit round-to-nearest, no FMA.
 // A node written by several elements gets identical bits from each.
-__constant__ double c_edge_t[4];
+__constant__ double c_edge_t[8];
 __global__ void k_key_dist(const double *__restrict__ vxy, const int32_t *__restrict__ tri,
                            const int32_t *__restrict__ mu, int64_t E, int P, double x0, double y0,
                            uint64_t *key) {
@@ -531,7 +531,7 @@ cudaError_t canonical_nodes(const int32_t *tri_or, int64_t nv, int64_t E, int P,
     const LocalNode *ln = local_nodes(P);
     if (!ln) return cudaErrorInvalidValue;
     const int Np = (P + 1) * (P + 2) / 2;
-    int h_ln[10][3] = {};
+    int h_ln[kMaxNp][3] = {};
     for (int p = 0; p < Np; p++) { h_ln[p][0] = ln[p].kind; h_ln[p][1] = ln[p].which; h_ln[p][2] = ln[p].m; }
     RET(cudaMemcpyToSymbolAsync(c_ln, h_ln, sizeof(h_ln), 0, cudaMemcpyHostToDevice, s));
     const int64_t n = 3 * E;

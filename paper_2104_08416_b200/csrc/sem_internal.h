@@ -10,7 +10,7 @@
 
 namespace sem {
 
-constexpr int kMaxNp = 10;
+constexpr int kMaxNp = 36;  // P = 7
 
 // ---------------------------------------------------------------------------
 // Reference triangle tables, derived on the host in long double (refelem.cpp).
@@ -28,6 +28,7 @@ struct RefTables {
     double Srr[kMaxNp][kMaxNp], Sss[kMaxNp][kMaxNp], Srs[kMaxNp][kMaxNp];
 };
 bool build_ref_tables(int P, RefTables &out);
+bool degree_supported(int P);  // P in {2, 3, 5, 7} (reading R21)
 
 // Local node kinds of the lattice order (R3): kind 0 = vertex (which = local
 // vertex), 1 = edge (which = local edge 0:v0v1 1:v0v2 2:v1v2, m = position from

@@ -172,7 +172,7 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
 
 // ---- K7 ---------------------------------------------------------------------------
 template <int NP, int B>
-__global__ void __launch_bounds__(B + 32, (B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -465,6 +465,8 @@ size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls) {
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
 K7Fn k7_fn(int np, int B) {
+    if (np == 21) return k7_step<21, 128>;  // P5 (R21): chunks of 128
+    if (np == 36) return k7_step<36, 64>;   // P7: chunks of 64
     if (np == 6)
         return B == 128 ? k7_step<6, 128> : B == 192 ? k7_step<6, 192> : B == 512 ? k7_step<6, 512> : k7_step<6, 256>;
     return B == 128 ? k7_step<10, 128> : B == 192 ? k7_step<10, 192> : B == 512 ? k7_step<10, 512> : k7_step<10, 256>;
@@ -495,7 +497,11 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer,
     cudaError_t e;
     if ((e = cudaMemsetAsync(dt2M, 0, sizeof(double) * (ch.N_tot + 2), s))) return e;
 #define MASS(NP_, B_) k_mass_chunk<NP_, B_><<<(unsigned)ch.nchunks, B_, 0, s>>>(ch, detJ, dt2, slot, dt2M)
-    if (ch.Np == 6) {
+    if (ch.Np == 21) {
+        MASS(21, 128);
+    } else if (ch.Np == 36) {
+        MASS(36, 64);
+    } else if (ch.Np == 6) {
         if (ch.B == 128) MASS(6, 128); else if (ch.B == 192) MASS(6, 192); else if (ch.B == 512) MASS(6, 512); else MASS(6, 256);
     } else {
         if (ch.B == 128) MASS(10, 128); else if (ch.B == 192) MASS(10, 192); else if (ch.B == 512) MASS(10, 512); else MASS(10, 256);

@@ -29,7 +29,7 @@ import numpy as np
 # Reading R8: CFL factors for dt = kappa * min(inradius / c). Chosen so that
 # dt sits well below the element-Gershgorin-safe step on every config
 # (tests/test_inputs.py checks it against the oracle's bound).
-KAPPA = {2: 0.35, 3: 0.15}
+KAPPA = {2: 0.35, 3: 0.15, 5: 0.05, 7: 0.01}  # P5, P7 (reading R21): measured dt_crit / min(inradius/c) = 0.17 (P5), 0.024 (P7; smallest weight 1.4e-4)
 
 
 @dataclasses.dataclass
@@ -206,7 +206,7 @@ def _finish(name, nat: Mesh, P, c_nat, f0, n_steps, s, dt=None, shuffled=True):
                    amplitude=1.0, dt=dt, n_steps=n_steps, natural=nat, c_natural=c_nat)
 
 
-def config(name: str, scale: int = 1, gpus: int = 1) -> Problem:
+def config(name: str, scale: int = 1, gpus: int = 1, degree: int | None = None) -> Problem:
     """Build a BASELINE.json configuration.
 
     name: C1..C5; `scale` divides the cell counts (tests use reduced sizes of the
@@ -249,6 +249,17 @@ def config(name: str, scale: int = 1, gpus: int = 1) -> Problem:
         speeds = rng.uniform(1500.0, 4500.0, size=10)
         c = layered_speed(nat, breaks, speeds)
         return _finish("C5", nat, 2, c, 10.0, 200, s)
+    if name == "B1":
+        # The paper's Benchmark 1: single-layered domain 2000 units
+        # wide and 1000 deep, homogeneous element sizes, 250k / 500k / 1M elements,
+        # orders 5-7.  Synthetic stand-in for its Gmsh mesh:
+        # 1000 x 500 cells -> 1M triangles at scale 1; +-0.2h jitter; c = 2000;
+        # Ricker 10 Hz at the centre.  Degree from `degree` (default 5).
+        s = 5
+        nx, ny = max(2, 1000 // scale), max(2, 500 // scale)
+        nat = grid_mesh(nx, ny, 2000.0, 1000.0, alpha=0.2, seed=s)
+        c = np.full(nat.ne, 2000.0)
+        return _finish("B1", nat, degree or 5, c, 10.0, 200, s)
     raise KeyError(name)
 
 

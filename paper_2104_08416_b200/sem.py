@@ -32,7 +32,7 @@ EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem
             "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version",
             "sem_debug_chunk_stats", "sem_debug_partition", "sem_nccl_unique_id",
             "sem_group_build_operators", "sem_group_step_n", "sem_set_integrator", "sem_read_velocity",
-            "sem_write_velocity", "sem_set_scatter"]
+            "sem_write_velocity", "sem_set_scatter", "sem_debug_ref_tables"]
 
 
 class SemError(RuntimeError):
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         L.sem_group_step_n.argtypes = [P, C.c_int, i64]
         L.sem_set_integrator.argtypes = [P, C.c_int]
         L.sem_set_scatter.argtypes = [P, C.c_int]
+        L.sem_debug_ref_tables.argtypes = [C.c_int, P, P, P, P, P, P]
         L.sem_read_velocity.argtypes = [P, P, C.POINTER(i64)]
         L.sem_write_velocity.argtypes = [P, P]
         L.sem_version.argtypes = []
@@ -264,6 +265,23 @@ def sem_debug_chunk_stats(mu, N: int, B: int = 256, want_maps: bool = False):
         d["int_of"] = int_of
         d["cmeta"] = cmeta.reshape(nch, 8)
     return d
+
+
+def sem_debug_ref_tables(degree: int) -> dict:
+    """Host-only: the library's reference tables (see include/sem.h)."""
+    L = load()
+    n = np.zeros(1, np.int32)
+    rc = L.sem_debug_ref_tables(degree, _ptr(n), None, None, None, None, None)
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_debug_ref_tables(%d)" % degree)
+    Np = int(n[0])
+    out = {"Np": Np, "nodes": np.empty((Np, 2)), "wK": np.empty(Np), "wM": np.empty(Np),
+           "Dr": np.empty((Np, Np)), "Ds": np.empty((Np, Np))}
+    rc = L.sem_debug_ref_tables(degree, _ptr(n), _ptr(out["nodes"]), _ptr(out["wK"]), _ptr(out["wM"]),
+                                _ptr(out["Dr"]), _ptr(out["Ds"]))
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_debug_ref_tables(%d)" % degree)
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -4,6 +4,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 from paper_2104_08416_b200 import build, sem
@@ -55,3 +56,22 @@ def test_no_gpu_fails_loudly(lib):
     with pytest.raises(sem.SemError) as e:
         sem.SemContext(0)
     assert e.value.status == sem.SEM_E_CUDA
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 7])
+def test_library_reference_tables_equal_oracle(P):
+    # host-only: the library derives its tables independently (80-bit / binary128
+    # Gauss-Jordan in refelem.cpp); they round to the oracle's fp64 values
+    # (sympy exact / 60-digit mpmath) bit for bit
+    from oracle import refelem
+    g = sem.sem_debug_ref_tables(P)
+    o = refelem.tables(P)
+    for k in ("nodes", "wK", "wM", "Dr", "Ds"):
+        assert np.array_equal(g[k], o[k]), k
+
+
+@pytest.mark.parametrize("P", [1, 4, 6, 8])
+def test_library_rejects_unsupported_degrees(P):
+    with pytest.raises(sem.SemError) as e:
+        sem.sem_debug_ref_tables(P)
+    assert e.value.status == sem.SEM_E_UNSUPPORTED

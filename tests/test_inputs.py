@@ -55,3 +55,16 @@ def test_layers():
     cen = mg.centroids(pb.mesh)
     depth = 4000.0 - cen[:, 1]
     assert (pb.c[depth < 1000.0] == 1500.0).all() and (pb.c[depth >= 2500.0] == 3500.0).all()
+
+
+@pytest.mark.parametrize("P", [5, 7])
+def test_b1_dt_below_half_cfl_high_order(P):
+    # the Benchmark 1 stand-in at orders 5 and 7 (reading R21 CFL factors)
+    pb = mg.config("B1", 50, degree=P)
+    assert pb.P == P and pb.mesh.ne == 2 * 20 * 10
+    o = OracleSEM(pb.mesh.vxy, pb.mesh.tri, P, pb.c)
+    assert pb.dt < 0.5 * 2.0 / math.sqrt(_lam_max(o))
+    # with the C2 recipe at P5/P7 too (graded-free jittered square, alpha 0.25)
+    pc = mg.config("C2", 32)
+    o2 = OracleSEM(pc.mesh.vxy, pc.mesh.tri, P, pc.c)
+    assert mg.cfl_dt(pc.natural, pc.c_natural, P) < 0.5 * 2.0 / math.sqrt(_lam_max(o2))
