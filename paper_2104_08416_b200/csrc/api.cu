@@ -245,6 +245,35 @@ cudaError_t upload(std::vector<void *> &list, T **dst, const std::vector<T> &src
     return cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s);
 }
 
+// SEM_CHUNK_CHECK=1: the GPU chunk builder's arrays against the host builder's.
+template <typename T>
+bool same_dev(const std::vector<T> &h, const T *dptr, size_t n, cudaStream_t s) {
+    if (h.size() < n) return false;
+    std::vector<T> g(n);
+    if (n && cudaMemcpyAsync(g.data(), dptr, sizeof(T) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
+    cudaStreamSynchronize(s);
+    return n == 0 || std::memcmp(g.data(), h.data(), sizeof(T) * n) == 0;
+}
+
+std::string compare_chunks(const ChunkMeta &h, const ChunkMeta &m, const DevChunks &d, const int32_t *d_int_of,
+                           cudaStream_t s) {
+    if (h.nchunks != m.nchunks || h.N_int != m.N_int || h.N_sh != m.N_sh || h.N_if != m.N_if ||
+        h.n_slots != m.n_slots || h.max_local != m.max_local || h.max_win != m.max_win ||
+        h.max_lptr != m.max_lptr || h.max_nsh != m.max_nsh)
+        return "scalars";
+    if (h.bnd_chunks != m.bnd_chunks || h.int_chunks != m.int_chunks) return "chunk lists";
+    if (!same_dev(h.cmeta, d.cmeta, h.cmeta.size(), s)) return "cmeta";
+    if (!same_dev(h.lidx, d.lidx, h.lidx.size(), s)) return "lidx";
+    if (!same_dev(h.lpos, d.lpos, h.lpos.size(), s)) return "lpos";
+    if (!same_dev(h.lptr, d.lptr, h.lptr.size(), s)) return "lptr";
+    if (!same_dev(h.sh_pstart, d.sh_pstart, h.sh_pstart.size(), s)) return "sh_pstart";
+    if (!same_dev(h.shl_node, d.shl_node, h.shl_node.size(), s)) return "shl_node";
+    if (!same_dev(h.shl_slot, d.shl_slot, h.shl_slot.size(), s)) return "shl_slot";
+    if (!same_dev(h.shl_cr, d.shl_cr, h.shl_cr.size(), s)) return "shl_cr";
+    if (!same_dev(h.int_of, d_int_of, h.int_of.size(), s)) return "int_of";
+    return "";
+}
+
 sem_status ensure_tables(sem_ctx *ctx) {
     if (g_const_P != ctx->P) {
         CK(upload_ref_tables(ctx->T, ctx->stream));
@@ -551,7 +580,19 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     CK(cudaStreamSynchronize(s));
     if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has detJ <= 0");
     ctx->src_int = -1;
-    if (src_vertex >= 0)  // vertex node: canonical id == input vertex id (R13)
+    if (src_vertex >= 0 && ctx->src_lookup.empty()) {  // one rank: search the device map
+        int32_t *d_l = nullptr;
+        CK(dalloc(tmp, &d_l, 1));
+        CK(launch_find_i32(ctx->d_loc_can, ctx->N, (int32_t)src_vertex, d_l, s));
+        int32_t l = INT_MAX;
+        CK(cudaMemcpyAsync(&l, d_l, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (l != INT_MAX) {
+            CK(cudaMemcpyAsync(&ctx->src_int, ctx->d_loc_int + l, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+    if (src_vertex >= 0)  // several ranks: host maps (vertex node: canonical id == input vertex id, R13)
         for (size_t l = 0; l < ctx->src_lookup.size(); l++)
             if (ctx->src_lookup[l] == (int32_t)src_vertex) { ctx->src_int = ctx->src_int_of[l]; break; }
     ctx->amp = amplitude;
@@ -833,13 +874,24 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
 
         tr.mark(s, "node numbering");
         // ---- host outputs ----
-        std::vector<int32_t> node_perm(N), mu_h((size_t)E * Np);
-        CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(mu_h.data(), d_mu_ft, sizeof(int32_t) * E * Np, cudaMemcpyDeviceToHost, s));
+        const bool one = ctx->world == 1;  // fast path: every node local, identity maps
+        // chunk metadata built on the GPU (chunks_gpu.cu) unless a host-side consumer needs mu
+        const bool gpu_chunks = one && ctx->scatter == SEM_SCATTER_CHUNK && getenv("SEM_HOST_CHUNKS") == nullptr;
+        const bool check_chunks = gpu_chunks && getenv("SEM_CHUNK_CHECK") != nullptr;
+        std::vector<int32_t> node_perm, mu_h;
+        if (!one) {  // the partition and the rank maps need it on the host
+            node_perm.resize(N);
+            CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+        }
+        if (node_perm_out)
+            CK(cudaMemcpyAsync(node_perm_out, d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+        if (!gpu_chunks || check_chunks) {
+            mu_h.resize((size_t)E * Np);
+            CK(cudaMemcpyAsync(mu_h.data(), d_mu_ft, sizeof(int32_t) * E * Np, cudaMemcpyDeviceToHost, s));
+        }
         if (elem_perm_out)
             CK(cudaMemcpyAsync(elem_perm_out, ctx->d_perm, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        if (node_perm_out) std::memcpy(node_perm_out, node_perm.data(), sizeof(int32_t) * N);
         if (n_nodes_out) *n_nodes_out = N;
         if (grid_wh_out) { grid_wh_out[0] = ctx->grid[0]; grid_wh_out[1] = ctx->grid[1]; }
 
@@ -847,7 +899,6 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         // ---- this rank's part: contiguous range of the global order ----
         Partition part;
         std::string err;
-        const bool one = ctx->world == 1;  // fast path: every node local, identity maps
         if (!one) {
             if (!build_partition(mu_h.data(), E, Np, N, ctx->rank, ctx->world, part, err))
                 return fail(ctx, SEM_E_MESH, err);
@@ -866,9 +917,26 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
 
         // ---- chunk metadata for the step kernel ----
         ChunkMeta m;
-        if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree), m, err,
-                          one ? nullptr : part.remote.data()))
+        DevChunks &d = ctx->dch;
+        auto &L = ctx->mesh_allocs;
+        if (gpu_chunks) {
+            const DeviceAlloc da = [&L](void **p, size_t bytes) { return dalloc(L, (char **)p, bytes); };
+            CK(build_chunks_gpu(d_mu_ft, E, Np, N, chunk_elems(degree), nullptr, da, m, d, &ctx->d_loc_int,
+                                &ctx->d_bnd, &ctx->d_intc, err, s));
+            if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
+            if (check_chunks) {
+                ChunkMeta h;
+                if (!build_chunks(mu_h.data(), E, Np, N, chunk_elems(degree), h, err)) return fail(ctx, SEM_E_MESH, err);
+                const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
+                if (!diff.empty()) return fail(ctx, SEM_E_MESH, "GPU chunk builder differs from the host's: " + diff);
+            }
+            std::vector<int32_t>().swap(mu_h);
+            tr.mark(s, "chunk builder (GPU)");
+        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree), m,
+                                 err, one ? nullptr : part.remote.data())) {
             return fail(ctx, SEM_E_MESH, err);
+        }
+        if (!gpu_chunks) {
         if (ctx->scatter != SEM_SCATTER_CHUNK) {
             if (!one) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters run with world_size 1");
             if (degree > 3) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters are built for P = 2, 3");
@@ -911,11 +979,9 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         }
         std::vector<int32_t>().swap(mu_h);
         tr.mark(s, "chunk builder (host)");
-        DevChunks &d = ctx->dch;
         d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
         d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
         d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
-        auto &L = ctx->mesh_allocs;
         int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
         uint16_t *p_lpos, *p_lptr, *p_lidx, *p_shcr;
         CK(upload(L, &p_cmeta, m.cmeta, s));
@@ -930,10 +996,11 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         d.shl_node = p_shn;
         d.shl_slot = p_shs;
         d.shl_cr = p_shcr;
+        }  // host-built chunks
         // node maps for I/O (local node l -> internal / canonical / reordered id)
         if (one) {
             // reordered id == local id; the device node_perm (reordered -> canonical) is kept
-            CK(upload(L, &ctx->d_loc_int, m.int_of, s));
+            if (!gpu_chunks) CK(upload(L, &ctx->d_loc_int, m.int_of, s));
             ctx->d_loc_can = d_node_perm;
             for (auto it = tmp.begin(); it != tmp.end(); ++it)
                 if (*it == (void *)d_node_perm) { L.push_back(*it); tmp.erase(it); break; }
@@ -942,8 +1009,8 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             ctx->d_own_can = ctx->d_loc_can;
             ctx->d_own_ft = nullptr;
             ctx->n_own = N;
-            ctx->src_lookup.swap(node_perm);   // for the source vertex lookup
-            ctx->src_int_of.swap(m.int_of);
+            ctx->src_lookup.clear();  // the source vertex is looked up on the device (d_loc_can)
+            ctx->src_int_of.clear();
         } else {
             std::vector<int32_t> loc_int(ctx->N), loc_can(ctx->N), own_int, own_can, own_ft;
             ctx->src_lookup.assign(ctx->N, -1);
@@ -976,8 +1043,10 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         ctx->nbr_off = part.nbr_off;
         ctx->n_bnd = (int64_t)m.bnd_chunks.size();
         ctx->n_intc = (int64_t)m.int_chunks.size();
-        CK(upload(L, &ctx->d_bnd, m.bnd_chunks, s));
-        CK(upload(L, &ctx->d_intc, m.int_chunks, s));
+        if (!gpu_chunks) {
+            CK(upload(L, &ctx->d_bnd, m.bnd_chunks, s));
+            CK(upload(L, &ctx->d_intc, m.int_chunks, s));
+        }
         CK(upload(L, &ctx->d_send_if, part.send_if, s));
         CK(upload(L, &ctx->d_sum_start, part.sum_start, s));
         CK(upload(L, &ctx->d_sum_src, part.sum_src, s));

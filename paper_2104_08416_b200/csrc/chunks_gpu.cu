@@ -1,0 +1,517 @@
+// chunks_gpu.cu -- the chunk builder of chunks.cpp on the GPU (product path).
+//
+// Same metadata, bit for bit (tests/test_gpu_chunks.py compares every array
+// with the host builder): chunks of B consecutive elements; nodes touched by
+// one chunk are interior (contiguous window per chunk, descending entry count
+// then ascending id), the others shared (non-interface ascending id, then
+// interface ascending id) with one node-major slot per touching chunk in
+// ascending chunk order; per-chunk local indices, CSR row pointers and CSR
+// positions.  Built from three radix sorts:
+//   1. entries (chunk, node) in [chunk][p][t] order -> (chunk, node) runs,
+//      entries of a run ascending in p*B + t (stable sort);
+//   2. runs by (chunk, shared?, 255 - count, id or shared index) -> the local
+//      order of every chunk (interior first, then shared);
+//   3. runs by (node, chunk) -> the rank of a chunk among a shared node's chunks
+//      (its slot).
+// Everything else is scans and scatters.  Replaces ~0.8 s of host work and
+// the 0.3 GB connectivity round trip on C4.
+#include <cub/cub.cuh>
+
+#include <climits>
+
+#include "kernels.h"
+
+namespace sem {
+
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned nb(int64_t n) {
+    int64_t b = (n + kT - 1) / kT;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+inline int bits_for(int64_t v) {  // smallest b with v < 2^b
+    int b = 1;
+    while (b < 63 && ((int64_t)1 << b) <= v) b++;
+    return b;
+}
+
+struct Tmp {
+    void *p = nullptr;
+    cudaStream_t s;
+    explicit Tmp(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, n ? n : 16, s); }
+    template <typename T> T *as() { return (T *)p; }
+    ~Tmp() { if (p) cudaFreeAsync(p, s); }
+};
+
+#define RET(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)
+
+template <typename T>
+cudaError_t excl_scan(const T *in, T *out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    RET(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    Tmp t(s);
+    RET(t.alloc(bytes));
+    return cub::DeviceScan::ExclusiveSum(t.p, bytes, in, out, n, s);
+}
+
+template <typename T>
+cudaError_t incl_scan(const T *in, T *out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    RET(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, n, s));
+    Tmp t(s);
+    RET(t.alloc(bytes));
+    return cub::DeviceScan::InclusiveSum(t.p, bytes, in, out, n, s);
+}
+
+cudaError_t sort_u64(const uint64_t *k, const int32_t *v, uint64_t *k2, int32_t *v2, int64_t n, int end_bit,
+                     cudaStream_t s) {
+    size_t bytes = 0;
+    RET(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, k2, v, v2, n, 0, end_bit, s));
+    Tmp t(s);
+    RET(t.alloc(bytes));
+    return cub::DeviceRadixSort::SortPairs(t.p, bytes, k, k2, v, v2, n, 0, end_bit, s);
+}
+
+// 1. entries in [chunk][p][t] order; padding entries get the largest key
+__global__ void k_entry_keys(const int32_t *__restrict__ mu, int64_t E, int Np, int B, int64_t n_ent, int bn,
+                             uint64_t pad_key, uint64_t *key, int32_t *val) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n_ent) return;
+    const int64_t c = k / ((int64_t)Np * B);
+    const int r = (int)(k % ((int64_t)Np * B));
+    const int p = r / B, t = r % B;
+    const int64_t e = c * B + t;
+    key[k] = (e < E) ? (((uint64_t)c << bn) | (uint32_t)mu[e * Np + p]) : pad_key;
+    val[k] = (int32_t)k;
+}
+
+__global__ void k_heads64(const uint64_t *__restrict__ key, int64_t n, int32_t *flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// run r starts at sorted position start[r]; rid = inclusive scan of heads
+__global__ void k_run_starts(const int32_t *__restrict__ flag, const int32_t *__restrict__ rid, int64_t n,
+                             int32_t *start) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) start[rid[i] - 1] = (int32_t)i;
+}
+
+__global__ void k_run_info(const uint64_t *__restrict__ key, const int32_t *__restrict__ start, int64_t nruns,
+                           int64_t n, int bn, int32_t *rc, int32_t *rg, int32_t *rlen, int32_t *nref) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    const uint64_t k = key[start[r]];
+    const int32_t g = (int32_t)(k & (((uint64_t)1 << bn) - 1));
+    rc[r] = (int32_t)(k >> bn);
+    rg[r] = g;
+    rlen[r] = (int32_t)((r + 1 < nruns ? start[r + 1] : n) - start[r]);
+    atomicAdd(&nref[g], 1);
+}
+
+__global__ void k_node_class(const int32_t *__restrict__ nref, const uint8_t *__restrict__ forced, int64_t N,
+                             int32_t *a, int32_t *b, int32_t *unused) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    const bool f = forced && forced[g];
+    a[g] = (nref[g] > 1 && !f) ? 1 : 0;
+    b[g] = f ? 1 : 0;
+    if (nref[g] == 0) atomicMin(unused, (int32_t)g);
+}
+
+// shared index of g: non-interface ascending id, then interface ascending id (-1 interior)
+__global__ void k_shared_index(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
+                               const int32_t *__restrict__ ea, const int32_t *__restrict__ eb, int64_t N,
+                               int32_t na, int32_t *s_of, int32_t *node_of_s) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    int32_t s = -1;
+    if (a[g]) s = ea[g];
+    else if (b[g]) s = na + eb[g];
+    s_of[g] = s;
+    if (s >= 0) node_of_s[s] = (int32_t)g;
+}
+
+// 2. local-order key of every run; per-chunk interior / shared counts
+__global__ void k_local_keys(const int32_t *__restrict__ rc, const int32_t *__restrict__ rg,
+                             const int32_t *__restrict__ rlen, const int32_t *__restrict__ s_of, int64_t nruns,
+                             int bx, uint64_t *key, int32_t *val, int32_t *nint, int32_t *nsh) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    const int32_t c = rc[r], g = rg[r], s = s_of[g];
+    const bool sh = s >= 0;
+    const uint32_t cnt = (uint32_t)min(rlen[r], 255);
+    const uint64_t x = sh ? (uint32_t)s : (uint32_t)g;
+    key[r] = ((uint64_t)c << (9 + bx)) | ((uint64_t)(sh ? 1 : 0) << (8 + bx)) | ((uint64_t)(255 - cnt) << bx) | x;
+    val[r] = (int32_t)r;
+    atomicAdd(sh ? &nsh[c] : &nint[c], 1);
+}
+
+__global__ void k_chunk_sizes(const int32_t *__restrict__ nint, const int32_t *__restrict__ nsh, int64_t nch,
+                              int32_t *tot, int32_t *ni_al, int32_t *nsh8, int32_t *lpw) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    const int32_t ni = nint[c], ns = nsh[c];
+    const int32_t al = (ni + 1) & ~1;
+    tot[c] = ni + ns;
+    ni_al[c] = al;
+    nsh8[c] = (ns + 7) & ~7;
+    lpw[c] = (al + ns + 1 + 7) & ~7;
+}
+
+// local index of every run; int_of of every node
+__global__ void k_local_index(const int32_t *__restrict__ order, const int32_t *__restrict__ rc,
+                              const int32_t *__restrict__ rg, const int32_t *__restrict__ s_of,
+                              const int32_t *__restrict__ cs, const int32_t *__restrict__ nint,
+                              const int32_t *__restrict__ ni_al, const int32_t *__restrict__ i0, int64_t nruns,
+                              int64_t N_int, int32_t *local, int32_t *int_of) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= nruns) return;
+    const int32_t r = order[j], c = rc[r], g = rg[r];
+    const int32_t pos = (int32_t)(j - cs[c]);
+    const int32_t s = s_of[g];
+    if (s < 0) {
+        local[r] = pos;
+        int_of[g] = i0[c] + pos;
+    } else {
+        local[r] = ni_al[c] + (pos - nint[c]);
+        int_of[g] = (int32_t)(N_int + s);
+    }
+}
+
+// 3. rank of the chunk among the chunks of its node
+__global__ void k_node_chunk_keys(const int32_t *__restrict__ rc, const int32_t *__restrict__ rg, int64_t nruns,
+                                  int bc, uint64_t *key, int32_t *val) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    key[r] = ((uint64_t)(uint32_t)rg[r] << bc) | (uint32_t)rc[r];
+    val[r] = (int32_t)r;
+}
+
+__global__ void k_count_of_s(const int32_t *__restrict__ node_of_s, const int32_t *__restrict__ nref, int64_t nsh,
+                             int32_t *cnt) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s < nsh) cnt[s] = nref[node_of_s[s]];
+}
+
+__global__ void k_slots(const uint64_t *__restrict__ key3, const int32_t *__restrict__ order3, int64_t nruns, int bc,
+                        const int32_t *__restrict__ s_of, const int32_t *__restrict__ nref,
+                        const int32_t *__restrict__ pstart, const int32_t *__restrict__ rc,
+                        const int32_t *__restrict__ local, const int32_t *__restrict__ ni_al,
+                        const int32_t *__restrict__ s0, int32_t *shl_node, int32_t *shl_slot, uint16_t *shl_cr) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= nruns) return;
+    const int32_t g = (int32_t)(key3[j] >> bc);
+    const int32_t s = s_of[g];
+    if (s < 0) return;
+    const int32_t n = nref[g];
+    // the node's runs are consecutive in key3 order: rank = j - first position
+    int32_t rank = 0;
+    while (rank < n && j - rank - 1 >= 0 && (int32_t)(key3[j - rank - 1] >> bc) == g) rank++;
+    const int32_t r = order3[j], c = rc[r];
+    const int64_t k = (int64_t)s0[c] + (local[r] - ni_al[c]);
+    shl_node[k] = s;
+    shl_slot[k] = pstart[s] + rank;
+    shl_cr[k] = (uint16_t)((n << 8) | rank);
+}
+
+// CSR counts at lp0[c] + local + 1, later turned into per-chunk row pointers
+__global__ void k_csr_counts(const int32_t *__restrict__ rc, const int32_t *__restrict__ rlen,
+                             const int32_t *__restrict__ local, const int32_t *__restrict__ lp0, int64_t nruns,
+                             int32_t *cnt) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < nruns) cnt[lp0[rc[r]] + local[r] + 1] = rlen[r];
+}
+
+__global__ void k_nlocal(const int32_t *__restrict__ ni_al, const int32_t *__restrict__ nsh, int64_t nch,
+                         int32_t *nloc) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < nch) nloc[c] = ni_al[c] + nsh[c];
+}
+
+__global__ void k_csr_ptr(const int32_t *__restrict__ glob, const int32_t *__restrict__ lp0,
+                          const int32_t *__restrict__ nloc, int64_t nch, int64_t total, uint16_t *lptr) {
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (x >= total) return;
+    int64_t lo = 0, hi = nch;  // chunk c with lp0[c] <= x < lp0[c+1]
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (lp0[mid] <= x) lo = mid;
+        else hi = mid;
+    }
+    const int32_t base = lp0[lo];
+    lptr[x] = (x - base <= nloc[lo]) ? (uint16_t)(glob[x] - glob[base]) : (uint16_t)0;
+}
+
+__global__ void k_entry_local(const int32_t *__restrict__ flag_rid, const int32_t *__restrict__ v1,
+                              const int32_t *__restrict__ rstart, const int32_t *__restrict__ rc,
+                              const int32_t *__restrict__ local, const int32_t *__restrict__ lp0,
+                              const uint16_t *__restrict__ lptr, int64_t n, uint16_t *lidx, uint16_t *lpos) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t r = flag_rid[i] - 1, k = v1[i];
+    const int32_t l = local[r];
+    lidx[k] = (uint16_t)l;
+    lpos[k] = (uint16_t)(lptr[lp0[rc[r]] + l] + (i - rstart[r]));
+}
+
+__global__ void k_cmeta(const int32_t *__restrict__ i0, const int32_t *__restrict__ nint,
+                        const int32_t *__restrict__ s0, const int32_t *__restrict__ nsh,
+                        const int32_t *__restrict__ ni_al, const int32_t *__restrict__ lp0, int64_t nch, int64_t E,
+                        int B, int32_t *cmeta, int32_t *mx) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    int32_t *cm = cmeta + 8 * c;
+    const int64_t e1 = min(E, (c + 1) * (int64_t)B);
+    cm[0] = i0[c];
+    cm[1] = nint[c];
+    cm[2] = s0[c];
+    cm[3] = nsh[c];
+    cm[4] = 0;
+    cm[5] = (int32_t)(e1 - c * B);
+    cm[6] = ni_al[c];
+    cm[7] = lp0[c];
+    const int32_t ns = nsh[c];
+    atomicMax(&mx[0], ni_al[c] + ((ns + 1) & ~1));    // max_local
+    atomicMax(&mx[1], ni_al[c]);                      // max_win
+    atomicMax(&mx[2], (ni_al[c] + ns + 1 + 7) & ~7);  // max_lptr
+    atomicMax(&mx[3], (ns + 7) & ~7);                 // max_nsh
+}
+
+__global__ void k_bnd_flag(const int32_t *__restrict__ rc, const int32_t *__restrict__ rg,
+                           const uint8_t *__restrict__ forced, int64_t nruns, int32_t *bnd) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < nruns && forced && forced[rg[r]]) bnd[rc[r]] = 1;
+}
+
+__global__ void k_iota32(int32_t *a, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int32_t)i;
+}
+
+}  // namespace
+
+cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, int B, const uint8_t *d_forced,
+                             const DeviceAlloc &dalloc, ChunkMeta &m, DevChunks &d, int32_t **d_int_of,
+                             int32_t **d_bnd, int32_t **d_intc, std::string &err, cudaStream_t s) {
+    m = ChunkMeta();
+    m.B = B;
+    m.Np = Np;
+    m.E = E;
+    m.N = N;
+    const int64_t nch = (E + B - 1) / B;
+    m.nchunks = nch;
+    const int64_t n_ent = nch * Np * B, n = E * Np;
+    const int bn = bits_for(N), bc = bits_for(nch + 1);
+    if (bc + bn > 62 || bc + 9 + bn > 64) { err = "build_chunks_gpu: mesh too large for 64-bit keys"; return cudaSuccess; }
+    const uint64_t pad_key = ((uint64_t)1 << (bc + bn)) - 1;
+
+    // ---- 1. entries -> (chunk, node) runs ----
+    Tmp k1(s), v1(s), k1s(s), v1s(s), flag(s), rid(s);
+    RET(k1.alloc(8 * n_ent));
+    RET(v1.alloc(4 * n_ent));
+    RET(k1s.alloc(8 * n_ent));
+    RET(v1s.alloc(4 * n_ent));
+    k_entry_keys<<<nb(n_ent), kT, 0, s>>>(d_mu, E, Np, B, n_ent, bn, pad_key, k1.as<uint64_t>(), v1.as<int32_t>());
+    RET(sort_u64(k1.as<uint64_t>(), v1.as<int32_t>(), k1s.as<uint64_t>(), v1s.as<int32_t>(), n_ent, bc + bn, s));
+    RET(flag.alloc(4 * n));
+    RET(rid.alloc(4 * n));
+    k_heads64<<<nb(n), kT, 0, s>>>(k1s.as<uint64_t>(), n, flag.as<int32_t>());
+    RET(incl_scan(flag.as<int32_t>(), rid.as<int32_t>(), n, s));
+    int32_t nr32 = 0;
+    RET(cudaMemcpyAsync(&nr32, rid.as<int32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaStreamSynchronize(s));
+    const int64_t nruns = nr32;
+    Tmp rstart(s), rc(s), rg(s), rlen(s), nref(s);
+    RET(rstart.alloc(4 * nruns));
+    RET(rc.alloc(4 * nruns));
+    RET(rg.alloc(4 * nruns));
+    RET(rlen.alloc(4 * nruns));
+    RET(nref.alloc(4 * N));
+    RET(cudaMemsetAsync(nref.p, 0, 4 * N, s));
+    k_run_starts<<<nb(n), kT, 0, s>>>(flag.as<int32_t>(), rid.as<int32_t>(), n, rstart.as<int32_t>());
+    k_run_info<<<nb(nruns), kT, 0, s>>>(k1s.as<uint64_t>(), rstart.as<int32_t>(), nruns, n, bn, rc.as<int32_t>(),
+                                        rg.as<int32_t>(), rlen.as<int32_t>(), nref.as<int32_t>());
+
+    // ---- classification and shared indices ----
+    Tmp fa(s), fb(s), ea(s), eb(s), s_of(s), bad(s);
+    RET(fa.alloc(4 * (N + 1)));
+    RET(fb.alloc(4 * (N + 1)));
+    RET(ea.alloc(4 * (N + 1)));
+    RET(eb.alloc(4 * (N + 1)));
+    RET(s_of.alloc(4 * N));
+    RET(bad.alloc(4));
+    int32_t big = INT_MAX;
+    RET(cudaMemcpyAsync(bad.p, &big, 4, cudaMemcpyHostToDevice, s));
+    RET(cudaMemsetAsync(fa.as<int32_t>() + N, 0, 4, s));
+    RET(cudaMemsetAsync(fb.as<int32_t>() + N, 0, 4, s));
+    k_node_class<<<nb(N), kT, 0, s>>>(nref.as<int32_t>(), d_forced, N, fa.as<int32_t>(), fb.as<int32_t>(),
+                                      bad.as<int32_t>());
+    RET(excl_scan(fa.as<int32_t>(), ea.as<int32_t>(), N + 1, s));
+    RET(excl_scan(fb.as<int32_t>(), eb.as<int32_t>(), N + 1, s));
+    int32_t hb[3];
+    RET(cudaMemcpyAsync(&hb[0], ea.as<int32_t>() + N, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaMemcpyAsync(&hb[1], eb.as<int32_t>() + N, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaMemcpyAsync(&hb[2], bad.p, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaStreamSynchronize(s));
+    if (hb[2] != INT_MAX) {
+        err = "node " + std::to_string(hb[2]) + " is not used by any element";
+        return cudaSuccess;
+    }
+    const int64_t na = hb[0], nif = hb[1], nsh_tot = na + nif;
+    m.N_sh = nsh_tot;
+    m.N_if = nif;
+    Tmp node_of_s(s);
+    RET(node_of_s.alloc(4 * (nsh_tot + 1)));
+    k_shared_index<<<nb(N), kT, 0, s>>>(fa.as<int32_t>(), fb.as<int32_t>(), ea.as<int32_t>(), eb.as<int32_t>(), N,
+                                        (int32_t)na, s_of.as<int32_t>(), node_of_s.as<int32_t>());
+
+    // ---- 2. local order per chunk ----
+    Tmp k2(s), v2(s), k2s(s), order(s), nint(s), nsh(s);
+    RET(k2.alloc(8 * nruns));
+    RET(v2.alloc(4 * nruns));
+    RET(k2s.alloc(8 * nruns));
+    RET(order.alloc(4 * nruns));
+    RET(nint.alloc(4 * (nch + 1)));
+    RET(nsh.alloc(4 * (nch + 1)));
+    RET(cudaMemsetAsync(nint.p, 0, 4 * (nch + 1), s));
+    RET(cudaMemsetAsync(nsh.p, 0, 4 * (nch + 1), s));
+    k_local_keys<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rg.as<int32_t>(), rlen.as<int32_t>(), s_of.as<int32_t>(),
+                                          nruns, bn, k2.as<uint64_t>(), v2.as<int32_t>(), nint.as<int32_t>(),
+                                          nsh.as<int32_t>());
+    RET(sort_u64(k2.as<uint64_t>(), v2.as<int32_t>(), k2s.as<uint64_t>(), order.as<int32_t>(), nruns, bc + 9 + bn, s));
+    Tmp tot(s), ni_al(s), nsh8(s), lpw(s), cs(s), i0(s), s0(s), lp0(s);
+    for (Tmp *t : {&tot, &ni_al, &nsh8, &lpw, &cs, &i0, &s0, &lp0}) RET(t->alloc(4 * (nch + 1)));
+    for (Tmp *t : {&tot, &ni_al, &nsh8, &lpw}) RET(cudaMemsetAsync(t->p, 0, 4 * (nch + 1), s));
+    k_chunk_sizes<<<nb(nch), kT, 0, s>>>(nint.as<int32_t>(), nsh.as<int32_t>(), nch, tot.as<int32_t>(),
+                                         ni_al.as<int32_t>(), nsh8.as<int32_t>(), lpw.as<int32_t>());
+    RET(excl_scan(tot.as<int32_t>(), cs.as<int32_t>(), nch + 1, s));
+    RET(excl_scan(ni_al.as<int32_t>(), i0.as<int32_t>(), nch + 1, s));
+    RET(excl_scan(nsh8.as<int32_t>(), s0.as<int32_t>(), nch + 1, s));
+    RET(excl_scan(lpw.as<int32_t>(), lp0.as<int32_t>(), nch + 1, s));
+    int32_t hN_int = 0, hs0 = 0, hlp = 0;
+    RET(cudaMemcpyAsync(&hN_int, i0.as<int32_t>() + nch, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaMemcpyAsync(&hs0, s0.as<int32_t>() + nch, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaMemcpyAsync(&hlp, lp0.as<int32_t>() + nch, 4, cudaMemcpyDeviceToHost, s));
+    RET(cudaStreamSynchronize(s));
+    m.N_int = hN_int;
+    m.N_tot = m.N_int + m.N_sh;
+    Tmp local(s);
+    RET(local.alloc(4 * nruns));
+    int32_t *int_of = nullptr;
+    RET(dalloc((void **)&int_of, 4 * (size_t)N));
+    *d_int_of = int_of;
+    k_local_index<<<nb(nruns), kT, 0, s>>>(order.as<int32_t>(), rc.as<int32_t>(), rg.as<int32_t>(),
+                                           s_of.as<int32_t>(), cs.as<int32_t>(), nint.as<int32_t>(),
+                                           ni_al.as<int32_t>(), i0.as<int32_t>(), nruns, m.N_int, local.as<int32_t>(),
+                                           int_of);
+
+    // ---- 3. slots: node-major, chunks of a node in ascending order ----
+    int32_t *sh_pstart = nullptr, *shl_node = nullptr, *shl_slot = nullptr;
+    uint16_t *shl_cr = nullptr;
+    RET(dalloc((void **)&sh_pstart, 4 * (size_t)(nsh_tot + 1)));
+    RET(dalloc((void **)&shl_node, 4 * (size_t)(hs0 + 8)));
+    RET(dalloc((void **)&shl_slot, 4 * (size_t)(hs0 + 8)));
+    RET(dalloc((void **)&shl_cr, 2 * (size_t)(hs0 + 8)));
+    RET(cudaMemsetAsync(shl_node, 0, 4 * (size_t)(hs0 + 8), s));
+    RET(cudaMemsetAsync(shl_slot, 0, 4 * (size_t)(hs0 + 8), s));
+    RET(cudaMemsetAsync(shl_cr, 0, 2 * (size_t)(hs0 + 8), s));
+    {
+        Tmp cnt(s);
+        RET(cnt.alloc(4 * (nsh_tot + 1)));
+        RET(cudaMemsetAsync(cnt.p, 0, 4 * (nsh_tot + 1), s));
+        k_count_of_s<<<nb(nsh_tot), kT, 0, s>>>(node_of_s.as<int32_t>(), nref.as<int32_t>(), nsh_tot,
+                                                cnt.as<int32_t>());
+        RET(excl_scan(cnt.as<int32_t>(), sh_pstart, nsh_tot + 1, s));
+        int32_t hslots = 0;
+        RET(cudaMemcpyAsync(&hslots, sh_pstart + nsh_tot, 4, cudaMemcpyDeviceToHost, s));
+        Tmp k3(s), v3(s), k3s(s), o3(s);
+        RET(k3.alloc(8 * nruns));
+        RET(v3.alloc(4 * nruns));
+        RET(k3s.alloc(8 * nruns));
+        RET(o3.alloc(4 * nruns));
+        k_node_chunk_keys<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rg.as<int32_t>(), nruns, bc, k3.as<uint64_t>(),
+                                                   v3.as<int32_t>());
+        RET(sort_u64(k3.as<uint64_t>(), v3.as<int32_t>(), k3s.as<uint64_t>(), o3.as<int32_t>(), nruns, bc + bn, s));
+        k_slots<<<nb(nruns), kT, 0, s>>>(k3s.as<uint64_t>(), o3.as<int32_t>(), nruns, bc, s_of.as<int32_t>(),
+                                         nref.as<int32_t>(), sh_pstart, rc.as<int32_t>(), local.as<int32_t>(),
+                                         ni_al.as<int32_t>(), s0.as<int32_t>(), shl_node, shl_slot, shl_cr);
+        RET(cudaStreamSynchronize(s));
+        m.n_slots = nsh_tot ? hslots : 0;
+    }
+
+    // ---- local indices, CSR row pointers and positions ----
+    uint16_t *lidx = nullptr, *lpos = nullptr, *lptr = nullptr;
+    int32_t *cmeta = nullptr;
+    RET(dalloc((void **)&lidx, 2 * (size_t)n_ent));
+    RET(dalloc((void **)&lpos, 2 * (size_t)n_ent));
+    RET(dalloc((void **)&lptr, 2 * (size_t)(hlp + 8)));
+    RET(dalloc((void **)&cmeta, 4 * 8 * (size_t)nch));
+    RET(cudaMemsetAsync(lidx, 0, 2 * (size_t)n_ent, s));
+    RET(cudaMemsetAsync(lpos, 0, 2 * (size_t)n_ent, s));
+    RET(cudaMemsetAsync(lptr, 0, 2 * (size_t)(hlp + 8), s));
+    {
+        // the block of chunk c holds nlocal + 1 = ni_al + nsh + 1 row pointers
+        Tmp cnt(s), glob(s), nloc(s);
+        RET(cnt.alloc(4 * (size_t)(hlp + 1)));
+        RET(glob.alloc(4 * (size_t)(hlp + 1)));
+        RET(nloc.alloc(4 * (nch + 1)));
+        RET(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)(hlp + 1), s));
+        k_csr_counts<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rlen.as<int32_t>(), local.as<int32_t>(),
+                                              lp0.as<int32_t>(), nruns, cnt.as<int32_t>());
+        RET(incl_scan(cnt.as<int32_t>(), glob.as<int32_t>(), hlp, s));
+        k_nlocal<<<nb(nch), kT, 0, s>>>(ni_al.as<int32_t>(), nsh.as<int32_t>(), nch, nloc.as<int32_t>());
+        k_csr_ptr<<<nb(hlp), kT, 0, s>>>(glob.as<int32_t>(), lp0.as<int32_t>(), nloc.as<int32_t>(), nch, hlp, lptr);
+    }
+    k_entry_local<<<nb(n), kT, 0, s>>>(rid.as<int32_t>(), v1s.as<int32_t>(), rstart.as<int32_t>(), rc.as<int32_t>(),
+                                       local.as<int32_t>(), lp0.as<int32_t>(), lptr, n, lidx, lpos);
+    Tmp mx(s);
+    RET(mx.alloc(16));
+    RET(cudaMemsetAsync(mx.p, 0, 16, s));
+    k_cmeta<<<nb(nch), kT, 0, s>>>(i0.as<int32_t>(), nint.as<int32_t>(), s0.as<int32_t>(), nsh.as<int32_t>(),
+                                   ni_al.as<int32_t>(), lp0.as<int32_t>(), nch, E, B, cmeta, mx.as<int32_t>());
+    int32_t hmx[4];
+    RET(cudaMemcpyAsync(hmx, mx.p, 16, cudaMemcpyDeviceToHost, s));
+
+    // ---- boundary (touching a rank-interface node) / interior chunk lists ----
+    int32_t *bnd = nullptr, *intc = nullptr;
+    std::vector<int32_t> hbnd;
+    if (d_forced && nif > 0) {
+        Tmp bf(s);
+        RET(bf.alloc(4 * nch));
+        RET(cudaMemsetAsync(bf.p, 0, 4 * nch, s));
+        k_bnd_flag<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rg.as<int32_t>(), d_forced, nruns, bf.as<int32_t>());
+        hbnd.resize(nch);
+        RET(cudaMemcpyAsync(hbnd.data(), bf.p, 4 * nch, cudaMemcpyDeviceToHost, s));
+    }
+    RET(cudaStreamSynchronize(s));
+    m.max_local = hmx[0];
+    m.max_win = hmx[1];
+    m.max_lptr = hmx[2];
+    m.max_nsh = hmx[3];
+    m.max_colors = 0;
+    for (int64_t c = 0; c < nch; c++)
+        ((!hbnd.empty() && hbnd[c]) ? m.bnd_chunks : m.int_chunks).push_back((int32_t)c);
+    RET(dalloc((void **)&bnd, 4 * (m.bnd_chunks.size() + 1)));
+    RET(dalloc((void **)&intc, 4 * (m.int_chunks.size() + 1)));
+    if (!m.bnd_chunks.empty())
+        RET(cudaMemcpyAsync(bnd, m.bnd_chunks.data(), 4 * m.bnd_chunks.size(), cudaMemcpyHostToDevice, s));
+    if (!m.int_chunks.empty())
+        RET(cudaMemcpyAsync(intc, m.int_chunks.data(), 4 * m.int_chunks.size(), cudaMemcpyHostToDevice, s));
+    *d_bnd = bnd;
+    *d_intc = intc;
+
+    d.B = B; d.Np = Np; d.E = E; d.N = N; d.nchunks = nch;
+    d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
+    d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
+    d.cmeta = cmeta; d.lidx = lidx; d.lpos = lpos; d.lptr = lptr; d.sh_pstart = sh_pstart;
+    d.shl_node = shl_node; d.shl_slot = shl_slot; d.shl_cr = shl_cr;
+    RET(cudaStreamSynchronize(s));
+    return cudaGetLastError();
+}
+
+}  // namespace sem

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
+#include <string>
 
 #include "sem_internal.h"
 
@@ -63,6 +65,8 @@ void free_node_graph(DevGraph &g, cudaStream_t s);
 cudaError_t strategy_order(const int32_t *mu_can, const double *vxy, const int32_t *tri_or, int64_t E, int P,
                            int64_t N, int strategy, const DevGraph &g, const double *edge_t, double x0, double y0,
                            int32_t *elem_perm, int32_t *order, int64_t *n_levels, cudaStream_t s);
+// *first = smallest i < n with a[i] == v (INT_MAX if none)
+cudaError_t launch_find_i32(const int32_t *a, int64_t n, int32_t v, int32_t *first, cudaStream_t s);
 // label_of[node_perm[i]] = i, then mu_out = label_of[mu]
 cudaError_t relabel_from_perm(const int32_t *mu, int64_t n, const int32_t *node_perm, int64_t N, int32_t *mu_out,
                               cudaStream_t s);
@@ -82,6 +86,17 @@ struct DevChunks {  // device view of ChunkMeta
     const int32_t *shl_slot;   // per chunk: the slot it writes
     const uint16_t *shl_cr;    // per chunk: (slots of the node << 8) | rank of this chunk among them
 };
+
+// ------------------------------ chunks_gpu.cu --------------------------------
+// The chunk builder of chunks.cpp on the GPU, same arrays bit for bit.  mu: device
+// [E][Np]; forced: device [N] flags of rank-interface nodes or nullptr.  Persistent
+// arrays come from `dalloc` (owned by the caller); `err` is set (and cudaSuccess
+// returned) for mesh errors.  Fills the scalars and lists of m (no host arrays),
+// the device view d, the node -> internal id map and the chunk lists.
+using DeviceAlloc = std::function<cudaError_t(void **, size_t)>;
+cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, int B, const uint8_t *d_forced,
+                             const DeviceAlloc &dalloc, ChunkMeta &m, DevChunks &d, int32_t **d_int_of,
+                             int32_t **d_bnd, int32_t **d_intc, std::string &err, cudaStream_t s);
 
 cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s);
 // K6: per element (new order) G = c^2 detJ J^-1 J^-T and detJ.

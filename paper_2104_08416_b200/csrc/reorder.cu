@@ -448,6 +448,11 @@ __global__ void k_elem_first_pos(const int32_t *__restrict__ mu, int64_t E, int 
     ids[e] = (int32_t)e;
 }
 
+__global__ void k_find_i32(const int32_t *__restrict__ a, int64_t n, int32_t v, int32_t *first) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && a[i] == v) atomicMin(first, (int32_t)i);
+}
+
 __global__ void k_i32_to_i64(const int32_t *__restrict__ a, int64_t n, int64_t *out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i <= n) out[i] = (i < n) ? a[i] : 0;
@@ -731,6 +736,12 @@ cudaError_t strategy_order(const int32_t *mu_can, const double *vxy, const int32
     k_elem_first_pos<<<blocks_for(E), kThreads, 0, s>>>(mu_can, E, Np, (int32_t *)pos.p, (uint64_t *)key.p,
                                                         (int32_t *)ids.p);
     RET(sort_pairs_u64((uint64_t *)key.p, (int32_t *)ids.p, (uint64_t *)key2.p, elem_perm, E, 64, s));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_find_i32(const int32_t *a, int64_t n, int32_t v, int32_t *first, cudaStream_t s) {
+    k_fill_i32<<<1, 32, 0, s>>>(first, 1, INT_MAX);
+    k_find_i32<<<blocks_for(n), kThreads, 0, s>>>(a, n, v, first);
     return cudaGetLastError();
 }
 

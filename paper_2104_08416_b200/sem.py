@@ -177,7 +177,7 @@ class SemContext:
                                             C.byref(nn), _ptr(grid)))
         self.N = nn.value
         self.E = E
-        return {"keys": keys, "elem_perm": eperm, "node_perm": nperm[: nn.value].copy(),
+        return {"keys": keys, "elem_perm": eperm, "node_perm": nperm[: nn.value],
                 "n_nodes": nn.value, "grid": (int(grid[0]), int(grid[1]))}
 
     def sem_build_operators(self, c_elem, src_vertex: int, f0: float, t0: float, amplitude: float, dt: float):
