@@ -1054,7 +1054,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(dalloc(L, &ctx->d_sendbuf, ctx->n_send + 2));
         CK(cudaStreamSynchronize(s));
         tr.mark(s, "uploads + maps");
-        ctx->k7_grid = k7_grid(d);
+        ctx->k7_grid = k7_grid(d, false);
         tr.mark(s, "k7 occupancy");
         ctx->meta_info = ChunkMeta();
         ChunkMeta &mi = ctx->meta_info;

@@ -122,7 +122,7 @@ struct StepParams {
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
 };
-int k7_grid(const DevChunks &ch);
+int k7_grid(const DevChunks &ch, bool fused);
 // K7 over all chunks (list == nullptr) or over the chunk ids list[0..nlist).
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
                       const int32_t *list = nullptr, int64_t nlist = 0);

@@ -48,19 +48,24 @@ inline unsigned blocks_for(int64_t n, int threads = kThreads) {
 }
 
 // Shared-memory layout of one pipeline stage (all offsets 16-byte aligned).
+// Lf = Ls when K8 is fused (slot counters), else 0; Ws = the U^{n-1} / dt^2/M
+// window length when the windows travel in the stage (double-buffered with
+// it), else 0 (single-buffered windows outside the stages).
 struct StageLayout {
-    int lidx, lpos, lptr, shs, shn, scr, g, meta, u, size;
-    __host__ __device__ StageLayout(int np, int B, int L, int Lp, int Ls) {
+    int lidx, lpos, lptr, shs, shn, scr, g, meta, u, up, m, size;
+    __host__ __device__ StageLayout(int np, int B, int L, int Lp, int Ls, int Lf, int Ws) {
         lidx = 0;
         lpos = np * B * 2;
         lptr = lpos + np * B * 2;
         shs = lptr + Lp * 2;
         shn = shs + Ls * 4;
-        scr = shn + Ls * 4;
-        g = scr + Ls * 2;
+        scr = shn + Lf * 4;
+        g = scr + Lf * 2;
         meta = g + 3 * B * 8;
         u = meta + 32;
-        size = (u + L * 8 + 127) & ~127;
+        up = u + L * 8;
+        m = up + Ws * 8;
+        size = (m + Ws * 8 + 127) & ~127;
     }
 };
 
@@ -171,16 +176,16 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
 }
 
 // ---- K7 ---------------------------------------------------------------------------
-template <int NP, int B>
+template <int NP, int B, bool WIN2>
 __global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
     extern __shared__ __align__(128) unsigned char sm[];
-    const StageLayout lay(NP, B, L, Lp, Ls);
+    const StageLayout lay(NP, B, L, Lp, Ls, a.cnt ? Ls : 0, WIN2 ? W : 0);
     double *ebuf = reinterpret_cast<double *>(sm + kStages * lay.size);  // [NP][B] element slots
-    double *up_s = ebuf + NP * B;                                       // U^{n-1} window (single buffer)
-    double *m_s = up_s + W;                                             // dt^2/M window (single buffer)
-    uint64_t *full = reinterpret_cast<uint64_t *>(m_s + W);            // TMA blocks landed
+    double *up_w = ebuf + NP * B;                                       // U^{n-1} window (single buffer)
+    double *m_w = up_w + (WIN2 ? 0 : W);                                // dt^2/M window (single buffer)
+    uint64_t *full = reinterpret_cast<uint64_t *>(m_w + (WIN2 ? 0 : W));  // TMA blocks landed
     uint64_t *gath = full + kStages;                                    // shared-node gathers landed
     uint64_t *empty = gath + kStages;                                   // consumers done with stage
     uint64_t *wfull = empty + kStages;                                  // U^{n-1}, dt^2/M windows landed
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192
                 const int nsh8 = (nsh + 7) & ~7;
                 const bool fuse = a.cnt != nullptr;
                 const uint32_t bytes = 2 * NP * B * 2 + nlp * 2 + nsh8 * (fuse ? 10 : 4) + 3 * B * 8 +
-                                       (uint32_t)ni_al * 8;
+                                       (uint32_t)ni_al * (WIN2 ? 24 : 8);
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
                 tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
@@ -239,18 +244,22 @@ __global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192
                 tma_load(st + lay.g + B * 8, a.Gss + e0, B * 8, &full[s]);
                 tma_load(st + lay.g + 2 * B * 8, a.Grs + e0, B * 8, &full[s]);
                 if (ni_al > 0) tma_load(st + lay.u, a.U + i0, ni_al * 8, &full[s]);
+                if (WIN2 && ni_al > 0) {
+                    tma_load(st + lay.up, a.Uprev + i0, ni_al * 8, &full[s]);
+                    tma_load(st + lay.m, a.dt2M + i0, ni_al * 8, &full[s]);
+                }
             }
             double *u_sh = reinterpret_cast<double *>(st + lay.u) + ni_al;
             for (int j = lane; j < nsh; j += 32) cp_async8(u_sh + j, a.U + ch.N_int + ch.shl_node[s0 + j]);
             cp_async_arrive_noinc(&gath[s]);
             // the single U^{n-1} / dt^2/M window buffer: free once the previous
             // chunk's update is done; lands while this chunk's element phase runs
-            if (lane == 0) {
+            if (!WIN2 && lane == 0) {
                 if (k >= 1) mbar_wait(wempty, (k - 1) & 1);
                 mbar_arrive_expect_tx(wfull, (uint32_t)ni_al * 16);
                 if (ni_al > 0) {
-                    tma_load(up_s, a.Uprev + i0, ni_al * 8, wfull);
-                    tma_load(m_s, a.dt2M + i0, ni_al * 8, wfull);
+                    tma_load(up_w, a.Uprev + i0, ni_al * 8, wfull);
+                    tma_load(m_w, a.dt2M + i0, ni_al * 8, wfull);
                 }
             }
         }
@@ -303,7 +312,9 @@ __global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192
             for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = y[p];  // straight to the node's CSR run
         }
         consumer_sync<B>();
-        mbar_wait(wfull, k & 1);
+        if (!WIN2) mbar_wait(wfull, k & 1);
+        const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
+        const double *m_s = WIN2 ? reinterpret_cast<const double *>(st + lay.m) : m_w;
         // (B) node-centric gather of K U^n in fixed order + fused update;
         //     shared nodes: this chunk's partial into the node's slot
         double *Unew = a.Uprev;
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192
         consumer_sync<B>();
         if (t == 0) {
             mbar_arrive(&empty[s]);
-            mbar_arrive(wempty);
+            if (!WIN2) mbar_arrive(wempty);
         }
     }
 }
@@ -458,19 +469,35 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return e;
 }
 
-size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls) {
-    const StageLayout lay(np, B, L, Lp, Ls);
-    return (size_t)kStages * lay.size + (size_t)np * B * 8 + 2 * (size_t)W * 8 + (3 * kStages + 2) * 8;
+// SEM_K7_WIN=2 puts the U^{n-1} / dt^2/M windows into the stages (double-buffered)
+bool k7_win2() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("SEM_K7_WIN"); v = (e && atoi(e) == 2) ? 1 : 0; }
+    return v == 1;
+}
+
+size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
+    const bool w2 = k7_win2();
+    const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, w2 ? W : 0);
+    return (size_t)kStages * lay.size + (size_t)np * B * 8 + (w2 ? 0 : 2 * (size_t)W * 8) + (3 * kStages + 2) * 8;
 }
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
-K7Fn k7_fn(int np, int B) {
-    if (np == 21) return k7_step<21, 128>;  // P5 (R21): chunks of 128
-    if (np == 36) return k7_step<36, 64>;   // P7: chunks of 64
+template <bool W2>
+K7Fn k7_fn_w(int np, int B) {
+    if (np == 21) return k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
+    if (np == 36) return k7_step<36, 64, W2>;   // P7: chunks of 64
     if (np == 6)
-        return B == 128 ? k7_step<6, 128> : B == 192 ? k7_step<6, 192> : B == 512 ? k7_step<6, 512> : k7_step<6, 256>;
-    return B == 128 ? k7_step<10, 128> : B == 192 ? k7_step<10, 192> : B == 512 ? k7_step<10, 512> : k7_step<10, 256>;
+        return B == 128   ? k7_step<6, 128, W2>
+               : B == 192 ? k7_step<6, 192, W2>
+               : B == 512 ? k7_step<6, 512, W2>
+                          : k7_step<6, 256, W2>;
+    return B == 128   ? k7_step<10, 128, W2>
+           : B == 192 ? k7_step<10, 192, W2>
+           : B == 512 ? k7_step<10, 512, W2>
+                      : k7_step<10, 256, W2>;
 }
+K7Fn k7_fn(int np, int B) { return k7_win2() ? k7_fn_w<true>(np, B) : k7_fn_w<false>(np, B); }
 
 }  // namespace
 
@@ -511,14 +538,14 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer,
     return cudaGetLastError();
 }
 
-int k7_grid(const DevChunks &ch) {
+int k7_grid(const DevChunks &ch, bool fused) {
     static int nsm = 0;
     if (!nsm) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh);
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, fused);
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     set_smem(fn, smem);
     int occ = 0;
@@ -534,7 +561,7 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
     if (grid > n) grid = (int)n;
-    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh);
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, p.cnt != nullptr);
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     cudaError_t e = set_smem(fn, smem);
     if (e != cudaSuccess) return e;
