@@ -332,7 +332,17 @@ def scatter_ablation(ctx, pb, args, S):
     return res
 
 
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
+def fp64_peak():
+    """Measured FP64 FMA throughput (tools/dfma_peak.cu -> profiles/dfma_peak.json),
+    else the nominal 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "dfma_peak.json")) as f:
+            return float(json.load(f)["fp64_fma_tflops"]), "measured (profiles/dfma_peak.json)"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "nominal 148 x 64 DFMA/clk x 1.965 GHz"
+
+
+FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = fp64_peak()
 
 
 def orders_leg(ctx, args, S, peak, peaks):
@@ -373,7 +383,7 @@ def orders_leg(ctx, args, S, peak, peaks):
                 "alg_gbs": info["bytes_alg_per_step"] / (ms * 1e-3) / 1e9,
                 "k7_hbm_frac": b7 / (k7 * 1e-3) / 1e9 / peak,
                 "k7_fp64_tflops": tf, "k7_fp64_frac": tf / FP64_PEAK_TFLOPS,
-                "fp64_peak_tflops": FP64_PEAK_TFLOPS, "steps": K}
+                "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_peak_source": FP64_PEAK_SOURCE, "steps": K}
     return res
 
 

@@ -177,7 +177,7 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
 
 // ---- K7 ---------------------------------------------------------------------------
 template <int NP, int B, bool WIN2>
-__global__ void __launch_bounds__(B + 32, (NP > 10 ? 1 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
     extern __shared__ __align__(128) unsigned char sm[];
