@@ -214,3 +214,25 @@ def test_single_element_and_tiny(ctx):
         Ug, _ = ctx.sem_read_field()
         Uo, _ = o.leapfrog(0.01, 5, src=0, A=1.0, f0=5.0, t0=0.0, U=U0, Uprev=U0)
         assert rel_l2(Ug, Uo) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_bench_configuration(ctx, name):
+    """Full BASELINE.json size in the launch configuration bench.py times
+    (one rank, default chunks): one step from a seeded random state over the
+    whole mesh, and the configured Ricker run for 10 steps from zero."""
+    pb = mg.config(name)
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    rng = np.random.default_rng(7)
+    U0 = rng.standard_normal(o.N)
+    Up = U0 + 0.1 * rng.standard_normal(o.N)
+    Uo, _ = o.leapfrog(pb.dt, 1, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0, U=U0, Uprev=Up, step0=5)
+    Ug = run_gpu(ctx, pb, 1, state=(U0, Up), step0=5)
+    assert ctx.sem_get_info()["chunk_elems"] == 256
+    assert rel_l2(Ug, Uo) <= 1e-13, rel_l2(Ug, Uo)
+    pb2 = mg.Problem(**{**pb.__dict__, "t0": 3 * pb.dt, "f0": 1.0 / (8 * pb.dt)})
+    Uo, _ = o.leapfrog(pb2.dt, 10, src=pb2.src_vertex, A=1.0, f0=pb2.f0, t0=pb2.t0)
+    Ug = run_gpu(ctx, pb2, 10)
+    assert np.abs(Uo).max() > 0
+    assert rel_l2(Ug, Uo) <= REL_L2, rel_l2(Ug, Uo)
