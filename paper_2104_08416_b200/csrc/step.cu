@@ -176,10 +176,15 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
 }
 
 // ---- K7 ---------------------------------------------------------------------------
-template <int NP, int B, bool WIN2>
-__global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
+// G > 1 (high orders): G consumer threads per element.  Warp w takes elements
+// 32 (w / G) + lane and the row block w % G of y = K^e u, computed as
+// y_p = grr (Srr u)_p + gss (Sss u)_p + grs (Srs u)_p with the S tables staged in
+// shared memory (all lanes of a warp read the same entry: broadcast).
+template <int NP, int B, bool WIN2, int G = 1>
+__global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
+    constexpr int C = B * G;  // consumer threads
     extern __shared__ __align__(128) unsigned char sm[];
     const StageLayout lay(NP, B, L, Lp, Ls, a.cnt ? Ls : 0, WIN2 ? W : 0);
     double *ebuf = reinterpret_cast<double *>(sm + kStages * lay.size);  // [NP][B] element slots
@@ -190,9 +195,17 @@ __global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 
     uint64_t *empty = gath + kStages;                                   // consumers done with stage
     uint64_t *wfull = empty + kStages;                                  // U^{n-1}, dt^2/M windows landed
     uint64_t *wempty = wfull + 1;                                       // ... consumed
+    double *S_s = reinterpret_cast<double *>(wempty + 1);               // G > 1: Srr, Sss, Srs [NP][NP]
     const int t = threadIdx.x;
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
+    if (G > 1) {
+        for (int i = t; i < NP * NP; i += blockDim.x) {
+            S_s[i] = c_Srr[i / NP][i % NP];
+            S_s[NP * NP + i] = c_Sss[i / NP][i % NP];
+            S_s[2 * NP * NP + i] = c_Srs[i / NP][i % NP];
+        }
+    }
     if (t == 0) {
         for (int s = 0; s < kStages; s++) {
             mbar_init(&full[s], 1);
@@ -205,11 +218,11 @@ __global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 
     }
     __syncthreads();
 
-    if (t >= B) {
+    if (t >= C) {
         // ===== producer warp =====
         // lane 0 streams the chunk's contiguous blocks with TMA bulk copies; all
         // 32 lanes gather U^n of the chunk's shared nodes with cp.async.
-        const int lane = t - B;
+        const int lane = t - C;
         int k = 0;
         for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
             const int64_t c = list ? list[pos] : pos;
@@ -284,11 +297,37 @@ __global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 
         const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
         const double *g_s = reinterpret_cast<const double *>(st + lay.g);
 
+        if (G > 1) {
+            // (E, wide) this thread: element te, rows [p0, p1) of y = K^e u
+            constexpr int R = (NP + G - 1) / G;
+            const int w = t >> 5, te = ((w / G) << 5) + (t & 31), p0 = (w % G) * R;
+            if (te < ne) {
+                const double grr = g_s[te], gss = g_s[B + te], grs = g_s[2 * B + te];
+                double u[NP];
+#pragma unroll
+                for (int q = 0; q < NP; q++) u[q] = u_s[li_s[q * B + te]];
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const int p = p0 + r;
+                    if (p < NP) {
+                        const double *srr = S_s + p * NP, *sss = S_s + NP * NP + p * NP, *srs = S_s + 2 * NP * NP + p * NP;
+                        double arr = 0.0, ass = 0.0, ars = 0.0;
+#pragma unroll
+                        for (int q = 0; q < NP; q++) {
+                            arr = fma(srr[q], u[q], arr);
+                            ass = fma(sss[q], u[q], ass);
+                            ars = fma(srs[q], u[q], ars);
+                        }
+                        ebuf[lpo[p * B + te]] = fma(grr, arr, fma(gss, ass, grs * ars));
+                    }
+                }
+            }
+        }
         // (E) y = K^e u, K^e symmetric: each K_pq (p <= q) built once
         double y[NP];
 #pragma unroll
         for (int p = 0; p < NP; p++) y[p] = 0.0;
-        if (t < ne) {
+        if (G == 1 && t < ne) {
             const double grr = g_s[t], gss = g_s[B + t], grs = g_s[2 * B + t];
             double u[NP];
 #pragma unroll
@@ -307,18 +346,18 @@ __global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 
                 }
             }
         }
-        if (t < ne) {
+        if (G == 1 && t < ne) {
 #pragma unroll
             for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = y[p];  // straight to the node's CSR run
         }
-        consumer_sync<B>();
+        consumer_sync<C>();
         if (!WIN2) mbar_wait(wfull, k & 1);
         const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
         const double *m_s = WIN2 ? reinterpret_cast<const double *>(st + lay.m) : m_w;
         // (B) node-centric gather of K U^n in fixed order + fused update;
         //     shared nodes: this chunk's partial into the node's slot
         double *Unew = a.Uprev;
-        for (int i = t; i < nl; i += B) {
+        for (int i = t; i < nl; i += C) {
             const double yi = csr_sum(ebuf, lp, i);
             if (i < nint) {
                 const int id = i0 + i;
@@ -332,7 +371,7 @@ __global__ void __launch_bounds__(B + 32, (NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 
                                          reinterpret_cast<const uint16_t *>(st + lay.scr)[j], sl, u_s[i]);
             }
         }
-        consumer_sync<B>();
+        consumer_sync<C>();
         if (t == 0) {
             mbar_arrive(&empty[s]);
             if (!WIN2) mbar_arrive(wempty);
@@ -476,17 +515,29 @@ bool k7_win2() {
     return v == 1;
 }
 
+// consumer threads per element of the K7 instantiation used for np (1, or 4 at P7)
+int k7_group(int np) {
+    static int g7 = -1;
+    if (g7 < 0) { const char *e = getenv("SEM_K7_G"); g7 = e ? atoi(e) : 4; if (g7 != 1 && g7 != 2 && g7 != 4) g7 = 4; }
+    return np == 36 ? g7 : 1;
+}
+
 size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
     const bool w2 = k7_win2();
     const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, w2 ? W : 0);
-    return (size_t)kStages * lay.size + (size_t)np * B * 8 + (w2 ? 0 : 2 * (size_t)W * 8) + (3 * kStages + 2) * 8;
+    const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * np * 8 : 0;
+    return (size_t)kStages * lay.size + (size_t)np * B * 8 + (w2 ? 0 : 2 * (size_t)W * 8) + (3 * kStages + 2) * 8 +
+           stab;
 }
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
 template <bool W2>
 K7Fn k7_fn_w(int np, int B) {
     if (np == 21) return k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
-    if (np == 36) return k7_step<36, 64, W2>;   // P7: chunks of 64
+    if (np == 36) {                              // P7: chunks of 64, G threads per element
+        const int g = k7_group(36);
+        return g == 4 ? k7_step<36, 64, W2, 4> : g == 2 ? k7_step<36, 64, W2, 2> : k7_step<36, 64, W2, 1>;
+    }
     if (np == 6)
         return B == 128   ? k7_step<6, 128, W2>
                : B == 192 ? k7_step<6, 192, W2>
@@ -549,7 +600,7 @@ int k7_grid(const DevChunks &ch, bool fused) {
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     set_smem(fn, smem);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B + 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B * k7_group(ch.Np) + 32, smem);
     if (occ < 1) occ = 1;
     int64_t g = (int64_t)occ * nsm;
     if (g > ch.nchunks) g = ch.nchunks;
@@ -565,7 +616,8 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     cudaError_t e = set_smem(fn, smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, list, nlist);
+    fn<<<grid, ch.B * k7_group(ch.Np) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, list,
+                                                       nlist);
     return cudaGetLastError();
 }
 
