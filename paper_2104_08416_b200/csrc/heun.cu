@@ -216,13 +216,13 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                     ar[q] = sw * fma(F00, v[q], F01 * v[NP + q]);
                     as[q] = sw * fma(F10, v[q], F11 * v[NP + q]);
                 }
-                double r[NP];
+                double *eb = reinterpret_cast<double *>(ebuf);  // (r, k) pairs: r now, k below
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
                     double acc = 0.0;
 #pragma unroll
                     for (int q = 0; q < NP; q++) acc = fma(h_Dr[q][p], ar[q], fma(h_Ds[q][p], as[q], acc));
-                    r[p] = acc;
+                    eb[2 * lpo[p * B + t]] = acc;
                 }
                 // (3) y = K^e u, K^e = Grr Srr + Gss Sss + Grs Srs, G = sd F F^T
                 //     (= c^2 detJ J^-1 J^-T, reading R5)
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                     }
                 }
 #pragma unroll
-                for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = make_double2(r[p], y[p]);
+                for (int p = 0; p < NP; p++) eb[2 * lpo[p * B + t] + 1] = y[p];
             }
             consumer_sync<B>();
             mbar_wait(wfull, k & 1);
@@ -364,6 +364,7 @@ HFn heun_fn_b(int mode) {
     return mode == 0 ? k_heun<NP, B, 0> : mode == 1 ? k_heun<NP, B, 1> : k_heun<NP, B, 2>;
 }
 HFn heun_fn(int np, int B, int mode) {
+    if (np == 21) return heun_fn_b<21, 128>(mode);  // P5 (the paper's Benchmark 1 order)
     if (np == 6) return B == 128 ? heun_fn_b<6, 128>(mode) : heun_fn_b<6, 256>(mode);
     return B == 128 ? heun_fn_b<10, 128>(mode) : heun_fn_b<10, 256>(mode);
 }
@@ -372,7 +373,9 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n + 2
 
 }  // namespace
 
-bool heun_supported(int np, int B) { return (np == 6 || np == 10) && (B == 128 || B == 256); }
+bool heun_supported(int np, int B) {
+    return ((np == 6 || np == 10) && (B == 128 || B == 256)) || (np == 21 && B == 128);
+}
 
 cudaError_t upload_heun_tables(const RefTables &T, cudaStream_t s) {
     cudaError_t e;

@@ -168,3 +168,26 @@ def test_heun_loopback_group_unsupported():
         assert e.value.status == S.SEM_E_UNSUPPORTED
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("steps", [1, 10, 60])
+def test_heun_p5_parity(ctx, steps):
+    """The paper's Benchmark 1 order (P5) with its own integrator."""
+    pb = mg.config("B1", 30, degree=5)  # 33 x 16 cells: ragged last chunk of 128
+    m = pb.mesh
+    h = mg.heun_h(pb)
+    o = OracleSEM(m.vxy, m.tri, 5, pb.c)
+    rng = np.random.default_rng(steps)
+    U0 = rng.standard_normal(o.N)
+    V0 = rng.standard_normal((m.ne, o.Np, 2))
+    f0, t0 = shifted(pb, h)
+    Uo, Vo = o.heun(h, steps, src=pb.src_vertex, A=1.0, f0=f0, t0=t0, U=U0, V=V0)
+    setup_gpu(ctx, pb, h, f0=f0, t0=t0)
+    ctx.sem_write_state(U0, None)
+    ctx.sem_write_velocity(V0)
+    ctx.sem_step_n(steps)
+    Ug, _ = ctx.sem_read_field()
+    Vg, _ = ctx.sem_read_velocity()
+    tol = REL_STATE if steps <= 10 else REL_L2
+    assert rel_l2(Ug, Uo) <= tol, rel_l2(Ug, Uo)
+    assert rel_l2(Vg, Vo) <= tol, rel_l2(Vg, Vo)
