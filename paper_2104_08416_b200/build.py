@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsem.so")
-SOURCES = ["api.cu", "reorder.cu", "step.cu", "heun.cu", "chunks_gpu.cu", "chunks.cpp", "partition.cpp", "refelem.cpp"]
+SOURCES = ["api.cu", "reorder.cu", "step.cu", "heun.cu", "chunks_gpu.cu", "partition_gpu.cu", "chunks.cpp", "partition.cpp", "refelem.cpp"]
 HEADERS = ["kernels.h", "sem_internal.h", "dev_common.cuh"]
 
 NVCC_FLAGS = [

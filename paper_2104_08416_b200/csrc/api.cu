@@ -875,11 +875,12 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         tr.mark(s, "node numbering");
         // ---- host outputs ----
         const bool one = ctx->world == 1;  // fast path: every node local, identity maps
-        // chunk metadata built on the GPU (chunks_gpu.cu) unless a host-side consumer needs mu
-        const bool gpu_chunks = one && ctx->scatter == SEM_SCATTER_CHUNK && getenv("SEM_HOST_CHUNKS") == nullptr;
+        // partition and chunk metadata built on the GPU (partition_gpu.cu, chunks_gpu.cu)
+        // unless a host-side consumer (the ablation scatters) needs mu
+        const bool gpu_chunks = ctx->scatter == SEM_SCATTER_CHUNK && getenv("SEM_HOST_CHUNKS") == nullptr;
         const bool check_chunks = gpu_chunks && getenv("SEM_CHUNK_CHECK") != nullptr;
         std::vector<int32_t> node_perm, mu_h;
-        if (!one) {  // the partition and the rank maps need it on the host
+        if (!one && !gpu_chunks) {  // the host partition and the rank maps need it
             node_perm.resize(N);
             CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
         }
@@ -898,8 +899,38 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         tr.mark(s, "D2H outputs");
         // ---- this rank's part: contiguous range of the global order ----
         Partition part;
+        DevPartition dpart;
         std::string err;
-        if (!one) {
+        auto &L = ctx->mesh_allocs;
+        const DeviceAlloc da = [&L](void **p, size_t bytes) { return dalloc(L, (char **)p, bytes); };
+        if (!one && gpu_chunks) {
+            CK(build_partition_gpu(d_mu_ft, E, Np, N, ctx->rank, ctx->world, da, dpart, err, s));
+            if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
+            ctx->e0 = dpart.e0;
+            ctx->E = dpart.e1 - dpart.e0;
+            ctx->N = dpart.NL;
+            part.nbr = dpart.nbr;
+            part.nbr_off = dpart.nbr_off;
+            part.send_if = dpart.send_if;
+            part.sum_start = dpart.sum_start;
+            part.sum_src = dpart.sum_src;
+            if (check_chunks) {  // the host partition must agree
+                if (!build_partition(mu_h.data(), E, Np, N, ctx->rank, ctx->world, part, err))
+                    return fail(ctx, SEM_E_MESH, err);
+                std::string diff;
+                if (part.e0 != dpart.e0 || part.e1 != dpart.e1 || (int64_t)part.loc2glob.size() != dpart.NL ||
+                    (int64_t)part.if_local.size() != dpart.n_if)
+                    diff = "sizes";
+                else if (!same_dev(part.loc2glob, dpart.loc2glob, part.loc2glob.size(), s)) diff = "loc2glob";
+                else if (!same_dev(part.mu_local, dpart.mu_local, part.mu_local.size(), s)) diff = "mu_local";
+                else if (!same_dev(part.remote, dpart.remote, part.remote.size(), s)) diff = "remote";
+                else if (!same_dev(part.owned, dpart.owned, part.owned.size(), s)) diff = "owned";
+                else if (part.nbr != dpart.nbr || part.nbr_off != dpart.nbr_off || part.send_if != dpart.send_if ||
+                         part.sum_start != dpart.sum_start || part.sum_src != dpart.sum_src)
+                    diff = "exchange lists";
+                if (!diff.empty()) return fail(ctx, SEM_E_MESH, "GPU partition differs from the host's: " + diff);
+            }
+        } else if (!one) {
             if (!build_partition(mu_h.data(), E, Np, N, ctx->rank, ctx->world, part, err))
                 return fail(ctx, SEM_E_MESH, err);
             std::vector<int32_t>().swap(mu_h);
@@ -918,15 +949,16 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         // ---- chunk metadata for the step kernel ----
         ChunkMeta m;
         DevChunks &d = ctx->dch;
-        auto &L = ctx->mesh_allocs;
         if (gpu_chunks) {
-            const DeviceAlloc da = [&L](void **p, size_t bytes) { return dalloc(L, (char **)p, bytes); };
-            CK(build_chunks_gpu(d_mu_ft, E, Np, N, chunk_elems(degree), nullptr, da, m, d, &ctx->d_loc_int,
-                                &ctx->d_bnd, &ctx->d_intc, err, s));
+            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, chunk_elems(degree),
+                                one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd, &ctx->d_intc,
+                                err, s));
             if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
             if (check_chunks) {
                 ChunkMeta h;
-                if (!build_chunks(mu_h.data(), E, Np, N, chunk_elems(degree), h, err)) return fail(ctx, SEM_E_MESH, err);
+                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree), h,
+                                  err, one ? nullptr : part.remote.data()))
+                    return fail(ctx, SEM_E_MESH, err);
                 const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
                 if (!diff.empty()) return fail(ctx, SEM_E_MESH, "GPU chunk builder differs from the host's: " + diff);
             }
@@ -1011,6 +1043,12 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             ctx->n_own = N;
             ctx->src_lookup.clear();  // the source vertex is looked up on the device (d_loc_can)
             ctx->src_int_of.clear();
+        } else if (gpu_chunks) {  // several ranks, device maps; the source is looked up on the device
+            CK(partition_io_maps(dpart, d_node_perm, ctx->d_loc_int, da, &ctx->d_loc_can, &ctx->d_own_int,
+                                 &ctx->d_own_can, &ctx->d_own_ft, &ctx->n_own, s));
+            ctx->d_loc_ft = dpart.loc2glob;
+            ctx->src_lookup.clear();
+            ctx->src_int_of.clear();
         } else {
             std::vector<int32_t> loc_int(ctx->N), loc_can(ctx->N), own_int, own_can, own_ft;
             ctx->src_lookup.assign(ctx->N, -1);
@@ -1036,7 +1074,8 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         }
         // interface exchange buffers
         ctx->n_if = m.N_if;
-        if ((int64_t)part.if_local.size() != m.N_if)
+        const int64_t nif_part = (!one && gpu_chunks) ? dpart.n_if : (int64_t)part.if_local.size();
+        if (nif_part != m.N_if)
             return fail(ctx, SEM_E_MESH, "interface node count mismatch between partition and chunks");
         ctx->n_send = (int64_t)part.send_if.size();
         ctx->nbr = part.nbr;

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <functional>
 #include <string>
+#include <vector>
 
 #include "sem_internal.h"
 
@@ -97,6 +98,22 @@ using DeviceAlloc = std::function<cudaError_t(void **, size_t)>;
 cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, int B, const uint8_t *d_forced,
                              const DeviceAlloc &dalloc, ChunkMeta &m, DevChunks &d, int32_t **d_int_of,
                              int32_t **d_bnd, int32_t **d_intc, std::string &err, cudaStream_t s);
+
+// ----------------------------- partition_gpu.cu ------------------------------
+// partition.cpp on the GPU for world >= 2: device loc2glob / mu_local / remote /
+// owned (persistent, from dalloc), host neighbour and summation lists.
+struct DevPartition {
+    int64_t e0 = 0, e1 = 0, NL = 0, n_if = 0;
+    int32_t *loc2glob = nullptr, *mu_local = nullptr;
+    uint8_t *remote = nullptr, *owned = nullptr;
+    std::vector<int32_t> nbr, nbr_off, send_if, sum_start, sum_src;
+};
+cudaError_t build_partition_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, int rank, int world,
+                                const DeviceAlloc &dalloc, DevPartition &P, std::string &err, cudaStream_t s);
+// loc_can[l] = node_perm[loc2glob[l]]; the owned subset of (loc_int, loc_can, loc2glob)
+cudaError_t partition_io_maps(const DevPartition &P, const int32_t *d_node_perm, const int32_t *d_loc_int,
+                              const DeviceAlloc &dalloc, int32_t **loc_can, int32_t **own_int, int32_t **own_can,
+                              int32_t **own_ft, int64_t *n_own, cudaStream_t s);
 
 cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s);
 // K6: per element (new order) G = c^2 detJ J^-1 J^-T and detJ.

@@ -90,3 +90,20 @@ def test_loopback_bitwise_deterministic():
         finally:
             g.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("name,scale", [("C2", 8), ("C5", 128)])
+def test_gpu_partition_equals_host(monkeypatch, world, name, scale):
+    """SEM_CHUNK_CHECK=1: every rank's GPU partition (partition_gpu.cu) and GPU
+    chunk metadata are compared with the host builders (partition.cpp,
+    chunks.cpp), array by array; sem_mesh_reorder fails on any difference."""
+    monkeypatch.setenv("SEM_CHUNK_CHECK", "1")
+    pb = mg.config(name, scale)
+    g = S.LoopbackGroup(world)
+    try:
+        g.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, pb.P)
+        infos = [c.sem_get_info() for c in g.ctxs]
+        assert all(i["n_interface_nodes"] > 0 for i in infos)
+    finally:
+        g.close()
