@@ -198,7 +198,9 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps);
  * y(t)) with R = Algorithm 2 (B = -I) and y = Algorithm 3;
  * t_n = n h, the corrector's source at t_{n+1} (reading R18).  The state is
  * (U [N], V [E][Np][2]), zero after sem_build_operators; `dt` is h.  Heun runs
- * with world_size 1 and chunks of 128 or 256 elements.
+ * at P = 2, 3 (chunks of 128 or 256 elements) and P = 5, on one rank or
+ * several (interface exchange of the (R(V), K U) pairs; loopback groups too).
+ * Selecting HEUN before sem_mesh_reorder also picks its chunk size (128).
  * Errors: SEM_E_UNSUPPORTED (unknown integrator).
  */
 sem_status sem_set_integrator(sem_ctx *ctx, int integrator);
@@ -223,7 +225,9 @@ sem_status sem_set_scatter(sem_ctx *ctx, int mode);
 /*
  * Heun only: copy V^n to out_host[E][Np][2] (fp64; INPUT element order, local
  * node p in the lattice order of reading R3 after the orientation fix, then the
- * x and y components) and return the step index.  Synchronises.
+ * x and y components; E = all elements of the mesh, each rank writing the
+ * elements it owns and leaving the others as they were) and return the step
+ * index.  Synchronises.
  * Errors: SEM_E_STATE (no Heun operators), SEM_E_ARG, SEM_E_CUDA, SEM_E_NONFINITE.
  */
 sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out);

@@ -28,11 +28,12 @@ int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 
 // Elements per chunk (one CTA iteration of K7): 256 by default; SEM_CHUNK=128|192|512
 // selects the other compiled variants (design experiments).
-int chunk_elems(int P) {
+int chunk_elems(int P, bool heun) {
     const char *v = getenv("SEM_CHUNK");
     if (P == 5) return 128;  // shared-memory budget of the stage at 21 nodes per element
     if (P == 7) return 64;   // ... and at 36
-    const int b = v ? atoi(v) : 256;
+    // Heun (integrator selected before sem_mesh_reorder): 128 runs 2 CTAs per SM
+    const int b = v ? atoi(v) : (heun ? 128 : 256);
     return (b == 128 || b == 192 || b == 512) ? b : 256;
 }
 
@@ -322,15 +323,16 @@ sem_status check_usable(sem_ctx *ctx) {
 
 // ---- interface exchange ------------------------------------------------------------
 // NCCL: grouped send/recv of the packed partials with every neighbour rank.
-sem_status exchange_nccl(sem_ctx *ctx, cudaStream_t st) {
+// w = fp64 values per interface node (1: K U or the mass; 2: Heun's (R(V), K U)).
+sem_status exchange_nccl(sem_ctx *ctx, cudaStream_t st, int w = 1) {
     if (ctx->nbr.empty()) return SEM_OK;
     NcclApi &N = nccl();
     ncclResult_t r = N.GroupStart();
     for (size_t k = 0; r == ncclSuccess && k < ctx->nbr.size(); k++) {
         const size_t off = ctx->nbr_off[k], cnt = ctx->nbr_off[k + 1] - off;
-        r = N.Send(ctx->d_sendbuf + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, st);
+        r = N.Send(ctx->d_sendbuf + w * off, w * cnt, ncclFloat64, ctx->nbr[k], ctx->comm, st);
         if (r == ncclSuccess)
-            r = N.Recv(ctx->d_xbuf + ctx->n_if + off, cnt, ncclFloat64, ctx->nbr[k], ctx->comm, st);
+            r = N.Recv(ctx->d_xbuf + w * (ctx->n_if + off), w * cnt, ncclFloat64, ctx->nbr[k], ctx->comm, st);
     }
     ncclResult_t r2 = N.GroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
@@ -340,7 +342,7 @@ sem_status exchange_nccl(sem_ctx *ctx, cudaStream_t st) {
 }
 
 // Loopback: contexts of one process; rank r copies what rank q packed for it.
-sem_status exchange_loopback(sem_ctx **ctxs, int n) {
+sem_status exchange_loopback(sem_ctx **ctxs, int n, int w = 1) {
     for (int r = 0; r < n; r++) {
         sem_ctx *ctx = ctxs[r];
         CK(cudaSetDevice(ctx->device));
@@ -362,8 +364,8 @@ sem_status exchange_loopback(sem_ctx **ctxs, int n) {
             if ((size_t)(src->nbr_off[kq + 1] - src->nbr_off[kq]) != cnt)
                 return fail(ctx, SEM_E_MESH, "interface sizes differ between ranks");
             CK(cudaStreamWaitEvent(ctx->stream, src->xev, 0));
-            CK(cudaMemcpyAsync(ctx->d_xbuf + ctx->n_if + ctx->nbr_off[k], src->d_sendbuf + src->nbr_off[kq],
-                               cnt * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(ctx->d_xbuf + w * (ctx->n_if + ctx->nbr_off[k]), src->d_sendbuf + w * src->nbr_off[kq],
+                               w * cnt * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
         }
     }
     // a rank's send buffer must not be overwritten before its neighbours copied it
@@ -438,19 +440,46 @@ HeunParams heun_params(sem_ctx *ctx) {
     return p;
 }
 
-// One Heun step (heun.cu): element pass with the lagged V update, then the
-// shared-node fix-up.  Leaves V lagged by one W update.
-sem_status heun_step(sem_ctx *ctx) {
+// One Heun step (heun.cu), phase 1: element pass with the lagged V update
+// (boundary chunks first when there are rank-interface nodes, their (R(V), K U)
+// partials packed and exchanged on the comm stream while the interior chunks
+// run), then the rank-local shared-node fix-up.
+sem_status heun_phase1(sem_ctx *ctx, bool use_nccl) {
     CK(cudaSetDevice(ctx->device));
     ST(ensure_tables(ctx));
     const HeunParams p = heun_params(ctx);
+    const int mode = ctx->v_lag ? 1 : 0;
     if (ctx->timing) ST(record(ctx, ctx->ev7, true));
-    CK(launch_heun(ctx->dch, p, ctx->v_lag ? 1 : 0, ctx->stream));
+    if (ctx->n_if == 0) {
+        CK(launch_heun(ctx->dch, p, mode, ctx->stream));
+    } else {
+        CK(launch_heun(ctx->dch, p, mode, ctx->stream, ctx->d_bnd, ctx->n_bnd));
+        CK(launch_heun_if_partial(ctx->dch, ctx->d_slot, ctx->d_xbuf, ctx->d_send_if, ctx->n_send, ctx->d_sendbuf,
+                                  ctx->stream));
+        if (use_nccl) {
+            CK(cudaEventRecord(ctx->ev_packed, ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+            ST(exchange_nccl(ctx, ctx->comm_stream, 2));
+            CK(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
+        }
+        CK(launch_heun(ctx->dch, p, mode, ctx->stream, ctx->d_intc, ctx->n_intc));
+    }
     if (ctx->timing) ST(record(ctx, ctx->ev7, false));
     if (ctx->timing) ST(record(ctx, ctx->ev8, true));
     CK(launch_heun_fix(ctx->dch, p, ctx->stream));
-    if (ctx->timing) ST(record(ctx, ctx->ev8, false));
-    ctx->v_lag = true;
+    if (use_nccl && ctx->n_if > 0) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
+    if (ctx->timing && ctx->n_if == 0) ST(record(ctx, ctx->ev8, false));
+    return SEM_OK;
+}
+
+// Heun phase 2: rank-ordered interface sums + update; advance the step.
+sem_status heun_phase2(sem_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->n_if > 0) {
+        CK(launch_heun_if(ctx->dch, heun_params(ctx), ctx->d_xbuf, ctx->d_sum_start, ctx->d_sum_src, ctx->stream));
+        if (ctx->timing) ST(record(ctx, ctx->ev8, false));
+    }
+    ctx->v_lag = true;  // V now lags W by one update
     ctx->step++;
     if (ctx->timing && ctx->ev7.size() >= 4096) ST(drain_events(ctx));
     return SEM_OK;
@@ -514,8 +543,6 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     if (ctx->integrator == SEM_INTEGRATOR_HEUN) {
         if (ctx->mesh_scatter != SEM_SCATTER_CHUNK)
             return fail(ctx, SEM_E_UNSUPPORTED, "the ablation scatters run the leapfrog only");
-        if (ctx->world > 1)
-            return fail(ctx, SEM_E_UNSUPPORTED, "the Heun integrator runs on one rank (world_size 1)");
         if (!heun_supported(ctx->Np, ctx->dch.B))
             return fail(ctx, SEM_E_UNSUPPORTED, "Heun kernels are built for chunks of 128 or 256 elements");
     }
@@ -607,7 +634,8 @@ sem_status build_phase2(sem_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     const double t = now_ms();
-    CK(launch_mass_if(ctx->dch, ctx->d_xbuf, ctx->d_sum_start, ctx->d_sum_src, ctx->dt, ctx->d_dt2M, s));
+    const double numer = ctx->ops_integrator == SEM_INTEGRATOR_HEUN ? 0.5 * ctx->dt : ctx->dt * ctx->dt;
+    CK(launch_mass_if(ctx->dch, ctx->d_xbuf, ctx->d_sum_start, ctx->d_sum_src, numer, ctx->d_dt2M, s));
     CK(cudaStreamSynchronize(s));
     ctx->step = 0;
     ctx->cur = 0;
@@ -950,13 +978,13 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         ChunkMeta m;
         DevChunks &d = ctx->dch;
         if (gpu_chunks) {
-            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, chunk_elems(degree),
+            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN),
                                 one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd, &ctx->d_intc,
                                 err, s));
             if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
             if (check_chunks) {
                 ChunkMeta h;
-                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree), h,
+                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN), h,
                                   err, one ? nullptr : part.remote.data()))
                     return fail(ctx, SEM_E_MESH, err);
                 const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
@@ -964,7 +992,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             }
             std::vector<int32_t>().swap(mu_h);
             tr.mark(s, "chunk builder (GPU)");
-        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree), m,
+        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN), m,
                                  err, one ? nullptr : part.remote.data())) {
             return fail(ctx, SEM_E_MESH, err);
         }
@@ -1089,8 +1117,8 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(upload(L, &ctx->d_send_if, part.send_if, s));
         CK(upload(L, &ctx->d_sum_start, part.sum_start, s));
         CK(upload(L, &ctx->d_sum_src, part.sum_src, s));
-        CK(dalloc(L, &ctx->d_xbuf, ctx->n_if + ctx->n_send + 2));
-        CK(dalloc(L, &ctx->d_sendbuf, ctx->n_send + 2));
+        CK(dalloc(L, &ctx->d_xbuf, 2 * (ctx->n_if + ctx->n_send) + 4));  // room for the Heun double2 payload
+        CK(dalloc(L, &ctx->d_sendbuf, 2 * ctx->n_send + 4));
         CK(cudaStreamSynchronize(s));
         tr.mark(s, "uploads + maps");
         ctx->k7_grid = k7_grid(d, false);
@@ -1127,7 +1155,10 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
     if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions step with sem_group_step_n");
     if (n_steps < 0) return fail(ctx, SEM_E_ARG, "n_steps < 0");
     if (ctx->ops_integrator == SEM_INTEGRATOR_HEUN) {
-        for (int64_t k = 0; k < n_steps; k++) ST(heun_step(ctx));
+        for (int64_t k = 0; k < n_steps; k++) {
+            ST(heun_phase1(ctx, ctx->world > 1));
+            ST(heun_phase2(ctx));
+        }
         return SEM_OK;
     }
     if (ctx->mesh_scatter != SEM_SCATTER_CHUNK) {
@@ -1163,13 +1194,16 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps) {
     for (int r = 0; r < n; r++) {
         ST(check_usable(ctxs[r]));
         if (!ctxs[r]->have_ops) return fail(ctxs[r], SEM_E_STATE, "sem_group_step_n before build");
-        if (ctxs[r]->ops_integrator != SEM_INTEGRATOR_LEAPFROG)
-            return fail(ctxs[r], SEM_E_UNSUPPORTED, "loopback groups step the leapfrog only");
+        if (ctxs[r]->ops_integrator != ctxs[0]->ops_integrator)
+            return fail(ctxs[r], SEM_E_STATE, "loopback group contexts built for different integrators");
+        if (ctxs[r]->mesh_scatter != SEM_SCATTER_CHUNK)
+            return fail(ctxs[r], SEM_E_UNSUPPORTED, "loopback groups use the chunk scatter");
     }
+    const bool heun = ctxs[0]->ops_integrator == SEM_INTEGRATOR_HEUN;
     for (int64_t k = 0; k < n_steps; k++) {
-        for (int r = 0; r < n; r++) ST(step_phase1(ctxs[r], false));
-        ST(exchange_loopback(ctxs, n));
-        for (int r = 0; r < n; r++) ST(step_phase2(ctxs[r]));
+        for (int r = 0; r < n; r++) ST(heun ? heun_phase1(ctxs[r], false) : step_phase1(ctxs[r], false));
+        ST(exchange_loopback(ctxs, n, heun ? 2 : 1));
+        for (int r = 0; r < n; r++) ST(heun ? heun_phase2(ctxs[r]) : step_phase2(ctxs[r]));
     }
     return SEM_OK;
 }
@@ -1200,16 +1234,25 @@ sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out) 
     std::vector<void *> tmp;
     struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
     double *d_out = nullptr;
-    const int64_t n = ctx->E * ctx->Np * 2;
+    const int64_t n = ctx->E_glob * ctx->Np * 2;  // this rank fills its own elements only
     CK(dalloc(tmp, &d_out, n));
-    CK(launch_v_out(ctx->d_V, ctx->d_perm, ctx->E, ctx->Np, ctx->dch.B, d_out, s));
+    if (ctx->world > 1) CK(cudaMemcpyAsync(d_out, out_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CK(launch_v_out(ctx->d_V, ctx->d_perm + ctx->e0, ctx->E, ctx->Np, ctx->dch.B, d_out, s));
     CK(cudaMemcpyAsync(out_host, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> mine;
+    if (ctx->world > 1) {
+        mine.resize(ctx->E);
+        CK(cudaMemcpyAsync(mine.data(), ctx->d_perm + ctx->e0, sizeof(int32_t) * ctx->E, cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
     if (step_out) *step_out = ctx->step;
-    for (int64_t i = 0; i < n; i++)
-        if (!std::isfinite(out_host[i]))
-            return fail(ctx, SEM_E_NONFINITE, "non-finite velocity at step " + std::to_string(ctx->step) +
-                                                  " (element " + std::to_string(i / (2 * ctx->Np)) + ")");
+    for (int64_t k = 0; k < ctx->E; k++) {
+        const int64_t e = mine.empty() ? k : mine[k];
+        for (int j = 0; j < 2 * ctx->Np; j++)
+            if (!std::isfinite(out_host[e * 2 * ctx->Np + j]))
+                return fail(ctx, SEM_E_NONFINITE, "non-finite velocity at step " + std::to_string(ctx->step) +
+                                                      " (element " + std::to_string(e) + ")");
+    }
     return SEM_OK;
 }
 
@@ -1222,13 +1265,13 @@ sem_status sem_write_velocity(sem_ctx *ctx, const double *v_host) {
     std::vector<void *> tmp;
     struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
     double *d_in = nullptr;
-    const int64_t n = ctx->E * ctx->Np * 2;
+    const int64_t n = ctx->E_glob * ctx->Np * 2;  // global array; each rank takes its elements
     if (v_host) {
         CK(dalloc(tmp, &d_in, n));
         CK(cudaMemcpyAsync(d_in, v_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     }
     CK(cudaMemsetAsync(ctx->d_V, 0, sizeof(double) * ctx->dch.nchunks * ctx->dch.B * 2 * ctx->Np, s));
-    CK(launch_v_in(d_in, ctx->d_perm, ctx->E, ctx->Np, ctx->dch.B, ctx->d_V, s));
+    CK(launch_v_in(d_in, ctx->d_perm + ctx->e0, ctx->E, ctx->Np, ctx->dch.B, ctx->d_V, s));
     CK(cudaStreamSynchronize(s));
     ctx->v_lag = false;
     return SEM_OK;

@@ -148,7 +148,11 @@ __global__ void k_local_keys(const int32_t *__restrict__ rc, const int32_t *__re
     const uint64_t x = sh ? (uint32_t)s : (uint32_t)g;
     key[r] = ((uint64_t)c << (9 + bx)) | ((uint64_t)(sh ? 1 : 0) << (8 + bx)) | ((uint64_t)(255 - cnt) << bx) | x;
     val[r] = (int32_t)r;
-    atomicAdd(sh ? &nsh[c] : &nint[c], 1);
+    // runs come in (chunk, node) order: lanes of a warp mostly share (c, sh), so
+    // aggregate the count per warp before the atomic
+    const int tag = 2 * c + (sh ? 1 : 0);
+    const unsigned peers = __match_any_sync(__activemask(), tag);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(sh ? &nsh[c] : &nint[c], __popc(peers));
 }
 
 __global__ void k_chunk_sizes(const int32_t *__restrict__ nint, const int32_t *__restrict__ nsh, int64_t nch,

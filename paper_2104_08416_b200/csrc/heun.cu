@@ -83,7 +83,8 @@ __device__ __forceinline__ double src_term(const HeunParams &a, int64_t id, int6
 // update; 2: finalise V only.
 template <int NP, int B, int MODE>
 __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
-    k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls) {
+    k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls, const int32_t *__restrict__ list,
+           int64_t nlist) {
     constexpr bool kLag = MODE >= 1, kStep = MODE <= 1, kFin = MODE == 2;
     extern __shared__ __align__(128) unsigned char sm[];
     const HeunLayout lay(NP, B, L, Lp, Ls);
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
     uint64_t *wfull = empty + kStagesH;
     uint64_t *wempty = wfull + 1;
     const int t = threadIdx.x;
-    const int64_t nch = ch.nchunks;
+    const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
     if (t == 0) {
         for (int s = 0; s < kStagesH; s++) {
@@ -113,7 +114,8 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
         // ===== producer warp =====
         const int lane = t - B;
         int k = 0;
-        for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+        for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
+            const int64_t c = list ? list[pos] : pos;
             const int s = k % kStagesH;
             if (k >= kStagesH && lane == 0) mbar_wait(&empty[s], ((k / kStagesH) & 1) ^ 1);
             __syncwarp();
@@ -160,7 +162,8 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
 
     // ===== consumer warps =====
     int k = 0;
-    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, k++) {
+    for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
+        const int64_t c = list ? list[pos] : pos;
         const int s = k % kStagesH;
         // this element's V (layout [chunk][2 NP][B]): issued before the stage wait
         double *vg = a.V + (c * 2 * NP) * B + t;
@@ -358,7 +361,7 @@ size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
     return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (3 * kStagesH + 2) * 8;
 }
 
-using HFn = void (*)(const DevChunks, const HeunParams, int, int, int, int);
+using HFn = void (*)(const DevChunks, const HeunParams, int, int, int, int, const int32_t *, int64_t);
 template <int NP, int B>
 HFn heun_fn_b(int mode) {
     return mode == 0 ? k_heun<NP, B, 0> : mode == 1 ? k_heun<NP, B, 1> : k_heun<NP, B, 2>;
@@ -413,13 +416,66 @@ int heun_grid(const DevChunks &ch, int mode) {
     return (int)g;
 }
 
-cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cudaStream_t s) {
-    if (ch.nchunks == 0) return cudaSuccess;
+cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cudaStream_t s, const int32_t *list,
+                        int64_t nlist) {
+    const int64_t n = list ? nlist : ch.nchunks;
+    if (n == 0) return cudaSuccess;
     const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, mode);
     const HFn fn = heun_fn(ch.Np, ch.B, mode);
     cudaError_t e = set_smem_h(fn, smem);
     if (e != cudaSuccess) return e;
-    fn<<<heun_grid(ch, mode), ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh);
+    int grid = heun_grid(ch, mode);
+    if (grid > n) grid = (int)n;
+    fn<<<grid, ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, list, nlist);
+    return cudaGetLastError();
+}
+
+// ---- multi-GPU interface (SURVEY §8e with the Heun payload: (R(V), K U) pairs) ----
+__global__ void k_if_partial2(const DevChunks ch, const double2 *__restrict__ slot, double2 *__restrict__ xbuf) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ch.N_if) return;
+    const int64_t s = ch.N_sh - ch.N_if + i;
+    double2 y = make_double2(0.0, 0.0);
+    for (int j = ch.sh_pstart[s]; j < ch.sh_pstart[s + 1]; j++) { y.x += slot[j].x; y.y += slot[j].y; }
+    xbuf[i] = y;
+}
+
+__global__ void k_pack2(const double2 *__restrict__ xbuf, const int32_t *__restrict__ send_if, int64_t n,
+                        double2 *__restrict__ sendbuf) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) sendbuf[k] = xbuf[send_if[k]];
+}
+
+// all ranks' (R(V), K U) of interface node i in ascending rank order, then the
+// Heun update of U and W (identical bits on every rank holding the node)
+__global__ void k_heun_if(const DevChunks ch, const HeunParams a, const double2 *__restrict__ xbuf,
+                          const int32_t *__restrict__ sum_start, const int32_t *__restrict__ sum_src) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ch.N_if) return;
+    double2 ab = make_double2(0.0, 0.0);
+    for (int j = sum_start[i]; j < sum_start[i + 1]; j++) { ab.x += xbuf[sum_src[j]].x; ab.y += xbuf[sum_src[j]].y; }
+    const int64_t id = ch.N_int + ch.N_sh - ch.N_if + i;
+    const double u0 = a.U[id], hm = a.hM[id];
+    const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
+    a.W[id] = u0 + hm * (ab.x + yn);
+    a.U[id] = u0 + hm * ((2.0 * ab.x - a.h * ab.y) + (yn + yn1));
+}
+
+cudaError_t launch_heun_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
+                                   int64_t n_send, double *sendbuf, cudaStream_t s) {
+    if (ch.N_if == 0) return cudaSuccess;
+    k_if_partial2<<<nblk(ch.N_if), 256, 0, s>>>(ch, reinterpret_cast<const double2 *>(slot),
+                                                reinterpret_cast<double2 *>(xbuf));
+    if (n_send > 0)
+        k_pack2<<<nblk(n_send), 256, 0, s>>>(reinterpret_cast<const double2 *>(xbuf), send_if, n_send,
+                                             reinterpret_cast<double2 *>(sendbuf));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_heun_if(const DevChunks &ch, const HeunParams &p, const double *xbuf, const int32_t *sum_start,
+                           const int32_t *sum_src, cudaStream_t s) {
+    if (ch.N_if == 0) return cudaSuccess;
+    k_heun_if<<<nblk(ch.N_if), 256, 0, s>>>(ch, p, reinterpret_cast<const double2 *>(xbuf), sum_start, sum_src);
     return cudaGetLastError();
 }
 

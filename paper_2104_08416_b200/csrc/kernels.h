@@ -151,7 +151,7 @@ cudaError_t launch_if_partial(const DevChunks &ch, const double *slot, double *x
 cudaError_t launch_k8_if(const DevChunks &ch, const StepParams &p, const double *xbuf, const int32_t *sum_start,
                          const int32_t *sum_src, cudaStream_t s);
 cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_t *sum_start, const int32_t *sum_src,
-                           double dt, double *dt2M, cudaStream_t s);
+                           double numer, double *dt2M, cudaStream_t s);
 // ------------------------------- heun.cu -----------------------------------
 // The paper's Heun predictor-corrector on (U, V) (NEXT-1).
 struct HeunParams {
@@ -171,7 +171,14 @@ cudaError_t launch_geometry_heun(const double *vxy, const int32_t *tri_or, const
                                  int64_t E, int64_t Epad, double *const geo[5], double *detJ, int32_t *bad,
                                  cudaStream_t s);
 // mode 0: step (V current), 1: step with the lagged V update, 2: V update only
-cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cudaStream_t s);
+cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cudaStream_t s,
+                        const int32_t *list = nullptr, int64_t nlist = 0);
+// multi-GPU Heun: interface (R(V), K U) partials of this rank (+ per-neighbour pack, double2), then
+// the rank-ordered sums and the U, W update of the interface nodes
+cudaError_t launch_heun_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
+                                   int64_t n_send, double *sendbuf, cudaStream_t s);
+cudaError_t launch_heun_if(const DevChunks &ch, const HeunParams &p, const double *xbuf, const int32_t *sum_start,
+                           const int32_t *sum_src, cudaStream_t s);
 cudaError_t launch_heun_fix(const DevChunks &ch, const HeunParams &p, cudaStream_t s);
 // V (chunk layout) <-> host layout [E][Np][2] in input element order; in == nullptr -> zeros
 cudaError_t launch_v_out(const double *V, const int32_t *perm, int64_t E, int np, int B, double *out, cudaStream_t s);

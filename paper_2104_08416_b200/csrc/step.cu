@@ -643,9 +643,9 @@ cudaError_t launch_k8_if(const DevChunks &ch, const StepParams &p, const double 
 }
 
 cudaError_t launch_mass_if(const DevChunks &ch, const double *xbuf, const int32_t *sum_start, const int32_t *sum_src,
-                           double dt, double *dt2M, cudaStream_t s) {
+                           double numer, double *dt2M, cudaStream_t s) {
     if (ch.N_if == 0) return cudaSuccess;
-    k_mass_if<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, xbuf, sum_start, sum_src, dt * dt, dt2M);
+    k_mass_if<<<blocks_for(ch.N_if), kThreads, 0, s>>>(ch, xbuf, sum_start, sum_src, numer, dt2M);
     return cudaGetLastError();
 }
 

@@ -207,10 +207,12 @@ class SemContext:
     def sem_set_integrator(self, integrator: int):
         self._check(self.L.sem_set_integrator(self.h, int(integrator)))
 
-    def sem_read_velocity(self):
-        """Heun: V^n as [E, Np, 2] in input element order."""
+    def sem_read_velocity(self, out=None):
+        """Heun: V^n as [E, Np, 2] in input element order; with several ranks
+        only this rank's elements are written into `out` (merge ranks by passing
+        the same array)."""
         info = self.sem_get_info()
-        out = np.empty((self.E, info["nodes_per_elem"], 2))
+        out = np.full((self.E, info["nodes_per_elem"], 2), np.nan) if out is None else out
         step = C.c_int64(0)
         self._check(self.L.sem_read_velocity(self.h, _ptr(out), C.byref(step)))
         return out, step.value
@@ -326,6 +328,20 @@ class LoopbackGroup:
     def sem_set_step(self, n):
         for c in self.ctxs:
             c.sem_set_step(n)
+
+    def sem_set_integrator(self, integrator):
+        for c in self.ctxs:
+            c.sem_set_integrator(integrator)
+
+    def sem_write_velocity(self, V):
+        for c in self.ctxs:
+            c.sem_write_velocity(V)
+
+    def sem_read_velocity(self):
+        out, step = None, None
+        for c in self.ctxs:
+            out, step = c.sem_read_velocity(out=out)
+        return out, step
 
     def sem_read_field(self, numbering=SEM_NUMBERING_CANONICAL):
         out = np.full(self.ctxs[0].N, np.nan)

@@ -156,16 +156,48 @@ def test_heun_zero_source_stays_zero_and_errors(ctx):
     assert e.value.status == S.SEM_E_STATE
 
 
-def test_heun_loopback_group_unsupported():
-    pb = mg.config("C1", 4)
-    g = S.LoopbackGroup(2)
+@pytest.mark.parametrize("world,name,scale,P", [(2, "C2", 8, None), (3, "C1", 1, None), (4, "C3", 20, None),
+                                                 (8, "C5", 128, None), (3, "B1", 25, 5)])
+def test_heun_multirank_loopback(ctx, world, name, scale, P):
+    """Heun across G partitions (SURVEY §8e with the (R(V), K U) payload, loopback
+    transport on one GPU): equal to the oracle (<= 1e-10 after a Ricker run,
+    <= 1e-12 from a random state) and to the one-rank run (rounding level)."""
+    pb = mg.config(name, scale, degree=P) if P else mg.config(name, scale)
+    m = pb.mesh
+    h = mg.heun_h(pb)
+    f0, t0 = shifted(pb, h)
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    steps = 60
+    Uo, Vo = o.heun(h, steps, src=pb.src_vertex, A=1.0, f0=f0, t0=t0)
+    setup_gpu(ctx, pb, h, f0=f0, t0=t0)
+    ctx.sem_step_n(steps)
+    U1, _ = ctx.sem_read_field()
+    V1, _ = ctx.sem_read_velocity()
+    g = S.LoopbackGroup(world)
     try:
-        for c in g.ctxs:
-            c.sem_set_integrator(S.SEM_INTEGRATOR_HEUN)
-        g.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, pb.P)
-        with pytest.raises(S.SemError) as e:
-            g.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, mg.heun_h(pb))
-        assert e.value.status == S.SEM_E_UNSUPPORTED
+        g.sem_set_integrator(S.SEM_INTEGRATOR_HEUN)
+        g.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        assert all(c.sem_get_info()["n_interface_nodes"] > 0 for c in g.ctxs)
+        g.sem_build_operators(pb.c, pb.src_vertex, f0, t0, 1.0, h)
+        g.sem_step_n(steps // 2)
+        g.sem_read_velocity()  # mid-run finalise on every rank
+        g.sem_step_n(steps - steps // 2)
+        Ug, n = g.sem_read_field()
+        Vg, _ = g.sem_read_velocity()
+        assert n == steps and not np.isnan(Ug).any() and not np.isnan(Vg).any()
+        assert rel_l2(Ug, Uo) <= REL_L2 and rel_l2(Vg, Vo) <= REL_L2
+        assert rel_l2(Ug, U1) <= 1e-13 and rel_l2(Vg, V1) <= 1e-13
+        # random state, 5 steps
+        rng = np.random.default_rng(world)
+        U0, V0 = rng.standard_normal(o.N), rng.standard_normal((m.ne, o.Np, 2))
+        Uo, Vo = o.heun(h, 5, src=pb.src_vertex, A=1.0, f0=f0, t0=t0, U=U0, V=V0, step0=9)
+        g.sem_write_state(U0, None)
+        g.sem_write_velocity(V0)
+        g.sem_set_step(9)
+        g.sem_step_n(5)
+        Ug, _ = g.sem_read_field()
+        Vg, _ = g.sem_read_velocity()
+        assert rel_l2(Ug, Uo) <= REL_STATE and rel_l2(Vg, Vo) <= REL_STATE
     finally:
         g.close()
 
