@@ -82,7 +82,7 @@ __device__ __forceinline__ double src_term(const HeunParams &a, int64_t id, int6
 // MODE 0: step with V^n stored (no lag); 1: step with V lagged by one W
 // update; 2: finalise V only.
 template <int NP, int B, int MODE>
-__global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
+__global__ void __launch_bounds__(B + 32, (B <= 128 && NP <= 10) ? 3 : B <= 128 ? 2 : 1)
     k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls, const int32_t *__restrict__ list,
            int64_t nlist) {
     constexpr bool kLag = MODE >= 1, kStep = MODE <= 1, kFin = MODE == 2;
@@ -219,13 +219,18 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                     ar[q] = sw * fma(F00, v[q], F01 * v[NP + q]);
                     as[q] = sw * fma(F10, v[q], F11 * v[NP + q]);
                 }
-                double *eb = reinterpret_cast<double *>(ebuf);  // (r, k) pairs: r now, k below
+                // (r, k) pairs: at P5 r goes to shared memory now (registers), else it
+                // stays in registers and the pair is stored with one 16-byte store
+                constexpr bool kSplit = NP > 10;
+                double *eb = reinterpret_cast<double *>(ebuf);
+                double r[kSplit ? 1 : NP];
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
                     double acc = 0.0;
 #pragma unroll
                     for (int q = 0; q < NP; q++) acc = fma(h_Dr[q][p], ar[q], fma(h_Ds[q][p], as[q], acc));
-                    eb[2 * lpo[p * B + t]] = acc;
+                    if (kSplit) eb[2 * lpo[p * B + t]] = acc;
+                    else r[kSplit ? 0 : p] = acc;
                 }
                 // (3) y = K^e u, K^e = Grr Srr + Gss Sss + Grs Srs, G = sd F F^T
                 //     (= c^2 detJ J^-1 J^-T, reading R5)
@@ -249,7 +254,10 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                     }
                 }
 #pragma unroll
-                for (int p = 0; p < NP; p++) eb[2 * lpo[p * B + t] + 1] = y[p];
+                for (int p = 0; p < NP; p++) {
+                    if (kSplit) eb[2 * lpo[p * B + t] + 1] = y[p];
+                    else ebuf[lpo[p * B + t]] = make_double2(r[kSplit ? 0 : p], y[p]);
+                }
             }
             consumer_sync<B>();
             mbar_wait(wfull, k & 1);
