@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <vector>
 
 #include "dev_common.cuh"
 #include "kernels.h"
@@ -40,11 +41,12 @@ namespace {
 constexpr int kStagesH = 2;
 constexpr int kDH = 8;  // CSR entries per node loaded together
 
-__constant__ double h_Dr[kMaxNp][kMaxNp];  // h_Dr[p][q] = dN_q/dr at node p
-__constant__ double h_Ds[kMaxNp][kMaxNp];
-__constant__ double h_Srr[kMaxNp][kMaxNp];
-__constant__ double h_Sss[kMaxNp][kMaxNp];
-__constant__ double h_Srs[kMaxNp][kMaxNp];
+// tables packed densely for the current degree: h_Dr[p * Np + q] = dN_q/dr at node p
+__constant__ double h_Dr[kMaxNp * kMaxNp];
+__constant__ double h_Ds[kMaxNp * kMaxNp];
+__constant__ double h_Srr[kMaxNp * kMaxNp];
+__constant__ double h_Sss[kMaxNp * kMaxNp];
+__constant__ double h_Srs[kMaxNp * kMaxNp];
 __constant__ double h_wK[kMaxNp];
 
 // Shared-memory layout of one stage (offsets 16-byte aligned).
@@ -82,7 +84,7 @@ __device__ __forceinline__ double src_term(const HeunParams &a, int64_t id, int6
 // MODE 0: step with V^n stored (no lag); 1: step with V lagged by one W
 // update; 2: finalise V only.
 template <int NP, int B, int MODE>
-__global__ void __launch_bounds__(B + 32, (B <= 128 && NP <= 10) ? 3 : B <= 128 ? 2 : 1)
+__global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
     k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls, const int32_t *__restrict__ list,
            int64_t nlist) {
     constexpr bool kLag = MODE >= 1, kStep = MODE <= 1, kFin = MODE == 2;
@@ -193,8 +195,8 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 && NP <= 10) ? 3 : B <= 128 
                 double gr = 0.0, gs = 0.0;
 #pragma unroll
                 for (int q = 0; q < NP; q++) {
-                    gr = fma(h_Dr[p][q], w[q], gr);
-                    gs = fma(h_Ds[p][q], w[q], gs);
+                    gr = fma(h_Dr[p * NP + q], w[q], gr);
+                    gs = fma(h_Ds[p * NP + q], w[q], gs);
                 }
                 v[p] = fma(hF00, gr, fma(hF10, gs, v[p]));
                 v[NP + p] = fma(hF01, gr, fma(hF11, gs, v[NP + p]));
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 && NP <= 10) ? 3 : B <= 128 
                 for (int p = 0; p < NP; p++) {
                     double acc = 0.0;
 #pragma unroll
-                    for (int q = 0; q < NP; q++) acc = fma(h_Dr[q][p], ar[q], fma(h_Ds[q][p], as[q], acc));
+                    for (int q = 0; q < NP; q++) acc = fma(h_Dr[q * NP + p], ar[q], fma(h_Ds[q * NP + p], as[q], acc));
                     if (kSplit) eb[2 * lpo[p * B + t]] = acc;
                     else r[kSplit ? 0 : p] = acc;
                 }
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(B + 32, (B <= 128 && NP <= 10) ? 3 : B <= 128 
                 for (int p = 0; p < NP; p++) {
 #pragma unroll
                     for (int q = p; q < NP; q++) {
-                        const double kk = fma(grr, h_Srr[p][q], fma(gss, h_Sss[p][q], grs * h_Srs[p][q]));
+                        const double kk = fma(grr, h_Srr[p * NP + q], fma(gss, h_Sss[p * NP + q], grs * h_Srs[p * NP + q]));
                         if (q == p) {
                             y[p] = fma(kk, u[p], y[p]);
                         } else {
@@ -390,11 +392,19 @@ bool heun_supported(int np, int B) {
 
 cudaError_t upload_heun_tables(const RefTables &T, cudaStream_t s) {
     cudaError_t e;
-    if ((e = cudaMemcpyToSymbolAsync(h_Dr, T.Dr, sizeof(T.Dr), 0, cudaMemcpyHostToDevice, s))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(h_Ds, T.Ds, sizeof(T.Ds), 0, cudaMemcpyHostToDevice, s))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(h_Srr, T.Srr, sizeof(T.Srr), 0, cudaMemcpyHostToDevice, s))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(h_Sss, T.Sss, sizeof(T.Sss), 0, cudaMemcpyHostToDevice, s))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(h_Srs, T.Srs, sizeof(T.Srs), 0, cudaMemcpyHostToDevice, s))) return e;
+    const int n = T.Np;  // packed [p * n + q]; pageable copies are staged before returning
+    std::vector<double> pk[5];
+    const double(*src[5])[kMaxNp] = {T.Dr, T.Ds, T.Srr, T.Sss, T.Srs};
+    for (int k = 0; k < 5; k++) {
+        pk[k].resize(n * n);
+        for (int p = 0; p < n; p++)
+            for (int q = 0; q < n; q++) pk[k][p * n + q] = src[k][p][q];
+    }
+    if ((e = cudaMemcpyToSymbolAsync(h_Dr, pk[0].data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Ds, pk[1].data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Srr, pk[2].data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Sss, pk[3].data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(h_Srs, pk[4].data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
     return cudaMemcpyToSymbolAsync(h_wK, T.wK, sizeof(T.wK), 0, cudaMemcpyHostToDevice, s);
 }
 

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <vector>
 
 #include "dev_common.cuh"
 #include "kernels.h"
@@ -36,9 +37,11 @@ constexpr int kThreads = 256;
 constexpr int kStages = 2;
 constexpr int kD = 8;    // entries per node loaded together (mesh vertex degree <= 8 typical)
 
-__constant__ double c_Srr[kMaxNp][kMaxNp];
-__constant__ double c_Sss[kMaxNp][kMaxNp];
-__constant__ double c_Srs[kMaxNp][kMaxNp];
+// S tables packed densely for the current degree ([p * Np + q]): at P3 the three
+// tables span 2.4 KB of the constant cache instead of rows strided by kMaxNp
+__constant__ double c_Srr[kMaxNp * kMaxNp];
+__constant__ double c_Sss[kMaxNp * kMaxNp];
+__constant__ double c_Srs[kMaxNp * kMaxNp];
 __constant__ double c_wM[kMaxNp];
 
 inline unsigned blocks_for(int64_t n, int threads = kThreads) {
@@ -201,9 +204,9 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
 
     if (G > 1) {
         for (int i = t; i < NP * NP; i += blockDim.x) {
-            S_s[i] = c_Srr[i / NP][i % NP];
-            S_s[NP * NP + i] = c_Sss[i / NP][i % NP];
-            S_s[2 * NP * NP + i] = c_Srs[i / NP][i % NP];
+            S_s[i] = c_Srr[i];
+            S_s[NP * NP + i] = c_Sss[i];
+            S_s[2 * NP * NP + i] = c_Srs[i];
         }
     }
     if (t == 0) {
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             for (int p = 0; p < NP; p++) {
 #pragma unroll
                 for (int q = p; q < NP; q++) {
-                    const double kk = fma(grr, c_Srr[p][q], fma(gss, c_Sss[p][q], grs * c_Srs[p][q]));
+                    const double kk = fma(grr, c_Srr[p * NP + q], fma(gss, c_Sss[p * NP + q], grs * c_Srs[p * NP + q]));
                     if (q == p) {
                         y[p] = fma(kk, u[p], y[p]);
                     } else {
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(256) k_abl_elem(const int32_t *__restrict__ mu
     for (int p = 0; p < NP; p++) {
 #pragma unroll
         for (int q = p; q < NP; q++) {
-            const double kk = fma(grr, c_Srr[p][q], fma(gss, c_Sss[p][q], grs * c_Srs[p][q]));
+            const double kk = fma(grr, c_Srr[p * NP + q], fma(gss, c_Sss[p * NP + q], grs * c_Srs[p * NP + q]));
             if (q == p) {
                 y[p] = fma(kk, u[p], y[p]);
             } else {
@@ -554,9 +557,15 @@ K7Fn k7_fn(int np, int B) { return k7_win2() ? k7_fn_w<true>(np, B) : k7_fn_w<fa
 
 cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s) {
     cudaError_t e;
-    if ((e = cudaMemcpyToSymbolAsync(c_Srr, T.Srr, sizeof(T.Srr), 0, cudaMemcpyHostToDevice, s))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(c_Sss, T.Sss, sizeof(T.Sss), 0, cudaMemcpyHostToDevice, s))) return e;
-    if ((e = cudaMemcpyToSymbolAsync(c_Srs, T.Srs, sizeof(T.Srs), 0, cudaMemcpyHostToDevice, s))) return e;
+    // pageable source: the copies return once the data is staged, so the packed
+    // buffers may go out of scope
+    const int n = T.Np;
+    std::vector<double> rr(n * n), ss(n * n), rs(n * n);
+    for (int p = 0; p < n; p++)
+        for (int q = 0; q < n; q++) { rr[p * n + q] = T.Srr[p][q]; ss[p * n + q] = T.Sss[p][q]; rs[p * n + q] = T.Srs[p][q]; }
+    if ((e = cudaMemcpyToSymbolAsync(c_Srr, rr.data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(c_Sss, ss.data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemcpyToSymbolAsync(c_Srs, rs.data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
     return cudaMemcpyToSymbolAsync(c_wM, T.wM, sizeof(T.wM), 0, cudaMemcpyHostToDevice, s);
 }
 
