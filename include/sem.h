@@ -173,7 +173,10 @@ sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t 
  *   U^{n+1} = 2 U^n - U^{n-1} + (dt^2 / M-bar) (A r(n dt) e_src - K U^n)
  * where K U^n is the element-by-element stiffness apply with gather and
  * conflict-free scatter (Algorithms 1-2, fused).
- * Enqueued on the context stream; returns without synchronising.
+ * Enqueued on the context stream; returns without synchronising.  With one
+ * rank (leapfrog, chunk scatter, kernel timing off) whole blocks of 32 steps
+ * replay a captured CUDA graph (step index in a device counter); the
+ * environment variable SEM_GRAPH=0 disables it.
  * Errors: SEM_E_STATE (no operators), SEM_E_ARG (n_steps < 0), SEM_E_CUDA.
  */
 sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps);

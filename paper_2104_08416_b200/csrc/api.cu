@@ -119,6 +119,8 @@ struct sem_ctx {
     double *d_U[2] = {nullptr, nullptr};
     double *d_slot = nullptr;
     int32_t *d_cnt = nullptr;  // shared-node arrival counters (K8 fused into K7, SEM_FUSE_K8=1)
+    cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};  // captured step loop per U parity
+    int64_t *d_nstep = nullptr;                          // its device step counter
     bool fuse_k8 = false;      // measured slower: off by default
     int cur = 0;
     // Heun (NEXT-1): U = d_U[0], hM = (h/2)/M-bar in d_dt2M, double2 slots in d_slot
@@ -191,7 +193,11 @@ void free_list(std::vector<void *> &l) {
     l.clear();
 }
 
+void destroy_graphs(sem_ctx *ctx);
+
 void reset_ops(sem_ctx *ctx) {
+    destroy_graphs(ctx);
+    ctx->d_nstep = nullptr;
     free_list(ctx->ops_allocs);
     ctx->d_Grr = ctx->d_Gss = ctx->d_Grs = ctx->d_dt2M = nullptr;
     ctx->d_U[0] = ctx->d_U[1] = nullptr;
@@ -393,7 +399,61 @@ StepParams step_params(sem_ctx *ctx) {
     p.U = ctx->d_U[ctx->cur];
     p.Uprev = ctx->d_U[1 - ctx->cur];
     p.n = ctx->step;
+    p.n_dev = nullptr;
     return p;
+}
+
+// ---- CUDA-graph step loop (one rank, leapfrog, chunk scatter, timing off) ----------
+// kGraphSteps consecutive steps (K7, K8, counter += 1 each; an even count, so the
+// U / U^{n-1} ping-pong returns to the same parity) are captured once per parity
+// and replayed; the step index comes from a device counter.  Removes the
+// per-launch host overhead that dominates small meshes.  SEM_GRAPH=0 disables.
+constexpr int kGraphSteps = 32;
+
+bool graph_ok(sem_ctx *ctx) {
+    static const bool env_off = getenv("SEM_GRAPH") && atoi(getenv("SEM_GRAPH")) == 0;
+    return !env_off && ctx->world == 1 && !ctx->timing && ctx->stream != nullptr &&
+           ctx->ops_integrator == SEM_INTEGRATOR_LEAPFROG && ctx->mesh_scatter == SEM_SCATTER_CHUNK &&
+           ctx->d_cnt == nullptr;
+}
+
+void destroy_graphs(sem_ctx *ctx) {
+    for (auto &g : ctx->graph_exec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
+    CK(cudaSetDevice(ctx->device));
+    ST(ensure_tables(ctx));
+    cudaStream_t s = ctx->stream;
+    cudaGraphExec_t &ex = ctx->graph_exec[ctx->cur];
+    if (!ex) {
+        if (!ctx->d_nstep) CK(dalloc(ctx->ops_allocs, &ctx->d_nstep, 1));
+        // one ordinary step's worth of attribute setting happens outside the capture
+        (void)k7_grid(ctx->dch, false);
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = cudaSuccess;
+        for (int k = 0; k < kGraphSteps && e == cudaSuccess; k++) {
+            StepParams p = step_params(ctx);
+            p.U = ctx->d_U[(ctx->cur + k) & 1];
+            p.Uprev = ctx->d_U[1 - ((ctx->cur + k) & 1)];
+            p.n_dev = ctx->d_nstep;
+            e = launch_k7(ctx->dch, p, ctx->k7_grid, s);
+            if (e == cudaSuccess) e = launch_k8(ctx->dch, p, s);
+            if (e == cudaSuccess) e = launch_step_inc(ctx->d_nstep, s);
+        }
+        cudaError_t e2 = cudaStreamEndCapture(s, &g);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture");
+        if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+    }
+    CK(launch_step_set(ctx->d_nstep, ctx->step, s));
+    for (int64_t r = 0; r < reps; r++) CK(cudaGraphLaunch(ex, s));
+    ctx->step += reps * kGraphSteps;
+    return SEM_OK;
 }
 
 // Step phase 1: stiffness + update of everything local; pack interface partials.
@@ -1165,7 +1225,13 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
         for (int64_t k = 0; k < n_steps; k++) ST(ablation_step(ctx));
         return SEM_OK;
     }
-    for (int64_t k = 0; k < n_steps; k++) {
+    int64_t k = 0;
+    if (graph_ok(ctx) && n_steps >= kGraphSteps) {
+        const int64_t reps = n_steps / kGraphSteps;
+        ST(graph_steps(ctx, reps));
+        k = reps * kGraphSteps;
+    }
+    for (; k < n_steps; k++) {
         ST(step_phase1(ctx, ctx->world > 1));
         ST(step_phase2(ctx));
     }

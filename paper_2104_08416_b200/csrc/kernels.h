@@ -138,8 +138,12 @@ struct StepParams {
     int32_t src;       // internal node id of the source (-1 none)
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
+    const int64_t *n_dev;  // if set: the step index lives in device memory (CUDA-graph step loop)
 };
 int k7_grid(const DevChunks &ch, bool fused);
+// device step counter of the graph-captured step loop: += 1, = v
+cudaError_t launch_step_inc(int64_t *n, cudaStream_t s);
+cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s);
 // K7 over all chunks (list == nullptr) or over the chunk ids list[0..nlist).
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
                       const int32_t *list = nullptr, int64_t nlist = 0);

@@ -44,6 +44,14 @@ __constant__ double c_Sss[kMaxNp * kMaxNp];
 __constant__ double c_Srs[kMaxNp * kMaxNp];
 __constant__ double c_wM[kMaxNp];
 
+// step index of U: from device memory when the step loop runs as a CUDA graph
+// (one graph replays many steps; k_step_inc advances the counter), else the
+// launch argument
+__device__ __forceinline__ int64_t step_index(const StepParams &a) { return a.n_dev ? *a.n_dev : a.n; }
+
+__global__ void k_step_inc(int64_t *n) { *n += 1; }
+__global__ void k_step_set(int64_t *n, int64_t v) { *n = v; }
+
 inline unsigned blocks_for(int64_t n, int threads = kThreads) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -173,7 +181,7 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
     for (int d = 1; d < 4; d++) y += part[d];
     for (int j = j0 + 4; j < j1; j++) y += __ldcg(&a.slot[j]);
     const int64_t id = ch.N_int + sg;
-    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
     a.Uprev[id] = 2.0 * u - a.Uprev[id] + a.dt2M[id] * (f - y);
     a.cnt[sg] = 0;
 }
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             const double yi = csr_sum(ebuf, lp, i);
             if (i < nint) {
                 const int id = i0 + i;
-                const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+                const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
                 Unew[id] = 2.0 * u_s[i] - up_s[i] + m_s[i] * (f - yi);
             } else if (i >= ni_al) {
                 const int j = i - ni_al;
@@ -396,7 +404,7 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
 #pragma unroll
     for (int d = 1; d < 4; d++) y += part[d];
     for (int j = j0 + 4; j < j1; j++) y += a.slot[j];
-    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
     a.Uprev[id] = 2.0 * u - up + m * (f - y);
 }
 
@@ -427,7 +435,7 @@ __global__ void k8_if(const DevChunks ch, const StepParams a, const double *__re
     for (int j = sum_start[i]; j < sum_start[i + 1]; j++) y += xbuf[sum_src[j]];
     const int64_t s = ch.N_sh - ch.N_if + i;
     const int64_t id = ch.N_int + s;
-    const double f = (id == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
     a.Uprev[id] = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
 }
 
@@ -493,7 +501,7 @@ __global__ void __launch_bounds__(256) k_abl_elem(const int32_t *__restrict__ mu
 __global__ void k_abl_update(int64_t n, const StepParams a, double *KU) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double f = (i == a.src) ? a.amp * ricker_dev((double)a.n * a.dt, a.f0, a.t0) : 0.0;
+    const double f = (i == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
     const double y = KU[i];
     KU[i] = 0.0;
     a.Uprev[i] = 2.0 * a.U[i] - a.Uprev[i] + a.dt2M[i] * (f - y);
@@ -674,6 +682,16 @@ cudaError_t launch_abl_elem(int np, bool atomic, const int32_t *mu, const int32_
 
 cudaError_t launch_abl_update(int64_t n, const StepParams &p, double *KU, cudaStream_t s) {
     k_abl_update<<<blocks_for(n), kThreads, 0, s>>>(n, p, KU);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step_inc(int64_t *n, cudaStream_t s) {
+    k_step_inc<<<1, 1, 0, s>>>(n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s) {
+    k_step_set<<<1, 1, 0, s>>>(n, v);
     return cudaGetLastError();
 }
 

@@ -236,3 +236,29 @@ def test_full_size_bench_configuration(ctx, name):
     Ug = run_gpu(ctx, pb2, 10)
     assert np.abs(Uo).max() > 0
     assert rel_l2(Ug, Uo) <= REL_L2, rel_l2(Ug, Uo)
+
+
+def test_graph_step_loop_bitwise_equal(monkeypatch):
+    """The CUDA-graph step loop (32 captured steps per replay, device step
+    counter) gives the same bits as launching step by step, and matches the
+    oracle; mixed with plain steps and timing on/off across calls."""
+    pb = mg.config("C2", 16)
+    pb = mg.Problem(**{**pb.__dict__, "t0": 10 * pb.dt, "f0": 1.0 / (8 * pb.dt)})
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    Uo, _ = o.leapfrog(pb.dt, 150, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
+    out = []
+    for graph in ("1", "0"):
+        monkeypatch.setenv("SEM_GRAPH", graph)
+        with S.SemContext(0) as c:  # graph_ok reads SEM_GRAPH once per process: use the timing switch too
+            c.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+            c.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+            c.sem_set_kernel_timing(graph == "0")  # timing forces the plain launch path
+            c.sem_step_n(70)   # 2 graph replays + 6 plain steps
+            c.sem_step_n(3)
+            c.sem_step_n(77)   # odd parity at entry: the other captured graph
+            U, n = c.sem_read_field()
+            assert n == 150
+            out.append(U)
+    assert np.array_equal(out[0], out[1])
+    assert rel_l2(out[0], Uo) <= REL_L2
