@@ -252,6 +252,66 @@ cudaError_t upload(std::vector<void *> &list, T **dst, const std::vector<T> &src
     return cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s);
 }
 
+// NEXT-4 ablation scatters: rows of mu in internal ids; COLOR: greedy global
+// element colouring in element order (smallest colour absent from every node's
+// elements), elements grouped by colour, ascending within a colour.
+sem_status prepare_ablation(sem_ctx *ctx, const std::vector<int32_t> &mu_h, int64_t E, int Np, int64_t N,
+                            int degree, bool one, const ChunkMeta &m, cudaStream_t s) {
+    if (!one) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters run with world_size 1");
+    if (degree > 3) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters are built for P = 2, 3");
+    std::vector<int32_t> rows((size_t)E * Np), eidx, color;
+    int ncol = 1;
+    if (ctx->scatter == SEM_SCATTER_COLOR) {
+        std::vector<uint64_t> used((size_t)N, 0);
+        color.assign((size_t)E, 0);
+        for (int64_t e = 0; e < E; e++) {
+            uint64_t mask = 0;
+            for (int p = 0; p < Np; p++) mask |= used[mu_h[e * Np + p]];
+            if (~mask == 0) return fail(ctx, SEM_E_MESH, "global colouring needs more than 64 colours");
+            const int c = __builtin_ctzll(~mask);
+            color[e] = c;
+            if (c + 1 > ncol) ncol = c + 1;
+            for (int p = 0; p < Np; p++) used[mu_h[e * Np + p]] |= (uint64_t)1 << c;
+        }
+    }
+    ctx->color_off.assign((size_t)ncol + 1, 0);
+    if (ctx->scatter == SEM_SCATTER_COLOR) {
+        for (int64_t e = 0; e < E; e++) ctx->color_off[color[e] + 1]++;
+        for (int c = 0; c < ncol; c++) ctx->color_off[c + 1] += ctx->color_off[c];
+        std::vector<int64_t> fillc(ctx->color_off.begin(), ctx->color_off.end() - 1);
+        eidx.resize((size_t)E);
+        for (int64_t e = 0; e < E; e++) eidx[fillc[color[e]]++] = (int32_t)e;
+    } else {
+        ctx->color_off[1] = E;
+    }
+    for (int64_t k = 0; k < E; k++) {
+        const int64_t e = eidx.empty() ? k : eidx[k];
+        for (int p = 0; p < Np; p++) rows[k * Np + p] = m.int_of[mu_h[e * Np + p]];
+    }
+    CK(upload(ctx->mesh_allocs, &ctx->d_mu_abl, rows, s));
+    if (!eidx.empty()) CK(upload(ctx->mesh_allocs, &ctx->d_eidx_abl, eidx, s));
+    ctx->mesh_scatter = ctx->scatter;
+    return SEM_OK;
+}
+
+// Host-built chunk metadata (chunks.cpp) -> device arrays and the device view.
+cudaError_t upload_chunks(std::vector<void *> &L, const ChunkMeta &m, DevChunks &d, cudaStream_t s) {
+    d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
+    d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
+    d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
+    int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
+    uint16_t *p_lpos, *p_lptr, *p_lidx, *p_shcr;
+    cudaError_t e;
+    if ((e = upload(L, &p_cmeta, m.cmeta, s)) || (e = upload(L, &p_lidx, m.lidx, s)) ||
+        (e = upload(L, &p_lpos, m.lpos, s)) || (e = upload(L, &p_lptr, m.lptr, s)) ||
+        (e = upload(L, &p_pstart, m.sh_pstart, s)) || (e = upload(L, &p_shn, m.shl_node, s)) ||
+        (e = upload(L, &p_shs, m.shl_slot, s)) || (e = upload(L, &p_shcr, m.shl_cr, s)))
+        return e;
+    d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.lptr = p_lptr; d.sh_pstart = p_pstart;
+    d.shl_node = p_shn; d.shl_slot = p_shs; d.shl_cr = p_shcr;
+    return cudaSuccess;
+}
+
 // SEM_CHUNK_CHECK=1: the GPU chunk builder's arrays against the host builder's.
 template <typename T>
 bool same_dev(const std::vector<T> &h, const T *dptr, size_t n, cudaStream_t s) {
@@ -746,6 +806,20 @@ sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
         return SEM_E_CUDA;
     }
     if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+    {
+        // The preparation's temporaries come from the device's default stream-ordered
+        // pool.  Keep up to 16 GB of freed pool memory mapped between calls instead of
+        // releasing it at every synchronisation (the default), so a later
+        // sem_mesh_reorder does not re-map it (SEM_POOL_KEEP_GB overrides; 0 = default).
+        cudaMemPool_t pool;
+        const char *kv = getenv("SEM_POOL_KEEP_GB");
+        const uint64_t keep = (uint64_t)(kv ? atof(kv) : 16.0) * (1ull << 30);
+        if (keep > 0 && cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t cur = 0;
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
+            if (cur < keep) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, (void *)&keep);
+        }
+    }
     if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
     else {
         if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
@@ -1035,16 +1109,17 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         tr.mark(s, "partition");
 
         // ---- chunk metadata for the step kernel ----
+        const int B_chunk = chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN);
         ChunkMeta m;
         DevChunks &d = ctx->dch;
         if (gpu_chunks) {
-            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN),
+            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, B_chunk,
                                 one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd, &ctx->d_intc,
                                 err, s));
             if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
             if (check_chunks) {
                 ChunkMeta h;
-                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN), h,
+                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, h,
                                   err, one ? nullptr : part.remote.data()))
                     return fail(ctx, SEM_E_MESH, err);
                 const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
@@ -1052,71 +1127,16 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             }
             std::vector<int32_t>().swap(mu_h);
             tr.mark(s, "chunk builder (GPU)");
-        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN), m,
+        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m,
                                  err, one ? nullptr : part.remote.data())) {
             return fail(ctx, SEM_E_MESH, err);
         }
         if (!gpu_chunks) {
-        if (ctx->scatter != SEM_SCATTER_CHUNK) {
-            if (!one) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters run with world_size 1");
-            if (degree > 3) return fail(ctx, SEM_E_UNSUPPORTED, "ablation scatters are built for P = 2, 3");
-            // rows of mu in internal ids; COLOR: greedy global element colouring in
-            // element order (smallest colour absent from every node's elements,
-            // PAPER.md:516), elements grouped by colour, ascending within a colour
-            std::vector<int32_t> rows((size_t)E * Np), eidx;
-            std::vector<int32_t> color;
-            int ncol = 1;
-            if (ctx->scatter == SEM_SCATTER_COLOR) {
-                std::vector<uint64_t> used((size_t)N, 0);
-                color.assign((size_t)E, 0);
-                for (int64_t e = 0; e < E; e++) {
-                    uint64_t mask = 0;
-                    for (int p = 0; p < Np; p++) mask |= used[mu_h[e * Np + p]];
-                    if (~mask == 0) return fail(ctx, SEM_E_MESH, "global colouring needs more than 64 colours");
-                    const int c = __builtin_ctzll(~mask);
-                    color[e] = c;
-                    if (c + 1 > ncol) ncol = c + 1;
-                    for (int p = 0; p < Np; p++) used[mu_h[e * Np + p]] |= (uint64_t)1 << c;
-                }
-            }
-            ctx->color_off.assign((size_t)ncol + 1, 0);
-            if (ctx->scatter == SEM_SCATTER_COLOR) {
-                for (int64_t e = 0; e < E; e++) ctx->color_off[color[e] + 1]++;
-                for (int c = 0; c < ncol; c++) ctx->color_off[c + 1] += ctx->color_off[c];
-                std::vector<int64_t> fillc(ctx->color_off.begin(), ctx->color_off.end() - 1);
-                eidx.resize((size_t)E);
-                for (int64_t e = 0; e < E; e++) eidx[fillc[color[e]]++] = (int32_t)e;
-            } else {
-                ctx->color_off[1] = E;
-            }
-            for (int64_t k = 0; k < E; k++) {
-                const int64_t e = eidx.empty() ? k : eidx[k];
-                for (int p = 0; p < Np; p++) rows[k * Np + p] = m.int_of[mu_h[e * Np + p]];
-            }
-            CK(upload(ctx->mesh_allocs, &ctx->d_mu_abl, rows, s));
-            if (!eidx.empty()) CK(upload(ctx->mesh_allocs, &ctx->d_eidx_abl, eidx, s));
-            ctx->mesh_scatter = ctx->scatter;
+            if (ctx->scatter != SEM_SCATTER_CHUNK) ST(prepare_ablation(ctx, mu_h, E, Np, N, degree, one, m, s));
+            std::vector<int32_t>().swap(mu_h);
+            tr.mark(s, "chunk builder (host)");
+            CK(upload_chunks(L, m, d, s));
         }
-        std::vector<int32_t>().swap(mu_h);
-        tr.mark(s, "chunk builder (host)");
-        d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
-        d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
-        d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
-        int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
-        uint16_t *p_lpos, *p_lptr, *p_lidx, *p_shcr;
-        CK(upload(L, &p_cmeta, m.cmeta, s));
-        CK(upload(L, &p_lidx, m.lidx, s));
-        CK(upload(L, &p_lpos, m.lpos, s));
-        CK(upload(L, &p_lptr, m.lptr, s));
-        CK(upload(L, &p_pstart, m.sh_pstart, s));
-        CK(upload(L, &p_shn, m.shl_node, s));
-        CK(upload(L, &p_shs, m.shl_slot, s));
-        CK(upload(L, &p_shcr, m.shl_cr, s));
-        d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.lptr = p_lptr; d.sh_pstart = p_pstart;
-        d.shl_node = p_shn;
-        d.shl_slot = p_shs;
-        d.shl_cr = p_shcr;
-        }  // host-built chunks
         // node maps for I/O (local node l -> internal / canonical / reordered id)
         if (one) {
             // reordered id == local id; the device node_perm (reordered -> canonical) is kept

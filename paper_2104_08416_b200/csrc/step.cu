@@ -528,9 +528,10 @@ bool k7_win2() {
 
 // consumer threads per element of the K7 instantiation used for np (1, or 4 at P7)
 int k7_group(int np) {
-    static int g7 = -1;
+    static int g7 = -1, g5 = -1;
     if (g7 < 0) { const char *e = getenv("SEM_K7_G"); g7 = e ? atoi(e) : 4; if (g7 != 1 && g7 != 2 && g7 != 4) g7 = 4; }
-    return np == 36 ? g7 : 1;
+    if (g5 < 0) { const char *e = getenv("SEM_K7_G5"); g5 = e ? atoi(e) : 1; if (g5 != 1 && g5 != 2) g5 = 1; }
+    return np == 36 ? g7 : np == 21 ? g5 : 1;
 }
 
 size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
@@ -544,7 +545,7 @@ size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
 template <bool W2>
 K7Fn k7_fn_w(int np, int B) {
-    if (np == 21) return k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
+    if (np == 21) return k7_group(21) == 2 ? k7_step<21, 128, W2, 2> : k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
     if (np == 36) {                              // P7: chunks of 64, G threads per element
         const int g = k7_group(36);
         return g == 4 ? k7_step<36, 64, W2, 4> : g == 2 ? k7_step<36, 64, W2, 2> : k7_step<36, 64, W2, 1>;
