@@ -1,0 +1,58 @@
+"""Host logic of the chunk builder (csrc/chunks.cpp, the twin of the GPU
+builder) on CPU through sem_debug_chunk_stats: the interior / shared split, the
+internal numbering and the slot count against brute force with Python sets."""
+import numpy as np
+import pytest
+
+from oracle import core
+from paper_2104_08416_b200 import meshgen as mg
+from paper_2104_08416_b200 import sem as S
+
+
+def reordered_mu(name, scale, P=None):
+    pb = mg.config(name, scale, degree=P) if P else mg.config(name, scale)
+    m = pb.mesh
+    t = core.orient(m.vxy, m.tri)
+    mu, N = core.canonical_nodes(t, m.nv, pb.P)
+    _, perm, _ = core.hilbert_order(m.vxy, m.tri)
+    _, mu_ft = core.first_touch(mu[perm], N)
+    return mu_ft, N
+
+
+@pytest.mark.parametrize("name,scale,P,B", [("C1", 1, None, 256), ("C2", 16, None, 256), ("C2", 16, None, 128),
+                                            ("C3", 40, None, 192), ("B1", 30, 5, 128), ("B1", 40, 7, 64)])
+def test_chunk_builder_brute_force(name, scale, P, B):
+    mu, N = reordered_mu(name, scale, P)
+    E, Np = mu.shape
+    st = S.sem_debug_chunk_stats(mu, N, B, want_maps=True)
+    nch = (E + B - 1) // B
+    assert st["nchunks"] == nch
+    touching = [set() for _ in range(N)]
+    for c in range(nch):
+        for g in np.unique(mu[c * B:(c + 1) * B]):
+            touching[g].add(c)
+    interior = np.array([len(s) == 1 for s in touching])
+    nsh = int((~interior).sum())
+    assert st["N_sh"] == nsh
+    assert st["sum_nint"] == int(interior.sum())
+    assert st["n_slots"] == sum(len(s) for s in touching if len(s) > 1)
+    int_of, cm = st["int_of"], st["cmeta"]
+    # internal ids: distinct; interior nodes inside their chunk's window, shared after N_int
+    assert len(set(int_of.tolist())) == N
+    N_int = st["N_int"]
+    assert (int_of[~interior] >= N_int).all() and (int_of[~interior] < N_int + nsh).all()
+    for g in np.nonzero(interior)[0][:: max(1, N // 2000)]:
+        c = next(iter(touching[g]))
+        i0, nint = cm[c, 0], cm[c, 1]
+        assert i0 % 2 == 0 and i0 <= int_of[g] < i0 + nint
+    # shared nodes in ascending id (no rank-interface nodes here)
+    sh_ids = np.nonzero(~interior)[0]
+    assert np.array_equal(int_of[sh_ids], N_int + np.arange(nsh))
+    # per-chunk counts and element counts
+    for c in range(nch):
+        ne = min(E, (c + 1) * B) - c * B
+        assert cm[c, 5] == ne
+        nodes = set(np.unique(mu[c * B:c * B + ne]).tolist())
+        assert cm[c, 1] == sum(1 for g in nodes if interior[g])
+        assert cm[c, 3] == sum(1 for g in nodes if not interior[g])
+        assert cm[c, 6] == cm[c, 1] + (cm[c, 1] & 1)
