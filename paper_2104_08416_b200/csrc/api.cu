@@ -178,6 +178,26 @@ sem_status cuda_fail(sem_ctx *c, cudaError_t e, const char *where) {
         if (_s != SEM_OK) return _s;    \
     } while (0)
 
+// Temporaries of one call: stream-ordered pool allocations, freed in stream
+// order when the call returns (no device-wide synchronisation of cudaFree).
+struct TmpList {
+    cudaStream_t s;
+    std::vector<void *> p;
+    ~TmpList() {
+        for (void *q : p) cudaFreeAsync(q, s);
+    }
+};
+
+template <typename T>
+cudaError_t dalloc(TmpList &t, T **p, size_t count) {
+    void *q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, sizeof(T) * (count ? count : 1), t.s);
+    if (e != cudaSuccess) return e;
+    t.p.push_back(q);
+    *p = (T *)q;
+    return cudaSuccess;
+}
+
 template <typename T>
 cudaError_t dalloc(std::vector<void *> &list, T **p, size_t count) {
     void *q = nullptr;
@@ -673,8 +693,7 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     const DevChunks &d = ctx->dch;
     const int64_t Epad = d.nchunks * d.B;
     auto &L = ctx->ops_allocs;
-    std::vector<void *> tmp;
-    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    TmpList tmp{ctx->stream, {}};
     double *d_c = nullptr, *d_detJ = nullptr;
     int32_t *d_bad = nullptr;
     CK(dalloc(tmp, &d_c, ctx->E_glob));
@@ -905,8 +924,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         ctx->E_glob = n_elements;
         if (!build_ref_tables(degree, ctx->T)) return fail(ctx, SEM_E_UNSUPPORTED, "reference tables");
         const int64_t E = n_elements, nv = n_vertices;
-        std::vector<void *> tmp;  // freed at the end of this call
-        struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+        TmpList tmp{ctx->stream, {}};  // freed (stream-ordered) at the end of this call
 
         CK(dalloc(ctx->mesh_allocs, &ctx->d_vxy, 2 * nv));
         CK(cudaMemcpyAsync(ctx->d_vxy, vxy_host, sizeof(double) * 2 * nv, cudaMemcpyHostToDevice, s));
@@ -1142,8 +1160,8 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             // reordered id == local id; the device node_perm (reordered -> canonical) is kept
             if (!gpu_chunks) CK(upload(L, &ctx->d_loc_int, m.int_of, s));
             ctx->d_loc_can = d_node_perm;
-            for (auto it = tmp.begin(); it != tmp.end(); ++it)
-                if (*it == (void *)d_node_perm) { L.push_back(*it); tmp.erase(it); break; }
+            for (auto it = tmp.p.begin(); it != tmp.p.end(); ++it)  // kept: becomes a persistent map
+                if (*it == (void *)d_node_perm) { L.push_back(*it); tmp.p.erase(it); break; }
             ctx->d_loc_ft = nullptr;
             ctx->d_own_int = ctx->d_loc_int;
             ctx->d_own_can = ctx->d_loc_can;
@@ -1317,8 +1335,7 @@ sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out) 
     if (!out_host) return fail(ctx, SEM_E_ARG, "out is NULL");
     ST(heun_finalize(ctx));
     cudaStream_t s = ctx->stream;
-    std::vector<void *> tmp;
-    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    TmpList tmp{ctx->stream, {}};
     double *d_out = nullptr;
     const int64_t n = ctx->E_glob * ctx->Np * 2;  // this rank fills its own elements only
     CK(dalloc(tmp, &d_out, n));
@@ -1348,8 +1365,7 @@ sem_status sem_write_velocity(sem_ctx *ctx, const double *v_host) {
         return fail(ctx, SEM_E_STATE, "sem_write_velocity needs operators built for the Heun integrator");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    std::vector<void *> tmp;
-    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    TmpList tmp{ctx->stream, {}};
     double *d_in = nullptr;
     const int64_t n = ctx->E_glob * ctx->Np * 2;  // global array; each rank takes its elements
     if (v_host) {
@@ -1371,8 +1387,7 @@ sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t
         return fail(ctx, SEM_E_ARG, "unknown numbering");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    std::vector<void *> tmp;
-    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    TmpList tmp{ctx->stream, {}};
     double *d_out = nullptr;
     int32_t *d_flag = nullptr;
     const int64_t NG = ctx->N_glob;
@@ -1404,8 +1419,7 @@ sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double
         return fail(ctx, SEM_E_ARG, "unknown numbering");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    std::vector<void *> tmp;
-    struct Guard { std::vector<void *> &l; ~Guard() { free_list(l); } } guard{tmp};
+    TmpList tmp{ctx->stream, {}};
     double *d_in = nullptr;
     CK(dalloc(tmp, &d_in, ctx->N_glob));
     const int32_t *imap = numbering == SEM_NUMBERING_CANONICAL ? ctx->d_loc_can : ctx->d_loc_ft;
