@@ -191,17 +191,20 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
 // 32 (w / G) + lane and the row block w % G of y = K^e u, computed as
 // y_p = grr (Srr u)_p + gss (Sss u)_p + grs (Srs u)_p with the S tables staged in
 // shared memory (all lanes of a warp read the same entry: broadcast).
-template <int NP, int B, bool WIN2, int G = 1>
+template <int NP, int B, int WM, int G = 1>
 __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
     constexpr int C = B * G;  // consumer threads
     extern __shared__ __align__(128) unsigned char sm[];
+    // WM: U^{n-1} / dt^2/M windows -- 0 read from global in the node phase, 1 single-buffered
+    // TMA window (default), 2 inside the double-buffered stages
+    constexpr bool WIN2 = WM == 2, WIN1 = WM == 1;
     const StageLayout lay(NP, B, L, Lp, Ls, a.cnt ? Ls : 0, WIN2 ? W : 0);
     double *ebuf = reinterpret_cast<double *>(sm + kStages * lay.size);  // [NP][B] element slots
     double *up_w = ebuf + NP * B;                                       // U^{n-1} window (single buffer)
-    double *m_w = up_w + (WIN2 ? 0 : W);                                // dt^2/M window (single buffer)
-    uint64_t *full = reinterpret_cast<uint64_t *>(m_w + (WIN2 ? 0 : W));  // TMA blocks landed
+    double *m_w = up_w + (WIN1 ? W : 0);                                // dt^2/M window (single buffer)
+    uint64_t *full = reinterpret_cast<uint64_t *>(m_w + (WIN1 ? W : 0));  // TMA blocks landed
     uint64_t *gath = full + kStages;                                    // shared-node gathers landed
     uint64_t *empty = gath + kStages;                                   // consumers done with stage
     uint64_t *wfull = empty + kStages;                                  // U^{n-1}, dt^2/M windows landed
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             cp_async_arrive_noinc(&gath[s]);
             // the single U^{n-1} / dt^2/M window buffer: free once the previous
             // chunk's update is done; lands while this chunk's element phase runs
-            if (!WIN2 && lane == 0) {
+            if (WIN1 && lane == 0) {
                 if (k >= 1) mbar_wait(wempty, (k - 1) & 1);
                 mbar_arrive_expect_tx(wfull, (uint32_t)ni_al * 16);
                 if (ni_al > 0) {
@@ -362,18 +365,23 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = y[p];  // straight to the node's CSR run
         }
         consumer_sync<C>();
-        if (!WIN2) mbar_wait(wfull, k & 1);
+        if (WIN1) mbar_wait(wfull, k & 1);
         const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
         const double *m_s = WIN2 ? reinterpret_cast<const double *>(st + lay.m) : m_w;
         // (B) node-centric gather of K U^n in fixed order + fused update;
         //     shared nodes: this chunk's partial into the node's slot
         double *Unew = a.Uprev;
         for (int i = t; i < nl; i += C) {
+            double upg = 0.0, mg = 0.0;
+            if (WM == 0 && i < nint) {  // coalesced global loads, issued before the shared-memory sum
+                upg = a.Uprev[i0 + i];
+                mg = __ldg(a.dt2M + i0 + i);
+            }
             const double yi = csr_sum(ebuf, lp, i);
             if (i < nint) {
                 const int id = i0 + i;
                 const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
-                Unew[id] = 2.0 * u_s[i] - up_s[i] + m_s[i] * (f - yi);
+                Unew[id] = 2.0 * u_s[i] - (WM == 0 ? upg : up_s[i]) + (WM == 0 ? mg : m_s[i]) * (f - yi);
             } else if (i >= ni_al) {
                 const int j = i - ni_al;
                 const int sl = shs[j];
@@ -385,7 +393,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         consumer_sync<C>();
         if (t == 0) {
             mbar_arrive(&empty[s]);
-            if (!WIN2) mbar_arrive(wempty);
+            if (WIN1) mbar_arrive(wempty);
         }
     }
 }
@@ -519,11 +527,12 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return e;
 }
 
-// SEM_K7_WIN=2 puts the U^{n-1} / dt^2/M windows into the stages (double-buffered)
-bool k7_win2() {
+// U^{n-1} / dt^2/M windows: SEM_K7_WIN=1 single-buffered TMA window (default),
+// 2 inside the double-buffered stages, 0 plain global loads in the node phase
+int k7_win() {
     static int v = -1;
-    if (v < 0) { const char *e = getenv("SEM_K7_WIN"); v = (e && atoi(e) == 2) ? 1 : 0; }
-    return v == 1;
+    if (v < 0) { const char *e = getenv("SEM_K7_WIN"); v = e ? atoi(e) : 1; if (v < 0 || v > 2) v = 1; }
+    return v;
 }
 
 // consumer threads per element of the K7 instantiation used for np (1, or 4 at P7)
@@ -535,15 +544,15 @@ int k7_group(int np) {
 }
 
 size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
-    const bool w2 = k7_win2();
-    const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, w2 ? W : 0);
+    const int wm = k7_win();
+    const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, wm == 2 ? W : 0);
     const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * np * 8 : 0;
-    return (size_t)kStages * lay.size + (size_t)np * B * 8 + (w2 ? 0 : 2 * (size_t)W * 8) + (3 * kStages + 2) * 8 +
-           stab;
+    return (size_t)kStages * lay.size + (size_t)np * B * 8 + (wm == 1 ? 2 * (size_t)W * 8 : 0) +
+           (3 * kStages + 2) * 8 + stab;
 }
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
-template <bool W2>
+template <int W2>
 K7Fn k7_fn_w(int np, int B) {
     if (np == 21) return k7_group(21) == 2 ? k7_step<21, 128, W2, 2> : k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
     if (np == 36) {                              // P7: chunks of 64, G threads per element
@@ -560,7 +569,10 @@ K7Fn k7_fn_w(int np, int B) {
            : B == 512 ? k7_step<10, 512, W2>
                       : k7_step<10, 256, W2>;
 }
-K7Fn k7_fn(int np, int B) { return k7_win2() ? k7_fn_w<true>(np, B) : k7_fn_w<false>(np, B); }
+K7Fn k7_fn(int np, int B) {
+    const int wm = k7_win();
+    return wm == 2 ? k7_fn_w<2>(np, B) : wm == 0 ? k7_fn_w<0>(np, B) : k7_fn_w<1>(np, B);
+}
 
 }  // namespace
 
