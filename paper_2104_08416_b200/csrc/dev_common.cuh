@@ -34,6 +34,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The same wait written out at the call site (distinct source lines for ncu's
+// per-line stall attribution: which barrier the consumers wait on).
+#define MBAR_WAIT_INLINE(bar, parity)                                              \
+    asm volatile(                                                                  \
+        "{\n"                                                                      \
+        ".reg .pred p;\n"                                                          \
+        "WAIT_%=:\n"                                                               \
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"                  \
+        "@!p bra WAIT_%=;\n"                                                       \
+        "}\n" ::"r"(smem_u32(bar)),                                                \
+        "r"(parity)                                                                \
+        : "memory")
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n"

@@ -297,8 +297,8 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     int k = 0;
     for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
         const int s = k % kStages;
-        mbar_wait(&full[s], (k / kStages) & 1);
-        mbar_wait(&gath[s], (k / kStages) & 1);
+        MBAR_WAIT_INLINE(&full[s], (k / kStages) & 1);  // stage blocks (TMA)
+        MBAR_WAIT_INLINE(&gath[s], (k / kStages) & 1);  // shared-node U gathers (cp.async)
         const unsigned char *st = sm + s * lay.size;
         const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
         const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = y[p];  // straight to the node's CSR run
         }
         consumer_sync<C>();
-        if (WIN1) mbar_wait(wfull, k & 1);
+        if (WIN1) MBAR_WAIT_INLINE(wfull, k & 1);  // U^{n-1} / dt^2/M window
         const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
         const double *m_s = WIN2 ? reinterpret_cast<const double *>(st + lay.m) : m_w;
         // (B) node-centric gather of K U^n in fixed order + fused update;

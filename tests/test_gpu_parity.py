@@ -290,3 +290,31 @@ def test_full_size_c5_properties(ctx):
     ctx.sem_step_n(20)
     Ug, n = ctx.sem_read_field()
     assert n == 20 and np.isfinite(Ug).all()
+
+
+def test_degenerate_inputs(ctx):
+    """Empty mesh, zero steps, unused vertices, more ranks than elements."""
+    vxy = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [5.0, 5.0]])
+    tri = np.array([[0, 1, 2]], np.int32)
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_mesh_reorder(vxy, np.zeros((0, 3), np.int32), 2)
+    assert e.value.status == S.SEM_E_ARG
+    with pytest.raises(S.SemError) as e:  # vertex 3 is used by no element: its M-bar would be 0
+        ctx.sem_mesh_reorder(vxy, tri, 2)
+    assert e.value.status == S.SEM_E_MESH and "vertex 3" in e.value.msg
+    bad = tri.copy()
+    bad[0, 2] = 7
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_mesh_reorder(vxy[:3], bad, 2)
+    assert e.value.status == S.SEM_E_MESH
+    ctx.sem_mesh_reorder(vxy[:3], tri, 3)
+    ctx.sem_build_operators(np.ones(1), 0, 5.0, 0.0, 1.0, 0.01)
+    ctx.sem_step_n(0)
+    U, n = ctx.sem_read_field()
+    assert n == 0 and (U == 0).all()
+    with pytest.raises(S.SemError) as e:
+        ctx.sem_step_n(-1)
+    assert e.value.status == S.SEM_E_ARG
+    with pytest.raises(S.SemError) as e:
+        S.LoopbackGroup(2).sem_mesh_reorder(vxy[:3], tri, 2)  # 1 element, 2 ranks
+    assert e.value.status == S.SEM_E_ARG
