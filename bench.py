@@ -366,13 +366,14 @@ FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = fp64_peak()
 
 def orders_leg(ctx, args, S, peak, peaks):
     """NEXT-2: the paper's Benchmark 1 shape (2000 x 1000 units, 1M elements,
-    PAPER.md:572) at its orders 5 and 7, Hilbert vs the
-    shuffled file order ("None").  P5/P7 are FP64-bound."""
+    PAPER.md:572) at its orders 5-7 and 4 (readings R21,
+    R21b), Hilbert vs the shuffled file order ("None").  FP64-bound from P5 on
+    (DESIGN.md)."""
     import torch
     from paper_2104_08416_b200 import meshgen as mg
     res = {}
     stream = torch.cuda.current_stream()
-    for P in (5, 7):
+    for P in (4, 5, 6, 7):
         pb = mg.config("B1", 1, degree=P)
         Np = (P + 1) * (P + 2) // 2
         flop_elem = 2.0 * (3 * Np * (Np + 1) / 2 + Np * Np)  # K^e entries (2 FMA + MUL) + symmetric mat-vec

@@ -40,7 +40,7 @@ typedef enum {
     SEM_E_ARG = 1,          /* invalid argument (range, NULL, c <= 0, dt <= 0 ...) */
     SEM_E_STATE = 2,        /* call out of order (e.g. step before build)          */
     SEM_E_MESH = 3,         /* degenerate / inconsistent mesh                      */
-    SEM_E_UNSUPPORTED = 4,  /* degree not in {2, 3}, unknown ordering ...           */
+    SEM_E_UNSUPPORTED = 4,  /* degree not in 2..7, unknown ordering ...             */
     SEM_E_CUDA = 5,         /* CUDA error (sticky)                                 */
     SEM_E_NCCL = 6,         /* NCCL error                                          */
     SEM_E_OOM = 7,          /* device or host allocation failed                    */
@@ -114,9 +114,11 @@ const char *sem_last_error(const sem_ctx *ctx);
  *  tri_host   [n_elements][3] int32 vertex ids of linear triangles.  A
  *             clockwise triangle is fixed by swapping its 2nd and 3rd vertex
  *             (the centroid used for the SFC key is taken before the fix).
- *  degree     polynomial order P in {2, 3}: Np = 6 or 10 local nodes,
- *             placed per DESIGN.md reading R3 (P2 midpoints; P3 Gauss-Lobatto
- *             edge points + centroid).
+ *  degree     polynomial order P in 2..7: Np = (P+1)(P+2)/2 local nodes,
+ *             placed per DESIGN.md readings R3 / R21 (P2 midpoints; P3
+ *             Gauss-Lobatto edge points + centroid; P >= 4 the Blyth-Pozrikidis
+ *             Lobatto grid).  P = 4, 6 use the consistent stiffness and the
+ *             HRZ-lumped mass (reading R21b; their nodal weights are negative).
  *  elem_order SEM_ORDER_*.  HILBERT follows PAPER.md:299-305: centroids ->
  *             bounding box w_b = ceil(sqrt(E)), h_b = ceil(sqrt(E)/r) of the
  *             vertex extents (r = w_m/h_m) -> generalized Hilbert curve over
@@ -340,10 +342,18 @@ sem_status sem_debug_partition(const int32_t *mu, int64_t E, int Np, int64_t N, 
  * library derives for `degree` (refelem.cpp; readings R3, R4, R21): *np_out = Np,
  * nodes_out [Np][2], wK_out / wM_out [Np] (stiffness / mass weights), Dr_out /
  * Ds_out [Np][Np] with Dr[k][p] = dN_p/dr at node k.  Any output may be NULL.
- * Errors: SEM_E_UNSUPPORTED (degree not in {2, 3, 5, 7}).
+ * Errors: SEM_E_UNSUPPORTED (degree not in 2..7).
  */
 sem_status sem_debug_ref_tables(int degree, int32_t *np_out, double *nodes_out, double *wK_out, double *wM_out,
                                 double *Dr_out, double *Ds_out);
+
+/*
+ * Host-only diagnostic: the element stiffness factors the step kernel uses,
+ * K^e = Grr Srr + Gss Sss + Grs Srs, as [Np][Np] each (nodal quadrature
+ * D^T W D for P = 2, 3, 5, 7; exact integrals for P = 4, 6, reading R21b).
+ * Errors: SEM_E_UNSUPPORTED.
+ */
+sem_status sem_debug_ref_stiffness(int degree, double *Srr_out, double *Sss_out, double *Srs_out);
 
 /* Library version string. */
 const char *sem_version(void);

@@ -59,8 +59,10 @@ def lib():
             L.orc_apply_R.restype = None
             L.orc_ricker.argtypes = [dbl, dbl, dbl]
             L.orc_ricker.restype = dbl
-            L.orc_leapfrog.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P,
+            L.orc_leapfrog.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P, P, P, P,
                                        i64, dbl, dbl, dbl, dbl, i64, i64, P, P]
+            L.orc_apply_R_tables.argtypes = [P, i64, C.c_int, i64, P, P, P, P, P, P, P, P, P]
+            L.orc_apply_R_tables.restype = None
             L.orc_leapfrog.restype = C.c_int
             L.orc_vdot.argtypes = [P, i64, C.c_int, P, P, P, P, P, P]
             L.orc_vdot.restype = None
@@ -257,6 +259,9 @@ class OracleSEM:
         lib().orc_lumped_mass(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.wM), _p(self.Mbar))
         self.c = np.ones(self.ne) if c_elem is None else np.ascontiguousarray(c_elem, np.float64)
         self._ebuf = None
+        # reading R21b (P = 4, 6): consistent stiffness from the exact S tables
+        self.S = (tuple(np.ascontiguousarray(self.T[k]) for k in ("Srr", "Sss", "Srs"))
+                  if self.T.get("consistent") else None)
 
     def set_c(self, c_elem):
         self.c = np.ascontiguousarray(c_elem, np.float64)
@@ -267,8 +272,12 @@ class OracleSEM:
         R = np.empty(self.N)
         if self._ebuf is None:
             self._ebuf = np.empty(self.ne * self.Np)
-        lib().orc_apply_R(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.Jinv), _p(self.c),
-                          _p(self.Dr), _p(self.Ds), _p(self.wK), _p(U), _p(R), _p(self._ebuf))
+        if self.S is not None:
+            lib().orc_apply_R_tables(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.Jinv),
+                                     _p(self.c), *(_p(x) for x in self.S), _p(U), _p(R), _p(self._ebuf))
+        else:
+            lib().orc_apply_R(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.Jinv), _p(self.c),
+                              _p(self.Dr), _p(self.Ds), _p(self.wK), _p(U), _p(R), _p(self._ebuf))
         return R
 
     def apply_K(self, U):
@@ -279,8 +288,9 @@ class OracleSEM:
         """n_steps of the leapfrog from (U^n, U^{n-1}) (zeros by default)."""
         U = np.zeros(self.N) if U is None else np.array(U, np.float64, copy=True)
         Up = np.zeros(self.N) if Uprev is None else np.array(Uprev, np.float64, copy=True)
+        S = (None, None, None) if self.S is None else tuple(_p(x) for x in self.S)
         rc = lib().orc_leapfrog(_p(self.mu), self.ne, self.Np, self.N, _p(self.detJ), _p(self.Jinv),
-                                _p(self.c), _p(self.Dr), _p(self.Ds), _p(self.wK), _p(self.Mbar),
+                                _p(self.c), _p(self.Dr), _p(self.Ds), _p(self.wK), _p(self.Mbar), *S,
                                 int(src), float(A), float(f0), float(t0), float(dt), int(step0),
                                 int(n_steps), _p(U), _p(Up))
         if rc != 0:

@@ -138,6 +138,10 @@ def tables(P: int):
 # (Blyth & Pozrikidis 2006; for P = 2, 3 it gives the R3 node sets above).
 # The paper cites these locations without printing them:
 # parity unpinned beyond the invariants of tests/test_oracle_refelem.py.
+# Reading R21b: for P = 4, 6 the nodal weights int N_p are negative at the
+# vertices, so the nodes cannot serve as the quadrature (lumped mass not
+# positive); these orders use the consistent stiffness S_ab = int dN/da dN/db
+# (exact, monomial integrals) and the HRZ-lumped mass, like P2's mass (R4).
 # --------------------------------------------------------------------------
 HP_DPS = 60
 
@@ -197,6 +201,35 @@ def tables_hp(P: int):
 
     Dr = [[dN(p, x, y, 0) for p in range(Np)] for (x, y) in nd]
     Ds = [[dN(p, x, y, 1) for p in range(Np)] for (x, y) in nd]
+
+    consistent = any(q <= 0 for q in w)  # P = 4, 6: reading R21b
+    if consistent:
+        # exact element matrices of the nodal basis: int N_p N_q (HRZ mass) and
+        # int dN_p/da dN_q/db (consistent stiffness), monomial by monomial
+        def mono(a, b):
+            return mp.mpf(factorial(a) * factorial(b)) / factorial(a + b + 2)
+
+        def grad_terms(p, d):  # derivative of N_p along d as (coef, a, b) terms
+            out = []
+            for m, (a, b) in enumerate(ex):
+                if d == 0 and a > 0:
+                    out.append((C[m, p] * a, a - 1, b))
+                if d == 1 and b > 0:
+                    out.append((C[m, p] * b, a, b - 1))
+            return out
+
+        def integ(t1, t2):
+            return mp.fsum(c1 * c2 * mono(a1 + a2, b1 + b2) for (c1, a1, b1) in t1 for (c2, a2, b2) in t2)
+
+        gr = [grad_terms(p, 0) for p in range(Np)]
+        gs = [grad_terms(p, 1) for p in range(Np)]
+        vals = [[(C[m, p], a, b) for m, (a, b) in enumerate(ex)] for p in range(Np)]
+        M2 = [integ(vals[p], vals[p]) for p in range(Np)]
+        tot = mp.fsum(M2)
+        wM = [q / (2 * tot) for q in M2]  # HRZ: the consistent diagonal rescaled to area 1/2
+        Srr = [[integ(gr[p], gr[q]) for q in range(Np)] for p in range(Np)]
+        Sss = [[integ(gs[p], gs[q]) for q in range(Np)] for p in range(Np)]
+        Srs = [[integ(gr[p], gs[q]) + integ(gs[p], gr[q]) for q in range(Np)] for p in range(Np)]
     def f(q):  # round once; |q| < 1e-40 is the 60-digit residue of an exact zero
         return 0.0 if abs(q) < mp.mpf("1e-40") else float(q)
 
@@ -205,12 +238,18 @@ def tables_hp(P: int):
         "Np": Np,
         "nodes": np.array([[f(x), f(y)] for (x, y) in nd], dtype=np.float64),
         "wK": np.array([f(q) for q in w], dtype=np.float64),
-        "wM": np.array([f(q) for q in w], dtype=np.float64),
+        "wM": np.array([f(q) for q in (wM if consistent else w)], dtype=np.float64),
         "Dr": np.array([[f(q) for q in row] for row in Dr], dtype=np.float64),
         "Ds": np.array([[f(q) for q in row] for row in Ds], dtype=np.float64),
         "C": C, "exps": ex,  # high-precision basis (pins only)
+        "consistent": consistent,
     }
-    for k in ("nodes", "wK", "wM", "Dr", "Ds"):
+    keys = ["nodes", "wK", "wM", "Dr", "Ds"]
+    if consistent:
+        for k, M in (("Srr", Srr), ("Sss", Sss), ("Srs", Srs)):
+            out[k] = np.array([[f(q) for q in row] for row in M], dtype=np.float64)
+            keys.append(k)
+    for k in keys:
         out[k].setflags(write=False)
     return out
 

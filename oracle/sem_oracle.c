@@ -437,6 +437,37 @@ void orc_apply_R(const int32_t *mu, int64_t ne, int Np, int64_t nn,
         for (int p = 0; p < Np; p++) R[mu[e * Np + p]] += ebuf[e * Np + p];
 }
 
+/* Reading R21b (P = 4, 6): R = -K U with the consistent element stiffness
+ * K^(e)_pq = int_e c_e^2 grad N_p . grad N_q, written out as its definition:
+ * with grad = J^-T grad^ (R5) and the reference integrals S_ab of the basis
+ * derivatives (oracle/refelem.py, exact), K^(e) = sum_ab G_ab S_ab where
+ * G_{jh jh'} = c^2 detJ sum_j K_{jh j} K_{jh' j}, K = J^-1 (Srs holds both
+ * mixed terms).  Serial scatter in element order, like orc_apply_R. */
+void orc_apply_R_tables(const int32_t *mu, int64_t ne, int Np, int64_t nn,
+                        const double *detJ, const double *Jinv, const double *c,
+                        const double *Srr, const double *Sss, const double *Srs,
+                        const double *U, double *R, double *ebuf) {
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < ne; e++) {
+        const double *Ki = Jinv + 4 * e;
+        double c2 = c[e] * c[e];
+        double grr = c2 * detJ[e] * (Ki[0] * Ki[0] + Ki[1] * Ki[1]);
+        double gss = c2 * detJ[e] * (Ki[2] * Ki[2] + Ki[3] * Ki[3]);
+        double grs = c2 * detJ[e] * (Ki[0] * Ki[2] + Ki[1] * Ki[3]);
+        for (int p = 0; p < Np; p++) {
+            double acc = 0.0;
+            for (int q = 0; q < Np; q++) {
+                double k = grr * Srr[p * Np + q] + gss * Sss[p * Np + q] + grs * Srs[p * Np + q];
+                acc += k * U[mu[e * Np + q]];
+            }
+            ebuf[e * Np + p] = -acc;
+        }
+    }
+    for (int64_t g = 0; g < nn; g++) R[g] = 0.0;
+    for (int64_t e = 0; e < ne; e++)
+        for (int p = 0; p < Np; p++) R[mu[e * Np + p]] += ebuf[e * Np + p];
+}
+
 /* Ricker wavelet (reading R7): r(t) = (1 - 2 pi^2 f0^2 tau^2) exp(-pi^2 f0^2 tau^2). */
 double orc_ricker(double t, double f0, double t0) {
     double tau = t - t0;
@@ -455,6 +486,7 @@ double orc_ricker(double t, double f0, double t0) {
 int orc_leapfrog(const int32_t *mu, int64_t ne, int Np, int64_t nn,
                  const double *detJ, const double *Jinv, const double *c,
                  const double *Dr, const double *Ds, const double *wK, const double *Mbar,
+                 const double *Srr, const double *Sss, const double *Srs, /* non-NULL: R21b */
                  int64_t src, double A, double f0, double t0, double dt,
                  int64_t step0, int64_t n_steps, double *U, double *Uprev) {
     double *R = (double *)malloc(sizeof(double) * nn);
@@ -462,7 +494,8 @@ int orc_leapfrog(const int32_t *mu, int64_t ne, int Np, int64_t nn,
     if (!R || !ebuf) { free(R); free(ebuf); return ORC_E_OOM; }
     for (int64_t s = 0; s < n_steps; s++) {
         int64_t n = step0 + s;
-        orc_apply_R(mu, ne, Np, nn, detJ, Jinv, c, Dr, Ds, wK, U, R, ebuf);
+        if (Srr) orc_apply_R_tables(mu, ne, Np, nn, detJ, Jinv, c, Srr, Sss, Srs, U, R, ebuf);
+        else orc_apply_R(mu, ne, Np, nn, detJ, Jinv, c, Dr, Ds, wK, U, R, ebuf);
         if (src >= 0) R[src] += A * orc_ricker((double)n * dt, f0, t0); /* Algorithm 3 */
 #pragma omp parallel for schedule(static)
         for (int64_t g = 0; g < nn; g++) {

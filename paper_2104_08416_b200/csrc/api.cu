@@ -30,8 +30,8 @@ int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 // selects the other compiled variants (design experiments).
 int chunk_elems(int P, bool heun) {
     const char *v = getenv("SEM_CHUNK");
-    if (P == 5) return 128;  // shared-memory budget of the stage at 21 nodes per element
-    if (P == 7) return 64;   // ... and at 36
+    if (P == 4 || P == 5) return 128;  // shared-memory budget of the stage at 15 / 21 nodes per element
+    if (P == 6 || P == 7) return 64;   // ... and at 28 / 36
     // Heun (integrator selected before sem_mesh_reorder): 128 runs 2 CTAs per SM
     const int b = v ? atoi(v) : (heun ? 128 : 256);
     return (b == 128 || b == 192 || b == 512) ? b : 256;
@@ -683,6 +683,8 @@ sem_status build_phase1(sem_ctx *ctx, const double *c_elem_host, int64_t src_ver
     if (ctx->integrator == SEM_INTEGRATOR_HEUN) {
         if (ctx->mesh_scatter != SEM_SCATTER_CHUNK)
             return fail(ctx, SEM_E_UNSUPPORTED, "the ablation scatters run the leapfrog only");
+        if (ctx->T.consistent)
+            return fail(ctx, SEM_E_UNSUPPORTED, "Heun needs the nodal quadrature (P = 2, 3, 5; reading R21b)");
         if (!heun_supported(ctx->Np, ctx->dch.B))
             return fail(ctx, SEM_E_UNSUPPORTED, "Heun kernels are built for chunks of 128 or 256 elements");
     }
@@ -894,8 +896,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
                             int32_t grid_wh_out[2]) {
     ST(check_usable(ctx));
     if (!degree_supported(degree))
-        return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) +
-                                                " (2, 3, 5 or 7; 4 and 6 have negative vertex weights, reading R21)");
+        return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) + " (2 to 7)");
     if (elem_order < 0 || elem_order > SEM_ORDER_DIST)
         return fail(ctx, SEM_E_UNSUPPORTED, "unknown element ordering " + std::to_string(elem_order));
     if (node_order < SEM_NODES_FIRST_TOUCH || node_order > SEM_NODES_VISIT)
@@ -1558,6 +1559,20 @@ sem_status sem_debug_ref_tables(int degree, int32_t *np_out, double *nodes_out, 
             if (Ds_out) Ds_out[p * Np + q] = T.Ds[p][q];
         }
     }
+    return SEM_OK;
+}
+
+sem_status sem_debug_ref_stiffness(int degree, double *Srr_out, double *Sss_out, double *Srs_out) {
+    if (!degree_supported(degree)) return SEM_E_UNSUPPORTED;
+    RefTables T;
+    if (!build_ref_tables(degree, T)) return SEM_E_UNSUPPORTED;
+    const int Np = T.Np;
+    for (int p = 0; p < Np; p++)
+        for (int q = 0; q < Np; q++) {
+            if (Srr_out) Srr_out[p * Np + q] = T.Srr[p][q];
+            if (Sss_out) Sss_out[p * Np + q] = T.Sss[p][q];
+            if (Srs_out) Srs_out[p * Np + q] = T.Srs[p][q];
+        }
     return SEM_OK;
 }
 

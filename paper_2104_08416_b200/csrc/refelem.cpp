@@ -42,7 +42,7 @@ long double ipow(long double x, int n) {
 // Lattice-order local nodes for any P (readings R3, R21): (i, j) is a vertex at
 // (0,0), (P,0), (0,P); on edge 0 (v0-v1) if j = 0, edge 1 (v0-v2) if i = 0,
 // edge 2 (v1-v2) if i + j = P; interior otherwise, numbered in lattice order.
-LocalNode kGen[2][kMaxNp];
+LocalNode kGen[4][kMaxNp];
 const LocalNode *lattice_nodes(int P, LocalNode *out) {
     int p = 0, m = 0;
     for (int j = 0; j <= P; j++)
@@ -145,11 +145,12 @@ bool build_tables_q(int P, RefTables &T) {
         return f;
     };
     static q128 w[kMaxNp], Dr[kMaxNp][kMaxNp], Ds[kMaxNp][kMaxNp];
+    bool consistent = false;  // reading R21b: some int N_p <= 0 (P = 4, 6)
     for (int pp = 0; pp < Np; pp++) {
         q128 s = 0;
         for (int m = 0; m < Np; m++) s += A[m][Np + pp] * mono_int_q(ea[m], eb[m]);
         w[pp] = s;
-        if (!(s > 0)) return false;  // P = 4, 6: negative vertex weights (R21)
+        if (!(s > 0)) consistent = true;
     }
     for (int k = 0; k < Np; k++)
         for (int pp = 0; pp < Np; pp++) {
@@ -162,13 +163,47 @@ bool build_tables_q(int P, RefTables &T) {
             Ds[k][pp] = ds;
         }
     auto rd = [](q128 x) { return qabs(x) < (q128)1e-24L ? 0.0 : (double)x; };  // residue of exact zeros
+    // R21b: HRZ mass (int N_p^2 rescaled to area 1/2) and the consistent stiffness
+    // int dN_a/dr dN_b/ds, monomial by monomial (exact)
+    static q128 wm[kMaxNp], cS[3][kMaxNp][kMaxNp];
+    if (consistent) {
+        q128 tot = 0;
+        for (int pp = 0; pp < Np; pp++) {
+            q128 m2 = 0;
+            for (int m = 0; m < Np; m++)
+                for (int n = 0; n < Np; n++)
+                    m2 += A[m][Np + pp] * A[n][Np + pp] * mono_int_q(ea[m] + ea[n], eb[m] + eb[n]);
+            wm[pp] = m2;
+            tot += m2;
+        }
+        for (int pp = 0; pp < Np; pp++) wm[pp] = wm[pp] / (2 * tot);
+        for (int a = 0; a < Np; a++)
+            for (int b = 0; b < Np; b++) {
+                q128 rr = 0, ss = 0, rs = 0, sr = 0;
+                for (int m = 0; m < Np; m++)
+                    for (int n = 0; n < Np; n++) {
+                        const q128 cc = A[m][Np + a] * A[n][Np + b];
+                        if (ea[m] > 0 && ea[n] > 0)
+                            rr += cc * ea[m] * ea[n] * mono_int_q(ea[m] + ea[n] - 2, eb[m] + eb[n]);
+                        if (eb[m] > 0 && eb[n] > 0)
+                            ss += cc * eb[m] * eb[n] * mono_int_q(ea[m] + ea[n], eb[m] + eb[n] - 2);
+                        if (ea[m] > 0 && eb[n] > 0)
+                            rs += cc * ea[m] * eb[n] * mono_int_q(ea[m] - 1 + ea[n], eb[m] + eb[n] - 1);
+                        if (eb[m] > 0 && ea[n] > 0)
+                            sr += cc * eb[m] * ea[n] * mono_int_q(ea[m] + ea[n] - 1, eb[m] - 1 + eb[n]);
+                    }
+                cS[0][a][b] = rr;
+                cS[1][a][b] = ss;
+                cS[2][a][b] = rs + sr;
+            }
+    }
     T.P = P;
     T.Np = Np;
     for (int pp = 0; pp < Np; pp++) {
         T.node[pp][0] = rd(nx[pp]);
         T.node[pp][1] = rd(ny[pp]);
         T.wK[pp] = rd(w[pp]);
-        T.wM[pp] = rd(w[pp]);
+        T.wM[pp] = rd(consistent ? wm[pp] : w[pp]);
         for (int k = 0; k < Np; k++) { T.Dr[k][pp] = rd(Dr[k][pp]); T.Ds[k][pp] = rd(Ds[k][pp]); }
     }
     std::memset(&T.Srr, 0, sizeof(T.Srr));
@@ -177,32 +212,38 @@ bool build_tables_q(int P, RefTables &T) {
     for (int a = 0; a < Np; a++)
         for (int b = 0; b < Np; b++) {
             q128 rr = 0, ss = 0, rs = 0;
-            for (int k = 0; k < Np; k++) {
-                rr += w[k] * Dr[k][a] * Dr[k][b];
-                ss += w[k] * Ds[k][a] * Ds[k][b];
-                rs += w[k] * (Dr[k][a] * Ds[k][b] + Ds[k][a] * Dr[k][b]);
+            if (consistent) {
+                rr = cS[0][a][b];
+                ss = cS[1][a][b];
+                rs = cS[2][a][b];
+            } else {  // nodal quadrature (the nodes are the quadrature points)
+                for (int k = 0; k < Np; k++) {
+                    rr += w[k] * Dr[k][a] * Dr[k][b];
+                    ss += w[k] * Ds[k][a] * Ds[k][b];
+                    rs += w[k] * (Dr[k][a] * Ds[k][b] + Ds[k][a] * Dr[k][b]);
+                }
             }
             T.Srr[a][b] = rd(rr);
             T.Sss[a][b] = rd(ss);
             T.Srs[a][b] = rd(rs);
         }
+    T.consistent = consistent;
     return true;
 }
 
 }  // namespace
 
-bool degree_supported(int P) { return P == 2 || P == 3 || P == 5 || P == 7; }
+bool degree_supported(int P) { return P >= 2 && P <= 7; }
 
 const LocalNode *local_nodes(int P) {
     if (P == 2) return kP2;
     if (P == 3) return kP3;
-    if (P == 5) return lattice_nodes(5, kGen[0]);
-    if (P == 7) return lattice_nodes(7, kGen[1]);
+    if (P >= 4 && P <= 7) return lattice_nodes(P, kGen[P - 4]);
     return nullptr;
 }
 
 bool build_ref_tables(int P, RefTables &T) {
-    if (P == 5 || P == 7) return build_tables_q(P, T);
+    if (P >= 4 && P <= 7) return build_tables_q(P, T);
     if (P != 2 && P != 3) return false;
     const int Np = (P + 1) * (P + 2) / 2;
     T.P = P;

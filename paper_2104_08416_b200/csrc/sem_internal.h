@@ -26,9 +26,10 @@ struct RefTables {
     // Element stiffness factors: K^e = Grr*Srr + Gss*Sss + Grs*Srs with
     // G = c^2 detJ J^-1 J^-T (Grs = off-diagonal entry).
     double Srr[kMaxNp][kMaxNp], Sss[kMaxNp][kMaxNp], Srs[kMaxNp][kMaxNp];
+    bool consistent = false;  // reading R21b (P = 4, 6): exact S, HRZ mass; no nodal quadrature
 };
 bool build_ref_tables(int P, RefTables &out);
-bool degree_supported(int P);  // P in {2, 3, 5, 7} (reading R21)
+bool degree_supported(int P);  // P in 2..7 (readings R21, R21b)
 
 // Local node kinds of the lattice order (R3): kind 0 = vertex (which = local
 // vertex), 1 = edge (which = local edge 0:v0v1 1:v0v2 2:v1v2, m = position from

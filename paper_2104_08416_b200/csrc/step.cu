@@ -540,7 +540,7 @@ int k7_group(int np) {
     static int g7 = -1, g5 = -1;
     if (g7 < 0) { const char *e = getenv("SEM_K7_G"); g7 = e ? atoi(e) : 4; if (g7 != 1 && g7 != 2 && g7 != 4) g7 = 4; }
     if (g5 < 0) { const char *e = getenv("SEM_K7_G5"); g5 = e ? atoi(e) : 1; if (g5 != 1 && g5 != 2) g5 = 1; }
-    return np == 36 ? g7 : np == 21 ? g5 : 1;
+    return (np == 36 || np == 28) ? g7 : np == 21 ? g5 : 1;
 }
 
 size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
@@ -554,7 +554,12 @@ size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
 template <int W2>
 K7Fn k7_fn_w(int np, int B) {
+    if (np == 15) return k7_step<15, 128, W2>;  // P4 (R21b): chunks of 128
     if (np == 21) return k7_group(21) == 2 ? k7_step<21, 128, W2, 2> : k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
+    if (np == 28) {                              // P6 (R21b): chunks of 64, G threads per element
+        const int g = k7_group(28);
+        return g == 4 ? k7_step<28, 64, W2, 4> : g == 2 ? k7_step<28, 64, W2, 2> : k7_step<28, 64, W2, 1>;
+    }
     if (np == 36) {                              // P7: chunks of 64, G threads per element
         const int g = k7_group(36);
         return g == 4 ? k7_step<36, 64, W2, 4> : g == 2 ? k7_step<36, 64, W2, 2> : k7_step<36, 64, W2, 1>;
@@ -605,8 +610,12 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer,
     cudaError_t e;
     if ((e = cudaMemsetAsync(dt2M, 0, sizeof(double) * (ch.N_tot + 2), s))) return e;
 #define MASS(NP_, B_) k_mass_chunk<NP_, B_><<<(unsigned)ch.nchunks, B_, 0, s>>>(ch, detJ, dt2, slot, dt2M)
-    if (ch.Np == 21) {
+    if (ch.Np == 15) {
+        MASS(15, 128);
+    } else if (ch.Np == 21) {
         MASS(21, 128);
+    } else if (ch.Np == 28) {
+        MASS(28, 64);
     } else if (ch.Np == 36) {
         MASS(36, 64);
     } else if (ch.Np == 6) {

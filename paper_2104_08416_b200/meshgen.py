@@ -29,7 +29,7 @@ import numpy as np
 # Reading R8: CFL factors for dt = kappa * min(inradius / c). Chosen so that
 # dt sits well below the element-Gershgorin-safe step on every config
 # (tests/test_inputs.py checks it against the oracle's bound).
-KAPPA = {2: 0.35, 3: 0.15, 5: 0.05, 7: 0.01}  # P5, P7 (reading R21): measured dt_crit / min(inradius/c) = 0.17 (P5), 0.024 (P7; smallest weight 1.4e-4)
+KAPPA = {2: 0.35, 3: 0.15, 4: 0.15, 5: 0.05, 6: 0.07, 7: 0.01}  # measured dt_crit / min(inradius/c): P4 0.40, P5 0.17, P6 0.19, P7 0.024 (R21, R21b)
 
 
 @dataclasses.dataclass

@@ -32,7 +32,7 @@ EXPORTED = ["sem_create", "sem_free", "sem_last_error", "sem_mesh_reorder", "sem
             "sem_get_info", "sem_set_kernel_timing", "sem_kernel_times", "sem_version",
             "sem_debug_chunk_stats", "sem_debug_partition", "sem_nccl_unique_id",
             "sem_group_build_operators", "sem_group_step_n", "sem_set_integrator", "sem_read_velocity",
-            "sem_write_velocity", "sem_set_scatter", "sem_debug_ref_tables"]
+            "sem_write_velocity", "sem_set_scatter", "sem_debug_ref_tables", "sem_debug_ref_stiffness"]
 
 
 class SemError(RuntimeError):
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
         L.sem_set_integrator.argtypes = [P, C.c_int]
         L.sem_set_scatter.argtypes = [P, C.c_int]
         L.sem_debug_ref_tables.argtypes = [C.c_int, P, P, P, P, P, P]
+        L.sem_debug_ref_stiffness.argtypes = [C.c_int, P, P, P]
         L.sem_read_velocity.argtypes = [P, P, C.POINTER(i64)]
         L.sem_write_velocity.argtypes = [P, P]
         L.sem_version.argtypes = []
@@ -283,6 +284,16 @@ def sem_debug_ref_tables(degree: int) -> dict:
                                 _ptr(out["Dr"]), _ptr(out["Ds"]))
     if rc != SEM_OK:
         raise SemError(rc, "sem_debug_ref_tables(%d)" % degree)
+    return out
+
+
+def sem_debug_ref_stiffness(degree: int) -> dict:
+    """Host-only: the library's Srr, Sss, Srs (see include/sem.h)."""
+    Np = sem_debug_ref_tables(degree)["Np"]
+    out = {k: np.empty((Np, Np)) for k in ("Srr", "Sss", "Srs")}
+    rc = load().sem_debug_ref_stiffness(degree, _ptr(out["Srr"]), _ptr(out["Sss"]), _ptr(out["Srs"]))
+    if rc != SEM_OK:
+        raise SemError(rc, "sem_debug_ref_stiffness(%d)" % degree)
     return out
 
 

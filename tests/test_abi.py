@@ -58,7 +58,7 @@ def test_no_gpu_fails_loudly(lib):
     assert e.value.status == sem.SEM_E_CUDA
 
 
-@pytest.mark.parametrize("P", [2, 3, 5, 7])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7])
 def test_library_reference_tables_equal_oracle(P):
     # host-only: the library derives its tables independently (80-bit / binary128
     # Gauss-Jordan in refelem.cpp); they round to the oracle's fp64 values
@@ -70,7 +70,25 @@ def test_library_reference_tables_equal_oracle(P):
         assert np.array_equal(g[k], o[k]), k
 
 
-@pytest.mark.parametrize("P", [1, 4, 6, 8])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7])
+def test_library_stiffness_tables_equal_oracle(P):
+    # P = 4, 6 (reading R21b): exact integrals, bitwise; nodal orders: D^T W D
+    # formed here from the oracle's own tables (rounding-level agreement)
+    from oracle import refelem
+    g = sem.sem_debug_ref_stiffness(P)
+    o = refelem.tables(P)
+    if o.get("consistent"):
+        for k in ("Srr", "Sss", "Srs"):
+            assert np.array_equal(g[k], o[k]), k
+    else:
+        W = np.diag(o["wK"])
+        ref = {"Srr": o["Dr"].T @ W @ o["Dr"], "Sss": o["Ds"].T @ W @ o["Ds"],
+               "Srs": o["Dr"].T @ W @ o["Ds"] + o["Ds"].T @ W @ o["Dr"]}
+        for k in ref:
+            assert np.abs(g[k] - ref[k]).max() <= 1e-13 * np.abs(ref[k]).max(), k
+
+
+@pytest.mark.parametrize("P", [1, 8])
 def test_library_rejects_unsupported_degrees(P):
     with pytest.raises(sem.SemError) as e:
         sem.sem_debug_ref_tables(P)

@@ -1,5 +1,5 @@
-"""GPU parity at the paper's benchmark orders 5 and 7 (NEXT-2; PAPER.md:572,
-:746-776; reading R21): reordering bit-exact, leapfrog field within rel L2
+"""GPU parity at the paper's benchmark orders 5-7 and order 4 (NEXT-2;
+PAPER.md:572, :746-776; readings R21, R21b): reordering bit-exact, leapfrog field within rel L2
 1e-10 of the oracle, random-state steps within 1e-12 (every element's G and mu
 row matters), on the Benchmark 1 recipe and the C2 recipe at reduced sizes."""
 import numpy as np
@@ -24,7 +24,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("P", [5, 7])
+@pytest.mark.parametrize("P", [4, 5, 6, 7])
 @pytest.mark.parametrize("elem_order,node_order", [(S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH),
                                                    (S.SEM_ORDER_CONN, S.SEM_NODES_VISIT),
                                                    (S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH_DEGREE)])
@@ -44,7 +44,7 @@ def test_reorder_bit_exact_high_order(ctx, P, elem_order, node_order):
     assert np.array_equal(r["node_perm"], npm)
 
 
-@pytest.mark.parametrize("P", [5, 7])
+@pytest.mark.parametrize("P", [4, 5, 6, 7])
 @pytest.mark.parametrize("name,scale,steps", [("B1", 25, 150), ("C2", 32, 120)])
 def test_leapfrog_parity_high_order(ctx, P, name, scale, steps):
     pb = mg.config(name, scale, degree=P) if name == "B1" else mg.config(name, scale)
@@ -61,7 +61,7 @@ def test_leapfrog_parity_high_order(ctx, P, name, scale, steps):
     assert rel(Ug, Uo) <= 1e-10, rel(Ug, Uo)
 
 
-@pytest.mark.parametrize("P", [5, 7])
+@pytest.mark.parametrize("P", [4, 5, 6, 7])
 @pytest.mark.parametrize("steps", [1, 10])
 def test_random_state_high_order(ctx, P, steps):
     pb = mg.config("B1", 30, degree=P)  # 33 x 16 cells: ragged last chunk at B = 128 and 64
@@ -82,7 +82,15 @@ def test_random_state_high_order(ctx, P, steps):
 
 def test_unsupported_orders(ctx):
     pb = mg.config("B1", 50, degree=5)
-    for P in (4, 6):
+    for P in (1, 8):
         with pytest.raises(S.SemError) as e:
             ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, P)
         assert e.value.status == S.SEM_E_UNSUPPORTED
+    # Heun needs the nodal quadrature: not at the R21b orders
+    for P in (4, 6):
+        ctx.sem_set_integrator(S.SEM_INTEGRATOR_HEUN)
+        ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, P)
+        with pytest.raises(S.SemError) as e:
+            ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        assert e.value.status == S.SEM_E_UNSUPPORTED
+    ctx.sem_set_integrator(S.SEM_INTEGRATOR_LEAPFROG)

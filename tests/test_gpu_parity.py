@@ -170,7 +170,7 @@ def test_errors(ctx):
     pb = mg.config("C1", 4)
     m = pb.mesh
     with pytest.raises(S.SemError) as e:
-        ctx.sem_mesh_reorder(m.vxy, m.tri, 4)
+        ctx.sem_mesh_reorder(m.vxy, m.tri, 8)
     assert e.value.status == S.SEM_E_UNSUPPORTED
     bad = m.vxy.copy()
     t = m.tri[5]

@@ -57,7 +57,7 @@ def test_layers():
     assert (pb.c[depth < 1000.0] == 1500.0).all() and (pb.c[depth >= 2500.0] == 3500.0).all()
 
 
-@pytest.mark.parametrize("P", [5, 7])
+@pytest.mark.parametrize("P", [4, 5, 6, 7])
 def test_b1_dt_below_half_cfl_high_order(P):
     # the Benchmark 1 stand-in at orders 5 and 7 (reading R21 CFL factors)
     pb = mg.config("B1", 50, degree=P)

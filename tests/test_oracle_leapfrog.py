@@ -38,7 +38,7 @@ def _lam_max(o, iters=300):
     return float(x @ o.apply_K(x) / (x @ (o.Mbar * x)))
 
 
-@pytest.mark.parametrize("P", [2, 3, 5, 7])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7])
 def test_energy_conservation_no_source(P):
     m = mg.shuffle(mg.grid_mesh(6, 5, 1.2, 1.0, alpha=0.2, seed=3), 4, 5)
     o = OracleSEM(m.vxy, m.tri, P, np.linspace(1.0, 2.0, m.ne))

@@ -197,3 +197,38 @@ def test_order_5_has_21_nodes_and_positive_weights_odd_orders_only():
         w = R.tables(P)["wK"]
         verts = [0, P, (P + 1) * (P + 2) // 2 - 1]
         assert (w[verts] < 0).all() and (np.delete(w, verts) > 0).all()
+
+
+@pytest.mark.parametrize("P", [4, 6])
+def test_consistent_tables_even_orders(P):
+    """Reading R21b: exact S tables against an independent quadrature (Gauss-
+    Legendre on the collapsed square, x = u (1 - v), y = v, Jacobian 1 - v,
+    exact for the degree-2P-2 integrands) and the HRZ mass."""
+    import mpmath as mp
+    T = R.tables_hp(P)
+    C, ex = T["C"], T["exps"]
+    Np = T["Np"]
+    n = P + 2
+    gx, gw = np.polynomial.legendre.leggauss(n)
+    u = 0.5 * (gx + 1.0)
+    wq = 0.5 * gw
+    X, Yq = np.meshgrid(u, u, indexing="ij")
+    W = np.outer(wq, wq) * (1.0 - Yq)
+    xx, yy = X * (1.0 - Yq), Yq
+    Cf = np.array([[float(C[m, p]) for p in range(Np)] for m in range(Np)])
+    dr = sum(Cf[m][:, None, None] * (a * xx ** max(a - 1, 0) * yy ** b if a else 0 * xx)
+             for m, (a, b) in enumerate(ex))
+    ds = sum(Cf[m][:, None, None] * (b * xx ** a * yy ** max(b - 1, 0) if b else 0 * xx)
+             for m, (a, b) in enumerate(ex))
+    val = sum(Cf[m][:, None, None] * xx ** a * yy ** b for m, (a, b) in enumerate(ex))
+    Srr = np.einsum("pij,qij,ij->pq", dr, dr, W)
+    Sss = np.einsum("pij,qij,ij->pq", ds, ds, W)
+    Srs = np.einsum("pij,qij,ij->pq", dr, ds, W)
+    Srs = Srs + Srs.T
+    for k, S in (("Srr", Srr), ("Sss", Sss), ("Srs", Srs)):
+        assert np.abs(T[k] - S).max() < 1e-9 * np.abs(S).max(), k
+        assert np.abs(T[k] - T[k].T).max() == 0.0 or np.abs(T[k] - T[k].T).max() < 1e-14 * np.abs(S).max()
+        assert np.abs(T[k].sum(axis=1)).max() < 1e-12 * np.abs(S).max()  # derivatives of sum N = 1 vanish
+    M2 = np.einsum("pij,pij,ij->p", val, val, W)
+    assert np.abs(T["wM"] - M2 * 0.5 / M2.sum()).max() < 1e-12
+    assert (T["wM"] > 0).all() and abs(T["wM"].sum() - 0.5) < 1e-15
