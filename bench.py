@@ -531,10 +531,25 @@ def cpu_baseline(pb, steps=2):
     t0 = time.perf_counter()
     o.leapfrog(pb.dt, steps, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
     dt = time.perf_counter() - t0
-    return {"value": m.ne * steps / dt, "unit": UNIT, "cores": core.num_threads(), "kind": "oracle",
+    cores = core.num_threads()
+    # also one thread on C1-C2 (C2 recipe, 2 steps)
+    from paper_2104_08416_b200 import meshgen as mg
+    c2 = mg.config("C2", 1)
+    o2 = OracleSEM(c2.mesh.vxy, c2.mesh.tri, c2.P, c2.c)
+    core.set_num_threads(1)
+    try:
+        o2.leapfrog(c2.dt, 1, src=c2.src_vertex, A=1.0, f0=c2.f0, t0=c2.t0)
+        t1 = time.perf_counter()
+        o2.leapfrog(c2.dt, 2, src=c2.src_vertex, A=1.0, f0=c2.f0, t0=c2.t0)
+        one = c2.mesh.ne * 2 / (time.perf_counter() - t1)
+    finally:
+        core.set_num_threads(cores)
+    return {"value": m.ne * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": "%d leapfrog steps of the full %s mesh (%d elements), oracle setup %.1f s excluded"
                       % (steps, pb.name, m.ne, setup),
-            "cpu": _cpu_model()}
+            "cpu": _cpu_model(),
+            "one_thread_C2": {"value": one, "unit": UNIT, "cores": 1,
+                              "sample": "2 leapfrog steps of the full C2 mesh (524288 elements, P3)"}}
 
 
 def _cpu_model():

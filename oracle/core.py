@@ -79,6 +79,8 @@ def lib():
             L.orc_strategy_order.restype = C.c_int
             L.orc_node_coords.argtypes = [P, P, P, i64, C.c_int, P, P]
             L.orc_node_coords.restype = None
+            L.orc_set_num_threads.argtypes = [C.c_int]
+            L.orc_set_num_threads.restype = None
             L.orc_num_threads.argtypes = []
             L.orc_num_threads.restype = C.c_int
             _lib = L
@@ -343,3 +345,7 @@ class OracleSEM:
 
 def num_threads() -> int:
     return lib().orc_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(int(n))

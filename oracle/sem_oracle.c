@@ -833,6 +833,15 @@ void orc_node_coords(const double *vxy, const int32_t *tri, const int32_t *mu, i
     }
 }
 
+/* Thread count of the oracle's OpenMP loops (bench: the 1-thread baseline). */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
