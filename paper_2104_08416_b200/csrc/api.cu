@@ -480,6 +480,9 @@ StepParams step_params(sem_ctx *ctx) {
     p.Uprev = ctx->d_U[1 - ctx->cur];
     p.n = ctx->step;
     p.n_dev = nullptr;
+    // fitted CSR load width in K7's node phase (default; SEM_K7_CSR=fixed: always 8 wide)
+    static const int fit = [] { const char *e = getenv("SEM_K7_CSR"); return (e && std::string(e) == "fixed") ? 0 : 1; }();
+    p.csr_fit = fit;
     return p;
 }
 

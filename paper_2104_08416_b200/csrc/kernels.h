@@ -139,6 +139,7 @@ struct StepParams {
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
     const int64_t *n_dev;  // if set: the step index lives in device memory (CUDA-graph step loop)
+    int csr_fit;           // node-phase sums with the load width fitted per warp (default; SEM_K7_CSR=fixed)
 };
 int k7_grid(const DevChunks &ch, bool fused);
 // device step counter of the graph-captured step loop: += 1, = v

@@ -141,6 +141,31 @@ __global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ slot, 
 // order (ascending e = p*B + t: a fixed order).  Up to kD entries are loaded
 // together (predicated); absent ones contribute an exact +0.  Local nodes are
 // sorted by degree, so a warp's lanes take the same path.
+template <int N>
+__device__ __forceinline__ double run_sum(const double *ebuf, int j0, int j1) {
+    double part[N];
+#pragma unroll
+    for (int d = 0; d < N; d++) part[d] = (j0 + d < j1) ? ebuf[j0 + d] : 0.0;
+    double y = part[0];
+#pragma unroll
+    for (int d = 1; d < N; d++) y += part[d];
+    return y;
+}
+
+// Same sum with the load width fitted to the warp's longest run (nodes are
+// sorted by entry count inside a chunk, so a warp's runs have similar lengths:
+// at P3 most nodes have 1 or 2 entries).  Only the sign of an exact zero can
+// differ from csr_sum.
+__device__ __forceinline__ double csr_sum_fit(const double *ebuf, const uint16_t *lp, int i) {
+    const int j0 = lp[i], j1 = lp[i + 1];
+    const int mx = __reduce_max_sync(__activemask(), j1 - j0);
+    if (mx <= 2) return run_sum<2>(ebuf, j0, j1);
+    if (mx <= 4) return run_sum<4>(ebuf, j0, j1);
+    double y = run_sum<kD>(ebuf, j0, j1);
+    for (int j = j0 + kD; j < j1; j++) y += ebuf[j];
+    return y;
+}
+
 __device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *lp, int i) {
     const int j0 = lp[i], j1 = lp[i + 1];
     double part[kD];
@@ -377,7 +402,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 upg = a.Uprev[i0 + i];
                 mg = __ldg(a.dt2M + i0 + i);
             }
-            const double yi = csr_sum(ebuf, lp, i);
+            const double yi = a.csr_fit ? csr_sum_fit(ebuf, lp, i) : csr_sum(ebuf, lp, i);
             if (i < nint) {
                 const int id = i0 + i;
                 const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
