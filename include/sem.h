@@ -7,8 +7,13 @@
  * Call order (the paper's problem statement, PAPER.md:540 mesh -> SEM nodes,
  * :296-321 reorder, :240-263 operators, :269 explicit stepping):
  *
- *   sem_create -> sem_mesh_reorder -> sem_build_operators -> sem_step_n* ->
- *   sem_read_field -> sem_free
+ *   sem_create -> [sem_set_integrator] [sem_set_scatter] -> sem_mesh_reorder ->
+ *   sem_build_operators -> sem_step_n* -> sem_read_field [sem_read_velocity] ->
+ *   sem_free
+ *
+ * Beyond the north_star leapfrog the library also runs the paper's own Heun
+ * integrator on (U, V), its other reordering strategies
+ * (PAPER.md:548-558), orders 2-7 and the scatter ablations; see DESIGN.md.
  *
  * Conventions (all entry points):
  *  - Pointers named *_host are HOST memory, borrowed for the duration of the
