@@ -319,11 +319,12 @@ sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches,
  * Host-only diagnostic (no GPU, no context): run the chunk builder of the step
  * kernel on a reordered connectivity mu [E][Np] (node ids in [0, N), elements in
  * their final order) with chunks of B elements.  stats_out[16] receives
- * {nchunks, N_int (padded), N_sh, n_slots, max_local, max_win, max_lptr,
- *  max_colors, sum_nint, sum_nsh, max_nsh, 0, 0, 0, 0, 0};
+ * {nchunks, N_int (padded), N_sh, n_slots, max_local, max_win, max_count (most
+ *  entries of one node in a chunk), max_colors, sum_nint, sum_nsh, max_nsh, 0, 0, 0, 0, 0};
  * int_of_out [N] (optional) the internal id of every node; cmeta_out
  * [nchunks*8] (optional) the per-chunk descriptors {i0, nint, s0, nsh, ncol,
- * ne, nint_al, lp0}.  Errors: SEM_E_ARG, SEM_E_MESH (unused node), SEM_E_OOM.
+ * ne, nint_al, end1} (end0/end1: ends of the interior / shared jagged-diagonal
+ * segments).  Errors: SEM_E_ARG, SEM_E_MESH (unused node), SEM_E_OOM.
  */
 sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
                                  int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out);

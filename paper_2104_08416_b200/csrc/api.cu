@@ -318,16 +318,16 @@ sem_status prepare_ablation(sem_ctx *ctx, const std::vector<int32_t> &mu_h, int6
 cudaError_t upload_chunks(std::vector<void *> &L, const ChunkMeta &m, DevChunks &d, cudaStream_t s) {
     d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
     d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
-    d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
+    d.max_local = m.max_local; d.max_win = m.max_win; d.max_count = m.max_count; d.max_nsh = m.max_nsh;
     int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
-    uint16_t *p_lpos, *p_lptr, *p_lidx, *p_shcr;
+    uint16_t *p_lpos, *p_jds, *p_lidx, *p_shcr;
     cudaError_t e;
     if ((e = upload(L, &p_cmeta, m.cmeta, s)) || (e = upload(L, &p_lidx, m.lidx, s)) ||
-        (e = upload(L, &p_lpos, m.lpos, s)) || (e = upload(L, &p_lptr, m.lptr, s)) ||
+        (e = upload(L, &p_lpos, m.lpos, s)) || (e = upload(L, &p_jds, m.jds, s)) ||
         (e = upload(L, &p_pstart, m.sh_pstart, s)) || (e = upload(L, &p_shn, m.shl_node, s)) ||
         (e = upload(L, &p_shs, m.shl_slot, s)) || (e = upload(L, &p_shcr, m.shl_cr, s)))
         return e;
-    d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.lptr = p_lptr; d.sh_pstart = p_pstart;
+    d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.jds = p_jds; d.sh_pstart = p_pstart;
     d.shl_node = p_shn; d.shl_slot = p_shs; d.shl_cr = p_shcr;
     return cudaSuccess;
 }
@@ -346,13 +346,13 @@ std::string compare_chunks(const ChunkMeta &h, const ChunkMeta &m, const DevChun
                            cudaStream_t s) {
     if (h.nchunks != m.nchunks || h.N_int != m.N_int || h.N_sh != m.N_sh || h.N_if != m.N_if ||
         h.n_slots != m.n_slots || h.max_local != m.max_local || h.max_win != m.max_win ||
-        h.max_lptr != m.max_lptr || h.max_nsh != m.max_nsh)
+        h.max_count != m.max_count || h.max_nsh != m.max_nsh)
         return "scalars";
     if (h.bnd_chunks != m.bnd_chunks || h.int_chunks != m.int_chunks) return "chunk lists";
     if (!same_dev(h.cmeta, d.cmeta, h.cmeta.size(), s)) return "cmeta";
     if (!same_dev(h.lidx, d.lidx, h.lidx.size(), s)) return "lidx";
     if (!same_dev(h.lpos, d.lpos, h.lpos.size(), s)) return "lpos";
-    if (!same_dev(h.lptr, d.lptr, h.lptr.size(), s)) return "lptr";
+    if (!same_dev(h.jds, d.jds, h.jds.size(), s)) return "jds";
     if (!same_dev(h.sh_pstart, d.sh_pstart, h.sh_pstart.size(), s)) return "sh_pstart";
     if (!same_dev(h.shl_node, d.shl_node, h.shl_node.size(), s)) return "shl_node";
     if (!same_dev(h.shl_slot, d.shl_slot, h.shl_slot.size(), s)) return "shl_slot";
@@ -480,9 +480,6 @@ StepParams step_params(sem_ctx *ctx) {
     p.Uprev = ctx->d_U[1 - ctx->cur];
     p.n = ctx->step;
     p.n_dev = nullptr;
-    // fitted CSR load width in K7's node phase (default; SEM_K7_CSR=fixed: always 8 wide)
-    static const int fit = [] { const char *e = getenv("SEM_K7_CSR"); return (e && std::string(e) == "fixed") ? 0 : 1; }();
-    p.csr_fit = fit;
     return p;
 }
 
@@ -1536,7 +1533,7 @@ sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N
             if (m.cmeta[8 * c + 3] > max_nsh) max_nsh = m.cmeta[8 * c + 3];
         }
         const int64_t st[16] = {m.nchunks, m.N_int, m.N_sh, m.n_slots, m.max_local, m.max_win,
-                                m.max_lptr, m.max_colors, sum_nint, sum_nsh, max_nsh, 0, 0, 0, 0, 0};
+                                m.max_count, m.max_colors, sum_nint, sum_nsh, max_nsh, 0, 0, 0, 0, 0};
         std::memcpy(stats_out, st, sizeof(st));
         if (int_of_out) std::memcpy(int_of_out, m.int_of.data(), sizeof(int32_t) * N);
         if (cmeta_out) std::memcpy(cmeta_out, m.cmeta.data(), sizeof(int32_t) * m.cmeta.size());

@@ -231,7 +231,6 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     m.lidx.assign((size_t)nch * Np * B, 0);
     m.lpos.assign((size_t)nch * Np * B, 0);
     m.cmeta.assign((size_t)nch * 8, 0);
-    m.lp0.assign(nch + 1, 0);
     std::vector<int32_t> nlocal(nch, 0);
     int max_local = 0, max_win = 0;
 #pragma omp parallel for schedule(dynamic, 64) reduction(max : max_local, max_win)
@@ -271,36 +270,57 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
         cm[6] = ni_al;
     }
     tr.mark("local indices");
-    // CSR blocks: chunk c owns lptr[lp0[c] .. lp0[c] + nlocal+1) (start aligned
-    // to 8 entries = 16 bytes for TMA) and lpos[c*Np*B .. (c+1)*Np*B).
-    for (int64_t c = 0; c < nch; c++) m.lp0[c + 1] = (int32_t)((m.lp0[c] + nlocal[c] + 1 + 7) & ~7);
-    m.lptr.assign((size_t)m.lp0[nch] + 8, 0);
-    int max_lp = 0;
-#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_lp)
+    // Jagged diagonals (JDS) of the per-chunk node sums.  The local nodes of a
+    // segment (interior [0, nint), shared [ni_al, ni_al + ns)) are sorted by
+    // entry count, descending; diagonal d holds the d-th entry of every node
+    // with more than d entries, nodes in local order.  jds[c][32 s + d] = start
+    // of diagonal d of segment s in the chunk's entry buffer (absolute);
+    // cmeta[4] / cmeta[7] = end of segment 0 / 1.  lpos[e] = jds[...][rank] +
+    // node index in its segment, rank = position of entry e = p*B + t among
+    // its node's entries in ascending e.  A node's sum runs over d in order:
+    // the same order as a CSR run, and a warp's lanes read consecutive words.
+    m.jds.assign((size_t)nch * kJdsW * 2, 0);
+    int max_cnt = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_cnt)
     for (int64_t c = 0; c < nch; c++) {
         const int nl = nlocal[c];
         const int ne = (int)(std::min<int64_t>(E, (c + 1) * B) - c * B);
-        std::vector<int> cnt(nl + 1, 0);
+        int32_t *cm = &m.cmeta[(size_t)c * 8];
+        const int ni = cm[1], ni_al = cm[6];
+        std::vector<int> cnt(nl, 0), rank(nl, 0);
         const uint16_t *li = &m.lidx[(size_t)c * Np * B];
         for (int p = 0; p < Np; p++)
-            for (int t = 0; t < ne; t++) cnt[li[p * B + t] + 1]++;
-        for (int i = 0; i < nl; i++) cnt[i + 1] += cnt[i];
-        uint16_t *lp = &m.lptr[m.lp0[c]];
-        for (int i = 0; i <= nl; i++) lp[i] = (uint16_t)cnt[i];
-        // entries visited in ascending e = p*B + t order -> each node's run is
-        // ascending; lpos[e] = CSR position of entry e (where y_e[p] goes)
+            for (int t = 0; t < ne; t++) cnt[li[p * B + t]]++;
+        uint16_t *jd = &m.jds[(size_t)c * kJdsW * 2];
+        int base = 0;
+        for (int sg = 0; sg < 2; sg++) {
+            const int a = sg == 0 ? 0 : ni_al, b = sg == 0 ? ni : nl;
+            int nd[kJdsW + 1] = {0};
+            for (int i = a; i < b; i++) {
+                if (cnt[i] > max_cnt) max_cnt = cnt[i];
+                for (int d = 0; d < cnt[i] && d < kJdsW; d++) nd[d]++;
+            }
+            for (int d = 0; d < kJdsW; d++) { jd[sg * kJdsW + d] = (uint16_t)base; base += nd[d]; }
+            cm[sg == 0 ? 4 : 7] = base;
+        }
         uint16_t *lpo = &m.lpos[(size_t)c * Np * B];
         for (int p = 0; p < Np; p++)
-            for (int t = 0; t < ne; t++) lpo[p * B + t] = (uint16_t)(cnt[li[p * B + t]]++);
-        m.cmeta[(size_t)c * 8 + 7] = m.lp0[c];
-        const int w = (nl + 1 + 7) & ~7;
-        if (w > max_lp) max_lp = w;
+            for (int t = 0; t < ne; t++) {
+                const int i = li[p * B + t];
+                const int sg = i < ni_al ? 0 : 1;
+                const int r = rank[i]++;
+                if (r < kJdsW) lpo[p * B + t] = (uint16_t)(jd[sg * kJdsW + r] + (sg == 0 ? i : i - ni_al));
+            }
+    }
+    if (max_cnt > kJdsW) {
+        err = "build_chunks: a node has more than 32 entries in one chunk";
+        return false;
     }
     m.max_local = max_local;
     m.max_win = max_win;
-    m.max_lptr = max_lp;
+    m.max_count = max_cnt;
     m.max_colors = 0;
-    tr.mark("CSR");
+    tr.mark("JDS");
     return true;
 }
 

@@ -5,12 +5,13 @@
 // one chunk are interior (contiguous window per chunk, descending entry count
 // then ascending id), the others shared (non-interface ascending id, then
 // interface ascending id) with one node-major slot per touching chunk in
-// ascending chunk order; per-chunk local indices, CSR row pointers and CSR
-// positions.  Built from three radix sorts:
+// ascending chunk order; per-chunk local indices, jagged-diagonal starts and
+// entry positions.  Built from three radix sorts:
 //   1. entries (chunk, node) in [chunk][p][t] order -> (chunk, node) runs,
 //      entries of a run ascending in p*B + t (stable sort);
 //   2. runs by (chunk, shared?, 255 - count, id or shared index) -> the local
-//      order of every chunk (interior first, then shared);
+//      order of every chunk (interior first, then shared) and its jagged
+//      diagonals;
 //   3. runs by (node, chunk) -> the rank of a chunk among a shared node's chunks
 //      (its slot).
 // Everything else is scans and scatters.  Replaces ~0.8 s of host work and
@@ -156,7 +157,7 @@ __global__ void k_local_keys(const int32_t *__restrict__ rc, const int32_t *__re
 }
 
 __global__ void k_chunk_sizes(const int32_t *__restrict__ nint, const int32_t *__restrict__ nsh, int64_t nch,
-                              int32_t *tot, int32_t *ni_al, int32_t *nsh8, int32_t *lpw) {
+                              int32_t *tot, int32_t *ni_al, int32_t *nsh8) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nch) return;
     const int32_t ni = nint[c], ns = nsh[c];
@@ -164,7 +165,6 @@ __global__ void k_chunk_sizes(const int32_t *__restrict__ nint, const int32_t *_
     tot[c] = ni + ns;
     ni_al[c] = al;
     nsh8[c] = (ns + 7) & ~7;
-    lpw[c] = (al + ns + 1 + 7) & ~7;
 }
 
 // local index of every run; int_of of every node
@@ -223,50 +223,52 @@ __global__ void k_slots(const uint64_t *__restrict__ key3, const int32_t *__rest
     shl_cr[k] = (uint16_t)((n << 8) | rank);
 }
 
-// CSR counts at lp0[c] + local + 1, later turned into per-chunk row pointers
-__global__ void k_csr_counts(const int32_t *__restrict__ rc, const int32_t *__restrict__ rlen,
-                             const int32_t *__restrict__ local, const int32_t *__restrict__ lp0, int64_t nruns,
-                             int32_t *cnt) {
+// Jagged diagonals (chunks.cpp): nodes of a segment with more than d entries
+// per diagonal d (order-free integer counts), then the diagonal starts.
+__global__ void k_jds_counts(const int32_t *__restrict__ rc, const int32_t *__restrict__ rlen,
+                             const int32_t *__restrict__ local, const int32_t *__restrict__ nint, int64_t nruns,
+                             int32_t *nd, int32_t *mx) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r < nruns) cnt[lp0[rc[r]] + local[r] + 1] = rlen[r];
+    if (r >= nruns) return;
+    const int32_t c = rc[r], len = rlen[r];
+    const int sg = local[r] < nint[c] ? 0 : 1;
+    atomicMax(&mx[2], len);  // max_count
+    for (int d = 0; d < len && d < kJdsW; d++) atomicAdd(&nd[((int64_t)c * 2 + sg) * kJdsW + d], 1);
 }
 
-__global__ void k_nlocal(const int32_t *__restrict__ ni_al, const int32_t *__restrict__ nsh, int64_t nch,
-                         int32_t *nloc) {
+__global__ void k_jds_starts(const int32_t *__restrict__ nd, int64_t nch, uint16_t *jds, int32_t *end0,
+                             int32_t *end1) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < nch) nloc[c] = ni_al[c] + nsh[c];
-}
-
-__global__ void k_csr_ptr(const int32_t *__restrict__ glob, const int32_t *__restrict__ lp0,
-                          const int32_t *__restrict__ nloc, int64_t nch, int64_t total, uint16_t *lptr) {
-    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (x >= total) return;
-    int64_t lo = 0, hi = nch;  // chunk c with lp0[c] <= x < lp0[c+1]
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) / 2;
-        if (lp0[mid] <= x) lo = mid;
-        else hi = mid;
+    if (c >= nch) return;
+    int base = 0;
+    for (int sg = 0; sg < 2; sg++) {
+        for (int d = 0; d < kJdsW; d++) {
+            jds[(c * 2 + sg) * kJdsW + d] = (uint16_t)base;
+            base += nd[(c * 2 + sg) * kJdsW + d];
+        }
+        (sg == 0 ? end0 : end1)[c] = base;
     }
-    const int32_t base = lp0[lo];
-    lptr[x] = (x - base <= nloc[lo]) ? (uint16_t)(glob[x] - glob[base]) : (uint16_t)0;
 }
 
 __global__ void k_entry_local(const int32_t *__restrict__ flag_rid, const int32_t *__restrict__ v1,
                               const int32_t *__restrict__ rstart, const int32_t *__restrict__ rc,
-                              const int32_t *__restrict__ local, const int32_t *__restrict__ lp0,
-                              const uint16_t *__restrict__ lptr, int64_t n, uint16_t *lidx, uint16_t *lpos) {
+                              const int32_t *__restrict__ local, const int32_t *__restrict__ nint,
+                              const int32_t *__restrict__ ni_al, const uint16_t *__restrict__ jds, int64_t n,
+                              uint16_t *lidx, uint16_t *lpos) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t r = flag_rid[i] - 1, k = v1[i];
-    const int32_t l = local[r];
+    const int32_t l = local[r], c = rc[r], rank = (int32_t)(i - rstart[r]);
     lidx[k] = (uint16_t)l;
-    lpos[k] = (uint16_t)(lptr[lp0[rc[r]] + l] + (i - rstart[r]));
+    if (rank >= kJdsW) return;  // reported through max_count
+    const int sg = l < nint[c] ? 0 : 1;
+    lpos[k] = (uint16_t)(jds[((int64_t)c * 2 + sg) * kJdsW + rank] + (sg == 0 ? l : l - ni_al[c]));
 }
 
 __global__ void k_cmeta(const int32_t *__restrict__ i0, const int32_t *__restrict__ nint,
                         const int32_t *__restrict__ s0, const int32_t *__restrict__ nsh,
-                        const int32_t *__restrict__ ni_al, const int32_t *__restrict__ lp0, int64_t nch, int64_t E,
-                        int B, int32_t *cmeta, int32_t *mx) {
+                        const int32_t *__restrict__ ni_al, const int32_t *__restrict__ end0,
+                        const int32_t *__restrict__ end1, int64_t nch, int64_t E, int B, int32_t *cmeta, int32_t *mx) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nch) return;
     int32_t *cm = cmeta + 8 * c;
@@ -275,14 +277,13 @@ __global__ void k_cmeta(const int32_t *__restrict__ i0, const int32_t *__restric
     cm[1] = nint[c];
     cm[2] = s0[c];
     cm[3] = nsh[c];
-    cm[4] = 0;
+    cm[4] = end0[c];
     cm[5] = (int32_t)(e1 - c * B);
     cm[6] = ni_al[c];
-    cm[7] = lp0[c];
+    cm[7] = end1[c];
     const int32_t ns = nsh[c];
     atomicMax(&mx[0], ni_al[c] + ((ns + 1) & ~1));    // max_local
     atomicMax(&mx[1], ni_al[c]);                      // max_win
-    atomicMax(&mx[2], (ni_al[c] + ns + 1 + 7) & ~7);  // max_lptr
     atomicMax(&mx[3], (ns + 7) & ~7);                 // max_nsh
 }
 
@@ -388,19 +389,17 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
                                           nruns, bn, k2.as<uint64_t>(), v2.as<int32_t>(), nint.as<int32_t>(),
                                           nsh.as<int32_t>());
     RET(sort_u64(k2.as<uint64_t>(), v2.as<int32_t>(), k2s.as<uint64_t>(), order.as<int32_t>(), nruns, bc + 9 + bn, s));
-    Tmp tot(s), ni_al(s), nsh8(s), lpw(s), cs(s), i0(s), s0(s), lp0(s);
-    for (Tmp *t : {&tot, &ni_al, &nsh8, &lpw, &cs, &i0, &s0, &lp0}) RET(t->alloc(4 * (nch + 1)));
-    for (Tmp *t : {&tot, &ni_al, &nsh8, &lpw}) RET(cudaMemsetAsync(t->p, 0, 4 * (nch + 1), s));
+    Tmp tot(s), ni_al(s), nsh8(s), cs(s), i0(s), s0(s);
+    for (Tmp *t : {&tot, &ni_al, &nsh8, &cs, &i0, &s0}) RET(t->alloc(4 * (nch + 1)));
+    for (Tmp *t : {&tot, &ni_al, &nsh8}) RET(cudaMemsetAsync(t->p, 0, 4 * (nch + 1), s));
     k_chunk_sizes<<<nb(nch), kT, 0, s>>>(nint.as<int32_t>(), nsh.as<int32_t>(), nch, tot.as<int32_t>(),
-                                         ni_al.as<int32_t>(), nsh8.as<int32_t>(), lpw.as<int32_t>());
+                                         ni_al.as<int32_t>(), nsh8.as<int32_t>());
     RET(excl_scan(tot.as<int32_t>(), cs.as<int32_t>(), nch + 1, s));
     RET(excl_scan(ni_al.as<int32_t>(), i0.as<int32_t>(), nch + 1, s));
     RET(excl_scan(nsh8.as<int32_t>(), s0.as<int32_t>(), nch + 1, s));
-    RET(excl_scan(lpw.as<int32_t>(), lp0.as<int32_t>(), nch + 1, s));
-    int32_t hN_int = 0, hs0 = 0, hlp = 0;
+    int32_t hN_int = 0, hs0 = 0;
     RET(cudaMemcpyAsync(&hN_int, i0.as<int32_t>() + nch, 4, cudaMemcpyDeviceToHost, s));
     RET(cudaMemcpyAsync(&hs0, s0.as<int32_t>() + nch, 4, cudaMemcpyDeviceToHost, s));
-    RET(cudaMemcpyAsync(&hlp, lp0.as<int32_t>() + nch, 4, cudaMemcpyDeviceToHost, s));
     RET(cudaStreamSynchronize(s));
     m.N_int = hN_int;
     m.N_tot = m.N_int + m.N_sh;
@@ -449,35 +448,30 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     }
 
     // ---- local indices, CSR row pointers and positions ----
-    uint16_t *lidx = nullptr, *lpos = nullptr, *lptr = nullptr;
+    uint16_t *lidx = nullptr, *lpos = nullptr, *jds = nullptr;
     int32_t *cmeta = nullptr;
     RET(dalloc((void **)&lidx, 2 * (size_t)n_ent));
     RET(dalloc((void **)&lpos, 2 * (size_t)n_ent));
-    RET(dalloc((void **)&lptr, 2 * (size_t)(hlp + 8)));
+    RET(dalloc((void **)&jds, 2 * (size_t)(nch * 2 * kJdsW)));
     RET(dalloc((void **)&cmeta, 4 * 8 * (size_t)nch));
     RET(cudaMemsetAsync(lidx, 0, 2 * (size_t)n_ent, s));
     RET(cudaMemsetAsync(lpos, 0, 2 * (size_t)n_ent, s));
-    RET(cudaMemsetAsync(lptr, 0, 2 * (size_t)(hlp + 8), s));
-    {
-        // the block of chunk c holds nlocal + 1 = ni_al + nsh + 1 row pointers
-        Tmp cnt(s), glob(s), nloc(s);
-        RET(cnt.alloc(4 * (size_t)(hlp + 1)));
-        RET(glob.alloc(4 * (size_t)(hlp + 1)));
-        RET(nloc.alloc(4 * (nch + 1)));
-        RET(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)(hlp + 1), s));
-        k_csr_counts<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rlen.as<int32_t>(), local.as<int32_t>(),
-                                              lp0.as<int32_t>(), nruns, cnt.as<int32_t>());
-        RET(incl_scan(cnt.as<int32_t>(), glob.as<int32_t>(), hlp, s));
-        k_nlocal<<<nb(nch), kT, 0, s>>>(ni_al.as<int32_t>(), nsh.as<int32_t>(), nch, nloc.as<int32_t>());
-        k_csr_ptr<<<nb(hlp), kT, 0, s>>>(glob.as<int32_t>(), lp0.as<int32_t>(), nloc.as<int32_t>(), nch, hlp, lptr);
-    }
-    k_entry_local<<<nb(n), kT, 0, s>>>(rid.as<int32_t>(), v1s.as<int32_t>(), rstart.as<int32_t>(), rc.as<int32_t>(),
-                                       local.as<int32_t>(), lp0.as<int32_t>(), lptr, n, lidx, lpos);
-    Tmp mx(s);
+    Tmp mx(s), nd(s), end0(s), end1(s);
     RET(mx.alloc(16));
     RET(cudaMemsetAsync(mx.p, 0, 16, s));
+    RET(nd.alloc(4 * (size_t)(nch * 2 * kJdsW)));
+    RET(end0.alloc(4 * (nch + 1)));
+    RET(end1.alloc(4 * (nch + 1)));
+    RET(cudaMemsetAsync(nd.p, 0, 4 * (size_t)(nch * 2 * kJdsW), s));
+    k_jds_counts<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rlen.as<int32_t>(), local.as<int32_t>(), nint.as<int32_t>(),
+                                          nruns, nd.as<int32_t>(), mx.as<int32_t>());
+    k_jds_starts<<<nb(nch), kT, 0, s>>>(nd.as<int32_t>(), nch, jds, end0.as<int32_t>(), end1.as<int32_t>());
+    k_entry_local<<<nb(n), kT, 0, s>>>(rid.as<int32_t>(), v1s.as<int32_t>(), rstart.as<int32_t>(), rc.as<int32_t>(),
+                                       local.as<int32_t>(), nint.as<int32_t>(), ni_al.as<int32_t>(), jds, n, lidx,
+                                       lpos);
     k_cmeta<<<nb(nch), kT, 0, s>>>(i0.as<int32_t>(), nint.as<int32_t>(), s0.as<int32_t>(), nsh.as<int32_t>(),
-                                   ni_al.as<int32_t>(), lp0.as<int32_t>(), nch, E, B, cmeta, mx.as<int32_t>());
+                                   ni_al.as<int32_t>(), end0.as<int32_t>(), end1.as<int32_t>(), nch, E, B, cmeta,
+                                   mx.as<int32_t>());
     int32_t hmx[4];
     RET(cudaMemcpyAsync(hmx, mx.p, 16, cudaMemcpyDeviceToHost, s));
 
@@ -495,7 +489,11 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     RET(cudaStreamSynchronize(s));
     m.max_local = hmx[0];
     m.max_win = hmx[1];
-    m.max_lptr = hmx[2];
+    m.max_count = hmx[2];
+    if (m.max_count > kJdsW) {
+        err = "build_chunks: a node has more than 32 entries in one chunk";
+        return cudaSuccess;
+    }
     m.max_nsh = hmx[3];
     m.max_colors = 0;
     for (int64_t c = 0; c < nch; c++)
@@ -511,8 +509,8 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
 
     d.B = B; d.Np = Np; d.E = E; d.N = N; d.nchunks = nch;
     d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
-    d.max_local = m.max_local; d.max_win = m.max_win; d.max_lptr = m.max_lptr; d.max_nsh = m.max_nsh;
-    d.cmeta = cmeta; d.lidx = lidx; d.lpos = lpos; d.lptr = lptr; d.sh_pstart = sh_pstart;
+    d.max_local = m.max_local; d.max_win = m.max_win; d.max_count = m.max_count; d.max_nsh = m.max_nsh;
+    d.cmeta = cmeta; d.lidx = lidx; d.lpos = lpos; d.jds = jds; d.sh_pstart = sh_pstart;
     d.shl_node = shl_node; d.shl_slot = shl_slot; d.shl_cr = shl_cr;
     RET(cudaStreamSynchronize(s));
     return cudaGetLastError();

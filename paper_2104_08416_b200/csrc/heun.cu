@@ -39,7 +39,6 @@ namespace sem {
 namespace {
 
 constexpr int kStagesH = 2;
-constexpr int kDH = 8;  // CSR entries per node loaded together
 
 // tables packed densely for the current degree: h_Dr[p * Np + q] = dN_q/dr at node p
 __constant__ double h_Dr[kMaxNp * kMaxNp];
@@ -51,12 +50,12 @@ __constant__ double h_wK[kMaxNp];
 
 // Shared-memory layout of one stage (offsets 16-byte aligned).
 struct HeunLayout {
-    int lidx, lpos, lptr, shs, g, meta, u, w, size;
+    int lidx, lpos, jds, shs, g, meta, u, w, size;
     __host__ __device__ HeunLayout(int np, int B, int L, int Lp, int Ls) {
         lidx = 0;
         lpos = np * B * 2;
-        lptr = lpos + np * B * 2;
-        shs = lptr + Lp * 2;
+        jds = lpos + np * B * 2;
+        shs = jds + Lp * 2;
         g = shs + Ls * 4;
         meta = g + 5 * B * 8;
         u = meta + 32;
@@ -65,15 +64,17 @@ struct HeunLayout {
     }
 };
 
-__device__ __forceinline__ double2 csr_sum2(const double2 *ebuf, const uint16_t *lp, int i) {
-    const int j0 = lp[i], j1 = lp[i + 1];
-    double2 part[kDH];
-#pragma unroll
-    for (int d = 0; d < kDH; d++) part[d] = (j0 + d < j1) ? ebuf[j0 + d] : make_double2(0.0, 0.0);
-    double2 y = part[0];
-#pragma unroll
-    for (int d = 1; d < kDH; d++) { y.x += part[d].x; y.y += part[d].y; }
-    for (int j = j0 + kDH; j < j1; j++) { const double2 e = ebuf[j]; y.x += e.x; y.y += e.y; }
+// (R(V), K U) of a local node from the jagged-diagonal entry buffer (see
+// jds_sum in step.cu): diagonals in order, a warp's lanes on consecutive pairs
+__device__ __forceinline__ double2 jds_sum2(const double2 *ebuf, const uint16_t *jo, int end, int ii) {
+    double2 y = ebuf[jo[0] + ii];
+    for (int d = 1; d < kJdsW; d++) {
+        const int nd = (d + 1 < kJdsW ? (int)jo[d + 1] : end) - (int)jo[d];
+        if (ii >= nd) break;
+        const double2 e = ebuf[jo[d] + ii];
+        y.x += e.x;
+        y.y += e.y;
+    }
     return y;
 }
 
@@ -124,14 +125,13 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             unsigned char *st = sm + s * lay.size;
             const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
             const int4 m1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
-            const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z, lp0 = m1.w;
+            const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z;
             if (lane == 0) {
                 reinterpret_cast<int4 *>(st + lay.meta)[0] = m0;
                 reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
-                const int nlp = (ni_al + nsh + 1 + 7) & ~7;
                 const int nsh4 = (nsh + 3) & ~3;
                 uint32_t bytes = NP * B * 2 + 5 * B * 8;
-                if (kStep) bytes += NP * B * 2 + nlp * 2 + nsh4 * 4 + (uint32_t)ni_al * 8;
+                if (kStep) bytes += NP * B * 2 + 2 * kJdsW * 2 + nsh4 * 4 + (uint32_t)ni_al * 8;
                 if (kLag) bytes += (uint32_t)ni_al * 8;
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                 for (int g = 0; g < 5; g++) tma_load(st + lay.g + g * B * 8, a.geo[g] + e0, B * 8, &full[s]);
                 if (kStep) {
                     tma_load(st + lay.lpos, ch.lpos + e0 * NP, NP * B * 2, &full[s]);
-                    tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
+                    tma_load(st + lay.jds, ch.jds + c * 2 * kJdsW, 2 * kJdsW * 2, &full[s]);
                     if (nsh4 > 0) tma_load(st + lay.shs, ch.shl_slot + s0, nsh4 * 4, &full[s]);
                     if (ni_al > 0) tma_load(st + lay.u, a.U + i0, ni_al * 8, &full[s]);
                 }
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
 
         if (kStep) {
             const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
-            const uint16_t *lp = reinterpret_cast<const uint16_t *>(st + lay.lptr);
+            const uint16_t *jd = reinterpret_cast<const uint16_t *>(st + lay.jds);
             const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
             const double *u_s = reinterpret_cast<const double *>(st + lay.u);
             if (t < ne) {
@@ -263,10 +263,11 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             }
             consumer_sync<B>();
             mbar_wait(wfull, k & 1);
-            // (4) node-centric reduction in fixed CSR order + fused Heun update
+            // (4) node-centric reduction in fixed (JDS diagonal) order + fused Heun update
             const int nl = ni_al + nsh;
             for (int i = t; i < nl; i += B) {
-                const double2 ab = csr_sum2(ebuf, lp, i);
+                if (i >= nint && i < ni_al) continue;  // the alignment hole
+                const double2 ab = i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al);
                 if (i < nint) {
                     const int64_t id = i0 + i;
                     const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
@@ -423,7 +424,7 @@ int heun_grid(const DevChunks &ch, int mode) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, mode);
+    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode);
     const HFn fn = heun_fn(ch.Np, ch.B, mode);
     set_smem_h(fn, smem);
     int occ = 0;
@@ -438,13 +439,13 @@ cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cuda
                         int64_t nlist) {
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
-    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, mode);
+    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode);
     const HFn fn = heun_fn(ch.Np, ch.B, mode);
     cudaError_t e = set_smem_h(fn, smem);
     if (e != cudaSuccess) return e;
     int grid = heun_grid(ch, mode);
     if (grid > n) grid = (int)n;
-    fn<<<grid, ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, list, nlist);
+    fn<<<grid, ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list, nlist);
     return cudaGetLastError();
 }
 

@@ -77,11 +77,11 @@ struct DevChunks {  // device view of ChunkMeta
     int B, Np;
     int64_t E, N, nchunks, N_int, N_sh, N_tot, n_slots;
     int64_t N_if;              // interface nodes: the last N_if of the shared range
-    int max_local, max_win, max_lptr, max_nsh;
+    int max_local, max_win, max_count, max_nsh;
     const int32_t *cmeta;      // [nchunks][8]
     const uint16_t *lidx;      // [nchunks][Np][B] chunk-local node of (p, t)
-    const uint16_t *lpos;      // [nchunks][Np*B] CSR position of entry p*B + t
-    const uint16_t *lptr;      // per-chunk CSR row pointers (block at cmeta[7])
+    const uint16_t *lpos;      // [nchunks][Np*B] entry-buffer (JDS) position of entry p*B + t
+    const uint16_t *jds;       // [nchunks][2 kJdsW] jagged-diagonal starts (interior, shared segment)
     const int32_t *sh_pstart;  // [N_sh+1] node-major slots of shared node s
     const int32_t *shl_node;   // per chunk (block at cmeta[2]): shared index of each local shared node
     const int32_t *shl_slot;   // per chunk: the slot it writes
@@ -139,7 +139,6 @@ struct StepParams {
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
     const int64_t *n_dev;  // if set: the step index lives in device memory (CUDA-graph step loop)
-    int csr_fit;           // node-phase sums with the load width fitted per warp (default; SEM_K7_CSR=fixed)
 };
 int k7_grid(const DevChunks &ch, bool fused);
 // device step counter of the graph-captured step loop: += 1, = v

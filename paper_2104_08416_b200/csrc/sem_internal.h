@@ -11,6 +11,7 @@
 namespace sem {
 
 constexpr int kMaxNp = 36;  // P = 7
+constexpr int kJdsW = 32;   // jagged diagonals per segment = max entries of a node in a chunk
 
 // ---------------------------------------------------------------------------
 // Reference triangle tables, derived on the host in long double (refelem.cpp).
@@ -50,16 +51,15 @@ struct ChunkMeta {
     int64_t E = 0, N = 0, nchunks = 0;
     int64_t N_int = 0, N_sh = 0, N_tot = 0, n_slots = 0;
     int64_t N_if = 0;                // forced-shared (rank-interface) nodes, last N_if of the shared range
-    int max_local = 0, max_win = 0, max_colors = 0, max_lptr = 0, max_nsh = 0;  // max_nsh: multiple of 8
+    int max_local = 0, max_win = 0, max_colors = 0, max_count = 0, max_nsh = 0;  // max_nsh: multiple of 8
     std::vector<int32_t> i0;         // [nchunks+1] interior window starts (even)
     std::vector<int32_t> s0;         // [nchunks+1] chunk blocks in shl_node / shl_slot / shl_cr (multiple of 8)
     std::vector<int32_t> shl_node;   // shared index s of each chunk-local shared node
     std::vector<int32_t> shl_slot;   // node-major slot written by that chunk
     std::vector<uint16_t> shl_cr;    // (slots of the node << 8) | this chunk's rank among them
-    std::vector<int32_t> cmeta;      // [nchunks][8] {i0, nint, s0, nsh, ncol, ne, nint_al, lp0}
-    std::vector<int32_t> lp0;        // [nchunks+1] start of chunk c's block in lptr (multiple of 8)
-    std::vector<uint16_t> lptr;      // per chunk: CSR row pointers over local nodes (nlocal+1)
-    std::vector<uint16_t> lpos;      // [nchunks][Np*B] CSR position of entry p*B + t (runs ascending in e)
+    std::vector<int32_t> cmeta;      // [nchunks][8] {i0, nint, s0, nsh, end0, ne, nint_al, end1}
+    std::vector<uint16_t> jds;       // [nchunks][2 kJdsW] start of each jagged diagonal per segment
+    std::vector<uint16_t> lpos;      // [nchunks][Np*B] entry-buffer position of entry p*B + t (JDS)
     std::vector<int32_t> sh_pstart;  // [N_sh+1] slots of shared node s (node-major, chunk order)
     std::vector<uint16_t> lidx;      // [nchunks][Np][B] chunk-local node index
     std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)

@@ -35,7 +35,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kStages = 2;
-constexpr int kD = 8;    // entries per node loaded together (mesh vertex degree <= 8 typical)
 
 // S tables packed densely for the current degree ([p * Np + q]): at P3 the three
 // tables span 2.4 KB of the constant cache instead of rows strided by kMaxNp
@@ -63,12 +62,12 @@ inline unsigned blocks_for(int64_t n, int threads = kThreads) {
 // window length when the windows travel in the stage (double-buffered with
 // it), else 0 (single-buffered windows outside the stages).
 struct StageLayout {
-    int lidx, lpos, lptr, shs, shn, scr, g, meta, u, up, m, size;
+    int lidx, lpos, jds, shs, shn, scr, g, meta, u, up, m, size;
     __host__ __device__ StageLayout(int np, int B, int L, int Lp, int Ls, int Lf, int Ws) {
         lidx = 0;
         lpos = np * B * 2;
-        lptr = lpos + np * B * 2;
-        shs = lptr + Lp * 2;
+        jds = lpos + np * B * 2;
+        shs = jds + Lp * 2;
         shn = shs + Ls * 4;
         scr = shn + Lf * 4;
         g = scr + Lf * 2;
@@ -102,6 +101,22 @@ __global__ void k_geometry(const double *__restrict__ vxy, const int32_t *__rest
     detJ[k] = det;
 }
 
+// Sum of a local node's element contributions in the jagged-diagonal (JDS)
+// entry buffer (chunks.cpp): jo = the node's segment's diagonal starts, end =
+// end of that segment, ii = node index in the segment.  Diagonal d holds the
+// d-th entry (ascending e = p*B + t) of every node with more than d entries;
+// diagonal lengths do not increase with d.  The sum runs over d in order (a
+// fixed order), and a warp's lanes read consecutive words of each diagonal.
+__device__ __forceinline__ double jds_sum(const double *ebuf, const uint16_t *jo, int end, int ii) {
+    double y = ebuf[jo[0] + ii];  // every local node has an entry
+    for (int d = 1; d < kJdsW; d++) {
+        const int nd = (d + 1 < kJdsW ? (int)jo[d + 1] : end) - (int)jo[d];
+        if (ii >= nd) break;
+        y += ebuf[jo[d] + ii];
+    }
+    return y;
+}
+
 // ---- lumped mass with the chunk machinery (one-time, not pipelined) -----------
 template <int NP, int B>
 __global__ void __launch_bounds__(B) k_mass_chunk(const DevChunks ch, const double *__restrict__ detJ,
@@ -110,7 +125,7 @@ __global__ void __launch_bounds__(B) k_mass_chunk(const DevChunks ch, const doub
     __shared__ double ybuf[NP * B];
     const int c = blockIdx.x, t = threadIdx.x;
     const int *cm = ch.cmeta + 8 * (int64_t)c;
-    const int i0 = cm[0], nint = cm[1], s0 = cm[2], nsh = cm[3], ne = cm[5], ni_al = cm[6], lp0 = cm[7];
+    const int i0 = cm[0], nint = cm[1], s0 = cm[2], nsh = cm[3], ne = cm[5], ni_al = cm[6];
     const int64_t e = (int64_t)c * B + t;
     if (t < ne) {
         const double dj = detJ[e];
@@ -119,12 +134,10 @@ __global__ void __launch_bounds__(B) k_mass_chunk(const DevChunks ch, const doub
         for (int p = 0; p < NP; p++) ybuf[lpo[p * B + t]] = 1.0 * dj * c_wM[p];
     }
     __syncthreads();
-    const uint16_t *lp = ch.lptr + lp0;
+    const uint16_t *jd = ch.jds + (int64_t)c * 2 * kJdsW;
     for (int i = t; i < ni_al + nsh; i += B) {
-        double m = 0.0;
-        for (int j = lp[i]; j < lp[i + 1]; j++) m += ybuf[j];
-        if (i < nint) dt2M[i0 + i] = dt2 / m;
-        else if (i >= ni_al) slot[ch.shl_slot[s0 + i - ni_al]] = m;
+        if (i < nint) dt2M[i0 + i] = dt2 / jds_sum(ybuf, jd, cm[4], i);
+        else if (i >= ni_al) slot[ch.shl_slot[s0 + i - ni_al]] = jds_sum(ybuf, jd + kJdsW, cm[7], i - ni_al);
     }
 }
 
@@ -137,46 +150,6 @@ __global__ void k_mass_fix(const DevChunks ch, const double *__restrict__ slot, 
     dt2M[ch.N_int + s] = dt2 / m;
 }
 
-// Sum of a local node's element contributions, stored contiguously in CSR
-// order (ascending e = p*B + t: a fixed order).  Up to kD entries are loaded
-// together (predicated); absent ones contribute an exact +0.  Local nodes are
-// sorted by degree, so a warp's lanes take the same path.
-template <int N>
-__device__ __forceinline__ double run_sum(const double *ebuf, int j0, int j1) {
-    double part[N];
-#pragma unroll
-    for (int d = 0; d < N; d++) part[d] = (j0 + d < j1) ? ebuf[j0 + d] : 0.0;
-    double y = part[0];
-#pragma unroll
-    for (int d = 1; d < N; d++) y += part[d];
-    return y;
-}
-
-// Same sum with the load width fitted to the warp's longest run (nodes are
-// sorted by entry count inside a chunk, so a warp's runs have similar lengths:
-// at P3 most nodes have 1 or 2 entries).  Only the sign of an exact zero can
-// differ from csr_sum.
-__device__ __forceinline__ double csr_sum_fit(const double *ebuf, const uint16_t *lp, int i) {
-    const int j0 = lp[i], j1 = lp[i + 1];
-    const int mx = __reduce_max_sync(__activemask(), j1 - j0);
-    if (mx <= 2) return run_sum<2>(ebuf, j0, j1);
-    if (mx <= 4) return run_sum<4>(ebuf, j0, j1);
-    double y = run_sum<kD>(ebuf, j0, j1);
-    for (int j = j0 + kD; j < j1; j++) y += ebuf[j];
-    return y;
-}
-
-__device__ __forceinline__ double csr_sum(const double *ebuf, const uint16_t *lp, int i) {
-    const int j0 = lp[i], j1 = lp[i + 1];
-    double part[kD];
-#pragma unroll
-    for (int d = 0; d < kD; d++) part[d] = (j0 + d < j1) ? ebuf[j0 + d] : 0.0;
-    double y = part[0];
-#pragma unroll
-    for (int d = 1; d < kD; d++) y += part[d];
-    for (int j = j0 + kD; j < j1; j++) y += ebuf[j];
-    return y;
-}
 
 // Fused K8 (shared nodes finalised by their last chunk): after writing its
 // partial into slot `sl`, a chunk counts its arrival on the node's counter with
@@ -271,20 +244,19 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             unsigned char *st = sm + s * lay.size;
             const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
             const int4 m1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
-            const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z, lp0 = m1.w;
+            const int i0 = m0.x, s0 = m0.z, nsh = m0.w, ni_al = m1.z;
             if (lane == 0) {
                 reinterpret_cast<int4 *>(st + lay.meta)[0] = m0;
                 reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
-                const int nlp = (ni_al + nsh + 1 + 7) & ~7;
                 const int nsh8 = (nsh + 7) & ~7;
                 const bool fuse = a.cnt != nullptr;
-                const uint32_t bytes = 2 * NP * B * 2 + nlp * 2 + nsh8 * (fuse ? 10 : 4) + 3 * B * 8 +
+                const uint32_t bytes = 2 * NP * B * 2 + 2 * kJdsW * 2 + nsh8 * (fuse ? 10 : 4) + 3 * B * 8 +
                                        (uint32_t)ni_al * (WIN2 ? 24 : 8);
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
                 tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
                 tma_load(st + lay.lpos, ch.lpos + e0 * NP, NP * B * 2, &full[s]);
-                tma_load(st + lay.lptr, ch.lptr + lp0, nlp * 2, &full[s]);
+                tma_load(st + lay.jds, ch.jds + c * 2 * kJdsW, 2 * kJdsW * 2, &full[s]);
                 if (nsh8 > 0) {
                     tma_load(st + lay.shs, ch.shl_slot + s0, nsh8 * 4, &full[s]);
                     if (fuse) {
@@ -332,7 +304,8 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         const double *u_s = reinterpret_cast<const double *>(st + lay.u);
         const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
         const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
-        const uint16_t *lp = reinterpret_cast<const uint16_t *>(st + lay.lptr);
+        const uint16_t *jd = reinterpret_cast<const uint16_t *>(st + lay.jds);
+        const int end0 = m1.x, end1 = m1.w;
         const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
         const double *g_s = reinterpret_cast<const double *>(st + lay.g);
 
@@ -402,7 +375,8 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 upg = a.Uprev[i0 + i];
                 mg = __ldg(a.dt2M + i0 + i);
             }
-            const double yi = a.csr_fit ? csr_sum_fit(ebuf, lp, i) : csr_sum(ebuf, lp, i);
+            if (i >= nint && i < ni_al) continue;  // the alignment hole
+            const double yi = i < nint ? jds_sum(ebuf, jd, end0, i) : jds_sum(ebuf, jd + kJdsW, end1, i - ni_al);
             if (i < nint) {
                 const int id = i0 + i;
                 const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
@@ -660,7 +634,7 @@ int k7_grid(const DevChunks &ch, bool fused) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, fused);
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, fused);
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     set_smem(fn, smem);
     int occ = 0;
@@ -676,11 +650,11 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
     if (grid > n) grid = (int)n;
-    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, p.cnt != nullptr);
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, p.cnt != nullptr);
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     cudaError_t e = set_smem(fn, smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, ch.B * k7_group(ch.Np) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, ch.max_lptr, ch.max_nsh, list,
+    fn<<<grid, ch.B * k7_group(ch.Np) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list,
                                                        nlist);
     return cudaGetLastError();
 }

@@ -247,7 +247,7 @@ def version() -> str:
     return load().sem_version().decode()
 
 
-CHUNK_STAT_KEYS = ["nchunks", "N_int", "N_sh", "n_slots", "max_local", "max_win", "max_lptr",
+CHUNK_STAT_KEYS = ["nchunks", "N_int", "N_sh", "n_slots", "max_local", "max_win", "max_count",
                    "max_colors", "sum_nint", "sum_nsh", "max_nsh"]
 
 
