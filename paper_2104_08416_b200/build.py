@@ -39,11 +39,12 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile the library (out/defines: experiment variants, e.g. out=libsem_alt.so)."""
+    if not force and out == LIB and not stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB + ".tmp", "-lgomp", "-ldl"]
+    cmd = [_nvcc(), *NVCC_FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           *[os.path.join(CSRC, f) for f in SOURCES], "-o", out + ".tmp", "-lgomp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr
     with open(os.path.join(CSRC, "build.log"), "w") as f:
@@ -51,10 +52,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed (see %s)" % os.path.join(CSRC, "build.log"))
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(out + ".tmp", out)
     if verbose:
         sys.stdout.write(log)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

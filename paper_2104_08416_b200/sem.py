@@ -15,7 +15,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsem.so")
+# SEM_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("SEM_LIB") or os.path.join(_HERE, "libsem.so")
 
 SEM_OK, SEM_E_ARG, SEM_E_STATE, SEM_E_MESH, SEM_E_UNSUPPORTED = 0, 1, 2, 3, 4
 SEM_E_CUDA, SEM_E_NCCL, SEM_E_OOM, SEM_E_NONFINITE = 5, 6, 7, 8
