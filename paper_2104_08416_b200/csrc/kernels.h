@@ -141,6 +141,8 @@ struct StepParams {
     const int64_t *n_dev;  // if set: the step index lives in device memory (CUDA-graph step loop)
 };
 int k7_grid(const DevChunks &ch, bool fused);
+// resident K7 CTAs per SM for chunks of B elements with these per-chunk maxima (shared-memory stages)
+int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused);
 // device step counter of the graph-captured step loop: += 1, = v
 cudaError_t launch_step_inc(int64_t *n, cudaStream_t s);
 cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s);

@@ -34,7 +34,10 @@ namespace sem {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kStages = 2;
+#ifndef SEM_KSTAGES
+#define SEM_KSTAGES 2
+#endif
+constexpr int kStages = SEM_KSTAGES;  // pipeline depth of K7 (A/B: -DSEM_KSTAGES=3)
 
 // S tables packed densely for the current degree ([p * Np + q]): at P3 the three
 // tables span 2.4 KB of the constant cache instead of rows strided by kMaxNp
@@ -627,6 +630,15 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer,
     return cudaGetLastError();
 }
 
+int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused) {
+    const size_t smem = k7_smem_bytes(np, B, max_local, max_win, 2 * kJdsW, max_nsh, fused);
+    const K7Fn fn = k7_fn(np, B);
+    set_smem(fn, smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, B * k7_group(np) + 32, smem);
+    return occ < 1 ? 1 : occ;
+}
+
 int k7_grid(const DevChunks &ch, bool fused) {
     static int nsm = 0;
     if (!nsm) {
@@ -634,12 +646,7 @@ int k7_grid(const DevChunks &ch, bool fused) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, fused);
-    const K7Fn fn = k7_fn(ch.Np, ch.B);
-    set_smem(fn, smem);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B * k7_group(ch.Np) + 32, smem);
-    if (occ < 1) occ = 1;
+    const int occ = k7_ctas_per_sm(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_nsh, fused);
     int64_t g = (int64_t)occ * nsm;
     if (g > ch.nchunks) g = ch.nchunks;
     return (int)g;

@@ -34,7 +34,7 @@ def test_gpu_chunks_equal_host(ctx, name, scale, deg, elem_order, node_order):
     assert info["n_chunks"] >= 1 and info["n_shared_nodes"] > 0
 
 
-@pytest.mark.parametrize("B", ["128", "192", "512"])
+@pytest.mark.parametrize("B", ["128", "192", "256", "512"])
 def test_gpu_chunks_equal_host_chunk_sizes(ctx, monkeypatch, B):
     monkeypatch.setenv("SEM_CHUNK", B)
     pb = mg.config("C2", 8)
