@@ -91,6 +91,20 @@ NcclApi &nccl() {
 }
 }  // namespace
 
+// Device arrays that live as long as a mesh or its operators: stream-ordered pool
+// allocations on the context's stream (the pool keeps freed memory mapped, so a
+// later sem_mesh_reorder does not pay cudaMalloc's page mapping again).
+struct AllocList {
+    cudaStream_t s = nullptr;
+    std::vector<void *> p;
+    size_t size() const { return p.size(); }
+    void push_back(void *q) { p.push_back(q); }
+    void release_from(size_t n) {  // free the entries [n, size)
+        for (size_t i = n; i < p.size(); i++) cudaFreeAsync(p[i], s);
+        p.resize(n);
+    }
+};
+
 struct sem_ctx {
     int device = 0, rank = 0, world = 1;
     bool loopback = false;  // world > 1 without NCCL: only the sem_group_* calls may step it
@@ -107,7 +121,7 @@ struct sem_ctx {
     int64_t E_glob = 0, N_glob = 0, e0 = 0;
     int32_t grid[2] = {0, 0};
     RefTables T;
-    std::vector<void *> mesh_allocs, ops_allocs;
+    AllocList mesh_allocs, ops_allocs;
     double *d_vxy = nullptr;
     int32_t *d_tri_or = nullptr;  // oriented triangles, INPUT order
     int32_t *d_perm = nullptr;    // new -> input (global order)
@@ -211,18 +225,18 @@ cudaError_t dalloc(TmpList &t, T **p, size_t count) {
 }
 
 template <typename T>
-cudaError_t dalloc(std::vector<void *> &list, T **p, size_t count) {
+cudaError_t dalloc(AllocList &list, T **p, size_t count) {
     void *q = nullptr;
-    cudaError_t e = cudaMalloc(&q, sizeof(T) * (count ? count : 1));
+    cudaError_t e = cudaMallocAsync(&q, sizeof(T) * (count ? count : 1), list.s);
     if (e != cudaSuccess) return e;
     list.push_back(q);
     *p = (T *)q;
     return cudaSuccess;
 }
 
-void free_list(std::vector<void *> &l) {
-    for (void *p : l) cudaFree(p);
-    l.clear();
+void free_list(AllocList &l) {
+    if (l.size()) cudaDeviceSynchronize();  // as cudaFree did: no stream (main or comm) still uses them
+    l.release_from(0);
 }
 
 void destroy_graphs(sem_ctx *ctx);
@@ -277,7 +291,7 @@ struct PhaseTrace {  // SEM_TRACE=1: wall time of each preparation phase on stde
 };
 
 template <typename T>
-cudaError_t upload(std::vector<void *> &list, T **dst, const std::vector<T> &src, cudaStream_t s) {
+cudaError_t upload(AllocList &list, T **dst, const std::vector<T> &src, cudaStream_t s) {
     cudaError_t e = dalloc(list, dst, src.size());
     if (e != cudaSuccess) return e;
     if (src.empty()) return cudaSuccess;
@@ -327,7 +341,7 @@ sem_status prepare_ablation(sem_ctx *ctx, const std::vector<int32_t> &mu_h, int6
 }
 
 // Host-built chunk metadata (chunks.cpp) -> device arrays and the device view.
-cudaError_t upload_chunks(std::vector<void *> &L, const ChunkMeta &m, DevChunks &d, cudaStream_t s) {
+cudaError_t upload_chunks(AllocList &L, const ChunkMeta &m, DevChunks &d, cudaStream_t s) {
     d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
     d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
     d.max_local = m.max_local; d.max_win = m.max_win; d.max_count = m.max_count; d.max_nsh = m.max_nsh;
@@ -859,6 +873,7 @@ sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
             return cuda_fail(ctx, e, "cudaStreamCreate");
         ctx->own_stream = true;
     }
+    ctx->mesh_allocs.s = ctx->ops_allocs.s = ctx->stream;
     if ((e = cudaEventCreateWithFlags(&ctx->xev, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming)) != cudaSuccess)
@@ -1166,9 +1181,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             }
             const int again = attempt == 0 ? chunk_fallback(degree, heun, m) : 0;
             if (!again) break;
-            CK(cudaStreamSynchronize(s));  // drop this build's device arrays and rebuild
-            for (size_t i = n_alloc; i < L.size(); i++) cudaFree(L[i]);
-            L.resize(n_alloc);
+            L.release_from(n_alloc);  // drop this build's device arrays and rebuild
             B_chunk = again;
         }
         if (gpu_chunks) {

@@ -18,7 +18,10 @@
 // the 0.3 GB connectivity round trip on C4.
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -298,6 +301,21 @@ __global__ void k_iota32(int32_t *a, int64_t n) {
     if (i < n) a[i] = (int32_t)i;
 }
 
+struct SubTrace {  // SEM_TRACE=1: wall time of each builder section on stderr
+    bool on = getenv("SEM_TRACE") != nullptr;
+    double t = ms();
+    static double ms() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+    void mark(cudaStream_t s, const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const double n = ms();
+        fprintf(stderr, "[sem chunk builder]   %-28s %8.1f ms\n", what, n - t);
+        t = n;
+    }
+};
+
 }  // namespace
 
 cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, int B, const uint8_t *d_forced,
@@ -314,6 +332,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     const int bn = bits_for(N), bc = bits_for(nch + 1);
     if (bc + bn > 62 || bc + 9 + bn > 64) { err = "build_chunks_gpu: mesh too large for 64-bit keys"; return cudaSuccess; }
     const uint64_t pad_key = ((uint64_t)1 << (bc + bn)) - 1;
+    SubTrace tr;
 
     // ---- 1. entries -> (chunk, node) runs ----
     Tmp k1(s), v1(s), k1s(s), v1s(s), flag(s), rid(s);
@@ -342,6 +361,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     k_run_info<<<nb(nruns), kT, 0, s>>>(k1s.as<uint64_t>(), rstart.as<int32_t>(), nruns, n, bn, rc.as<int32_t>(),
                                         rg.as<int32_t>(), rlen.as<int32_t>(), nref.as<int32_t>());
 
+    tr.mark(s, "runs");
     // ---- classification and shared indices ----
     Tmp fa(s), fb(s), ea(s), eb(s), s_of(s), bad(s);
     RET(fa.alloc(4 * (N + 1)));
@@ -375,6 +395,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     k_shared_index<<<nb(N), kT, 0, s>>>(fa.as<int32_t>(), fb.as<int32_t>(), ea.as<int32_t>(), eb.as<int32_t>(), N,
                                         (int32_t)na, s_of.as<int32_t>(), node_of_s.as<int32_t>());
 
+    tr.mark(s, "classification");
     // ---- 2. local order per chunk ----
     Tmp k2(s), v2(s), k2s(s), order(s), nint(s), nsh(s);
     RET(k2.alloc(8 * nruns));
@@ -403,6 +424,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     RET(cudaStreamSynchronize(s));
     m.N_int = hN_int;
     m.N_tot = m.N_int + m.N_sh;
+    tr.mark(s, "local order sort");
     Tmp local(s);
     RET(local.alloc(4 * nruns));
     int32_t *int_of = nullptr;
@@ -413,6 +435,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
                                            ni_al.as<int32_t>(), i0.as<int32_t>(), nruns, m.N_int, local.as<int32_t>(),
                                            int_of);
 
+    tr.mark(s, "local index");
     // ---- 3. slots: node-major, chunks of a node in ascending order ----
     int32_t *sh_pstart = nullptr, *shl_node = nullptr, *shl_slot = nullptr;
     uint16_t *shl_cr = nullptr;
@@ -447,6 +470,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
         m.n_slots = nsh_tot ? hslots : 0;
     }
 
+    tr.mark(s, "slots");
     // ---- local indices, CSR row pointers and positions ----
     uint16_t *lidx = nullptr, *lpos = nullptr, *jds = nullptr;
     int32_t *cmeta = nullptr;
@@ -475,6 +499,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     int32_t hmx[4];
     RET(cudaMemcpyAsync(hmx, mx.p, 16, cudaMemcpyDeviceToHost, s));
 
+    tr.mark(s, "jds + entries");
     // ---- boundary (touching a rank-interface node) / interior chunk lists ----
     int32_t *bnd = nullptr, *intc = nullptr;
     std::vector<int32_t> hbnd;
@@ -507,6 +532,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     *d_bnd = bnd;
     *d_intc = intc;
 
+    tr.mark(s, "lists");
     d.B = B; d.Np = Np; d.E = E; d.N = N; d.nchunks = nch;
     d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
     d.max_local = m.max_local; d.max_win = m.max_win; d.max_count = m.max_count; d.max_nsh = m.max_nsh;

@@ -162,24 +162,37 @@ class SemContext:
 
     # -- API --
     def sem_mesh_reorder(self, vxy, tri, degree: int, elem_order=SEM_ORDER_HILBERT,
-                         node_order=SEM_NODES_FIRST_TOUCH, seed: int = 0):
-        """Returns dict(keys, elem_perm, node_perm, n_nodes, grid)."""
+                         node_order=SEM_NODES_FIRST_TOUCH, seed: int = 0, out=None):
+        """Returns dict(keys, elem_perm, node_perm, n_nodes, grid).
+
+        `out`: optional dict of caller-owned host arrays (e.g. pinned) with keys
+        "keys" (uint32 [E]), "elem_perm" (int32 [E]), "node_perm" (int32, at least
+        V + 3E(P-1) + E*nI entries); a key mapped to None skips that output."""
         vxy = np.ascontiguousarray(vxy, np.float64)
         tri = np.ascontiguousarray(tri, np.int32)
         E, nv = tri.shape[0], vxy.shape[0]
-        keys = np.empty(E, np.uint32)
-        eperm = np.empty(E, np.int32)
         nI = (degree - 1) * (degree - 2) // 2 if degree >= 1 else 0
         nmax = nv + 3 * E * max(degree - 1, 0) + E * nI
-        nperm = np.empty(max(nmax, 1), np.int32)
+        want = {"keys": (np.uint32, E), "elem_perm": (np.int32, E), "node_perm": (np.int32, max(nmax, 1))}
+        bufs = {}
+        for k, (dt, n) in want.items():
+            if out is not None and k in out:
+                a = out[k]
+                if a is not None and (a.dtype != dt or a.size < n or not a.flags.c_contiguous):
+                    raise ValueError("out[%r] must be a contiguous %s array of at least %d entries" % (k, dt.__name__, n))
+                bufs[k] = a
+            else:
+                bufs[k] = np.empty(n, dt)
         nn = C.c_int64(0)
         grid = np.zeros(2, np.int32)
         self._check(self.L.sem_mesh_reorder(self.h, _ptr(vxy), nv, _ptr(tri), E, degree, elem_order,
-                                            node_order, seed, _ptr(keys), _ptr(eperm), _ptr(nperm),
-                                            C.byref(nn), _ptr(grid)))
+                                            node_order, seed, _ptr(bufs["keys"]), _ptr(bufs["elem_perm"]),
+                                            _ptr(bufs["node_perm"]), C.byref(nn), _ptr(grid)))
         self.N = nn.value
         self.E = E
-        return {"keys": keys, "elem_perm": eperm, "node_perm": nperm[: nn.value],
+        keys, eperm, nperm = bufs["keys"], bufs["elem_perm"], bufs["node_perm"]
+        return {"keys": None if keys is None else keys[:E], "elem_perm": None if eperm is None else eperm[:E],
+                "node_perm": None if nperm is None else nperm[: nn.value],
                 "n_nodes": nn.value, "grid": (int(grid[0]), int(grid[1]))}
 
     def sem_build_operators(self, c_elem, src_vertex: int, f0: float, t0: float, amplitude: float, dt: float):

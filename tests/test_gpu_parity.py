@@ -65,6 +65,28 @@ def test_reorder_bit_exact(ctx, name, scale):
     assert np.array_equal(r["node_perm"], node_perm)
 
 
+def test_reorder_caller_buffers(ctx):
+    """Outputs written into caller-owned (pinned) arrays, or skipped with None,
+    carry the same bits as the binding's own arrays."""
+    import torch
+    pb = mg.config("C3", 8)
+    m = pb.mesh
+    ref = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+    nmax = m.nv + 3 * m.ne * (pb.P - 1) + m.ne * (pb.P - 1) * (pb.P - 2) // 2
+    out = {"keys": torch.full((m.ne,), -1, dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+           "elem_perm": np.full(m.ne, -1, np.int32),
+           "node_perm": torch.full((nmax + 5,), -1, dtype=torch.int32).pin_memory().numpy()}
+    r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, out=out)
+    for k in ("keys", "elem_perm", "node_perm"):
+        assert np.array_equal(r[k], ref[k]), k
+    assert np.all(out["node_perm"][r["n_nodes"]:] == -1)  # nothing written past N
+    r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, out={"keys": None, "elem_perm": None})
+    assert r["keys"] is None and r["elem_perm"] is None
+    assert np.array_equal(r["node_perm"], ref["node_perm"])
+    with pytest.raises(ValueError):
+        ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, out={"elem_perm": np.zeros(m.ne - 1, np.int32)})
+
+
 @pytest.mark.parametrize("elem_order,node_order", [(S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
                                                    (S.SEM_ORDER_RANDOM, S.SEM_NODES_FIRST_TOUCH),
                                                    (S.SEM_ORDER_HILBERT, S.SEM_NODES_CANONICAL),
