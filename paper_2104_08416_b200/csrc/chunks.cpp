@@ -159,17 +159,26 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     m.N_if = nif;
     m.N_tot = m.N_int + nsh;
 
-    // interior ids: per chunk, descending entry count then ascending id
-    // (stable counting sort; the unique list is ascending in id)
+    // interior ids: per chunk, descending entry count then ascending id (stable counting
+    // sort; the unique list is ascending in id).  Element-interior nodes (lattice-interior
+    // local p) come after the count-1 nodes: K7 finalises them per element.
+    std::vector<uint8_t> inner;
+    if (lattice_n_interior(Np) > 0) {
+        inner.assign(N, 0);
+        for (int p = 0; p < Np; p++)
+            if (lattice_interior(Np, p))
+                for (int64_t e = 0; e < E; e++) inner[mu[e * Np + p]] = 1;
+    }
+    auto bucket = [&](const Uniq &u) { return (!inner.empty() && inner[u.g]) ? 255 : 255 - std::min(u.cnt, 255); };
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t c = 0; c < nch; c++) {
         int off[256] = {0};
         for (const Uniq &u : uq[c])
-            if (interior(u.g)) off[255 - std::min(u.cnt, 255)]++;
+            if (interior(u.g)) off[bucket(u)]++;
         int acc = 0;
         for (int b = 0; b < 256; b++) { const int h = off[b]; off[b] = acc; acc += h; }
         for (const Uniq &u : uq[c])
-            if (interior(u.g)) m.int_of[u.g] = (int32_t)(m.i0[c] + off[255 - std::min(u.cnt, 255)]++);
+            if (interior(u.g)) m.int_of[u.g] = (int32_t)(m.i0[c] + off[bucket(u)]++);
     }
     tr.mark("internal numbering");
 

@@ -141,16 +141,22 @@ __global__ void k_shared_index(const int32_t *__restrict__ a, const int32_t *__r
 }
 
 // 2. local-order key of every run; per-chunk interior / shared counts
+// Local order key: (chunk, shared?, 255 - entry count, id).  Element-interior nodes (the
+// run's entry sits at a lattice-interior p, inner_mask bit p) take the bucket after the
+// count-1 nodes, so they close the interior segment (K7 finalises them per element).
 __global__ void k_local_keys(const int32_t *__restrict__ rc, const int32_t *__restrict__ rg,
-                             const int32_t *__restrict__ rlen, const int32_t *__restrict__ s_of, int64_t nruns,
-                             int bx, uint64_t *key, int32_t *val, int32_t *nint, int32_t *nsh) {
+                             const int32_t *__restrict__ rlen, const int32_t *__restrict__ s_of,
+                             const int32_t *__restrict__ v1s, const int32_t *__restrict__ rstart, int Np, int B,
+                             uint64_t inner_mask, int64_t nruns, int bx, uint64_t *key, int32_t *val, int32_t *nint,
+                             int32_t *nsh) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= nruns) return;
     const int32_t c = rc[r], g = rg[r], s = s_of[g];
     const bool sh = s >= 0;
-    const uint32_t cnt = (uint32_t)min(rlen[r], 255);
+    const int p = (int)((v1s[rstart[r]] % ((int64_t)Np * B)) / B);
+    const uint32_t bucket = (!sh && ((inner_mask >> p) & 1)) ? 255u : 255u - (uint32_t)min(rlen[r], 255);
     const uint64_t x = sh ? (uint32_t)s : (uint32_t)g;
-    key[r] = ((uint64_t)c << (9 + bx)) | ((uint64_t)(sh ? 1 : 0) << (8 + bx)) | ((uint64_t)(255 - cnt) << bx) | x;
+    key[r] = ((uint64_t)c << (9 + bx)) | ((uint64_t)(sh ? 1 : 0) << (8 + bx)) | ((uint64_t)bucket << bx) | x;
     val[r] = (int32_t)r;
     // runs come in (chunk, node) order: lanes of a warp mostly share (c, sh), so
     // aggregate the count per warp before the atomic
@@ -406,9 +412,12 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     RET(nsh.alloc(4 * (nch + 1)));
     RET(cudaMemsetAsync(nint.p, 0, 4 * (nch + 1), s));
     RET(cudaMemsetAsync(nsh.p, 0, 4 * (nch + 1), s));
+    uint64_t inner_mask = 0;
+    for (int p = 0; p < Np; p++)
+        if (lattice_interior(Np, p)) inner_mask |= (uint64_t)1 << p;
     k_local_keys<<<nb(nruns), kT, 0, s>>>(rc.as<int32_t>(), rg.as<int32_t>(), rlen.as<int32_t>(), s_of.as<int32_t>(),
-                                          nruns, bn, k2.as<uint64_t>(), v2.as<int32_t>(), nint.as<int32_t>(),
-                                          nsh.as<int32_t>());
+                                          v1s.as<int32_t>(), rstart.as<int32_t>(), Np, B, inner_mask, nruns, bn,
+                                          k2.as<uint64_t>(), v2.as<int32_t>(), nint.as<int32_t>(), nsh.as<int32_t>());
     RET(sort_u64(k2.as<uint64_t>(), v2.as<int32_t>(), k2s.as<uint64_t>(), order.as<int32_t>(), nruns, bc + 9 + bn, s));
     Tmp tot(s), ni_al(s), nsh8(s), cs(s), i0(s), s0(s);
     for (Tmp *t : {&tot, &ni_al, &nsh8, &cs, &i0, &s0}) RET(t->alloc(4 * (nch + 1)));

@@ -13,6 +13,32 @@ namespace sem {
 constexpr int kMaxNp = 36;  // P = 7
 constexpr int kJdsW = 32;   // jagged diagonals per segment = max entries of a node in a chunk
 
+#ifdef __CUDACC__
+#define SEM_HD __host__ __device__
+#else
+#define SEM_HD
+#endif
+
+// Local node p of the lattice order (refelem.cpp: row j outer, i inner) is interior to
+// the element when 1 <= i, 1 <= j, i + j <= P - 1; folded at compile time in unrolled loops.
+SEM_HD constexpr int lattice_degree(int np) {
+    int P = 0;
+    while ((P + 1) * (P + 2) / 2 < np) P++;
+    return P;
+}
+SEM_HD constexpr bool lattice_interior(int np, int p) {
+    const int P = lattice_degree(np);
+    int q = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, q++)
+            if (q == p) return i >= 1 && j >= 1 && i + j <= P - 1;
+    return false;
+}
+SEM_HD constexpr int lattice_n_interior(int np) {
+    const int P = lattice_degree(np);
+    return P >= 3 ? (P - 1) * (P - 2) / 2 : 0;
+}
+
 // ---------------------------------------------------------------------------
 // Reference triangle tables, derived on the host in long double (refelem.cpp).
 // Readings R3 (node sets, lattice order) and R4 (weights) of DESIGN.md.

@@ -4,16 +4,18 @@
 //      assemble_mass    M-bar_nu = sum detJ w^M_q, then dt^2 / M-bar
 //  K7  launch_k7        persistent, warp-specialised: a producer warp streams
 //                       each chunk's contiguous blocks into shared memory with
-//                       TMA bulk copies (cp.async.bulk + mbarrier, 2 stages);
-//                       8 consumer warps: (E) u_e gathered through the chunk's
-//                       local index table, y_e = K^e u_e (one element per
-//                       thread, written to [p][t] slots), (B) node-centric gather of
-//                       y in fixed CSR order fused with the leapfrog update of
-//                       the chunk's interior nodes, partial sums of its shared
-//                       nodes into the chunk's slot block  (Alg. 1+2+3)
+//                       TMA bulk copies (cp.async.bulk + mbarrier, 2 stages) and
+//                       gathers U^n of the chunk's shared nodes (cp.async);
+//                       B/32 consumer warps: (E) u_e gathered through the chunk's
+//                       local index table, y_e = K^e u_e (one element per thread at
+//                       P <= 5, G threads at P6/P7), written to the chunk's
+//                       jagged-diagonal entry buffer; each element's own interior
+//                       nodes are finalised by its thread; (B) node-centric sums of
+//                       the entries in a fixed order fused with the leapfrog update
+//                       of the chunk's interior nodes, partial sums of its shared
+//                       nodes into their slots  (Alg. 1+2+3)
 //  K8  launch_k8        shared nodes: add the slots in ascending chunk order,
-//                       same fused update, write U^{n+1} back into the slots
-//                       (halo copies for the next step)
+//                       same fused update
 //
 // Element stiffness (readings R2, R5): K^e = Grr*Srr + Gss*Sss + Grs*Srs, with
 // S_ab = D_a^T W D_b (+ transpose for rs) from the reference tables: the
@@ -168,6 +170,17 @@ __device__ __forceinline__ int atomic_add_acq_rel(int32_t *p, int v) {
     return old;
 }
 
+// The leapfrog update U^{n+1} = 2 U^n - U^{n-1} + (dt^2/M) (f - (K U^n)) (north_star,
+// reading R1), spelled with explicit roundings so every kernel that finalises a node
+// (K7 element or node phase, K8, the interface and ablation kernels) yields the same bits.
+__device__ __forceinline__ double leap_update(double u, double up, double m, double f, double y) {
+#ifdef SEM_LEAP_PLAIN
+    return 2.0 * u - up + m * (f - y);
+#else
+    return __fma_rn(m, __dsub_rn(f, y), __dsub_rn(__dmul_rn(2.0, u), up));
+#endif
+}
+
 __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepParams &a, int32_t sg, uint16_t cr,
                                               int sl, double u) {
     if (sg >= ch.N_sh - ch.N_if) return;
@@ -183,7 +196,7 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
     for (int j = j0 + 4; j < j1; j++) y += __ldcg(&a.slot[j]);
     const int64_t id = ch.N_int + sg;
     const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
-    a.Uprev[id] = 2.0 * u - a.Uprev[id] + a.dt2M[id] * (f - y);
+    a.Uprev[id] = leap_update(u, a.Uprev[id], a.dt2M[id], f, y);
     a.cnt[sg] = 0;
 }
 
@@ -197,6 +210,9 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
     constexpr int C = B * G;  // consumer threads
+    constexpr int kNI = lattice_n_interior(NP);  // element-interior nodes per element
+    // finalised by the element's thread (P3, P4; at P5 this measured 0.8 % slower, 168 registers)
+    constexpr bool kInnerFin = G == 1 && kNI > 0 && NP < 21;
     extern __shared__ __align__(128) unsigned char sm[];
     // WM: U^{n-1} / dt^2/M windows -- 0 read from global in the node phase, 1 single-buffered
     // TMA window (default), 2 inside the double-buffered stages
@@ -294,6 +310,9 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     }
 
     // ===== consumer warps =====
+    // the Ricker source term of this step (Alg. 3), once per thread instead of inline at every
+    // finalising site (keeps the cold exp() code out of the element and node loops)
+    const double fsrc = a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0);
     int k = 0;
     for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
         const int s = k % kStages;
@@ -303,7 +322,6 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
         const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
         const int i0 = m0.x, nint = m0.y, nsh = m0.w, ne = m1.y, ni_al = m1.z;
-        const int nl = ni_al + nsh;
         const double *u_s = reinterpret_cast<const double *>(st + lay.u);
         const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
         const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
@@ -361,30 +379,49 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 }
             }
         }
+        const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
+        const double *m_s = WIN2 ? reinterpret_cast<const double *>(st + lay.m) : m_w;
+        double *Unew = a.Uprev;
+        // Element-interior nodes (lattice interior of the element, e.g. the P3 centroid) have one
+        // entry, and the chunk builder places them last in the interior segment: the node phase
+        // covers [0, nint - ne * kNI) and each element's thread finalises its own interior nodes
+        // after the barrier (with the U^{n-1} / dt^2/M window); their K U is y_e[p] alone.
+        const int nint_np = nint - (kInnerFin ? ne * kNI : 0);  // interior nodes left to the node phase
         if (G == 1 && t < ne) {
 #pragma unroll
-            for (int p = 0; p < NP; p++) ebuf[lpo[p * B + t]] = y[p];  // straight to the node's CSR run
+            for (int p = 0; p < NP; p++)
+                if (!(kInnerFin && lattice_interior(NP, p))) ebuf[lpo[p * B + t]] = y[p];  // the node's JDS entry
         }
         consumer_sync<C>();
         if (WIN1) MBAR_WAIT_INLINE(wfull, k & 1);  // U^{n-1} / dt^2/M window
-        const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
-        const double *m_s = WIN2 ? reinterpret_cast<const double *>(st + lay.m) : m_w;
+        if (kInnerFin && t < ne) {
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                if (!lattice_interior(NP, p)) continue;
+                const int li = li_s[p * B + t];
+                const int id = i0 + li;
+                const double up = WM == 0 ? a.Uprev[id] : up_s[li];
+                const double m = WM == 0 ? __ldg(a.dt2M + id) : m_s[li];
+                Unew[id] = leap_update(u_s[li], up, m, id == a.src ? fsrc : 0.0, y[p]);
+            }
+        }
         // (B) node-centric gather of K U^n in fixed order + fused update;
-        //     shared nodes: this chunk's partial into the node's slot
-        double *Unew = a.Uprev;
-        for (int i = t; i < nl; i += C) {
+        //     shared nodes: this chunk's partial into the node's slot.  Work item w:
+        //     interior node w < nint_np, else shared node ni_al + (w - nint_np) (skips
+        //     the element-interior nodes and the alignment hole)
+        const int nwork = nint_np + nsh;
+        for (int w = t; w < nwork; w += C) {
+            const int i = w < nint_np ? w : ni_al + (w - nint_np);
             double upg = 0.0, mg = 0.0;
             if (WM == 0 && i < nint) {  // coalesced global loads, issued before the shared-memory sum
                 upg = a.Uprev[i0 + i];
                 mg = __ldg(a.dt2M + i0 + i);
             }
-            if (i >= nint && i < ni_al) continue;  // the alignment hole
             const double yi = i < nint ? jds_sum(ebuf, jd, end0, i) : jds_sum(ebuf, jd + kJdsW, end1, i - ni_al);
             if (i < nint) {
                 const int id = i0 + i;
-                const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
-                Unew[id] = 2.0 * u_s[i] - (WM == 0 ? upg : up_s[i]) + (WM == 0 ? mg : m_s[i]) * (f - yi);
-            } else if (i >= ni_al) {
+                Unew[id] = leap_update(u_s[i], WM == 0 ? upg : up_s[i], WM == 0 ? mg : m_s[i], id == a.src ? fsrc : 0.0, yi);
+            } else {
                 const int j = i - ni_al;
                 const int sl = shs[j];
                 a.slot[sl] = yi;
@@ -415,7 +452,7 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     for (int d = 1; d < 4; d++) y += part[d];
     for (int j = j0 + 4; j < j1; j++) y += a.slot[j];
     const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
-    a.Uprev[id] = 2.0 * u - up + m * (f - y);
+    a.Uprev[id] = leap_update(u, up, m, f, y);
 }
 
 // ---- multi-GPU interface -----------------------------------------
@@ -446,7 +483,7 @@ __global__ void k8_if(const DevChunks ch, const StepParams a, const double *__re
     const int64_t s = ch.N_sh - ch.N_if + i;
     const int64_t id = ch.N_int + s;
     const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
-    a.Uprev[id] = 2.0 * a.U[id] - a.Uprev[id] + a.dt2M[id] * (f - y);
+    a.Uprev[id] = leap_update(a.U[id], a.Uprev[id], a.dt2M[id], f, y);
 }
 
 __global__ void k_mass_if(const DevChunks ch, const double *__restrict__ xbuf, const int32_t *__restrict__ sum_start,
@@ -514,7 +551,7 @@ __global__ void k_abl_update(int64_t n, const StepParams a, double *KU) {
     const double f = (i == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
     const double y = KU[i];
     KU[i] = 0.0;
-    a.Uprev[i] = 2.0 * a.U[i] - a.Uprev[i] + a.dt2M[i] * (f - y);
+    a.Uprev[i] = leap_update(a.U[i], a.Uprev[i], a.dt2M[i], f, y);
 }
 
 // The max-dynamic-smem attribute is per function (process-wide), and several

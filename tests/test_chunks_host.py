@@ -56,3 +56,43 @@ def test_chunk_builder_brute_force(name, scale, P, B):
         assert cm[c, 1] == sum(1 for g in nodes if interior[g])
         assert cm[c, 3] == sum(1 for g in nodes if not interior[g])
         assert cm[c, 6] == cm[c, 1] + (cm[c, 1] & 1)
+
+
+def lattice_interior_positions(P):
+    """Local positions p (lattice order: row j outer, i inner) of the element's own
+    interior nodes: 1 <= i, 1 <= j, i + j <= P - 1."""
+    out, p = [], 0
+    for j in range(P + 1):
+        for i in range(P + 1 - j):
+            if i >= 1 and j >= 1 and i + j <= P - 1:
+                out.append(p)
+            p += 1
+    return out
+
+
+@pytest.mark.parametrize("name,scale,P,B", [("C2", 16, None, 192), ("C3", 40, None, 256), ("B1", 30, 5, 128)])
+def test_element_interior_nodes_close_the_interior_segment(name, scale, P, B):
+    """K7 finalises each element's own interior nodes in the element phase and its node
+    phase covers only the first nint - ne * nI interior ids of a chunk: the builder must
+    place exactly those nodes (one entry each) at the end of every chunk's window, and
+    keep the other interior nodes in descending entry count."""
+    mu, N = reordered_mu(name, scale, P)
+    E, Np = mu.shape
+    deg = int(round((np.sqrt(8 * Np + 1) - 3) / 2))
+    inner_p = lattice_interior_positions(deg)
+    assert len(inner_p) == (deg - 1) * (deg - 2) // 2
+    st = S.sem_debug_chunk_stats(mu, N, B, want_maps=True)
+    int_of, cm = st["int_of"], st["cmeta"]
+    nch = (E + B - 1) // B
+    for c in list(range(0, nch, max(1, nch // 25))) + [nch - 1]:
+        i0, nint, ne = cm[c, 0], cm[c, 1], cm[c, 5]
+        rows = mu[c * B:c * B + ne]
+        inner = rows[:, inner_p].ravel()
+        assert len(np.unique(inner)) == inner.size  # one entry each
+        tail0 = i0 + nint - inner.size
+        assert np.array_equal(np.sort(int_of[inner]), np.arange(tail0, i0 + nint))
+        # the rest of the window: descending entry count
+        ids, cnt = np.unique(rows, return_counts=True)
+        win = (int_of[ids] >= i0) & (int_of[ids] < tail0)
+        order = np.argsort(int_of[ids[win]])
+        assert (np.diff(cnt[win][order]) <= 0).all()
