@@ -40,6 +40,12 @@ constexpr int kThreads = 256;
 #define SEM_KSTAGES 2
 #endif
 constexpr int kStages = SEM_KSTAGES;  // pipeline depth of K7 (A/B: -DSEM_KSTAGES=3)
+// The producer reads the chunk's shared-node ids from a TMA copy in the stage (own
+// mbarrier) instead of one dependent global load per cp.async gather (A/B: -DSEM_K7_IDS_TMA=0)
+#ifndef SEM_K7_IDS_TMA
+#define SEM_K7_IDS_TMA 1
+#endif
+constexpr bool kIdsTma = SEM_K7_IDS_TMA != 0;
 
 // S tables packed densely for the current degree ([p * Np + q]): at P3 the three
 // tables span 2.4 KB of the constant cache instead of rows strided by kMaxNp
@@ -74,7 +80,7 @@ struct StageLayout {
         jds = lpos + np * B * 2;
         shs = jds + Lp * 2;
         shn = shs + Ls * 4;
-        scr = shn + Lf * 4;
+        scr = shn + (kIdsTma ? Ls : Lf) * 4;
         g = scr + Lf * 2;
         meta = g + 3 * B * 8;
         u = meta + 32;
@@ -226,7 +232,8 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     uint64_t *empty = gath + kStages;                                   // consumers done with stage
     uint64_t *wfull = empty + kStages;                                  // U^{n-1}, dt^2/M windows landed
     uint64_t *wempty = wfull + 1;                                       // ... consumed
-    double *S_s = reinterpret_cast<double *>(wempty + 1);               // G > 1: Srr, Sss, Srs [NP][NP]
+    uint64_t *idb = wempty + 1;                                         // shared-node ids landed
+    double *S_s = reinterpret_cast<double *>(idb + kStages);            // G > 1: Srr, Sss, Srs [NP][NP]
     const int t = threadIdx.x;
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
@@ -242,6 +249,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             mbar_init(&full[s], 1);
             mbar_init(&gath[s], 32);
             mbar_init(&empty[s], 1);
+            mbar_init(&idb[s], 1);
         }
         mbar_init(wfull, 1);
         mbar_init(wempty, 1);
@@ -269,8 +277,12 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 reinterpret_cast<int4 *>(st + lay.meta)[1] = m1;
                 const int nsh8 = (nsh + 7) & ~7;
                 const bool fuse = a.cnt != nullptr;
-                const uint32_t bytes = 2 * NP * B * 2 + 2 * kJdsW * 2 + nsh8 * (fuse ? 10 : 4) + 3 * B * 8 +
-                                       (uint32_t)ni_al * (WIN2 ? 24 : 8);
+                const uint32_t bytes = 2 * NP * B * 2 + 2 * kJdsW * 2 + nsh8 * (fuse ? (kIdsTma ? 6 : 10) : 4) +
+                                       3 * B * 8 + (uint32_t)ni_al * (WIN2 ? 24 : 8);
+                if (kIdsTma) {  // first: the ids the gathers below wait for
+                    mbar_arrive_expect_tx(&idb[s], nsh8 * 4);
+                    if (nsh8 > 0) tma_load(st + lay.shn, ch.shl_node + s0, nsh8 * 4, &idb[s]);
+                }
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
                 tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 if (nsh8 > 0) {
                     tma_load(st + lay.shs, ch.shl_slot + s0, nsh8 * 4, &full[s]);
                     if (fuse) {
-                        tma_load(st + lay.shn, ch.shl_node + s0, nsh8 * 4, &full[s]);
+                        if (!kIdsTma) tma_load(st + lay.shn, ch.shl_node + s0, nsh8 * 4, &full[s]);
                         tma_load(st + lay.scr, ch.shl_cr + s0, nsh8 * 2, &full[s]);
                     }
                 }
@@ -293,7 +305,14 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 }
             }
             double *u_sh = reinterpret_cast<double *>(st + lay.u) + ni_al;
-            for (int j = lane; j < nsh; j += 32) cp_async8(u_sh + j, a.U + ch.N_int + ch.shl_node[s0 + j]);
+            if (kIdsTma) {
+                __syncwarp();
+                mbar_wait(&idb[s], (k / kStages) & 1);
+                const int32_t *ids = reinterpret_cast<const int32_t *>(st + lay.shn);
+                for (int j = lane; j < nsh; j += 32) cp_async8(u_sh + j, a.U + ch.N_int + ids[j]);
+            } else {
+                for (int j = lane; j < nsh; j += 32) cp_async8(u_sh + j, a.U + ch.N_int + ch.shl_node[s0 + j]);
+            }
             cp_async_arrive_noinc(&gath[s]);
             // the single U^{n-1} / dt^2/M window buffer: free once the previous
             // chunk's update is done; lands while this chunk's element phase runs
@@ -587,7 +606,7 @@ size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
     const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, wm == 2 ? W : 0);
     const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * np * 8 : 0;
     return (size_t)kStages * lay.size + (size_t)np * B * 8 + (wm == 1 ? 2 * (size_t)W * 8 : 0) +
-           (3 * kStages + 2) * 8 + stab;
+           (4 * kStages + 2) * 8 + stab;
 }
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
