@@ -49,14 +49,19 @@ __constant__ double h_Srs[kMaxNp * kMaxNp];
 __constant__ double h_wK[kMaxNp];
 
 // Shared-memory layout of one stage (offsets 16-byte aligned).
+// The producer reads the gathers' shared-node ids from a TMA copy in the stage at P >= 5
+// (B1 Heun P5 1.102 -> 1.045 ms); at P2/P3 the dependent global loads measured 0.7 % faster.
+__host__ __device__ constexpr bool ids_tma(int np) { return np > 10; }
+
 struct HeunLayout {
-    int lidx, lpos, jds, shs, g, meta, u, w, size;
+    int lidx, lpos, jds, shs, shn, g, meta, u, w, size;
     __host__ __device__ HeunLayout(int np, int B, int L, int Lp, int Ls) {
         lidx = 0;
         lpos = np * B * 2;
         jds = lpos + np * B * 2;
         shs = jds + Lp * 2;
-        g = shs + Ls * 4;
+        shn = shs + Ls * 4;  // P >= 5: the shared-node ids of the producer's gathers (TMA, own mbarrier)
+        g = shn + (ids_tma(np) ? Ls * 4 : 0);
         meta = g + 5 * B * 8;
         u = meta + 32;
         w = u + L * 8;
@@ -98,6 +103,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
     uint64_t *empty = gath + kStagesH;
     uint64_t *wfull = empty + kStagesH;
     uint64_t *wempty = wfull + 1;
+    uint64_t *idb = wempty + 1;  // shared-node ids landed
     const int t = threadIdx.x;
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             mbar_init(&full[s], 1);
             mbar_init(&gath[s], 32);
             mbar_init(&empty[s], 1);
+            mbar_init(&idb[s], 1);
         }
         mbar_init(wfull, 1);
         mbar_init(wempty, 1);
@@ -133,6 +140,10 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                 uint32_t bytes = NP * B * 2 + 5 * B * 8;
                 if (kStep) bytes += NP * B * 2 + 2 * kJdsW * 2 + nsh4 * 4 + (uint32_t)ni_al * 8;
                 if (kLag) bytes += (uint32_t)ni_al * 8;
+                if (ids_tma(NP)) {  // first: the ids the gathers wait for
+                    mbar_arrive_expect_tx(&idb[s], nsh4 * 4);
+                    if (nsh4 > 0) tma_load(st + lay.shn, ch.shl_node + s0, nsh4 * 4, &idb[s]);
+                }
                 mbar_arrive_expect_tx(&full[s], bytes);
                 const int64_t e0 = c * B;
                 tma_load(st + lay.lidx, ch.lidx + e0 * NP, NP * B * 2, &full[s]);
@@ -147,8 +158,13 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             }
             double *u_sh = reinterpret_cast<double *>(st + lay.u) + ni_al;
             double *w_sh = reinterpret_cast<double *>(st + lay.w) + ni_al;
+            const int32_t *ids = ids_tma(NP) ? reinterpret_cast<const int32_t *>(st + lay.shn) : ch.shl_node + s0;
+            if (ids_tma(NP)) {
+                __syncwarp();
+                mbar_wait(&idb[s], (k / kStagesH) & 1);
+            }
             for (int j = lane; j < nsh; j += 32) {
-                const int64_t g = ch.N_int + ch.shl_node[s0 + j];
+                const int64_t g = ch.N_int + ids[j];
                 if (kStep) cp_async8(u_sh + j, a.U + g);
                 if (kLag) cp_async8(w_sh + j, a.W + g);
             }
@@ -369,7 +385,7 @@ cudaError_t set_smem_h(K kernel, size_t bytes) {
 size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
     const HeunLayout lay(np, B, L, Lp, Ls);
     const bool step = mode <= 1;
-    return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (3 * kStagesH + 2) * 8;
+    return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8;
 }
 
 using HFn = void (*)(const DevChunks, const HeunParams, int, int, int, int, const int32_t *, int64_t);
