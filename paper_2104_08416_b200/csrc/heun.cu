@@ -87,6 +87,15 @@ __device__ __forceinline__ double src_term(const HeunParams &a, int64_t id, int6
     return (id == a.src) ? a.amp * ricker_dev((double)n * a.h, a.f0, a.t0) : 0.0;
 }
 
+// The Heun update of a node from its assembled (R(V), K U) = (r, y) (PAPER.md:269-291,
+// reading R19): W = U + hM (r + f^n), U' = U + hM ((2 r - h y) + (f^n + f^{n+1})), spelled
+// with explicit roundings so every kernel that finalises a node yields the same bits.
+__device__ __forceinline__ void heun_update(double u0, double hm, double r, double y, double yn, double yn1,
+                                            double h, double &w_out, double &u_out) {
+    w_out = __fma_rn(hm, __dadd_rn(r, yn), u0);
+    u_out = __fma_rn(hm, __dadd_rn(__fma_rn(-h, y, __dmul_rn(2.0, r)), __dadd_rn(yn, yn1)), u0);
+}
+
 // MODE 0: step with V^n stored (no lag); 1: step with V lagged by one W
 // update; 2: finalise V only.
 template <int NP, int B, int MODE>
@@ -179,6 +188,12 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
     }
 
     // ===== consumer warps =====
+    // the source terms f^n, f^{n+1} of this step, once per thread (cold exp() code out of the loops)
+    const double f_n = src_term(a, a.src, a.n), f_n1 = src_term(a, a.src, a.n + 1);
+    // each element's own interior nodes (one entry each, last in the interior segment:
+    // chunk builders) are finalised by the element's thread; the node phase skips them
+    // (P3; at P5 this measured 4 % slower at the 168-register cap, as in K7)
+    constexpr int kNI = NP < 21 ? lattice_n_interior(NP) : 0;
     int k = 0;
     for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
         const int64_t c = list ? list[pos] : pos;
@@ -224,6 +239,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
         if (kStep) {
             const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
             const uint16_t *jd = reinterpret_cast<const uint16_t *>(st + lay.jds);
+            double rin[NP], yin[NP];  // element-interior rows (registers only at those p)
             const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
             const double *u_s = reinterpret_cast<const double *>(st + lay.u);
             if (t < ne) {
@@ -241,14 +257,14 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                 // stays in registers and the pair is stored with one 16-byte store
                 constexpr bool kSplit = NP > 10;
                 double *eb = reinterpret_cast<double *>(ebuf);
-                double r[kSplit ? 1 : NP];
+                double r[NP];  // at P5 only the element-interior rows stay in registers
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
                     double acc = 0.0;
 #pragma unroll
                     for (int q = 0; q < NP; q++) acc = fma(h_Dr[q * NP + p], ar[q], fma(h_Ds[q * NP + p], as[q], acc));
-                    if (kSplit) eb[2 * lpo[p * B + t]] = acc;
-                    else r[kSplit ? 0 : p] = acc;
+                    if (kSplit && !(kNI > 0 && lattice_interior(NP, p))) eb[2 * lpo[p * B + t]] = acc;
+                    else r[p] = acc;
                 }
                 // (3) y = K^e u, K^e = Grr Srr + Gss Sss + Grs Srs, G = sd F F^T
                 //     (= c^2 detJ J^-1 J^-T, reading R5)
@@ -273,24 +289,40 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                 }
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
-                    if (kSplit) eb[2 * lpo[p * B + t] + 1] = y[p];
-                    else ebuf[lpo[p * B + t]] = make_double2(r[kSplit ? 0 : p], y[p]);
+                    if (kNI > 0 && lattice_interior(NP, p)) {
+                        rin[p] = r[p];
+                        yin[p] = y[p];
+                    } else if (kSplit) {
+                        eb[2 * lpo[p * B + t] + 1] = y[p];
+                    } else {
+                        ebuf[lpo[p * B + t]] = make_double2(r[p], y[p]);
+                    }
                 }
             }
             consumer_sync<B>();
             mbar_wait(wfull, k & 1);
+            if (kNI > 0 && t < ne) {
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    if (!lattice_interior(NP, p)) continue;
+                    const int li = li_s[p * B + t];
+                    const int64_t id = i0 + li;
+                    const bool src = id == a.src;
+                    heun_update(u_s[li], m_s[li], rin[p], yin[p], src ? f_n : 0.0, src ? f_n1 : 0.0, a.h, a.W[id],
+                                a.U[id]);
+                }
+            }
             // (4) node-centric reduction in fixed (JDS diagonal) order + fused Heun update
-            const int nl = ni_al + nsh;
-            for (int i = t; i < nl; i += B) {
-                if (i >= nint && i < ni_al) continue;  // the alignment hole
+            const int nint_np = nint - ne * kNI;  // interior nodes left to the node phase
+            const int nwork = nint_np + nsh;
+            for (int w = t; w < nwork; w += B) {
+                const int i = w < nint_np ? w : ni_al + (w - nint_np);  // skips the element-interior nodes and the hole
                 const double2 ab = i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al);
                 if (i < nint) {
                     const int64_t id = i0 + i;
-                    const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
-                    const double u0 = u_s[i], hm = m_s[i];
-                    a.W[id] = u0 + hm * (ab.x + yn);
-                    a.U[id] = u0 + hm * ((2.0 * ab.x - a.h * ab.y) + (yn + yn1));
-                } else if (i >= ni_al) {
+                    const bool src = id == a.src;
+                    heun_update(u_s[i], m_s[i], ab.x, ab.y, src ? f_n : 0.0, src ? f_n1 : 0.0, a.h, a.W[id], a.U[id]);
+                } else {
                     reinterpret_cast<double2 *>(a.slot)[shs[i - ni_al]] = ab;
                 }
             }
@@ -319,8 +351,7 @@ __global__ void k_heun_fix(const DevChunks ch, const HeunParams a) {
     for (int d = 1; d < 4; d++) { ab.x += part[d].x; ab.y += part[d].y; }
     for (int j = j0 + 4; j < j1; j++) { ab.x += sl[j].x; ab.y += sl[j].y; }
     const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
-    a.W[id] = u0 + hm * (ab.x + yn);
-    a.U[id] = u0 + hm * ((2.0 * ab.x - a.h * ab.y) + (yn + yn1));
+    heun_update(u0, hm, ab.x, ab.y, yn, yn1, a.h, a.W[id], a.U[id]);
 }
 
 // Per element (new order, padded): F = c^2 J^-1 (F[jh][j] = c^2 (J^-1)_{jh j}),
@@ -492,8 +523,7 @@ __global__ void k_heun_if(const DevChunks ch, const HeunParams a, const double2 
     const int64_t id = ch.N_int + ch.N_sh - ch.N_if + i;
     const double u0 = a.U[id], hm = a.hM[id];
     const double yn = src_term(a, id, a.n), yn1 = src_term(a, id, a.n + 1);
-    a.W[id] = u0 + hm * (ab.x + yn);
-    a.U[id] = u0 + hm * ((2.0 * ab.x - a.h * ab.y) + (yn + yn1));
+    heun_update(u0, hm, ab.x, ab.y, yn, yn1, a.h, a.W[id], a.U[id]);
 }
 
 cudaError_t launch_heun_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
