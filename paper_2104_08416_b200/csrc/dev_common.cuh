@@ -81,4 +81,10 @@ __device__ __forceinline__ void consumer_sync() {
 }
 
 }  // namespace
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream start its
+// prologue now / wait until the preceding kernel has completed and its writes are visible.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace sem

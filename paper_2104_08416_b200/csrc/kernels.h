@@ -144,12 +144,14 @@ int k7_grid(const DevChunks &ch, bool fused);
 // resident K7 CTAs per SM for chunks of B elements with these per-chunk maxima (shared-memory stages)
 int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused);
 // device step counter of the graph-captured step loop: += 1, = v
-cudaError_t launch_step_inc(int64_t *n, cudaStream_t s);
+// pdl: programmatic dependent launch (the graph-captured step loop, SEM_PDL): the kernel may
+// start while its predecessor drains and waits in griddepcontrol.wait before any data access
+cudaError_t launch_step_inc(int64_t *n, cudaStream_t s, bool pdl = false);
 cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s);
 // K7 over all chunks (list == nullptr) or over the chunk ids list[0..nlist).
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
-                      const int32_t *list = nullptr, int64_t nlist = 0);
-cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s);
+                      const int32_t *list = nullptr, int64_t nlist = 0, bool pdl = false);
+cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s, bool pdl = false);
 // Multi-GPU interface: local partials (+ pack per neighbour), then the
 // rank-ordered sum and update (step) or dt^2/M (mass).
 cudaError_t launch_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,

@@ -59,7 +59,11 @@ __constant__ double c_wM[kMaxNp];
 // launch argument
 __device__ __forceinline__ int64_t step_index(const StepParams &a) { return a.n_dev ? *a.n_dev : a.n; }
 
-__global__ void k_step_inc(int64_t *n) { *n += 1; }
+__global__ void k_step_inc(int64_t *n) {
+    pdl_trigger();
+    pdl_wait();
+    *n += 1;
+}
 __global__ void k_step_set(int64_t *n, int64_t v) { *n = v; }
 
 inline unsigned blocks_for(int64_t n, int threads = kThreads) {
@@ -236,6 +240,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     double *S_s = reinterpret_cast<double *>(idb + kStages);            // G > 1: Srr, Sss, Srs [NP][NP]
     const int t = threadIdx.x;
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
+    pdl_trigger();  // the next kernel (K8) may be scheduled; it waits for this grid to complete
 
     if (G > 1) {
         for (int i = t; i < NP * NP; i += blockDim.x) {
@@ -256,6 +261,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();  // graph step loop: the previous step's K8 / step counter are complete
 
     if (t >= C) {
         // ===== producer warp =====
@@ -458,6 +464,8 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
 
 // ---- K8: shared-node fix-up --------------------------------------------------
 __global__ void k8_fix(const DevChunks ch, const StepParams a) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh - ch.N_if) return;  // interface nodes: k_if_partial / k8_if
     const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
@@ -708,8 +716,24 @@ int k7_grid(const DevChunks &ch, bool fused) {
     return (int)g;
 }
 
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*fn)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, bool pdl,
+                      Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, args...);
+}
+
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
-                      const int32_t *list, int64_t nlist) {
+                      const int32_t *list, int64_t nlist, bool pdl) {
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
     if (grid > n) grid = (int)n;
@@ -717,15 +741,13 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
     const K7Fn fn = k7_fn(ch.Np, ch.B);
     cudaError_t e = set_smem(fn, smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, ch.B * k7_group(ch.Np) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list,
-                                                       nlist);
-    return cudaGetLastError();
+    return launch_ex(fn, (unsigned)grid, ch.B * k7_group(ch.Np) + 32, smem, s, pdl, ch, p, ch.max_local, ch.max_win,
+                     2 * kJdsW, ch.max_nsh, list, nlist);
 }
 
-cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s) {
+cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s, bool pdl) {
     if (ch.N_sh - ch.N_if == 0) return cudaSuccess;
-    k8_fix<<<blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s>>>(ch, p);
-    return cudaGetLastError();
+    return launch_ex(k8_fix, blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s, pdl, ch, p);
 }
 
 cudaError_t launch_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
@@ -769,9 +791,8 @@ cudaError_t launch_abl_update(int64_t n, const StepParams &p, double *KU, cudaSt
     return cudaGetLastError();
 }
 
-cudaError_t launch_step_inc(int64_t *n, cudaStream_t s) {
-    k_step_inc<<<1, 1, 0, s>>>(n);
-    return cudaGetLastError();
+cudaError_t launch_step_inc(int64_t *n, cudaStream_t s, bool pdl) {
+    return launch_ex(k_step_inc, 1, 1, 0, s, pdl, n);
 }
 
 cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s) {
