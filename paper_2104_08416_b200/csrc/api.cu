@@ -941,9 +941,6 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
     if (n_elements * Np >= (int64_t)INT_MAX || n_vertices >= INT_MAX)
         return fail(ctx, SEM_E_ARG, "mesh too large for 32-bit indices");
     if (n_elements < ctx->world) return fail(ctx, SEM_E_ARG, "fewer elements than ranks");
-    for (int64_t i = 0; i < 3 * n_elements; i++)
-        if (tri_host[i] < 0 || tri_host[i] >= n_vertices)
-            return fail(ctx, SEM_E_MESH, "element " + std::to_string(i / 3) + " has a vertex id out of range");
     try {
         CK(cudaSetDevice(ctx->device));
         reset_mesh(ctx);
@@ -962,15 +959,17 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(cudaMemcpyAsync(ctx->d_vxy, vxy_host, sizeof(double) * 2 * nv, cudaMemcpyHostToDevice, s));
         int32_t *d_tri = nullptr, *d_bad = nullptr;
         CK(dalloc(tmp, &d_tri, 3 * E));
-        CK(dalloc(tmp, &d_bad, 1));
+        CK(dalloc(tmp, &d_bad, 2));  // zero-area element, vertex id out of range (checked on the GPU)
         CK(cudaMemcpyAsync(d_tri, tri_host, sizeof(int32_t) * 3 * E, cudaMemcpyHostToDevice, s));
         CK(dalloc(ctx->mesh_allocs, &ctx->d_tri_or, 3 * E));
-        CK(launch_fill_i32(d_bad, 1, INT_MAX, s));
-        CK(launch_orient(ctx->d_vxy, d_tri, E, ctx->d_tri_or, d_bad, s));
-        int32_t bad = 0;
-        CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(launch_fill_i32(d_bad, 2, INT_MAX, s));
+        CK(launch_orient(ctx->d_vxy, d_tri, E, nv, ctx->d_tri_or, d_bad, s));
+        int32_t bad[2] = {0, 0};
+        CK(cudaMemcpyAsync(bad, d_bad, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        if (bad != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad) + " has zero area");
+        if (bad[1] != INT_MAX)
+            return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad[1]) + " has a vertex id out of range");
+        if (bad[0] != INT_MAX) return fail(ctx, SEM_E_MESH, "element " + std::to_string(bad[0]) + " has zero area");
         tr.mark(s, "H2D + orientation");
 
         // ---- canonical SEM nodes (reading R13) ----

@@ -15,8 +15,9 @@ namespace sem {
 // ----------------------------- reorder.cu ---------------------------------
 // Vertex bounding box {xmin, ymin, xmax, ymax} -> out4 (device).
 cudaError_t launch_bbox(const double *vxy, int64_t nv, double *out4, cudaStream_t s);
-// Orientation fix (det < 0 -> swap v1,v2); *bad = min element with det == 0.
-cudaError_t launch_orient(const double *vxy, const int32_t *tri, int64_t E, int32_t *tri_or,
+// Orientation fix (det < 0 -> swap v1,v2); bad[0] = min element with det == 0, bad[1] = min
+// element with a vertex id outside [0, nv) (both INT_MAX when none).
+cudaError_t launch_orient(const double *vxy, const int32_t *tri, int64_t E, int64_t nv, int32_t *tri_or,
                           int32_t *bad, cudaStream_t s);
 // K1: generalized-Hilbert key of every element's centroid cell.
 cudaError_t launch_hilbert_keys(const double *vxy, const int32_t *tri, int64_t E, double xm0,

@@ -115,11 +115,15 @@ __global__ void k_bbox_final(const double *part, int nb, double *out) {
     for (int k = 0; k < 4; k++) out[k] = r[k];
 }
 
-__global__ void k_orient(const double *__restrict__ vxy, const int32_t *__restrict__ tri, int64_t E,
+__global__ void k_orient(const double *__restrict__ vxy, const int32_t *__restrict__ tri, int64_t E, int64_t nv,
                          int32_t *__restrict__ tri_or, int32_t *bad) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= E) return;
     const int32_t v0 = tri[3 * e], v1 = tri[3 * e + 1], v2 = tri[3 * e + 2];
+    if (v0 < 0 || v0 >= nv || v1 < 0 || v1 >= nv || v2 < 0 || v2 >= nv) {  // before any vertex access
+        atomicMin(bad + 1, (int32_t)e);
+        return;
+    }
     const double x0 = vxy[2 * v0], y0 = vxy[2 * v0 + 1];
     const double x1 = vxy[2 * v1], y1 = vxy[2 * v1 + 1];
     const double x2 = vxy[2 * v2], y2 = vxy[2 * v2 + 1];
@@ -480,9 +484,9 @@ cudaError_t launch_bbox(const double *vxy, int64_t nv, double *out4, cudaStream_
     return cudaGetLastError();
 }
 
-cudaError_t launch_orient(const double *vxy, const int32_t *tri, int64_t E, int32_t *tri_or,
+cudaError_t launch_orient(const double *vxy, const int32_t *tri, int64_t E, int64_t nv, int32_t *tri_or,
                           int32_t *bad, cudaStream_t s) {
-    k_orient<<<blocks_for(E), kThreads, 0, s>>>(vxy, tri, E, tri_or, bad);
+    k_orient<<<blocks_for(E), kThreads, 0, s>>>(vxy, tri, E, nv, tri_or, bad);
     return cudaGetLastError();
 }
 

@@ -200,6 +200,13 @@ def test_errors(ctx):
     with pytest.raises(S.SemError) as e:
         ctx.sem_mesh_reorder(bad, m.tri, 2)
     assert e.value.status == S.SEM_E_MESH and "zero area" in e.value.msg
+    for v in (m.nv, -1, 2**31 - 1):  # vertex ids outside [0, V): checked on the GPU before any access
+        tri = m.tri.copy()
+        tri[7, 1] = v
+        tri[9, 2] = v
+        with pytest.raises(S.SemError) as e:
+            ctx.sem_mesh_reorder(m.vxy, tri, 2)
+        assert e.value.status == S.SEM_E_MESH and "element 7 has a vertex id out of range" in e.value.msg
     ctx.sem_mesh_reorder(m.vxy, m.tri, 2)
     with pytest.raises(S.SemError) as e:
         ctx.sem_step_n(1)
