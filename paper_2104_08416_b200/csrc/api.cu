@@ -26,27 +26,15 @@ using namespace sem;
 namespace {
 int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 
-// Elements per chunk (one CTA iteration of K7). SEM_CHUNK=128|192|256|512 forces a compiled
-// variant (design experiments); otherwise the leapfrog at P2/P3 first tries 192 and
-// chunk_fallback() may move it to 256.
+// Elements per chunk (one CTA iteration of K7): 256 at P2/P3 (128 for Heun); SEM_CHUNK=128|192|512
+// selects the other compiled variants (design experiments, chunk size).
 int chunk_elems(int P, bool heun) {
     const char *v = getenv("SEM_CHUNK");
     if (P == 4 || P == 5) return 128;  // shared-memory budget of the stage at 15 / 21 nodes per element
     if (P == 6 || P == 7) return 64;   // ... and at 28 / 36
     // Heun (integrator selected before sem_mesh_reorder): 128 runs 2 CTAs per SM
-    const int b = v ? atoi(v) : (heun ? 128 : 192);
+    const int b = v ? atoi(v) : (heun ? 128 : 256);
     return (b == 128 || b == 192 || b == 512) ? b : 256;
-}
-
-// K7's stages are sized by per-chunk maxima (local nodes, window, shared nodes), so its
-// occupancy depends on the mesh: a graded mesh has outlier chunks. Chunks of 192 are kept
-// when K7 then holds at least as many resident elements per SM as chunks of 256 do at
-// 2 CTAs per SM (C4: 3 x 192 = 576); otherwise (C3: 2 x 192 = 384) the chunks are rebuilt
-// at 256 (chunk size). Returns the size to rebuild at, or 0.
-int chunk_fallback(int P, bool heun, const ChunkMeta &m) {
-    if (getenv("SEM_CHUNK") || heun || P > 3 || m.B != 192) return 0;
-    const int occ = k7_ctas_per_sm(m.Np, m.B, m.max_local, m.max_win, m.max_nsh, false);
-    return occ * m.B < 2 * 256 ? 256 : 0;
 }
 
 // ---- NCCL through dlopen (no link-time dependency; torch's copy is reused) ----
@@ -1158,38 +1146,27 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         tr.mark(s, "partition");
 
         // ---- chunk metadata for the step kernel ----
-        const bool heun = ctx->integrator == SEM_INTEGRATOR_HEUN;
-        int B_chunk = chunk_elems(degree, heun);
+        const int B_chunk = chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN);
         ChunkMeta m;
         DevChunks &d = ctx->dch;
-        for (int attempt = 0;; attempt++) {
-            const size_t n_alloc = L.size();
-            if (gpu_chunks) {
-                CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, B_chunk,
-                                    one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd,
-                                    &ctx->d_intc, err, s));
-                if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
-                if (check_chunks) {
-                    ChunkMeta h;
-                    if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, h,
-                                      err, one ? nullptr : part.remote.data()))
-                        return fail(ctx, SEM_E_MESH, err);
-                    const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
-                    if (!diff.empty())
-                        return fail(ctx, SEM_E_MESH, "GPU chunk builder differs from the host's: " + diff);
-                }
-            } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m,
-                                     err, one ? nullptr : part.remote.data())) {
-                return fail(ctx, SEM_E_MESH, err);
-            }
-            const int again = attempt == 0 ? chunk_fallback(degree, heun, m) : 0;
-            if (!again) break;
-            L.release_from(n_alloc);  // drop this build's device arrays and rebuild
-            B_chunk = again;
-        }
         if (gpu_chunks) {
+            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, B_chunk,
+                                one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd, &ctx->d_intc,
+                                err, s));
+            if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
+            if (check_chunks) {
+                ChunkMeta h;
+                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, h,
+                                  err, one ? nullptr : part.remote.data()))
+                    return fail(ctx, SEM_E_MESH, err);
+                const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
+                if (!diff.empty()) return fail(ctx, SEM_E_MESH, "GPU chunk builder differs from the host's: " + diff);
+            }
             std::vector<int32_t>().swap(mu_h);
             tr.mark(s, "chunk builder (GPU)");
+        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m,
+                                 err, one ? nullptr : part.remote.data())) {
+            return fail(ctx, SEM_E_MESH, err);
         }
         if (!gpu_chunks) {
             if (ctx->scatter != SEM_SCATTER_CHUNK) ST(prepare_ablation(ctx, mu_h, E, Np, N, degree, one, m, s));
