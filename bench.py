@@ -193,9 +193,10 @@ def run_ours(args):
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    # per-kernel CUDA events for the roofline: a second pass with launch-by-launch timing
+    # per-kernel CUDA events for the roofline: a second pass through the same CUDA-graph step
+    # loop, captured with event-record nodes around every K7 and K8 (whole replays of 32 steps)
     ctx.sem_set_kernel_timing(True)
-    ctx.sem_step_n(min(args.steps, 400))
+    ctx.sem_step_n(max(32, min(args.steps, 400) // 32 * 32))
     kt = ctx.sem_kernel_times()
     ctx.sem_set_kernel_timing(False)
     clk = clocks.stop()

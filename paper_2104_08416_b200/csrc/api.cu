@@ -134,6 +134,10 @@ struct sem_ctx {
     double *d_slot = nullptr;
     int32_t *d_cnt = nullptr;  // shared-node arrival counters (K8 fused into K7, SEM_FUSE_K8=1)
     cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};  // captured step loop per U parity
+    // kernel timing inside the graph: the same step loop with event-record nodes around K7 and
+    // K8 of every step (gev[3 j .. 3 j + 2] = before K7, after K7, after K8 of step j)
+    cudaGraphExec_t graph_exec_t[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> gev;
     int64_t *d_nstep = nullptr;                          // its device step counter
     bool fuse_k8 = false;      // measured slower: off by default
     int cur = 0;
@@ -506,21 +510,27 @@ constexpr int kGraphSteps = 32;
 
 bool graph_ok(sem_ctx *ctx) {
     static const bool env_off = getenv("SEM_GRAPH") && atoi(getenv("SEM_GRAPH")) == 0;
-    return !env_off && ctx->world == 1 && !ctx->timing && ctx->stream != nullptr &&
+    return !env_off && ctx->world == 1 && ctx->stream != nullptr &&
            ctx->ops_integrator == SEM_INTEGRATOR_LEAPFROG && ctx->mesh_scatter == SEM_SCATTER_CHUNK &&
            ctx->d_cnt == nullptr;
 }
 
 void destroy_graphs(sem_ctx *ctx) {
-    for (auto &g : ctx->graph_exec)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (auto *set : {ctx->graph_exec, ctx->graph_exec_t})
+        for (int i = 0; i < 2; i++)
+            if (set[i]) { cudaGraphExecDestroy(set[i]); set[i] = nullptr; }
 }
 
 sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
     CK(cudaSetDevice(ctx->device));
     ST(ensure_tables(ctx));
     cudaStream_t s = ctx->stream;
-    cudaGraphExec_t &ex = ctx->graph_exec[ctx->cur];
+    const bool timed = ctx->timing;
+    cudaGraphExec_t &ex = (timed ? ctx->graph_exec_t : ctx->graph_exec)[ctx->cur];
+    if (timed && ctx->gev.empty()) {
+        ctx->gev.resize(3 * kGraphSteps);
+        for (auto &e : ctx->gev) CK(cudaEventCreate(&e));
+    }
     if (!ex) {
         if (!ctx->d_nstep) CK(dalloc(ctx->ops_allocs, &ctx->d_nstep, 1));
         // one ordinary step's worth of attribute setting happens outside the capture
@@ -537,8 +547,11 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
             p.U = ctx->d_U[(ctx->cur + k) & 1];
             p.Uprev = ctx->d_U[1 - ((ctx->cur + k) & 1)];
             p.n_dev = ctx->d_nstep;
-            e = launch_k7(ctx->dch, p, ctx->k7_grid, s, nullptr, 0, pdl);
+            if (timed) e = cudaEventRecordWithFlags(ctx->gev[3 * k], s, cudaEventRecordExternal);
+            if (e == cudaSuccess) e = launch_k7(ctx->dch, p, ctx->k7_grid, s, nullptr, 0, pdl);
+            if (e == cudaSuccess && timed) e = cudaEventRecordWithFlags(ctx->gev[3 * k + 1], s, cudaEventRecordExternal);
             if (e == cudaSuccess) e = launch_k8(ctx->dch, p, s, pdl);
+            if (e == cudaSuccess && timed) e = cudaEventRecordWithFlags(ctx->gev[3 * k + 2], s, cudaEventRecordExternal);
             if (e == cudaSuccess) e = launch_step_inc(ctx->d_nstep, s, pdl);
         }
         cudaError_t e2 = cudaStreamEndCapture(s, &g);
@@ -549,7 +562,21 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
     }
     CK(launch_step_set(ctx->d_nstep, ctx->step, s));
-    for (int64_t r = 0; r < reps; r++) CK(cudaGraphLaunch(ex, s));
+    for (int64_t r = 0; r < reps; r++) {
+        CK(cudaGraphLaunch(ex, s));
+        if (timed) {  // read this replay's per-step kernel times before the next replay re-records them
+            ST(drain_events(ctx));
+            const bool k8 = ctx->dch.N_sh - ctx->dch.N_if > 0;
+            for (int j = 0; j < kGraphSteps; j++) {
+                float a = 0, b = 0;
+                CK(cudaEventElapsedTime(&a, ctx->gev[3 * j], ctx->gev[3 * j + 1]));
+                CK(cudaEventElapsedTime(&b, ctx->gev[3 * j + 1], ctx->gev[3 * j + 2]));
+                ctx->t7 += a;
+                ctx->n7++;
+                if (k8) { ctx->t8 += b; ctx->n8++; }
+            }
+        }
+    }
     ctx->step += reps * kGraphSteps;
     return SEM_OK;
 }
@@ -896,6 +923,7 @@ void sem_free(sem_ctx *ctx) {
     reset_mesh(ctx);
     for (auto *lst : {&ctx->ev7, &ctx->ev8, &ctx->pool})
         for (auto &ev : *lst) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    for (cudaEvent_t e : ctx->gev) cudaEventDestroy(e);
     if (ctx->xev) cudaEventDestroy(ctx->xev);
     if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
     if (ctx->ev_exchanged) cudaEventDestroy(ctx->ev_exchanged);
