@@ -184,7 +184,9 @@ sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t 
  * Enqueued on the context stream; returns without synchronising.  With one
  * rank (leapfrog, chunk scatter, kernel timing off) whole blocks of 32 steps
  * replay a captured CUDA graph (step index in a device counter); the
- * environment variable SEM_GRAPH=0 disables it.
+ * environment variable SEM_GRAPH=0 disables it.  n_steps = 0 advances nothing
+ * but captures that graph for the current U parity (a warm-up that keeps the
+ * capture out of a later timed call).
  * Errors: SEM_E_STATE (no operators), SEM_E_ARG (n_steps < 0), SEM_E_CUDA.
  */
 sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps);

@@ -561,6 +561,7 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
     }
+    if (reps == 0) return SEM_OK;
     CK(launch_step_set(ctx->d_nstep, ctx->step, s));
     for (int64_t r = 0; r < reps; r++) {
         CK(cudaGraphLaunch(ex, s));
@@ -1311,6 +1312,7 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
         return SEM_OK;
     }
     int64_t k = 0;
+    if (n_steps == 0 && graph_ok(ctx)) return graph_steps(ctx, 0);  // capture only (warm-up)
     if (graph_ok(ctx) && n_steps >= kGraphSteps) {
         const int64_t reps = n_steps / kGraphSteps;
         ST(graph_steps(ctx, reps));

@@ -269,29 +269,62 @@ def test_full_size_bench_configuration(ctx, name):
     assert rel_l2(Ug, Uo) <= REL_L2, rel_l2(Ug, Uo)
 
 
-def test_graph_step_loop_bitwise_equal(monkeypatch):
+_GRAPH_CHILD = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2104_08416_b200 import meshgen as mg, sem as S
+pb = mg.config("C2", 16)
+pb = mg.Problem(**{{**pb.__dict__, "t0": 10 * pb.dt, "f0": 1.0 / (8 * pb.dt)}})
+m = pb.mesh
+with S.SemContext(0) as c:
+    c.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+    c.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+    for n in (70, 3, 77):
+        c.sem_step_n(n)
+    U, n = c.sem_read_field()
+    assert n == 150
+    np.save({out!r}, U)
+"""
+
+
+def test_graph_step_loop_bitwise_equal(tmp_path):
     """The CUDA-graph step loop (32 captured steps per replay, device step
-    counter) gives the same bits as launching step by step, and matches the
-    oracle; mixed with plain steps and timing on/off across calls."""
+    counter) gives the same bits as launching step by step (SEM_GRAPH=0, read once
+    per process: a child process), with and without the kernel-timing events in
+    the graph and with a capture-only sem_step_n(0), and matches the oracle."""
+    import subprocess
+    import sys
     pb = mg.config("C2", 16)
     pb = mg.Problem(**{**pb.__dict__, "t0": 10 * pb.dt, "f0": 1.0 / (8 * pb.dt)})
     m = pb.mesh
     o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
     Uo, _ = o.leapfrog(pb.dt, 150, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0)
     out = []
-    for graph in ("1", "0"):
-        monkeypatch.setenv("SEM_GRAPH", graph)
-        with S.SemContext(0) as c:  # graph_ok reads SEM_GRAPH once per process: use the timing switch too
+    for timing in (False, True):
+        with S.SemContext(0) as c:
             c.sem_mesh_reorder(m.vxy, m.tri, pb.P)
             c.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
-            c.sem_set_kernel_timing(graph == "0")  # timing forces the plain launch path
+            c.sem_step_n(0)    # capture only: advances nothing
+            assert c.sem_read_field()[1] == 0
+            c.sem_set_kernel_timing(timing)  # timing: the graph with event-record nodes
             c.sem_step_n(70)   # 2 graph replays + 6 plain steps
             c.sem_step_n(3)
             c.sem_step_n(77)   # odd parity at entry: the other captured graph
             U, n = c.sem_read_field()
             assert n == 150
+            if timing:
+                kt = c.sem_kernel_times()
+                assert kt["k7_launches"] == 150 and kt["k7_ms"] > 0
             out.append(U)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    f = str(tmp_path / "plain.npy")
+    env = dict(os.environ, SEM_GRAPH="0")
+    r = subprocess.run([sys.executable, "-c", _GRAPH_CHILD.format(root=root, out=f)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out.append(np.load(f))
     assert np.array_equal(out[0], out[1])
+    assert np.array_equal(out[0], out[2])
     assert rel_l2(out[0], Uo) <= REL_L2
 
 
