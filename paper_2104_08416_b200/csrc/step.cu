@@ -747,7 +747,14 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
 
 cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s, bool pdl) {
     if (ch.N_sh - ch.N_if == 0) return cudaSuccess;
-    return launch_ex(k8_fix, blocks_for(ch.N_sh - ch.N_if), kThreads, 0, s, pdl, ch, p);
+    // threads per K8 block: 128 (C4 K8 0.0403 -> 0.0393 ms against 256; 64: 0.0655, 512: 0.0410,
+    // 1024: 0.0533 ms); SEM_K8_THREADS overrides (A/B)
+    static const int bt = [] {
+        const char *v = getenv("SEM_K8_THREADS");
+        const int b = v ? atoi(v) : 128;
+        return (b == 64 || b == 128 || b == 256 || b == 512 || b == 1024) ? b : 128;
+    }();
+    return launch_ex(k8_fix, blocks_for(ch.N_sh - ch.N_if, bt), (unsigned)bt, 0, s, pdl, ch, p);
 }
 
 cudaError_t launch_if_partial(const DevChunks &ch, const double *slot, double *xbuf, const int32_t *send_if,
