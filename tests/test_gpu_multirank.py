@@ -107,3 +107,12 @@ def test_gpu_partition_equals_host(monkeypatch, world, name, scale):
         assert all(i["n_interface_nodes"] > 0 for i in infos)
     finally:
         g.close()
+
+
+def test_nccl_unique_id_through_dlopen():
+    """The NCCL transport of the multi-GPU path: libsem dlopens libnccl (torch's copy) and
+    creates unique ids (the only NCCL step one GPU can run; the send/recv exchange needs
+    two devices and runs in the driver's scaling bench)."""
+    a, b = S.nccl_unique_id(), S.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128
+    assert any(a) and a != b
