@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <utility>
@@ -51,13 +52,32 @@ struct NcclApi {
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
+// Which libnccl.so.2 is loaded matters beyond this library: the dynamic linker
+// matches a later DT_NEEDED "libnccl.so.2" (libtorch_cuda's) by soname against the
+// objects already mapped, whatever RTLD_LOCAL/GLOBAL said.  Loading the system copy
+// (2.27) before torch therefore breaks `import torch` (it needs the 2.28 of its
+// wheel).  Resolution order, none of which can shadow torch's copy:
+//   1. a libnccl.so.2 already mapped in the process (RTLD_NOLOAD): torch's, if imported;
+//   2. SEM_NCCL_LIB, an absolute path -- the binding (sem.py) sets it to the nvidia-nccl
+//      wheel's library, the file torch itself loads;
+//   3. only then the default search path (plain C callers without torch).
 NcclApi &nccl() {
     static NcclApi api;
+    static std::mutex mu;
     static bool tried = false;
+    std::lock_guard<std::mutex> lock(mu);
     if (tried) return api;
     tried = true;
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char *env = getenv("SEM_NCCL_LIB");
+    if (!h && env && *env) {
+        h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            api.err = std::string("cannot load SEM_NCCL_LIB=") + env + ": " + dlerror();
+            return api;
+        }
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
         api.err = std::string("cannot load libnccl.so.2: ") + dlerror();
         return api;

@@ -65,6 +65,21 @@ _lib = None
 _lock = threading.Lock()
 
 
+def _torch_nccl_path():
+    """The libnccl.so.2 of the nvidia-nccl wheel (the file torch loads), found without
+    importing torch; None if the wheel is absent."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        f = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(f):
+            return f
+    return None
+
+
 def load(path: str = LIB_PATH):
     """Load libsem.so (raises if it has not been built: no fallback)."""
     global _lib
@@ -73,6 +88,13 @@ def load(path: str = LIB_PATH):
             return _lib
         if not os.path.exists(path):
             raise RuntimeError("libsem.so not built (%s); run `python -m paper_2104_08416_b200.build`" % path)
+        # libsem dlopens NCCL lazily; point it at torch's copy so that loading NCCL before
+        # `import torch` cannot map the older system library under the same soname
+        # (csrc/api.cu: nccl()).  An explicit SEM_NCCL_LIB wins.
+        if not os.environ.get("SEM_NCCL_LIB"):
+            f = _torch_nccl_path()
+            if f:
+                os.environ["SEM_NCCL_LIB"] = f
         L = C.CDLL(path)
         P, i64, i32, u64, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_double
         L.sem_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, P, P]

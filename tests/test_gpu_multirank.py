@@ -6,6 +6,8 @@ sequences the ranks with events, so no kernel ever waits on another rank.
 Results must match the oracle (rel L2 <= 1e-10) and the one-rank GPU run
 (rounding-level: only the summation order of interface nodes differs).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -113,6 +115,15 @@ def test_nccl_unique_id_through_dlopen():
     """The NCCL transport of the multi-GPU path: libsem dlopens libnccl (torch's copy) and
     creates unique ids (the only NCCL step one GPU can run; the send/recv exchange needs
     two devices and runs in the driver's scaling bench)."""
-    a, b = S.nccl_unique_id(), S.nccl_unique_id()
-    assert len(a) == 128 and len(b) == 128
-    assert any(a) and a != b
+    # in a subprocess: whichever libnccl this maps stays out of the pytest process
+    import subprocess
+    import sys
+    code = ("from paper_2104_08416_b200 import sem as S\n"
+            "a, b = S.nccl_unique_id(), S.nccl_unique_id()\n"
+            "assert len(a) == 128 and len(b) == 128\n"
+            "assert any(a) and a != b\n"
+            "import torch\n"
+            "assert torch.cuda.is_available()\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
