@@ -228,8 +228,7 @@ def run_ours(args):
                    "interface_nodes_rank0": info["n_interface_nodes"], "neighbors_rank0": info["n_neighbors"],
                    "l2": "no flush: per-step working set %.2f GB per GPU > 126 MB L2" % (info["bytes_alg_per_step"] / 1e9),
                    "chunk_elems": info["chunk_elems"], "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
-                   "step_loop": "CUDA graph of 32 steps" if world == 1 and os.environ.get("SEM_GRAPH", "1") != "0"
-                                else "stream launches",
+                   "step_loop": step_loop_label(args.steps, world),
                    "dt": pb.dt},
         "roofline": {"bound": "hbm", "kernel": "k7_step (stiffness apply + fused leapfrog)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -268,6 +267,20 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def step_loop_label(steps, world):
+    """How sem_step_n(steps) launches (api.cu: sem_step_n): one rank replays a captured CUDA
+    graph of 32 steps for each whole block of 32, the rest as stream launches."""
+    if world > 1 or os.environ.get("SEM_GRAPH", "1") == "0":
+        return "stream launches (%d steps)" % steps
+    g, r = divmod(steps, 32)
+    parts = []
+    if g:
+        parts.append("%d replays of a 32-step CUDA graph" % g)
+    if r:
+        parts.append("%d steps as stream launches" % r)
+    return " + ".join(parts) or "none"
 
 
 WORKLOADS = {

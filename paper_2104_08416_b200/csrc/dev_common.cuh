@@ -6,6 +6,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace sem {
 namespace {
@@ -78,6 +82,38 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
 template <int B>
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"r"(B) : "memory");
+}
+
+// ---- host helpers of the persistent launches -----------------------------------
+// cudaFuncSetAttribute applies per device context: the raised max-dynamic-smem value
+// is cached per (device, kernel), only ever raised, under a lock.
+inline cudaError_t raise_max_smem(const void *kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> cur;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &c = cur[{dev, kernel}];
+    if (bytes <= c) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c = bytes;
+    return e;
+}
+// SM count of the current device
+inline int current_sm_count() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 1;
+}
+// SEM_K7_GRID=n caps the persistent step kernels' grids (K7, KH7) at n CTAs, so tests can
+// force many chunks per CTA (stage reuse, window hand-off) on small meshes; 0/unset = none.
+// Read at every launch configuration (host side, outside any captured graph's replays).
+inline int64_t persistent_grid_cap() {
+    const char *e = getenv("SEM_K7_GRID");
+    const long long n = e ? atoll(e) : 0;
+    return (int64_t)(n > 0 ? n : 0);
 }
 
 }  // namespace

@@ -405,12 +405,7 @@ __global__ void k_v_in(const double *__restrict__ in, const int32_t *__restrict_
 
 template <typename K>
 cudaError_t set_smem_h(K kernel, size_t bytes) {
-    static std::map<const void *, size_t> cur;
-    size_t &c = cur[(const void *)kernel];
-    if (bytes <= c) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) c = bytes;
-    return e;
+    return raise_max_smem((const void *)kernel, bytes);
 }
 
 size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
@@ -465,19 +460,14 @@ cudaError_t launch_geometry_heun(const double *vxy, const int32_t *tri_or, const
 }
 
 int heun_grid(const DevChunks &ch, int mode) {
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
     const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode);
     const HFn fn = heun_fn(ch.Np, ch.B, mode);
     set_smem_h(fn, smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B + 32, smem);
     if (occ < 1) occ = 1;
-    int64_t g = (int64_t)occ * nsm;
+    int64_t g = (int64_t)occ * current_sm_count();
+    if (persistent_grid_cap() > 0 && g > persistent_grid_cap()) g = persistent_grid_cap();
     if (g > ch.nchunks) g = ch.nchunks;
     return (int)g;
 }

@@ -25,7 +25,6 @@
 // matrices, as PAPER.md:1568 suggests.
 #include <cuda_runtime.h>
 
-#include <map>
 #include <vector>
 
 #include "dev_common.cuh"
@@ -343,6 +342,9 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         const int s = k % kStages;
         MBAR_WAIT_INLINE(&full[s], (k / kStages) & 1);  // stage blocks (TMA)
         MBAR_WAIT_INLINE(&gath[s], (k / kStages) & 1);  // shared-node U gathers (cp.async)
+        // fused K8 reads the shared-node ids the idb copy wrote: wait on it directly rather than
+        // through the producer's wait -> cp.async arrive chain (already complete: near free)
+        if (kIdsTma && a.cnt) MBAR_WAIT_INLINE(&idb[s], (k / kStages) & 1);
         const unsigned char *st = sm + s * lay.size;
         const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
         const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
@@ -581,16 +583,9 @@ __global__ void k_abl_update(int64_t n, const StepParams a, double *KU) {
     a.Uprev[i] = leap_update(a.U[i], a.Uprev[i], a.dt2M[i], f, y);
 }
 
-// The max-dynamic-smem attribute is per function (process-wide), and several
-// contexts may launch the same kernel with different sizes: only ever raise it.
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
-    static std::map<const void *, size_t> cur;
-    size_t &c = cur[(const void *)kernel];
-    if (bytes <= c) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) c = bytes;
-    return e;
+    return raise_max_smem((const void *)kernel, bytes);
 }
 
 // U^{n-1} / dt^2/M windows: SEM_K7_WIN=1 single-buffered TMA window (default),
@@ -704,14 +699,9 @@ int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool 
 }
 
 int k7_grid(const DevChunks &ch, bool fused) {
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
     const int occ = k7_ctas_per_sm(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_nsh, fused);
-    int64_t g = (int64_t)occ * nsm;
+    int64_t g = (int64_t)occ * current_sm_count();
+    if (persistent_grid_cap() > 0 && g > persistent_grid_cap()) g = persistent_grid_cap();
     if (g > ch.nchunks) g = ch.nchunks;
     return (int)g;
 }
@@ -736,6 +726,7 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
                       const int32_t *list, int64_t nlist, bool pdl) {
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
+    if (persistent_grid_cap() > 0 && grid > persistent_grid_cap()) grid = (int)persistent_grid_cap();
     if (grid > n) grid = (int)n;
     const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, p.cnt != nullptr);
     const K7Fn fn = k7_fn(ch.Np, ch.B);
