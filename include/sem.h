@@ -325,12 +325,16 @@ sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches,
  * {nchunks, N_int (padded), N_sh, n_slots, max_local, max_win, max_count (most
  *  entries of one node in a chunk), max_colors, sum_nint, sum_nsh, max_nsh, 0, 0, 0, 0, 0};
  * int_of_out [N] (optional) the internal id of every node; cmeta_out
- * [nchunks*8] (optional) the per-chunk descriptors {i0, nint, s0, nsh, ncol,
+ * [nchunks*8] (optional) the per-chunk descriptors {i0, nint, s0, nsh, end0,
  * ne, nint_al, end1} (end0/end1: ends of the interior / shared jagged-diagonal
- * segments).  Errors: SEM_E_ARG, SEM_E_MESH (unused node), SEM_E_OOM.
+ * segments); own0_out [nchunks+1] (optional) the shared indices each chunk owns,
+ * [own0[c], own0[c+1]) (owner = the last chunk touching the node; the step kernel
+ * finalises them after that chunk).  Errors: SEM_E_ARG, SEM_E_MESH (unused node),
+ * SEM_E_OOM.
  */
 sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
-                                 int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out);
+                                 int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out,
+                                 int32_t *own0_out);
 
 /*
  * Host-only diagnostic of the multi-GPU partition (no GPU, no context): rank's

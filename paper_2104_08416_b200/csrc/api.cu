@@ -357,16 +357,17 @@ cudaError_t upload_chunks(AllocList &L, const ChunkMeta &m, DevChunks &d, cudaSt
     d.B = m.B; d.Np = m.Np; d.E = m.E; d.N = m.N; d.nchunks = m.nchunks;
     d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
     d.max_local = m.max_local; d.max_win = m.max_win; d.max_count = m.max_count; d.max_nsh = m.max_nsh;
-    int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs;
+    int32_t *p_cmeta, *p_pstart, *p_shn, *p_shs, *p_own0;
     uint16_t *p_lpos, *p_jds, *p_lidx, *p_shcr;
     cudaError_t e;
     if ((e = upload(L, &p_cmeta, m.cmeta, s)) || (e = upload(L, &p_lidx, m.lidx, s)) ||
         (e = upload(L, &p_lpos, m.lpos, s)) || (e = upload(L, &p_jds, m.jds, s)) ||
         (e = upload(L, &p_pstart, m.sh_pstart, s)) || (e = upload(L, &p_shn, m.shl_node, s)) ||
-        (e = upload(L, &p_shs, m.shl_slot, s)) || (e = upload(L, &p_shcr, m.shl_cr, s)))
+        (e = upload(L, &p_shs, m.shl_slot, s)) || (e = upload(L, &p_shcr, m.shl_cr, s)) ||
+        (e = upload(L, &p_own0, m.own0, s)))
         return e;
     d.cmeta = p_cmeta; d.lidx = p_lidx; d.lpos = p_lpos; d.jds = p_jds; d.sh_pstart = p_pstart;
-    d.shl_node = p_shn; d.shl_slot = p_shs; d.shl_cr = p_shcr;
+    d.shl_node = p_shn; d.shl_slot = p_shs; d.shl_cr = p_shcr; d.own0 = p_own0;
     return cudaSuccess;
 }
 
@@ -395,6 +396,7 @@ std::string compare_chunks(const ChunkMeta &h, const ChunkMeta &m, const DevChun
     if (!same_dev(h.shl_node, d.shl_node, h.shl_node.size(), s)) return "shl_node";
     if (!same_dev(h.shl_slot, d.shl_slot, h.shl_slot.size(), s)) return "shl_slot";
     if (!same_dev(h.shl_cr, d.shl_cr, h.shl_cr.size(), s)) return "shl_cr";
+    if (!same_dev(h.own0, d.own0, h.own0.size(), s)) return "own0";
     if (!same_dev(h.int_of, d_int_of, h.int_of.size(), s)) return "int_of";
     return "";
 }
@@ -1588,7 +1590,8 @@ sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches, d
 // Host-only diagnostics (no GPU needed), used by the CPU test-suite.
 // ---------------------------------------------------------------------------
 sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N, int B,
-                                 int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out) {
+                                 int64_t *stats_out, int32_t *int_of_out, int32_t *cmeta_out,
+                                 int32_t *own0_out) {
     if (!mu || !stats_out || E <= 0 || N <= 0) return SEM_E_ARG;
     try {
         ChunkMeta m;
@@ -1605,6 +1608,7 @@ sem_status sem_debug_chunk_stats(const int32_t *mu, int64_t E, int Np, int64_t N
         std::memcpy(stats_out, st, sizeof(st));
         if (int_of_out) std::memcpy(int_of_out, m.int_of.data(), sizeof(int32_t) * N);
         if (cmeta_out) std::memcpy(cmeta_out, m.cmeta.data(), sizeof(int32_t) * m.cmeta.size());
+        if (own0_out) std::memcpy(own0_out, m.own0.data(), sizeof(int32_t) * m.own0.size());
         return SEM_OK;
     } catch (const std::bad_alloc &) {
         return SEM_E_OOM;

@@ -20,8 +20,10 @@
 // i0_c even (16-byte aligned for TMA bulk copies, at most one hole per chunk),
 // ordered by descending entry count then ascending incoming id (so warps of
 // the reduction see nodes of equal degree); shared nodes follow at
-// [N_int, N_int+N_sh): non-interface ones in ascending id, then the
-// rank-interface ones (multi-GPU) in ascending id.
+// [N_int, N_int+N_sh): non-interface ones by (owner chunk, id) -- the owner is
+// the last chunk touching the node, and a chunk's owned nodes form the range
+// [own0[c], own0[c+1]) -- then the rank-interface ones (multi-GPU) in
+// ascending id.
 //
 // Parallel structure: one pass sorts every chunk's node ids (OpenMP over
 // chunks); the per-node facts (first chunk, number of touching chunks) come
@@ -80,7 +82,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     // ---- per chunk: sorted unique node ids with entry counts; per node: first
     //      touching chunk and number of touching chunks (atomics, order-free) ----
     std::vector<std::vector<Uniq>> uq(nch);
-    std::vector<int32_t> firstc(N, INT32_MAX), nref(N, 0);
+    std::vector<int32_t> firstc(N, INT32_MAX), lastc(N, -1), nref(N, 0);
     bool bad_id = false;
 #pragma omp parallel
     {
@@ -108,6 +110,11 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
             int32_t cur = __atomic_load_n(&firstc[u.g], __ATOMIC_RELAXED);
             while ((int32_t)c < cur &&
                    !__atomic_compare_exchange_n(&firstc[u.g], &cur, (int32_t)c, true, __ATOMIC_RELAXED,
+                                                __ATOMIC_RELAXED)) {
+            }
+            int32_t hi = __atomic_load_n(&lastc[u.g], __ATOMIC_RELAXED);
+            while ((int32_t)c > hi &&
+                   !__atomic_compare_exchange_n(&lastc[u.g], &hi, (int32_t)c, true, __ATOMIC_RELAXED,
                                                 __ATOMIC_RELAXED)) {
             }
         }
@@ -140,17 +147,27 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
     for (int64_t c = 0; c < nch; c++) m.i0[c + 1] = (int32_t)align2(m.i0[c] + nint[c]);
     m.N_int = m.i0[nch];
 
-    // shared indices: non-interface in ascending id, then interface in ascending id
+    // shared indices: non-interface by (owner chunk = last touching chunk, id) -- the nodes a
+    // chunk owns form the contiguous range [own0[c], own0[c+1]) that K7 finalises after
+    // the chunk (one launch walks the chunks in ascending order, so the owner comes last) --
+    // then interface in ascending id
     m.int_of.assign(N, -1);
     std::vector<int32_t> sh_index(N, -1);
     int64_t nsh = 0, nif = 0;
+    m.own0.assign(nch + 1, 0);
     for (int64_t g = 0; g < N; g++)
-        if (!interior(g)) { nsh++; nif += forced(g); }
+        if (!interior(g)) {
+            nsh++;
+            nif += forced(g);
+            if (!forced(g)) m.own0[lastc[g] + 1]++;
+        }
+    for (int64_t c = 0; c < nch; c++) m.own0[c + 1] += m.own0[c];
     {
-        int64_t s = 0, sf = nsh - nif;
-        for (int64_t g = 0; g < N; g++) {
+        std::vector<int32_t> cur(m.own0.begin(), m.own0.end() - 1);
+        int64_t sf = nsh - nif;
+        for (int64_t g = 0; g < N; g++) {  // ascending g within each owner
             if (interior(g)) continue;
-            const int64_t k = forced(g) ? sf++ : s++;
+            const int64_t k = forced(g) ? sf++ : cur[lastc[g]]++;
             sh_index[g] = (int32_t)k;
             m.int_of[g] = (int32_t)(m.N_int + k);
         }

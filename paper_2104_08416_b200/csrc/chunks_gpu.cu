@@ -3,8 +3,8 @@
 // Same metadata, bit for bit (tests/test_gpu_chunks.py compares every array
 // with the host builder): chunks of B consecutive elements; nodes touched by
 // one chunk are interior (contiguous window per chunk, descending entry count
-// then ascending id), the others shared (non-interface ascending id, then
-// interface ascending id) with one node-major slot per touching chunk in
+// then ascending id), the others shared (non-interface by (owner = last
+// touching chunk, id), then interface ascending id) with one node-major slot per touching chunk in
 // ascending chunk order; per-chunk local indices, jagged-diagonal starts and
 // entry positions.  Built from three radix sorts:
 //   1. entries (chunk, node) in [chunk][p][t] order -> (chunk, node) runs,
@@ -106,7 +106,8 @@ __global__ void k_run_starts(const int32_t *__restrict__ flag, const int32_t *__
 }
 
 __global__ void k_run_info(const uint64_t *__restrict__ key, const int32_t *__restrict__ start, int64_t nruns,
-                           int64_t n, int bn, int32_t *rc, int32_t *rg, int32_t *rlen, int32_t *nref) {
+                           int64_t n, int bn, int32_t *rc, int32_t *rg, int32_t *rlen, int32_t *nref,
+                           int32_t *lastc) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= nruns) return;
     const uint64_t k = key[start[r]];
@@ -115,6 +116,7 @@ __global__ void k_run_info(const uint64_t *__restrict__ key, const int32_t *__re
     rg[r] = g;
     rlen[r] = (int32_t)((r + 1 < nruns ? start[r + 1] : n) - start[r]);
     atomicAdd(&nref[g], 1);
+    atomicMax(&lastc[g], rc[r]);
 }
 
 __global__ void k_node_class(const int32_t *__restrict__ nref, const uint8_t *__restrict__ forced, int64_t N,
@@ -138,6 +140,37 @@ __global__ void k_shared_index(const int32_t *__restrict__ a, const int32_t *__r
     else if (b[g]) s = na + eb[g];
     s_of[g] = s;
     if (s >= 0) node_of_s[s] = (int32_t)g;
+}
+
+// non-interface shared nodes (old index i < na, ascending id) keyed by (owner chunk, id)
+__global__ void k_owner_keys(const int32_t *__restrict__ node_of_s, const int32_t *__restrict__ lastc, int64_t na,
+                             int bn, uint64_t *key, int32_t *val) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    const int32_t g = node_of_s[i];
+    key[i] = ((uint64_t)(uint32_t)lastc[g] << bn) | (uint32_t)g;
+    val[i] = g;
+}
+
+__global__ void k_owner_index(const int32_t *__restrict__ gs, int64_t na, int32_t *s_of, int32_t *node_of_s) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    const int32_t g = gs[i];
+    s_of[g] = (int32_t)i;
+    node_of_s[i] = g;
+}
+
+// own0[c] = first owner-sorted position whose owner chunk is >= c (c = 0..nch)
+__global__ void k_own0(const uint64_t *__restrict__ key, int64_t na, int bn, int64_t nch, int32_t *own0) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c > nch) return;
+    int64_t lo = 0, hi = na;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)(key[mid] >> bn) < c) lo = mid + 1;
+        else hi = mid;
+    }
+    own0[c] = (int32_t)lo;
 }
 
 // 2. local-order key of every run; per-chunk interior / shared counts
@@ -356,16 +389,19 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     RET(cudaMemcpyAsync(&nr32, rid.as<int32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, s));
     RET(cudaStreamSynchronize(s));
     const int64_t nruns = nr32;
-    Tmp rstart(s), rc(s), rg(s), rlen(s), nref(s);
+    Tmp rstart(s), rc(s), rg(s), rlen(s), nref(s), lastc(s);
     RET(rstart.alloc(4 * nruns));
     RET(rc.alloc(4 * nruns));
     RET(rg.alloc(4 * nruns));
     RET(rlen.alloc(4 * nruns));
     RET(nref.alloc(4 * N));
+    RET(lastc.alloc(4 * N));
     RET(cudaMemsetAsync(nref.p, 0, 4 * N, s));
+    RET(cudaMemsetAsync(lastc.p, 0xff, 4 * N, s));
     k_run_starts<<<nb(n), kT, 0, s>>>(flag.as<int32_t>(), rid.as<int32_t>(), n, rstart.as<int32_t>());
     k_run_info<<<nb(nruns), kT, 0, s>>>(k1s.as<uint64_t>(), rstart.as<int32_t>(), nruns, n, bn, rc.as<int32_t>(),
-                                        rg.as<int32_t>(), rlen.as<int32_t>(), nref.as<int32_t>());
+                                        rg.as<int32_t>(), rlen.as<int32_t>(), nref.as<int32_t>(),
+                                        lastc.as<int32_t>());
 
     tr.mark(s, "runs");
     // ---- classification and shared indices ----
@@ -400,6 +436,25 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     RET(node_of_s.alloc(4 * (nsh_tot + 1)));
     k_shared_index<<<nb(N), kT, 0, s>>>(fa.as<int32_t>(), fb.as<int32_t>(), ea.as<int32_t>(), eb.as<int32_t>(), N,
                                         (int32_t)na, s_of.as<int32_t>(), node_of_s.as<int32_t>());
+    // non-interface shared nodes renumbered by (owner chunk, id): a chunk's owned nodes are the
+    // contiguous range [own0[c], own0[c+1])
+    int32_t *own0 = nullptr;
+    RET(dalloc((void **)&own0, 4 * (size_t)(nch + 1)));
+    {
+        Tmp ok(s), ov(s), oks(s), ovs(s);
+        RET(ok.alloc(8 * (na + 1)));
+        RET(ov.alloc(4 * (na + 1)));
+        RET(oks.alloc(8 * (na + 1)));
+        RET(ovs.alloc(4 * (na + 1)));
+        if (na > 0) {
+            k_owner_keys<<<nb(na), kT, 0, s>>>(node_of_s.as<int32_t>(), lastc.as<int32_t>(), na, bn,
+                                               ok.as<uint64_t>(), ov.as<int32_t>());
+            RET(sort_u64(ok.as<uint64_t>(), ov.as<int32_t>(), oks.as<uint64_t>(), ovs.as<int32_t>(), na, bc + bn, s));
+            k_owner_index<<<nb(na), kT, 0, s>>>(ovs.as<int32_t>(), na, s_of.as<int32_t>(), node_of_s.as<int32_t>());
+        }
+        k_own0<<<nb(nch + 1), kT, 0, s>>>(oks.as<uint64_t>(), na, bn, nch, own0);
+        RET(cudaStreamSynchronize(s));
+    }
 
     tr.mark(s, "classification");
     // ---- 2. local order per chunk ----
@@ -546,7 +601,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     d.N_int = m.N_int; d.N_sh = m.N_sh; d.N_tot = m.N_tot; d.n_slots = m.n_slots; d.N_if = m.N_if;
     d.max_local = m.max_local; d.max_win = m.max_win; d.max_count = m.max_count; d.max_nsh = m.max_nsh;
     d.cmeta = cmeta; d.lidx = lidx; d.lpos = lpos; d.jds = jds; d.sh_pstart = sh_pstart;
-    d.shl_node = shl_node; d.shl_slot = shl_slot; d.shl_cr = shl_cr;
+    d.shl_node = shl_node; d.shl_slot = shl_slot; d.shl_cr = shl_cr; d.own0 = own0;
     RET(cudaStreamSynchronize(s));
     return cudaGetLastError();
 }

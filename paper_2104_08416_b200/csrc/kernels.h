@@ -87,6 +87,7 @@ struct DevChunks {  // device view of ChunkMeta
     const int32_t *shl_node;   // per chunk (block at cmeta[2]): shared index of each local shared node
     const int32_t *shl_slot;   // per chunk: the slot it writes
     const uint16_t *shl_cr;    // per chunk: (slots of the node << 8) | rank of this chunk among them
+    const int32_t *own0;       // [nchunks+1] shared indices owned by chunk c: [own0[c], own0[c+1])
 };
 
 // ------------------------------ chunks_gpu.cu --------------------------------

@@ -87,6 +87,8 @@ struct ChunkMeta {
     std::vector<uint16_t> jds;       // [nchunks][2 kJdsW] start of each jagged diagonal per segment
     std::vector<uint16_t> lpos;      // [nchunks][Np*B] entry-buffer position of entry p*B + t (JDS)
     std::vector<int32_t> sh_pstart;  // [N_sh+1] slots of shared node s (node-major, chunk order)
+    std::vector<int32_t> own0;       // [nchunks+1] shared indices owned (last touched) by chunk c:
+                                     // [own0[c], own0[c+1]) (non-interface nodes only)
     std::vector<uint16_t> lidx;      // [nchunks][Np][B] chunk-local node index
     std::vector<uint8_t> color;      // [nchunks*B] colour within the chunk (255 = pad)
     std::vector<int32_t> int_of;     // [N] node id (numbering of mu) -> internal id

@@ -113,7 +113,7 @@ def load(path: str = LIB_PATH):
         L.sem_get_info.argtypes = [P, C.POINTER(sem_info)]
         L.sem_set_kernel_timing.argtypes = [P, C.c_int]
         L.sem_kernel_times.argtypes = [P, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]
-        L.sem_debug_chunk_stats.argtypes = [P, i64, C.c_int, i64, C.c_int, P, P, P]
+        L.sem_debug_chunk_stats.argtypes = [P, i64, C.c_int, i64, C.c_int, P, P, P, P]
         L.sem_debug_partition.argtypes = [P, i64, C.c_int, i64, C.c_int, C.c_int, P, P, P, P, P, P, P, P]
         L.sem_nccl_unique_id.argtypes = [P]
         L.sem_group_build_operators.argtypes = [P, C.c_int, P, i64, dbl, dbl, dbl, dbl]
@@ -296,13 +296,15 @@ def sem_debug_chunk_stats(mu, N: int, B: int = 256, want_maps: bool = False):
     int_of = np.empty(N, np.int32) if want_maps else None
     nch = (E + B - 1) // B
     cmeta = np.empty(nch * 8, np.int32) if want_maps else None
-    rc = L.sem_debug_chunk_stats(_ptr(mu), E, Np, N, B, _ptr(st), _ptr(int_of), _ptr(cmeta))
+    own0 = np.empty(nch + 1, np.int32) if want_maps else None
+    rc = L.sem_debug_chunk_stats(_ptr(mu), E, Np, N, B, _ptr(st), _ptr(int_of), _ptr(cmeta), _ptr(own0))
     if rc != SEM_OK:
         raise SemError(rc, "sem_debug_chunk_stats failed")
     d = {k: int(v) for k, v in zip(CHUNK_STAT_KEYS, st)}
     if want_maps:
         d["int_of"] = int_of
         d["cmeta"] = cmeta.reshape(nch, 8)
+        d["own0"] = own0
     return d
 
 

@@ -45,9 +45,15 @@ def test_chunk_builder_brute_force(name, scale, P, B):
         c = next(iter(touching[g]))
         i0, nint = cm[c, 0], cm[c, 1]
         assert i0 % 2 == 0 and i0 <= int_of[g] < i0 + nint
-    # shared nodes in ascending id (no rank-interface nodes here)
+    # shared nodes by (owner = last touching chunk, id) (no rank-interface nodes here), so
+    # each chunk owns a contiguous range of shared indices
     sh_ids = np.nonzero(~interior)[0]
-    assert np.array_equal(int_of[sh_ids], N_int + np.arange(nsh))
+    owner = np.array([max(touching[g]) for g in sh_ids])
+    order = np.lexsort((sh_ids, owner))
+    assert np.array_equal(int_of[sh_ids[order]], N_int + np.arange(nsh))
+    own0 = st["own0"]
+    assert own0.shape == (nch + 1,) and own0[0] == 0 and own0[-1] == nsh
+    assert np.array_equal(np.diff(own0), np.bincount(owner, minlength=nch))
     # per-chunk counts and element counts
     for c in range(nch):
         ne = min(E, (c + 1) * B) - c * B
