@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -20,6 +21,39 @@ __device__ __forceinline__ double ricker_dev(double t, double f0, double t0) {
     a = a * a;
     return (1.0 - 2.0 * a) * exp(-a);
 }
+
+// ---- checked builds (-DSEM_CHECKED; tools/checked_build.sh) --------------------
+// compute-sanitizer is closed on this GPU pool, so the asynchronous pipelines are checked by
+// a build of their own: device-side bounds and consistency asserts (SEM_DCHECK: printf + trap,
+// which surfaces as SEM_E_CUDA), poisoning of every shared-memory buffer before it is handed
+// back to its producer (a read of a stage, window or entry buffer that the barriers did not
+// order after its refill sees NaN or an out-of-range index instead of stale data), and
+// pseudo-random delays (chaos_delay) that perturb the producer / consumer timing.
+#ifdef SEM_CHECKED
+#define SEM_DCHECK(cond, what)                                                                           \
+    do {                                                                                                 \
+        if (!(cond)) {                                                                                   \
+            printf("SEM_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,        \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                   \
+            __trap();                                                                                    \
+        }                                                                                                \
+    } while (0)
+constexpr bool kChecked = true;
+__device__ __forceinline__ void chaos_delay(unsigned key) {
+    unsigned h = key * 2654435761u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    if ((h & 3) == 0) __nanosleep(100 + (h >> 16) % 4000);
+}
+#else
+#define SEM_DCHECK(cond, what) \
+    do {                       \
+    } while (0)
+constexpr bool kChecked = false;
+__device__ __forceinline__ void chaos_delay(unsigned) {}
+#endif
+__device__ __forceinline__ double poison_f64() { return __longlong_as_double(0x7FF8DEADDEADDEADll); }
 
 // ---- PTX helpers: mbarrier + TMA bulk copy -----------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

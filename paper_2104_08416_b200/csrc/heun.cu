@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             const int64_t c = list ? list[pos] : pos;
             const int s = k % kStagesH;
             if (k >= kStagesH && lane == 0) mbar_wait(&empty[s], ((k / kStagesH) & 1) ^ 1);
+            if (lane == 0) chaos_delay(0x10000u * blockIdx.x + 2u * k);
             __syncwarp();
             unsigned char *st = sm + s * lay.size;
             const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
@@ -149,6 +150,10 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
                 uint32_t bytes = NP * B * 2 + 5 * B * 8;
                 if (kStep) bytes += NP * B * 2 + 2 * kJdsW * 2 + nsh4 * 4 + (uint32_t)ni_al * 8;
                 if (kLag) bytes += (uint32_t)ni_al * 8;
+                SEM_DCHECK(c >= 0 && c < ch.nchunks, "chunk id in range");
+                SEM_DCHECK(ni_al + ((nsh + 1) & ~1) <= L, "local nodes fit the stage's u / w buffers");
+                SEM_DCHECK(((nsh + 3) & ~3) <= Ls, "shared-node lists fit the stage");
+                SEM_DCHECK(!kStep || ni_al <= W, "(h/2)/M window fits");
                 if (ids_tma(NP)) {  // first: the ids the gathers wait for
                     mbar_arrive_expect_tx(&idb[s], nsh4 * 4);
                     if (nsh4 > 0) tma_load(st + lay.shn, ch.shl_node + s0, nsh4 * 4, &idb[s]);
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             cp_async_arrive_noinc(&gath[s]);
             if (kStep && lane == 0) {
                 if (k >= 1) mbar_wait(wempty, (k - 1) & 1);
+                chaos_delay(0x10000u * blockIdx.x + 2u * k + 1u);
                 mbar_arrive_expect_tx(wfull, (uint32_t)ni_al * 8);
                 if (ni_al > 0) tma_load(m_s, a.hM + i0, ni_al * 8, wfull);
             }
@@ -213,6 +219,17 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
         const double *g_s = reinterpret_cast<const double *>(st + lay.g);
         const double F00 = g_s[t], F01 = g_s[B + t], F10 = g_s[2 * B + t], F11 = g_s[3 * B + t];
         const double sd = g_s[4 * B + t];
+        if (kChecked) {  // the stage holds this chunk (a stale or foreign stage fails here)
+            const int4 r0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+            const int4 r1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
+            SEM_DCHECK(r0.x == m0.x && r0.y == m0.y && r0.z == m0.z && r0.w == m0.w && r1.x == m1.x &&
+                           r1.y == m1.y && r1.z == m1.z && r1.w == m1.w,
+                       "stage meta is this chunk's");
+            for (int e = t; e < NP * ne; e += B) {
+                const int li = li_s[(e / ne) * B + e % ne];
+                SEM_DCHECK(li < nint || (li >= ni_al && li < ni_al + nsh), "local index in range (poisoned?)");
+            }
+        }
 
         // (1) lagged V update: V^n = V^{n-1} + h Vdot(W^{n-1})  (Algorithm 1, E = 0)
         if (kLag && t < ne) {
@@ -328,6 +345,22 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             }
         }
         consumer_sync<B>();
+        if (kChecked) {  // poison everything handed back: only a refill may be read after this
+            unsigned char *stw = sm + s * lay.size;
+            double *uw = reinterpret_cast<double *>(stw + lay.u);
+            double *ww = reinterpret_cast<double *>(stw + lay.w);
+            double *gw = reinterpret_cast<double *>(stw + lay.g);
+            uint16_t *lw = reinterpret_cast<uint16_t *>(stw + lay.lidx);
+            for (int i = t; i < ni_al + nsh; i += B) { uw[i] = poison_f64(); ww[i] = poison_f64(); }
+            for (int i = t; i < 5 * B; i += B) gw[i] = poison_f64();
+            for (int i = t; i < (kStep ? 2 : 1) * NP * B; i += B) lw[i] = 0xFFFF;
+            if (kStep) {
+                for (int i = t; i < m1.w; i += B) ebuf[i] = make_double2(poison_f64(), poison_f64());
+                for (int i = t; i < ni_al; i += B) m_s[i] = poison_f64();
+            }
+            consumer_sync<B>();
+            if (t == 0) chaos_delay(0x20000u * blockIdx.x + k);
+        }
         if (t == 0) {
             mbar_arrive(&empty[s]);
             if (kStep) mbar_arrive(wempty);

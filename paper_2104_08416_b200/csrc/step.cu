@@ -272,6 +272,10 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             const int64_t c = list ? list[pos] : pos;
             const int s = k % kStages;
             if (k >= kStages && lane == 0) mbar_wait(&empty[s], ((k / kStages) & 1) ^ 1);
+            if (lane == 0) chaos_delay(0x10000u * blockIdx.x + 2u * k);
+#ifdef SEM_INJECT_RACE
+            if (lane == 0 && k >= kStages) __nanosleep(20000);  // a late refill the consumers do not wait for
+#endif
             __syncwarp();
             unsigned char *st = sm + s * lay.size;
             const int4 m0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
@@ -284,6 +288,12 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 const bool fuse = a.cnt != nullptr;
                 const uint32_t bytes = 2 * NP * B * 2 + 2 * kJdsW * 2 + nsh8 * (fuse ? (kIdsTma ? 6 : 10) : 4) +
                                        3 * B * 8 + (uint32_t)ni_al * (WIN2 ? 24 : 8);
+                SEM_DCHECK(c >= 0 && c < ch.nchunks, "chunk id in range");
+                SEM_DCHECK(ni_al + ((nsh + 1) & ~1) <= L, "local nodes fit the stage's u buffer");
+                SEM_DCHECK(nsh8 <= Ls, "shared-node lists fit the stage");
+                SEM_DCHECK(!(WIN1 || WIN2) || ni_al <= W, "interior window fits");
+                SEM_DCHECK(i0 % 2 == 0 && i0 + ni_al <= ch.N_int + 1, "interior window inside the interior range");
+                SEM_DCHECK(lay.meta + 32 <= lay.size && lay.u + L * 8 <= lay.size, "stage layout");
                 if (kIdsTma) {  // first: the ids the gathers below wait for
                     mbar_arrive_expect_tx(&idb[s], nsh8 * 4);
                     if (nsh8 > 0) tma_load(st + lay.shn, ch.shl_node + s0, nsh8 * 4, &idb[s]);
@@ -323,6 +333,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             // chunk's update is done; lands while this chunk's element phase runs
             if (WIN1 && lane == 0) {
                 if (k >= 1) mbar_wait(wempty, (k - 1) & 1);
+                chaos_delay(0x10000u * blockIdx.x + 2u * k + 1u);
                 mbar_arrive_expect_tx(wfull, (uint32_t)ni_al * 16);
                 if (ni_al > 0) {
                     tma_load(up_w, a.Uprev + i0, ni_al * 8, wfull);
@@ -340,8 +351,15 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     int k = 0;
     for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
         const int s = k % kStages;
-        MBAR_WAIT_INLINE(&full[s], (k / kStages) & 1);  // stage blocks (TMA)
-        MBAR_WAIT_INLINE(&gath[s], (k / kStages) & 1);  // shared-node U gathers (cp.async)
+#ifdef SEM_INJECT_RACE
+        // the checked build's own pin (tools/checked_build.sh): consumers read reused stages
+        // without waiting for their refill -- the poison and asserts must make this fail
+        if (k < kStages)
+#endif
+        {
+            MBAR_WAIT_INLINE(&full[s], (k / kStages) & 1);  // stage blocks (TMA)
+            MBAR_WAIT_INLINE(&gath[s], (k / kStages) & 1);  // shared-node U gathers (cp.async)
+        }
         // fused K8 reads the shared-node ids the idb copy wrote: wait on it directly rather than
         // through the producer's wait -> cp.async arrive chain (already complete: near free)
         if (kIdsTma && a.cnt) MBAR_WAIT_INLINE(&idb[s], (k / kStages) & 1);
@@ -356,6 +374,21 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         const int end0 = m1.x, end1 = m1.w;
         const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
         const double *g_s = reinterpret_cast<const double *>(st + lay.g);
+        if (kChecked) {  // the stage holds this chunk (a stale or foreign stage fails here)
+            const int64_t c = list ? list[pos] : pos;
+            const int4 r0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+            const int4 r1 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c + 1];
+            SEM_DCHECK(r0.x == m0.x && r0.y == m0.y && r0.z == m0.z && r0.w == m0.w && r1.x == m1.x &&
+                           r1.y == m1.y && r1.z == m1.z && r1.w == m1.w,
+                       "stage meta is this chunk's");
+            SEM_DCHECK(ne > 0 && ne <= B && end0 <= end1 && end1 <= NP * B, "chunk shape");
+            for (int e = t; e < NP * ne; e += C) {
+                const int q = e / ne, te = e % ne, li = li_s[q * B + te];
+                SEM_DCHECK(li < nint || (li >= ni_al && li < ni_al + nsh), "local index in range (poisoned?)");
+                SEM_DCHECK(lpo[q * B + te] < end1, "entry position in range (poisoned?)");
+            }
+            for (int j = t; j < nsh; j += C) SEM_DCHECK(shs[j] >= 0 && shs[j] < ch.n_slots, "slot id in range");
+        }
 
         if (G > 1) {
             // (E, wide) this thread: element te, rows [p0, p1) of y = K^e u
@@ -457,6 +490,20 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             }
         }
         consumer_sync<C>();
+        if (kChecked) {  // poison everything handed back: only a refill may be read after this
+            unsigned char *stw = sm + s * lay.size;
+            double *uw = reinterpret_cast<double *>(stw + lay.u);
+            double *gw = reinterpret_cast<double *>(stw + lay.g);
+            uint16_t *lw = reinterpret_cast<uint16_t *>(stw + lay.lidx);
+            for (int i = t; i < ni_al + nsh; i += C) uw[i] = poison_f64();
+            for (int i = t; i < 3 * B; i += C) gw[i] = poison_f64();
+            for (int i = t; i < 2 * NP * B; i += C) lw[i] = 0xFFFF;  // lidx and lpos
+            for (int i = t; i < end1; i += C) ebuf[i] = poison_f64();
+            if (WIN1)
+                for (int i = t; i < ni_al; i += C) { up_w[i] = poison_f64(); m_w[i] = poison_f64(); }
+            consumer_sync<C>();
+            if (t == 0) chaos_delay(0x20000u * blockIdx.x + k);
+        }
         if (t == 0) {
             mbar_arrive(&empty[s]);
             if (WIN1) mbar_arrive(wempty);
@@ -471,6 +518,7 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh - ch.N_if) return;  // interface nodes: k_if_partial / k8_if
     const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
+    SEM_DCHECK(j0 >= 0 && j0 < j1 && j1 <= ch.n_slots, "slot run of a shared node");
     const int64_t id = ch.N_int + s;
     const double u = a.U[id], up = a.Uprev[id], m = a.dt2M[id];  // independent of the slots
     double part[4];

@@ -1,13 +1,15 @@
-"""Small runs of every step kernel for compute-sanitizer.
+"""Small runs of every step kernel for the checked build.
 
-    SEM_K7_GRID=2 compute-sanitizer --tool racecheck python tools/sanitize_case.py
+    SEM_LIB=paper_2104_08416_b200/libsem_checked.so SEM_K7_GRID=2 python tools/pipeline_cases.py
 
+(compute-sanitizer is closed on this GPU pool: tools/checked_build.sh runs these cases and the
+GPU test-suite against a -DSEM_CHECKED build instead.)
 Each case is tiny (a few thousand elements) and, with the grid capped, walks several
 chunks per persistent CTA, so the pipeline's stage reuse (empty / wempty / idb
-mbarrier waits and parity flips) runs under the tool.  Kernels covered: K7 at P2, P3,
+mbarrier waits and parity flips) runs under the checks.  Kernels covered: K7 at P2, P3,
 P5, P7 (k7_step), K8 (k8_fix), the fused-K8 variant, Heun KH7 / KH8 (k_heun,
 k_heun_fix) at P3 and P5, and the multi-rank interface kernels (loopback group).
-Every case also checks its field against the oracle, so a sanitizer run that changes
+Every case also checks its field against the oracle, so a checked run that changes
 timing cannot hide a wrong answer.
 """
 import os
@@ -107,7 +109,7 @@ def main():
         heun(mg.config("B1", 40, degree=5), 5, steps)
     if "mr" in which:
         loopback(mg.config("C2", 16), 2, steps)
-    print("sanitize_case ok", flush=True)
+    print("pipeline_cases ok", flush=True)
 
 
 if __name__ == "__main__":
