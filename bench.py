@@ -250,8 +250,10 @@ def run_ours(args):
     # churn host and device memory
     if args.e2e:
         out["e2e"] = e2e(pb, args, S, local, rank, world, stream, dist)
-    if rank == 0 and world == 1 and (args.orderings or args.heun or args.orders):
+    if rank == 0 and world == 1 and (args.orderings or args.heun or args.orders or args.configs):
         ctx = S.SemContext(local, stream=stream.cuda_stream)
+        if args.configs:
+            out["configs"] = configs_leg(ctx, args, S, peak)
         if args.orderings:
             out["orderings"] = orderings(ctx, pb, args, S)
             out["scatter_ablation"] = scatter_ablation(ctx, pb, args, S)
@@ -377,6 +379,58 @@ def fp64_peak():
 
 
 FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = fp64_peak()
+
+
+# The other BASELINE.json configurations at one GPU, each with its own roofline line (SURVEY
+# §8(d): quote C3 and C5 beside the headline C4).  C5 runs at 1/4 linear size here (16.8 M P2
+# elements of the same graded, 10-layer recipe; about half its per-GPU share at 8 GPUs): the
+# full 268 M-element mesh takes minutes of host-side generation alone.
+CONFIG_LEG = [("C2", 1), ("C3", 1), ("C5", 4)]
+
+
+def configs_leg(ctx, args, S, peak):
+    import torch
+    from paper_2104_08416_b200 import meshgen as mg
+    res = {}
+    stream = torch.cuda.current_stream()
+    for name, scale in CONFIG_LEG:
+        pb = mg.config(name, scale)
+        m = pb.mesh
+        ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH)
+        ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt)
+        ctx.sem_step_n(max(3, args.warmup))
+        ctx.sem_step_n(0)  # capture the graph step loop outside the timed region
+        K = max(64, min(args.steps, 1024)) // 32 * 32
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ctx.sem_step_n(K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / K
+        ctx.sem_set_kernel_timing(True)
+        ctx.sem_step_n(min(K, 256))
+        kt = ctx.sem_kernel_times()
+        ctx.sem_set_kernel_timing(False)
+        info = ctx.sem_get_info()
+        b7, b8 = k7_bytes(info)
+        k7 = kt["k7_ms"] / max(kt["k7_launches"], 1)
+        k8 = kt["k8_ms"] / max(kt["k8_launches"], 1)
+        ach = b7 / (k7 * 1e-3) / 1e9
+        step_gbs = info["bytes_alg_per_step"] / (ms * 1e-3) / 1e9
+        res[name if scale == 1 else "%s/%d" % (name, scale)] = {
+            "workload": WORKLOADS[name] + ("" if scale == 1 else " (1/%d linear size)" % scale),
+            "elements": info["n_elements"], "degree": pb.P, "steps": K,
+            "element_updates_per_s": info["n_elements"] / (ms * 1e-3), "ms_per_step": ms,
+            "roofline": {"bound": "hbm", "kernel": "k7_step", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": ncu_traffic(name, "k7_step"), "bytes_per_launch": b7,
+                         "avg_launch_ms": k7},
+            "k8_avg_launch_ms": k8, "k8_bytes_per_launch": b8,
+            "step_alg_gbs": step_gbs, "step_alg_frac": step_gbs / peak,
+            "shared_node_frac": info["n_shared_nodes"] / info["n_nodes"],
+            "l2": "C2's 109 MB per step fits the 126 MB L2 (no flush: quoted as is)" if name == "C2" else
+                  "working set > L2"}
+    return res
 
 
 def orders_leg(ctx, args, S, peak, peaks):
@@ -644,6 +698,7 @@ def main():
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--no-heun", dest="heun", action="store_false")
     ap.add_argument("--no-orders", dest="orders", action="store_false")
+    ap.add_argument("--no-configs", dest="configs", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -8,7 +8,7 @@ out=gpurun_out/ab_$var.txt
 for rep in 1 2; do
   for v in $vals; do
     if [ "$v" = "-" ]; then unset $var; else export $var=$v; fi
-    timeout 300 python bench.py --steps $steps --warmup 20 --no-orderings --no-e2e --no-cpu --no-heun --no-orders "$@" \
+    timeout 300 python bench.py --steps $steps --warmup 20 --no-orderings --no-e2e --no-cpu --no-heun --no-orders --no-configs "$@" \
       > gpurun_out/ab_run.json 2> gpurun_out/ab_run.err
     echo "$var=$v" >> $out
     grep "^{" gpurun_out/ab_run.json >> $out || tail -3 gpurun_out/ab_run.err >> $out

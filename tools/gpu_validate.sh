@@ -9,6 +9,6 @@ timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 S=$(date +%s); timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$? seconds=$(( $(date +%s) - S ))"
 timeout 1200 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "reference rc=$?"
-A="--steps 20 --warmup 3 --no-orderings --no-e2e --no-cpu --no-heun --no-orders"
+A="--steps 20 --warmup 3 --no-orderings --no-e2e --no-cpu --no-heun --no-orders --no-configs"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py $A > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_step -s 4 -c 1 -o gpurun_out/k7_full python bench.py --steps 6 --warmup 3 --no-orderings --no-e2e --no-cpu --no-heun --no-orders > gpurun_out/ncu_full.log 2>&1; echo "ncu k7 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_step -s 4 -c 1 -o gpurun_out/k7_full python bench.py --steps 6 --warmup 3 --no-orderings --no-e2e --no-cpu --no-heun --no-orders --no-configs > gpurun_out/ncu_full.log 2>&1; echo "ncu k7 rc=$?"
