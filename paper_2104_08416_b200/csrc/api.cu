@@ -142,6 +142,13 @@ struct sem_ctx {
     DevChunks dch{};
     ChunkMeta meta_info;  // counts only
     int k7_grid = 0;
+    int k7_grid_ovl = 0;  // interior chunks while an interface exchange is in flight (SEM_COMM_SMS)
+    // one-GPU overlap probe (SEM_OVERLAP_PROBE_US): one rank, a chunk list split like the
+    // boundary / interior lists, a stand-in comm kernel between them
+    int32_t *d_probe_list = nullptr;
+    cudaEvent_t pev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double probe_acc[4] = {0, 0, 0, 0};
+    int64_t probe_n = 0;
     // interface exchange
     int64_t n_if = 0, n_send = 0;
     std::vector<int32_t> nbr, nbr_off;
@@ -277,6 +284,7 @@ void reset_mesh(sem_ctx *ctx) {
     ctx->src_lookup.clear();
     ctx->src_int_of.clear();
     ctx->dch = DevChunks{};
+    ctx->d_probe_list = nullptr;
     ctx->d_mu_abl = ctx->d_eidx_abl = nullptr;
     ctx->color_off.clear();
     ctx->mesh_scatter = SEM_SCATTER_CHUNK;
@@ -530,9 +538,22 @@ StepParams step_params(sem_ctx *ctx) {
 // per-launch host overhead that dominates small meshes.  SEM_GRAPH=0 disables.
 constexpr int kGraphSteps = 32;
 
+// SEM_COMM_SMS: SMs left to the exchange kernels (NCCL send/recv on the comm stream) while the
+// interior chunks run; SEM_OVERLAP_PROBE_US: one-rank overlap probe (stand-in comm kernel)
+int comm_sms() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("SEM_COMM_SMS"); v = e ? atoi(e) : 2; if (v < 0) v = 0; }
+    return v;
+}
+double probe_us() {
+    static double v = -1;
+    if (v < 0) { const char *e = getenv("SEM_OVERLAP_PROBE_US"); v = e ? atof(e) : 0.0; if (!(v > 0)) v = 0.0; }
+    return v;
+}
+
 bool graph_ok(sem_ctx *ctx) {
     static const bool env_off = getenv("SEM_GRAPH") && atoi(getenv("SEM_GRAPH")) == 0;
-    return !env_off && ctx->world == 1 && ctx->stream != nullptr &&
+    return !env_off && ctx->world == 1 && ctx->stream != nullptr && !(probe_us() > 0) &&
            ctx->ops_integrator == SEM_INTEGRATOR_LEAPFROG && ctx->mesh_scatter == SEM_SCATTER_CHUNK &&
            ctx->d_cnt == nullptr;
 }
@@ -607,9 +628,54 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
 // Step phase 1: stiffness + update of everything local; pack interface partials.
 // With NCCL (use_nccl) the exchange is issued on the comm stream right after
 // the boundary chunks are done and overlaps the interior chunks.
+// One rank, probe mode: chunks [0, n/8) stand in for the boundary chunks, the rest for the
+// interior ones; between them a stand-in comm kernel runs on the comm stream exactly where the
+// NCCL exchange would.  Events: before the "boundary" K7, around the "interior" K7, and at the
+// end of the stand-in (both streams, one device): the time the main stream waits for it is
+// the exposed exchange time.
+sem_status step_phase1_probe(sem_ctx *ctx) {
+    const DevChunks &d = ctx->dch;
+    if (!ctx->d_probe_list) {
+        CK(dalloc(ctx->mesh_allocs, &ctx->d_probe_list, d.nchunks));
+        CK(launch_iota(ctx->d_probe_list, d.nchunks, ctx->stream));
+        if (!ctx->comm_stream) CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+        for (auto &e : ctx->pev) CK(cudaEventCreate(&e));
+    }
+    const StepParams p = step_params(ctx);
+    const int64_t nb = d.nchunks / 8;
+    CK(cudaEventRecord(ctx->pev[0], ctx->stream));
+    CK(launch_k7(d, p, ctx->k7_grid, ctx->stream, ctx->d_probe_list, nb));
+    CK(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+    CK(launch_comm_standin(probe_us(), 4, ctx->comm_stream));
+    CK(cudaEventRecord(ctx->pev[3], ctx->comm_stream));
+    CK(cudaEventRecord(ctx->pev[1], ctx->stream));
+    CK(launch_k7(d, p, ctx->k7_grid_ovl, ctx->stream, ctx->d_probe_list + nb, d.nchunks - nb));
+    CK(launch_k8(d, p, ctx->stream));
+    CK(cudaEventRecord(ctx->pev[2], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->pev[3], 0));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float a = 0, b = 0, c = 0;
+    CK(cudaEventElapsedTime(&a, ctx->pev[0], ctx->pev[1]));  // boundary part
+    CK(cudaEventElapsedTime(&b, ctx->pev[1], ctx->pev[2]));  // interior part + K8
+    CK(cudaEventElapsedTime(&c, ctx->pev[1], ctx->pev[3]));  // stand-in done, from the interior start
+    ctx->probe_acc[0] += a;
+    ctx->probe_acc[1] += b;
+    ctx->probe_acc[2] += c;
+    ctx->probe_acc[3] += c > b ? c - b : 0.0;  // exposed: the main stream waits for the exchange
+    if (++ctx->probe_n % 200 == 0)
+        fprintf(stderr, "[overlap probe] comm SMs reserved %d, stand-in %.1f us on 4 CTAs: boundary K7 %.4f ms, "
+                        "interior K7+K8 %.4f ms, stand-in done %.4f ms after the interior start, exposed %.4f ms "
+                        "(averages over %lld steps)\n",
+                comm_sms(), probe_us(), ctx->probe_acc[0] / ctx->probe_n, ctx->probe_acc[1] / ctx->probe_n,
+                ctx->probe_acc[2] / ctx->probe_n, ctx->probe_acc[3] / ctx->probe_n, (long long)ctx->probe_n);
+    return SEM_OK;
+}
+
 sem_status step_phase1(sem_ctx *ctx, bool use_nccl) {
     CK(cudaSetDevice(ctx->device));
     ST(ensure_tables(ctx));
+    if (ctx->world == 1 && probe_us() > 0 && ctx->dch.nchunks >= 16 && !ctx->timing) return step_phase1_probe(ctx);
     const StepParams p = step_params(ctx);
     if (ctx->timing) ST(record(ctx, ctx->ev7, true));
     if (ctx->n_if == 0) {
@@ -624,7 +690,8 @@ sem_status step_phase1(sem_ctx *ctx, bool use_nccl) {
             ST(exchange_nccl(ctx, ctx->comm_stream));
             CK(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
         }
-        CK(launch_k7(ctx->dch, p, ctx->k7_grid, ctx->stream, ctx->d_intc, ctx->n_intc));
+        // interior chunks: with an exchange in flight, SEM_COMM_SMS SMs stay free for its kernels
+        CK(launch_k7(ctx->dch, p, use_nccl ? ctx->k7_grid_ovl : ctx->k7_grid, ctx->stream, ctx->d_intc, ctx->n_intc));
     }
     if (ctx->timing) ST(record(ctx, ctx->ev7, false));
     const bool k8 = p.cnt == nullptr;  // fused: K7 finalised the rank-local shared nodes
@@ -951,6 +1018,8 @@ void sem_free(sem_ctx *ctx) {
     if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
     if (ctx->ev_exchanged) cudaEventDestroy(ctx->ev_exchanged);
     if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    for (auto &e : ctx->pev)
+        if (e) cudaEventDestroy(e);
     if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1290,6 +1359,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         CK(cudaStreamSynchronize(s));
         tr.mark(s, "uploads + maps");
         ctx->k7_grid = k7_grid(d, false);
+        ctx->k7_grid_ovl = k7_grid(d, false, comm_sms());
         tr.mark(s, "k7 occupancy");
         ctx->meta_info = ChunkMeta();
         ChunkMeta &mi = ctx->meta_info;

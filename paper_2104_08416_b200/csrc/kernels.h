@@ -142,7 +142,9 @@ struct StepParams {
     int64_t n;         // step index of U
     const int64_t *n_dev;  // if set: the step index lives in device memory (CUDA-graph step loop)
 };
-int k7_grid(const DevChunks &ch, bool fused);
+// persistent K7 grid: resident CTAs per SM x SMs; reserve_sms SMs' worth of CTA slots are left free
+// (for the exchange kernels on the comm stream while the interior chunks run)
+int k7_grid(const DevChunks &ch, bool fused, int reserve_sms = 0);
 // resident K7 CTAs per SM for chunks of B elements with these per-chunk maxima (shared-memory stages)
 int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused);
 // device step counter of the graph-captured step loop: += 1, = v
@@ -150,6 +152,8 @@ int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool 
 // start while its predecessor drains and waits in griddepcontrol.wait before any data access
 cudaError_t launch_step_inc(int64_t *n, cudaStream_t s, bool pdl = false);
 cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s);
+// overlap probe: `ctas` small CTAs holding their SM slots for `us` microseconds (stand-in for NCCL)
+cudaError_t launch_comm_standin(double us, int ctas, cudaStream_t s);
 // K7 over all chunks (list == nullptr) or over the chunk ids list[0..nlist).
 cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaStream_t s,
                       const int32_t *list = nullptr, int64_t nlist = 0, bool pdl = false);

@@ -65,6 +65,21 @@ __global__ void k_step_inc(int64_t *n) {
 }
 __global__ void k_step_set(int64_t *n, int64_t v) { *n = v; }
 
+// One-GPU stand-in for the NCCL send/recv kernels of the interface exchange (overlap probe,
+// SEM_OVERLAP_PROBE_US): a few small CTAs that hold their SM slots for `ns` nanoseconds.
+__global__ void k_comm_standin(long long ns) {
+    extern __shared__ unsigned char standin_smem[];  // the footprint of the kernel it stands in for
+    if (threadIdx.x == 0) standin_smem[0] = 0;
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 >= ns) break;
+        __nanosleep(500);
+    }
+}
+
 inline unsigned blocks_for(int64_t n, int threads = kThreads) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -746,9 +761,11 @@ int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool 
     return occ < 1 ? 1 : occ;
 }
 
-int k7_grid(const DevChunks &ch, bool fused) {
+int k7_grid(const DevChunks &ch, bool fused, int reserve_sms) {
     const int occ = k7_ctas_per_sm(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_nsh, fused);
-    int64_t g = (int64_t)occ * current_sm_count();
+    const int nsm = current_sm_count();
+    if (reserve_sms >= nsm) reserve_sms = nsm - 1;
+    int64_t g = (int64_t)occ * (nsm - (reserve_sms > 0 ? reserve_sms : 0));
     if (persistent_grid_cap() > 0 && g > persistent_grid_cap()) g = persistent_grid_cap();
     if (g > ch.nchunks) g = ch.nchunks;
     return (int)g;
@@ -839,6 +856,15 @@ cudaError_t launch_abl_update(int64_t n, const StepParams &p, double *KU, cudaSt
 
 cudaError_t launch_step_inc(int64_t *n, cudaStream_t s, bool pdl) {
     return launch_ex(k_step_inc, 1, 1, 0, s, pdl, n);
+}
+
+cudaError_t launch_comm_standin(double us, int ctas, cudaStream_t s) {
+    static const int kb = [] { const char *e = getenv("SEM_OVERLAP_PROBE_SMEM_KB"); return e ? atoi(e) : 0; }();
+    const size_t smem = (size_t)(kb > 0 ? kb : 1) * 1024;
+    cudaError_t e = raise_max_smem((const void *)k_comm_standin, smem);
+    if (e != cudaSuccess) return e;
+    k_comm_standin<<<ctas, 128, smem, s>>>((long long)(us * 1e3));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s) {
