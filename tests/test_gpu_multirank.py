@@ -127,3 +127,53 @@ def test_nccl_unique_id_through_dlopen():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def _nccl_rank(rank, world, nccl_id, q):
+    from paper_2104_08416_b200 import meshgen as mg_
+    from paper_2104_08416_b200 import sem as S_
+    pb = mg_.config("C2", 8)
+    m = pb.mesh
+    rng = np.random.default_rng(5)
+    with S_.SemContext(rank, rank, world, nccl_id=nccl_id) as ctx:
+        r = ctx.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        U0 = rng.standard_normal(r["n_nodes"])
+        ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        ctx.sem_write_state(U0, U0)
+        ctx.sem_step_n(20)
+        out = np.full(r["n_nodes"], np.nan)
+        ctx.sem_read_field(out=out)
+    q.put((rank, out))
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available() or __import__("torch").cuda.device_count() < 2,
+                    reason="the NCCL transport needs two GPUs (the driver's GPU runs have one)")
+def test_nccl_two_gpus_bitwise_equal_to_loopback():
+    """The real transport: two processes, one GPU each, a real NCCL unique id; the merged
+    field must equal the in-process loopback group's bit for bit (same kernels, same
+    rank-ordered sums; only the transport differs)."""
+    import multiprocessing as mp
+    nid = S.nccl_unique_id()
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    ps = [ctx_mp.Process(target=_nccl_rank, args=(r, 2, nid, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    parts = dict(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    Un = np.where(np.isnan(parts[0]), parts[1], parts[0])
+    pb = mg.config("C2", 8)
+    m = pb.mesh
+    g = S.LoopbackGroup(2)
+    try:
+        r = g.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        U0 = np.random.default_rng(5).standard_normal(g.ctxs[0].N)
+        g.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        g.sem_write_state(U0, U0)
+        g.sem_step_n(20)
+        Ul, _ = g.sem_read_field()
+    finally:
+        g.close()
+    assert not np.isnan(Un).any()
+    assert np.array_equal(Un, Ul)
