@@ -98,10 +98,11 @@ __device__ __forceinline__ void heun_update(double u0, double hm, double r, doub
 
 // MODE 0: step with V^n stored (no lag); 1: step with V lagged by one W
 // update; 2: finalise V only.
-template <int NP, int B, int MODE>
-__global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
+template <int NP, int B, int MODE, int G = 1>
+__global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
     k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls, const int32_t *__restrict__ list,
            int64_t nlist) {
+    constexpr int C = B * G;  // consumer threads
     constexpr bool kLag = MODE >= 1, kStep = MODE <= 1, kFin = MODE == 2;
     extern __shared__ __align__(128) unsigned char sm[];
     const HeunLayout lay(NP, B, L, Lp, Ls);
@@ -113,6 +114,20 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
     uint64_t *wfull = empty + kStagesH;
     uint64_t *wempty = wfull + 1;
     uint64_t *idb = wempty + 1;  // shared-node ids landed
+    // G > 1: the five tables in shared memory, rows padded to an even length (16-byte pairs):
+    // Dr, Ds, Srr, Sss, Srs at tab + k * NP * kNPp.  Warp-uniform row, broadcast reads.
+    constexpr int kNPp = NP + (NP & 1);
+    double *tab = reinterpret_cast<double *>(idb + kStagesH);
+    if (G > 1) {
+        for (int i = threadIdx.x; i < NP * NP; i += blockDim.x) {
+            const int p = i / NP, q = i % NP;
+            tab[p * kNPp + q] = h_Dr[i];
+            tab[NP * kNPp + p * kNPp + q] = h_Ds[i];
+            tab[2 * NP * kNPp + p * kNPp + q] = h_Srr[i];
+            tab[3 * NP * kNPp + p * kNPp + q] = h_Sss[i];
+            tab[4 * NP * kNPp + p * kNPp + q] = h_Srs[i];
+        }
+    }
     const int t = threadIdx.x;
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
 
@@ -129,9 +144,9 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
     }
     __syncthreads();
 
-    if (t >= B) {
+    if (t >= C) {
         // ===== producer warp =====
-        const int lane = t - B;
+        const int lane = t - C;
         int k = 0;
         for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
             const int64_t c = list ? list[pos] : pos;
@@ -193,6 +208,193 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
         return;
     }
 
+    if constexpr (G > 1) {
+        // ===== consumer warps, G threads per element (high orders: P5 optionally, P7) =====
+        // Warp wi takes elements 32 (wi / G) + lane and the row block rb = wi % G (rows
+        // p = rb R + r) of every per-element product: the lagged V update (Algorithm 1) on its
+        // rows of V, its rows of Algorithm 2's aux = -detJ w J^-1 V handed to the element's
+        // other threads through shared memory (the entry buffer, before it holds entries), and
+        // its rows of r = D^T aux and y = K^e u (three products with the S tables, then
+        // combined with G_e).  The node phase is the G = 1 one with C threads.
+        constexpr int R = (NP + G - 1) / G;
+        const int wi = t >> 5, te = ((wi / G) << 5) + (t & 31), rb = wi % G;
+        const double f_n = src_term(a, a.src, a.n), f_n1 = src_term(a, a.src, a.n + 1);
+        double *xs = reinterpret_cast<double *>(ebuf);  // aux scratch [NP][2][B], aliases the entry buffer
+        int k = 0;
+        for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
+            const int64_t c = list ? list[pos] : pos;
+            const int s = k % kStagesH;
+            double *vg = a.V + (c * 2 * NP) * B + te;  // this element's V, layout [chunk][2 NP][B]
+            double v[2 * R];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const int p = rb * R + r;
+                v[r] = p < NP ? vg[p * B] : 0.0;
+                v[R + r] = p < NP ? vg[(NP + p) * B] : 0.0;
+            }
+            mbar_wait(&full[s], (k / kStagesH) & 1);
+            mbar_wait(&gath[s], (k / kStagesH) & 1);
+            const unsigned char *st = sm + s * lay.size;
+            const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
+            const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
+            const int i0 = m0.x, nint = m0.y, nsh = m0.w, ne = m1.y, ni_al = m1.z;
+            const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
+            const double *g_s = reinterpret_cast<const double *>(st + lay.g);
+            const bool act = te < ne;
+            const double F00 = g_s[te], F01 = g_s[B + te], F10 = g_s[2 * B + te], F11 = g_s[3 * B + te];
+            const double sd = g_s[4 * B + te];
+            if (kChecked) {
+                const int4 r0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+                SEM_DCHECK(r0.x == m0.x && r0.y == m0.y && r0.z == m0.z && r0.w == m0.w, "stage meta is this chunk's");
+                for (int e = t; e < NP * ne; e += C) {
+                    const int li = li_s[(e / ne) * B + e % ne];
+                    SEM_DCHECK(li < nint || (li >= ni_al && li < ni_al + nsh), "local index in range (poisoned?)");
+                }
+            }
+            // (1) lagged V update on this thread's rows: V^n = V^{n-1} + h F^T (D w)
+            if (kLag && act) {
+                const double *w_s = reinterpret_cast<const double *>(st + lay.w);
+                double gr[R], gs[R];
+#pragma unroll
+                for (int r = 0; r < R; r++) gr[r] = gs[r] = 0.0;
+                const double *tDr = tab + rb * R * kNPp, *tDs = tDr + NP * kNPp;
+#pragma unroll
+                for (int q = 0; q < NP; q += 2) {  // q pairs: one 16-byte broadcast read per table row
+                    const double w0 = w_s[li_s[q * B + te]];
+                    const double w1 = q + 1 < NP ? w_s[li_s[(q + 1) * B + te]] : 0.0;
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        if (rb * R + r < NP) {
+                            const double2 dr = *reinterpret_cast<const double2 *>(tDr + r * kNPp + q);
+                            const double2 ds = *reinterpret_cast<const double2 *>(tDs + r * kNPp + q);
+                            gr[r] = fma(dr.x, w0, gr[r]);
+                            gs[r] = fma(ds.x, w0, gs[r]);
+                            if (q + 1 < NP) {
+                                gr[r] = fma(dr.y, w1, gr[r]);
+                                gs[r] = fma(ds.y, w1, gs[r]);
+                            }
+                        }
+                    }
+                }
+                const double hF00 = a.h * F00, hF01 = a.h * F01, hF10 = a.h * F10, hF11 = a.h * F11;
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const int p = rb * R + r;
+                    if (p < NP) {
+                        v[r] = fma(hF00, gr[r], fma(hF10, gs[r], v[r]));
+                        v[R + r] = fma(hF01, gr[r], fma(hF11, gs[r], v[R + r]));
+                        vg[p * B] = v[r];
+                        vg[(NP + p) * B] = v[R + r];
+                    }
+                }
+            }
+            if (kStep) {
+                // (2a) Algorithm 2's aux on this thread's rows q: (ar, as)_q = -sd w_q F V_q
+                if (act) {
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        const int q = rb * R + r;
+                        if (q < NP) {
+                            const double sw = -sd * h_wK[q];
+                            xs[(2 * q) * B + te] = sw * fma(F00, v[r], F01 * v[R + r]);
+                            xs[(2 * q + 1) * B + te] = sw * fma(F10, v[r], F11 * v[R + r]);
+                        }
+                    }
+                }
+                consumer_sync<C>();
+                // (2b) r_p = sum_q Dr[q][p] ar_q + Ds[q][p] as_q; (3) y_p = (K^e u)_p, this thread's rows
+                double rr[R], yy[R];
+                const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
+                const double *u_s = reinterpret_cast<const double *>(st + lay.u);
+                if (act) {
+#pragma unroll
+                    for (int r = 0; r < R; r++) rr[r] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NP; q++) {
+                        const double ar = xs[(2 * q) * B + te], as = xs[(2 * q + 1) * B + te];
+                        const double *dq = tab + q * kNPp + rb * R;  // Dr[q][p], Ds[q][p]: row q, columns p
+#pragma unroll
+                        for (int r = 0; r < R; r++)
+                            if (rb * R + r < NP) rr[r] = fma(dq[r], ar, fma(dq[NP * kNPp + r], as, rr[r]));
+                    }
+                    const double grr = sd * fma(F00, F00, F01 * F01);
+                    const double gss = sd * fma(F10, F10, F11 * F11);
+                    const double grs = sd * fma(F00, F10, F01 * F11);
+                    double arr[R], ass[R], ars[R];
+#pragma unroll
+                    for (int r = 0; r < R; r++) arr[r] = ass[r] = ars[r] = 0.0;
+                    const double *tS = tab + 2 * NP * kNPp + rb * R * kNPp;
+#pragma unroll
+                    for (int q = 0; q < NP; q += 2) {
+                        const double u0 = u_s[li_s[q * B + te]];
+                        const double u1 = q + 1 < NP ? u_s[li_s[(q + 1) * B + te]] : 0.0;
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            if (rb * R + r < NP) {
+                                const double2 srr = *reinterpret_cast<const double2 *>(tS + r * kNPp + q);
+                                const double2 sss = *reinterpret_cast<const double2 *>(tS + NP * kNPp + r * kNPp + q);
+                                const double2 srs = *reinterpret_cast<const double2 *>(tS + 2 * NP * kNPp + r * kNPp + q);
+                                arr[r] = fma(srr.x, u0, arr[r]);
+                                ass[r] = fma(sss.x, u0, ass[r]);
+                                ars[r] = fma(srs.x, u0, ars[r]);
+                                if (q + 1 < NP) {
+                                    arr[r] = fma(srr.y, u1, arr[r]);
+                                    ass[r] = fma(sss.y, u1, ass[r]);
+                                    ars[r] = fma(srs.y, u1, ars[r]);
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < R; r++) yy[r] = fma(grr, arr[r], fma(gss, ass[r], grs * ars[r]));
+                }
+                consumer_sync<C>();  // every aux read before the entries overwrite it
+                if (act) {
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        const int p = rb * R + r;
+                        if (p < NP) ebuf[lpo[p * B + te]] = make_double2(rr[r], yy[r]);
+                    }
+                }
+                consumer_sync<C>();
+                mbar_wait(wfull, k & 1);
+                // (4) node-centric reduction in fixed (JDS diagonal) order + fused Heun update
+                const uint16_t *jd = reinterpret_cast<const uint16_t *>(st + lay.jds);
+                const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
+                const int nwork = nint + nsh;
+                for (int wk = t; wk < nwork; wk += C) {
+                    const int i = wk < nint ? wk : ni_al + (wk - nint);  // skips the alignment hole
+                    const double2 ab = i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al);
+                    if (i < nint) {
+                        const int64_t id = i0 + i;
+                        const bool src = id == a.src;
+                        heun_update(u_s[i], m_s[i], ab.x, ab.y, src ? f_n : 0.0, src ? f_n1 : 0.0, a.h, a.W[id],
+                                    a.U[id]);
+                    } else {
+                        reinterpret_cast<double2 *>(a.slot)[shs[i - ni_al]] = ab;
+                    }
+                }
+            }
+            consumer_sync<C>();
+            if (kChecked) {
+                unsigned char *stw = sm + s * lay.size;
+                double *uw = reinterpret_cast<double *>(stw + lay.u);
+                double *ww = reinterpret_cast<double *>(stw + lay.w);
+                uint16_t *lw = reinterpret_cast<uint16_t *>(stw + lay.lidx);
+                for (int i = t; i < ni_al + nsh; i += C) { uw[i] = poison_f64(); ww[i] = poison_f64(); }
+                for (int i = t; i < (kStep ? 2 : 1) * NP * B; i += C) lw[i] = 0xFFFF;
+                if (kStep) for (int i = t; i < ni_al; i += C) m_s[i] = poison_f64();
+                consumer_sync<C>();
+            }
+            if (t == 0) {
+                mbar_arrive(&empty[s]);
+                if (kStep) mbar_arrive(wempty);
+            }
+        }
+        return;
+    }
+
+    if constexpr (G == 1) {
     // ===== consumer warps =====
     // the source terms f^n, f^{n+1} of this step, once per thread (cold exp() code out of the loops)
     const double f_n = src_term(a, a.src, a.n), f_n1 = src_term(a, a.src, a.n + 1);
@@ -366,6 +568,7 @@ __global__ void __launch_bounds__(B + 32, B <= 128 ? 2 : 1)
             if (kStep) mbar_arrive(wempty);
         }
     }
+    }
 }
 
 // ---- KH8: shared-node fix-up ------------------------------------------------------
@@ -441,19 +644,33 @@ cudaError_t set_smem_h(K kernel, size_t bytes) {
     return raise_max_smem((const void *)kernel, bytes);
 }
 
+int heun_group(int np);
 size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
     const HeunLayout lay(np, B, L, Lp, Ls);
     const bool step = mode <= 1;
-    return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8;
+    const size_t tabs = heun_group(np) > 1 ? 5 * (size_t)np * (np + (np & 1)) * 8 : 0;
+    return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8 +
+           tabs;
 }
 
 using HFn = void (*)(const DevChunks, const HeunParams, int, int, int, int, const int32_t *, int64_t);
-template <int NP, int B>
+template <int NP, int B, int G = 1>
 HFn heun_fn_b(int mode) {
-    return mode == 0 ? k_heun<NP, B, 0> : mode == 1 ? k_heun<NP, B, 1> : k_heun<NP, B, 2>;
+    return mode == 0 ? k_heun<NP, B, 0, G> : mode == 1 ? k_heun<NP, B, 1, G> : k_heun<NP, B, 2, G>;
+}
+// consumer threads per element of the Heun kernel: P7 4 (chunks of 64), P5 SEM_HEUN_G5 (default 4:
+// B1 1.044 -> 0.779 ms per step against 1 thread per element; 2: 0.803)
+int heun_group(int np) {
+    static int g5 = -1;
+    if (g5 < 0) { const char *e = getenv("SEM_HEUN_G5"); g5 = e ? atoi(e) : 4; if (g5 != 1 && g5 != 2 && g5 != 4) g5 = 4; }
+    return np == 36 ? 4 : np == 21 ? g5 : 1;
 }
 HFn heun_fn(int np, int B, int mode) {
-    if (np == 21) return heun_fn_b<21, 128>(mode);  // P5 (the paper's Benchmark 1 order)
+    if (np == 36) return heun_fn_b<36, 64, 4>(mode);  // P7 (the paper's order-7 runs)
+    if (np == 21) {                                      // P5 (the paper's Benchmark 1 order)
+        const int g = heun_group(21);
+        return g == 4 ? heun_fn_b<21, 128, 4>(mode) : g == 2 ? heun_fn_b<21, 128, 2>(mode) : heun_fn_b<21, 128>(mode);
+    }
     if (np == 6) return B == 128 ? heun_fn_b<6, 128>(mode) : heun_fn_b<6, 256>(mode);
     return B == 128 ? heun_fn_b<10, 128>(mode) : heun_fn_b<10, 256>(mode);
 }
@@ -463,7 +680,7 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n + 2
 }  // namespace
 
 bool heun_supported(int np, int B) {
-    return ((np == 6 || np == 10) && (B == 128 || B == 256)) || (np == 21 && B == 128);
+    return ((np == 6 || np == 10) && (B == 128 || B == 256)) || (np == 21 && B == 128) || (np == 36 && B == 64);
 }
 
 cudaError_t upload_heun_tables(const RefTables &T, cudaStream_t s) {
@@ -497,7 +714,7 @@ int heun_grid(const DevChunks &ch, int mode) {
     const HFn fn = heun_fn(ch.Np, ch.B, mode);
     set_smem_h(fn, smem);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B + 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B * heun_group(ch.Np) + 32, smem);
     if (occ < 1) occ = 1;
     int64_t g = (int64_t)occ * current_sm_count();
     if (persistent_grid_cap() > 0 && g > persistent_grid_cap()) g = persistent_grid_cap();
@@ -515,7 +732,8 @@ cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cuda
     if (e != cudaSuccess) return e;
     int grid = heun_grid(ch, mode);
     if (grid > n) grid = (int)n;
-    fn<<<grid, ch.B + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list, nlist);
+    fn<<<grid, ch.B * heun_group(ch.Np) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list,
+                                                         nlist);
     return cudaGetLastError();
 }
 

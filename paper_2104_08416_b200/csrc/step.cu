@@ -256,11 +256,13 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     const int64_t nch = list ? nlist : ch.nchunks;  // chunks this launch walks
     pdl_trigger();  // the next kernel (K8) may be scheduled; it waits for this grid to complete
 
+    constexpr int kNPp = NP + (NP & 1);  // G > 1: S table rows padded to an even length (16-byte pairs)
     if (G > 1) {
         for (int i = t; i < NP * NP; i += blockDim.x) {
-            S_s[i] = c_Srr[i];
-            S_s[NP * NP + i] = c_Sss[i];
-            S_s[2 * NP * NP + i] = c_Srs[i];
+            const int p = i / NP, q = i % NP;
+            S_s[p * kNPp + q] = c_Srr[i];
+            S_s[NP * kNPp + p * kNPp + q] = c_Sss[i];
+            S_s[2 * NP * kNPp + p * kNPp + q] = c_Srs[i];
         }
     }
     if (t == 0) {
@@ -418,13 +420,21 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 for (int r = 0; r < R; r++) {
                     const int p = p0 + r;
                     if (p < NP) {
-                        const double *srr = S_s + p * NP, *sss = S_s + NP * NP + p * NP, *srs = S_s + 2 * NP * NP + p * NP;
+                        const double *srr = S_s + p * kNPp, *sss = srr + NP * kNPp, *srs = sss + NP * kNPp;
                         double arr = 0.0, ass = 0.0, ars = 0.0;
 #pragma unroll
-                        for (int q = 0; q < NP; q++) {
-                            arr = fma(srr[q], u[q], arr);
-                            ass = fma(sss[q], u[q], ass);
-                            ars = fma(srs[q], u[q], ars);
+                        for (int q = 0; q < NP; q += 2) {  // one 16-byte broadcast read per table and q pair
+                            const double2 a2 = *reinterpret_cast<const double2 *>(srr + q);
+                            const double2 b2 = *reinterpret_cast<const double2 *>(sss + q);
+                            const double2 c2 = *reinterpret_cast<const double2 *>(srs + q);
+                            arr = fma(a2.x, u[q], arr);
+                            ass = fma(b2.x, u[q], ass);
+                            ars = fma(c2.x, u[q], ars);
+                            if (q + 1 < NP) {
+                                arr = fma(a2.y, u[q + 1], arr);
+                                ass = fma(b2.y, u[q + 1], ass);
+                                ars = fma(c2.y, u[q + 1], ars);
+                            }
                         }
                         ebuf[lpo[p * B + te]] = fma(grr, arr, fma(gss, ass, grs * ars));
                     }
@@ -663,14 +673,14 @@ int k7_win() {
 int k7_group(int np) {
     static int g7 = -1, g5 = -1;
     if (g7 < 0) { const char *e = getenv("SEM_K7_G"); g7 = e ? atoi(e) : 4; if (g7 != 1 && g7 != 2 && g7 != 4) g7 = 4; }
-    if (g5 < 0) { const char *e = getenv("SEM_K7_G5"); g5 = e ? atoi(e) : 1; if (g5 != 1 && g5 != 2) g5 = 1; }
+    if (g5 < 0) { const char *e = getenv("SEM_K7_G5"); g5 = e ? atoi(e) : 1; if (g5 != 1 && g5 != 2 && g5 != 4) g5 = 1; }
     return (np == 36 || np == 28) ? g7 : np == 21 ? g5 : 1;
 }
 
 size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
     const int wm = k7_win();
     const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, wm == 2 ? W : 0);
-    const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * np * 8 : 0;
+    const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * (np + (np & 1)) * 8 : 0;
     return (size_t)kStages * lay.size + (size_t)np * B * 8 + (wm == 1 ? 2 * (size_t)W * 8 : 0) +
            (4 * kStages + 2) * 8 + stab;
 }
@@ -679,7 +689,10 @@ using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, con
 template <int W2>
 K7Fn k7_fn_w(int np, int B) {
     if (np == 15) return k7_step<15, 128, W2>;  // P4 (R21b): chunks of 128
-    if (np == 21) return k7_group(21) == 2 ? k7_step<21, 128, W2, 2> : k7_step<21, 128, W2>;  // P5 (R21): chunks of 128
+    if (np == 21) {  // P5 (R21): chunks of 128
+        const int g = k7_group(21);
+        return g == 4 ? k7_step<21, 128, W2, 4> : g == 2 ? k7_step<21, 128, W2, 2> : k7_step<21, 128, W2>;
+    }
     if (np == 28) {                              // P6 (R21b): chunks of 64, G threads per element
         const int g = k7_group(28);
         return g == 4 ? k7_step<28, 64, W2, 4> : g == 2 ? k7_step<28, 64, W2, 2> : k7_step<28, 64, W2, 1>;

@@ -157,7 +157,7 @@ def test_heun_zero_source_stays_zero_and_errors(ctx):
 
 
 @pytest.mark.parametrize("world,name,scale,P", [(2, "C2", 8, None), (3, "C1", 1, None), (4, "C3", 20, None),
-                                                 (8, "C5", 128, None), (3, "B1", 25, 5)])
+                                                 (8, "C5", 128, None), (3, "B1", 25, 5), (2, "B1", 30, 7)])
 def test_heun_multirank_loopback(ctx, world, name, scale, P):
     """Heun across G partitions (SURVEY §8e with the (R(V), K U) payload, loopback
     transport on one GPU): equal to the oracle (<= 1e-10 after a Ricker run,
@@ -202,13 +202,15 @@ def test_heun_multirank_loopback(ctx, world, name, scale, P):
         g.close()
 
 
+@pytest.mark.parametrize("P", [5, 7])
 @pytest.mark.parametrize("steps", [1, 10, 60])
-def test_heun_p5_parity(ctx, steps):
-    """The paper's Benchmark 1 order (P5) with its own integrator."""
-    pb = mg.config("B1", 30, degree=5)  # 33 x 16 cells: ragged last chunk of 128
+def test_heun_p5_parity(ctx, steps, P):
+    """The paper's Benchmark 1 orders 5 and 7 with its own
+    integrator (P7: 4 threads per element, chunks of 64)."""
+    pb = mg.config("B1", 30, degree=P)  # 33 x 16 cells: ragged last chunk of 128 / 64
     m = pb.mesh
     h = mg.heun_h(pb)
-    o = OracleSEM(m.vxy, m.tri, 5, pb.c)
+    o = OracleSEM(m.vxy, m.tri, P, pb.c)
     rng = np.random.default_rng(steps)
     U0 = rng.standard_normal(o.N)
     V0 = rng.standard_normal((m.ne, o.Np, 2))

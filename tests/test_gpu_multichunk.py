@@ -76,7 +76,7 @@ def test_leapfrog_many_chunks_per_cta(monkeypatch, P, grid_cap):
             assert np.array_equal(Ug, Ufull)
 
 
-@pytest.mark.parametrize("P", [2, 3, 5])
+@pytest.mark.parametrize("P", [2, 3, 5, 7])
 @pytest.mark.parametrize("grid_cap", [1, 3])
 def test_heun_many_chunks_per_cta(monkeypatch, P, grid_cap):
     monkeypatch.setenv("SEM_K7_GRID", str(grid_cap))
