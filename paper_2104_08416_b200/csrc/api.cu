@@ -31,6 +31,10 @@ int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 // selects the other compiled variants (design experiments, chunk size).
 int chunk_elems(int P, bool heun) {
     const char *v = getenv("SEM_CHUNK");
+    if (heun && (P == 5 || P == 7)) {  // Heun's wide kernel: SEM_CHUNK=32|64|128 (A/B)
+        const int b = v ? atoi(v) : (P == 5 ? 128 : 64);
+        return (b == 32 || b == 64 || (P == 5 && b == 128)) ? b : (P == 5 ? 128 : 64);
+    }
     if (P == 4 || P == 5) return 128;  // shared-memory budget of the stage at 15 / 21 nodes per element
     if (P == 6 || P == 7) return 64;   // ... and at 28 / 36
     // Heun (integrator selected before sem_mesh_reorder): 128 runs 2 CTAs per SM

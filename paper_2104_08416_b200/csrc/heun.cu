@@ -644,11 +644,11 @@ cudaError_t set_smem_h(K kernel, size_t bytes) {
     return raise_max_smem((const void *)kernel, bytes);
 }
 
-int heun_group(int np);
+int heun_group(int np, int B);
 size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
     const HeunLayout lay(np, B, L, Lp, Ls);
     const bool step = mode <= 1;
-    const size_t tabs = heun_group(np) > 1 ? 5 * (size_t)np * (np + (np & 1)) * 8 : 0;
+    const size_t tabs = heun_group(np, B) > 1 ? 5 * (size_t)np * (np + (np & 1)) * 8 : 0;
     return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8 +
            tabs;
 }
@@ -665,10 +665,15 @@ int heun_group(int np) {
     if (g5 < 0) { const char *e = getenv("SEM_HEUN_G5"); g5 = e ? atoi(e) : 4; if (g5 != 1 && g5 != 2 && g5 != 4) g5 = 4; }
     return np == 36 ? 4 : np == 21 ? g5 : 1;
 }
+int heun_group(int np, int B) {
+    return np == 21 && B < 128 ? 4 : heun_group(np);
+}
 HFn heun_fn(int np, int B, int mode) {
-    if (np == 36) return heun_fn_b<36, 64, 4>(mode);  // P7 (the paper's order-7 runs)
+    if (np == 36) return B == 32 ? heun_fn_b<36, 32, 4>(mode) : heun_fn_b<36, 64, 4>(mode);  // P7
     if (np == 21) {                                      // P5 (the paper's Benchmark 1 order)
         const int g = heun_group(21);
+        if (B == 64) return heun_fn_b<21, 64, 4>(mode);
+        if (B == 32) return heun_fn_b<21, 32, 4>(mode);
         return g == 4 ? heun_fn_b<21, 128, 4>(mode) : g == 2 ? heun_fn_b<21, 128, 2>(mode) : heun_fn_b<21, 128>(mode);
     }
     if (np == 6) return B == 128 ? heun_fn_b<6, 128>(mode) : heun_fn_b<6, 256>(mode);
@@ -680,7 +685,8 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n + 2
 }  // namespace
 
 bool heun_supported(int np, int B) {
-    return ((np == 6 || np == 10) && (B == 128 || B == 256)) || (np == 21 && B == 128) || (np == 36 && B == 64);
+    return ((np == 6 || np == 10) && (B == 128 || B == 256)) || (np == 21 && (B == 32 || B == 64 || B == 128)) ||
+           (np == 36 && (B == 32 || B == 64));
 }
 
 cudaError_t upload_heun_tables(const RefTables &T, cudaStream_t s) {
@@ -714,7 +720,7 @@ int heun_grid(const DevChunks &ch, int mode) {
     const HFn fn = heun_fn(ch.Np, ch.B, mode);
     set_smem_h(fn, smem);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B * heun_group(ch.Np) + 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B * heun_group(ch.Np, ch.B) + 32, smem);
     if (occ < 1) occ = 1;
     int64_t g = (int64_t)occ * current_sm_count();
     if (persistent_grid_cap() > 0 && g > persistent_grid_cap()) g = persistent_grid_cap();
@@ -732,7 +738,7 @@ cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cuda
     if (e != cudaSuccess) return e;
     int grid = heun_grid(ch, mode);
     if (grid > n) grid = (int)n;
-    fn<<<grid, ch.B * heun_group(ch.Np) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list,
+    fn<<<grid, ch.B * heun_group(ch.Np, ch.B) + 32, smem, s>>>(ch, p, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, list,
                                                          nlist);
     return cudaGetLastError();
 }

@@ -750,11 +750,11 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer,
     if (ch.Np == 15) {
         MASS(15, 128);
     } else if (ch.Np == 21) {
-        MASS(21, 128);
+        if (ch.B == 32) MASS(21, 32); else if (ch.B == 64) MASS(21, 64); else MASS(21, 128);
     } else if (ch.Np == 28) {
         MASS(28, 64);
     } else if (ch.Np == 36) {
-        MASS(36, 64);
+        if (ch.B == 32) MASS(36, 32); else MASS(36, 64);
     } else if (ch.Np == 6) {
         if (ch.B == 128) MASS(6, 128); else if (ch.B == 192) MASS(6, 192); else if (ch.B == 512) MASS(6, 512); else MASS(6, 256);
     } else {
