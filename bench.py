@@ -473,12 +473,15 @@ def orders_leg(ctx, args, S, peak, peaks):
                 "k7_hbm_frac": b7 / (k7 * 1e-3) / 1e9 / peak,
                 "k7_fp64_tflops": tf, "k7_fp64_frac": tf / FP64_PEAK_TFLOPS,
                 "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_peak_source": FP64_PEAK_SOURCE, "steps": K}
-    # the paper's own Benchmark 1 workload: Heun, order 5, 1M elements
-    pb = mg.config("B1", 1, degree=5)
-    for name, eo, no in [("hilbert", S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH),
-                         ("none", S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL)]:
+    # the paper's own Benchmark 1 workload: Heun, orders 5 and 7, 1M elements
+    # (Table avg_cpu_time_orders_exp_1)
+    for P, name, eo, no in [(5, "hilbert", S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH),
+                            (5, "none", S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL),
+                            (7, "hilbert", S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH),
+                            (7, "none", S.SEM_ORDER_INPUT, S.SEM_NODES_CANONICAL)]:
+        pb = mg.config("B1", 1, degree=P)
         ctx.sem_set_integrator(S.SEM_INTEGRATOR_HEUN)
-        ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, 5, eo, no)
+        ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, P, eo, no)
         ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, pb.amplitude, pb.dt * 0.2)
         ctx.sem_step_n(5)
         K = max(50, min(args.steps, 300))
@@ -491,12 +494,13 @@ def orders_leg(ctx, args, S, peak, peaks):
         ms = e0.elapsed_time(e1) / K
         info = ctx.sem_get_info()
         ctx.sem_set_integrator(S.SEM_INTEGRATOR_LEAPFROG)
-        paper_s = {"hilbert": 1.465, "none": 1.736}[name]  # PAPER.md:596, 1M elements, order 5, 32 threads
-        res["P5_heun_%s" % name] = {
+        # PAPER.md:764-770 (1M elements, 32 threads): order 5 SFC 1.465 s / None 1.736 s, order 7 3.414 / 4.010
+        paper_s = {(5, "hilbert"): 1.465, (5, "none"): 1.736, (7, "hilbert"): 3.414, (7, "none"): 4.010}[(P, name)]
+        res["P%d_heun_%s" % (P, name)] = {
             "elements": info["n_elements"], "element_updates_per_s": info["n_elements"] / (ms * 1e-3),
             "ms_per_step": ms, "alg_gbs": info["bytes_alg_per_step"] / (ms * 1e-3) / 1e9, "steps": K,
             "paper_context": {"s_per_step": paper_s, "machine": "Xeon E5-2698 v3, 32 threads",
-                              "source": "PAPER.md:596 (Table avg_cpu_time_threads_exp_1, SFC / None)",
+                              "source": "PAPER.md:764-770 (Table avg_cpu_time_orders_exp_1, SFC / None)",
                               "ratio_to_paper": paper_s / (ms * 1e-3)}}
     return res
 

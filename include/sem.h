@@ -211,9 +211,12 @@ sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps);
  * y(t)) with R = Algorithm 2 (B = -I) and y = Algorithm 3;
  * t_n = n h, the corrector's source at t_{n+1} (reading R18).  The state is
  * (U [N], V [E][Np][2]), zero after sem_build_operators; `dt` is h.  Heun runs
- * at P = 2, 3 (chunks of 128 or 256 elements) and P = 5, on one rank or
+ * at P = 2, 3 (chunks of 128 or 256 elements), P = 5 (chunks of 128) and P = 7
+ * (chunks of 64; the paper's order-7 runs), on one rank or
  * several (interface exchange of the (R(V), K U) pairs; loopback groups too).
- * Selecting HEUN before sem_mesh_reorder also picks its chunk size (128).
+ * P = 4, 6 have no nodal quadrature (reading R21b): SEM_E_UNSUPPORTED
+ * from sem_build_operators.  Selecting HEUN before sem_mesh_reorder also picks
+ * its chunk size.
  * Errors: SEM_E_UNSUPPORTED (unknown integrator).
  */
 sem_status sem_set_integrator(sem_ctx *ctx, int integrator);
