@@ -82,6 +82,22 @@ enum { SEM_NUMBERING_CANONICAL = 0, SEM_NUMBERING_INTERNAL = 1 };
 enum { SEM_INTEGRATOR_LEAPFROG = 0, SEM_INTEGRATOR_HEUN = 1 };
 
 /*
+ * Device-memory hook: every device allocation of a context -- its mesh and
+ * operator arrays and every temporary of its calls -- goes through alloc / free when a hook
+ * is given (e.g. a caching allocator of the caller's framework: sem.py can route it to
+ * PyTorch's), else through cudaMallocAsync / cudaFreeAsync.  alloc(bytes, stream, user)
+ * returns device memory usable in stream order on `stream` (the context's stream, a
+ * cudaStream_t) or NULL on failure (-> SEM_E_CUDA); free(ptr, stream, user) releases it in
+ * stream order.  The hook is copied by sem_create and called only from inside that
+ * context's calls, on the calling thread.
+ */
+typedef struct {
+    void *(*alloc)(size_t bytes, void *stream, void *user);
+    void (*free)(void *ptr, void *stream, void *user);
+    void *user;
+} sem_allocator;
+
+/*
  * Create a context on CUDA device `device`.
  *  rank, world_size : this process's place in a multi-GPU run (world_size = 1
  *                     for one GPU; at most 32).  Rank r owns the contiguous
@@ -95,12 +111,13 @@ enum { SEM_INTEGRATOR_LEAPFROG = 0, SEM_INTEGRATOR_HEUN = 1 };
  *                     sem_group_build_operators / sem_group_step_n.
  *  cuda_stream      : cudaStream_t to enqueue on (e.g. torch's current stream),
  *                     or NULL for a stream owned by the context.
+ *  alloc            : device-memory hook (above), or NULL for cudaMallocAsync.
  * Errors: SEM_E_ARG (bad rank/world/device), SEM_E_CUDA (no sm_100 device),
  *         SEM_E_NCCL (libnccl.so.2 not loadable / ncclCommInitRank failed).
  * On error *out may still hold a context carrying the message; free it.
  */
 sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
-                      const void *nccl_unique_id, void *cuda_stream);
+                      const void *nccl_unique_id, void *cuda_stream, const sem_allocator *alloc);
 
 /* 128-byte NCCL unique id for sem_create (call on rank 0, broadcast the bytes).
  * NCCL is loaded with dlopen("libnccl.so.2").  Errors: SEM_E_ARG, SEM_E_NCCL. */

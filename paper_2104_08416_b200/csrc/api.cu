@@ -103,6 +103,22 @@ NcclApi &nccl() {
 }
 }  // namespace
 
+// ---- device memory: the context's sem_allocator hook, or the stream-ordered pool ----
+namespace {
+thread_local const sem_allocator *t_alloc = nullptr;  // the hook of the API call running on this thread
+}
+cudaError_t sem::dev_malloc_raw(void **p, size_t bytes, cudaStream_t s) {
+    if (!t_alloc) return cudaMallocAsync(p, bytes, s);
+    *p = t_alloc->alloc(bytes, (void *)s, t_alloc->user);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+cudaError_t sem::dev_free(void *p, cudaStream_t s) {
+    if (!p) return cudaSuccess;
+    if (!t_alloc) return cudaFreeAsync(p, s);
+    t_alloc->free(p, (void *)s, t_alloc->user);
+    return cudaSuccess;
+}
+
 // Device arrays that live as long as a mesh or its operators: stream-ordered pool
 // allocations on the context's stream (the pool keeps freed memory mapped, so a
 // later sem_mesh_reorder does not pay cudaMalloc's page mapping again).
@@ -112,13 +128,15 @@ struct AllocList {
     size_t size() const { return p.size(); }
     void push_back(void *q) { p.push_back(q); }
     void release_from(size_t n) {  // free the entries [n, size)
-        for (size_t i = n; i < p.size(); i++) cudaFreeAsync(p[i], s);
+        for (size_t i = n; i < p.size(); i++) dev_free(p[i], s);
         p.resize(n);
     }
 };
 
 struct sem_ctx {
     int device = 0, rank = 0, world = 1;
+    sem_allocator alloc{};     // device-memory hook (sem.h); has_alloc = false: cudaMallocAsync
+    bool has_alloc = false;
     bool loopback = false;  // world > 1 without NCCL: only the sem_group_* calls may step it
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
@@ -215,6 +233,13 @@ sem_status cuda_fail(sem_ctx *c, cudaError_t e, const char *where) {
     return SEM_E_CUDA;
 }
 
+// Installs a context's device-memory hook on this thread for the duration of an API call.
+struct AllocScope {
+    const sem_allocator *prev;
+    explicit AllocScope(const sem_ctx *c) : prev(t_alloc) { t_alloc = (c && c->has_alloc) ? &c->alloc : nullptr; }
+    ~AllocScope() { t_alloc = prev; }
+};
+
 #define CK(call)                                                        \
     do {                                                                \
         cudaError_t _e = (call);                                        \
@@ -233,14 +258,14 @@ struct TmpList {
     cudaStream_t s;
     std::vector<void *> p;
     ~TmpList() {
-        for (void *q : p) cudaFreeAsync(q, s);
+        for (void *q : p) dev_free(q, s);
     }
 };
 
 template <typename T>
 cudaError_t dalloc(TmpList &t, T **p, size_t count) {
     void *q = nullptr;
-    cudaError_t e = cudaMallocAsync(&q, sizeof(T) * (count ? count : 1), t.s);
+    cudaError_t e = dev_malloc(&q, sizeof(T) * (count ? count : 1), t.s);
     if (e != cudaSuccess) return e;
     t.p.push_back(q);
     *p = (T *)q;
@@ -250,7 +275,7 @@ cudaError_t dalloc(TmpList &t, T **p, size_t count) {
 template <typename T>
 cudaError_t dalloc(AllocList &list, T **p, size_t count) {
     void *q = nullptr;
-    cudaError_t e = cudaMallocAsync(&q, sizeof(T) * (count ? count : 1), list.s);
+    cudaError_t e = dev_malloc(&q, sizeof(T) * (count ? count : 1), list.s);
     if (e != cudaSuccess) return e;
     list.push_back(q);
     *p = (T *)q;
@@ -942,13 +967,18 @@ sem_status sem_nccl_unique_id(void *out128) {
 }
 
 sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
-                      const void *nccl_unique_id, void *cuda_stream) {
+                      const void *nccl_unique_id, void *cuda_stream, const sem_allocator *alloc) {
     if (!out) return SEM_E_ARG;
     *out = nullptr;
     if (world_size < 1 || world_size > 32 || rank < 0 || rank >= world_size || device < 0) return SEM_E_ARG;
+    if (alloc && (!alloc->alloc || !alloc->free)) return SEM_E_ARG;
     sem_ctx *ctx = new (std::nothrow) sem_ctx();
     if (!ctx) return SEM_E_OOM;
     *out = ctx;
+    if (alloc) {
+        ctx->alloc = *alloc;
+        ctx->has_alloc = true;
+    }
     ctx->device = device;
     ctx->rank = rank;
     ctx->world = world_size;
@@ -1009,6 +1039,7 @@ sem_status sem_create(sem_ctx **out, int device, int rank, int world_size,
 }
 
 void sem_free(sem_ctx *ctx) {
+    AllocScope scope_(ctx);
     if (!ctx) return;
     if (!ctx->dead) {
         cudaSetDevice(ctx->device);
@@ -1037,6 +1068,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
                             uint32_t *hilbert_key_out, int32_t *elem_perm_out,
                             int32_t *node_perm_out, int64_t *n_nodes_out,
                             int32_t grid_wh_out[2]) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (!degree_supported(degree))
         return fail(ctx, SEM_E_UNSUPPORTED, "unsupported degree " + std::to_string(degree) + " (2 to 7)");
@@ -1380,6 +1412,7 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
 
 sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t src_vertex,
                                double f0, double t0, double amplitude, double dt) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions are built with sem_group_build_operators");
     try {
@@ -1392,6 +1425,7 @@ sem_status sem_build_operators(sem_ctx *ctx, const double *c_elem_host, int64_t 
 }
 
 sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_step_n before sem_build_operators");
     if (ctx->loopback) return fail(ctx, SEM_E_STATE, "loopback partitions step with sem_group_step_n");
@@ -1423,6 +1457,13 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
 
 sem_status sem_group_build_operators(sem_ctx **ctxs, int n, const double *c_elem_host, int64_t src_vertex,
                                      double f0, double t0, double amplitude, double dt) {
+    AllocScope scope_((ctxs && n > 0) ? ctxs[0] : nullptr);
+    for (int r = 1; ctxs && r < n; r++)  // one hook for the group (allocated and freed by each member)
+        if (!ctxs[r] || ctxs[r]->has_alloc != ctxs[0]->has_alloc ||
+            (ctxs[r]->has_alloc && (ctxs[r]->alloc.alloc != ctxs[0]->alloc.alloc ||
+                                    ctxs[r]->alloc.free != ctxs[0]->alloc.free ||
+                                    ctxs[r]->alloc.user != ctxs[0]->alloc.user)))
+            return SEM_E_ARG;
     if (!ctxs || n < 1) return SEM_E_ARG;
     for (int r = 0; r < n; r++) {
         ST(check_usable(ctxs[r]));
@@ -1439,6 +1480,13 @@ sem_status sem_group_build_operators(sem_ctx **ctxs, int n, const double *c_elem
 }
 
 sem_status sem_group_step_n(sem_ctx **ctxs, int n, int64_t n_steps) {
+    AllocScope scope_((ctxs && n > 0) ? ctxs[0] : nullptr);
+    for (int r = 1; ctxs && r < n; r++)  // one hook for the group (allocated and freed by each member)
+        if (!ctxs[r] || ctxs[r]->has_alloc != ctxs[0]->has_alloc ||
+            (ctxs[r]->has_alloc && (ctxs[r]->alloc.alloc != ctxs[0]->alloc.alloc ||
+                                    ctxs[r]->alloc.free != ctxs[0]->alloc.free ||
+                                    ctxs[r]->alloc.user != ctxs[0]->alloc.user)))
+            return SEM_E_ARG;
     if (!ctxs || n < 1 || n_steps < 0) return SEM_E_ARG;
     for (int r = 0; r < n; r++) {
         ST(check_usable(ctxs[r]));
@@ -1474,6 +1522,7 @@ sem_status sem_set_integrator(sem_ctx *ctx, int integrator) {
 }
 
 sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (!ctx->have_ops || ctx->ops_integrator != SEM_INTEGRATOR_HEUN)
         return fail(ctx, SEM_E_STATE, "sem_read_velocity needs operators built for the Heun integrator");
@@ -1505,6 +1554,7 @@ sem_status sem_read_velocity(sem_ctx *ctx, double *out_host, int64_t *step_out) 
 }
 
 sem_status sem_write_velocity(sem_ctx *ctx, const double *v_host) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (!ctx->have_ops || ctx->ops_integrator != SEM_INTEGRATOR_HEUN)
         return fail(ctx, SEM_E_STATE, "sem_write_velocity needs operators built for the Heun integrator");
@@ -1525,6 +1575,7 @@ sem_status sem_write_velocity(sem_ctx *ctx, const double *v_host) {
 }
 
 sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t *step_out) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_read_field before sem_build_operators");
     if (!out_host) return fail(ctx, SEM_E_ARG, "out is NULL");
@@ -1558,6 +1609,7 @@ sem_status sem_read_field(sem_ctx *ctx, double *out_host, int numbering, int64_t
 
 sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double *u_prev_host,
                            int numbering) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_write_state before sem_build_operators");
     if (numbering != SEM_NUMBERING_CANONICAL && numbering != SEM_NUMBERING_INTERNAL)
@@ -1584,6 +1636,7 @@ sem_status sem_write_state(sem_ctx *ctx, const double *u_curr_host, const double
 }
 
 sem_status sem_set_step(sem_ctx *ctx, int64_t step) {
+    AllocScope scope_(ctx);
     if (!ctx) return SEM_E_ARG;
     if (!ctx->have_ops) return fail(ctx, SEM_E_STATE, "sem_set_step before sem_build_operators");
     if (step < 0) return fail(ctx, SEM_E_ARG, "step < 0");
@@ -1592,6 +1645,7 @@ sem_status sem_set_step(sem_ctx *ctx, int64_t step) {
 }
 
 sem_status sem_sync(sem_ctx *ctx) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1641,6 +1695,7 @@ sem_status sem_get_info(sem_ctx *ctx, sem_info *o) {
 }
 
 sem_status sem_set_kernel_timing(sem_ctx *ctx, int enable) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     ST(drain_events(ctx));
     ctx->timing = enable != 0;
@@ -1651,6 +1706,7 @@ sem_status sem_set_kernel_timing(sem_ctx *ctx, int enable) {
 
 sem_status sem_kernel_times(sem_ctx *ctx, double *k7_ms, int64_t *k7_launches, double *k8_ms,
                             int64_t *k8_launches) {
+    AllocScope scope_(ctx);
     ST(check_usable(ctx));
     ST(drain_events(ctx));
     if (k7_ms) *k7_ms = ctx->t7;

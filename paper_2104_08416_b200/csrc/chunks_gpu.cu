@@ -46,9 +46,9 @@ struct Tmp {
     void *p = nullptr;
     cudaStream_t s;
     explicit Tmp(cudaStream_t st) : s(st) {}
-    cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, n ? n : 16, s); }
+    cudaError_t alloc(size_t n) { return dev_malloc(&p, n ? n : 16, s); }
     template <typename T> T *as() { return (T *)p; }
-    ~Tmp() { if (p) cudaFreeAsync(p, s); }
+    ~Tmp() { if (p) dev_free(p, s); }
 };
 
 #define RET(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)

@@ -12,6 +12,16 @@
 
 namespace sem {
 
+// Device memory of every call goes through the calling context's sem_allocator hook (sem.h), or
+// cudaMallocAsync / cudaFreeAsync without one.  The hook is installed per thread for the
+// duration of an API call (api.cu: AllocScope).
+cudaError_t dev_malloc_raw(void **p, size_t bytes, cudaStream_t s);
+cudaError_t dev_free(void *p, cudaStream_t s);
+template <typename T>
+inline cudaError_t dev_malloc(T **p, size_t bytes, cudaStream_t s) {
+    return dev_malloc_raw(reinterpret_cast<void **>(p), bytes, s);
+}
+
 // ----------------------------- reorder.cu ---------------------------------
 // Vertex bounding box {xmin, ymin, xmax, ymax} -> out4 (device).
 cudaError_t launch_bbox(const double *vxy, int64_t nv, double *out4, cudaStream_t s);

@@ -73,9 +73,9 @@ cudaError_t excl_scan(const T *in, T *out, int64_t n, cudaStream_t s) {
     size_t bytes = 0;
     RET(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
     void *t = nullptr;
-    RET(cudaMallocAsync(&t, bytes ? bytes : 16, s));
+    RET(dev_malloc(&t, bytes ? bytes : 16, s));
     cudaError_t e = cub::DeviceScan::ExclusiveSum(t, bytes, in, out, n, s);
-    cudaFreeAsync(t, s);
+    dev_free(t, s);
     return e;
 }
 
@@ -121,10 +121,10 @@ cudaError_t build_partition_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t 
     const uint32_t me = 1u << rank;
     uint32_t *mask = nullptr;
     int32_t *flag = nullptr, *g2l = nullptr;
-    RET(cudaMallocAsync((void **)&mask, 4 * (N + 1), s));
-    RET(cudaMallocAsync((void **)&flag, 4 * (N + 1), s));
-    RET(cudaMallocAsync((void **)&g2l, 4 * (N + 1), s));
-    struct F { cudaStream_t s; void *a, *b, *c; ~F() { cudaFreeAsync(a, s); cudaFreeAsync(b, s); cudaFreeAsync(c, s); } }
+    RET(dev_malloc((void **)&mask, 4 * (N + 1), s));
+    RET(dev_malloc((void **)&flag, 4 * (N + 1), s));
+    RET(dev_malloc((void **)&g2l, 4 * (N + 1), s));
+    struct F { cudaStream_t s; void *a, *b, *c; ~F() { dev_free(a, s); dev_free(b, s); dev_free(c, s); } }
     fr{s, mask, flag, g2l};
     RET(cudaMemsetAsync(mask, 0, 4 * (N + 1), s));
     RET(cudaMemsetAsync(flag, 0, 4 * (N + 1), s));
@@ -142,9 +142,9 @@ cudaError_t build_partition_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t 
     RET(dalloc((void **)&P.mu_local, 4 * (size_t)(El * Np + 1)));
     int32_t *rflag = nullptr, *ridx = nullptr;
     uint32_t *lmask = nullptr;
-    RET(cudaMallocAsync((void **)&rflag, 4 * (NL + 1), s));
-    RET(cudaMallocAsync((void **)&ridx, 4 * (NL + 1), s));
-    RET(cudaMallocAsync((void **)&lmask, 4 * (NL + 1), s));
+    RET(dev_malloc((void **)&rflag, 4 * (NL + 1), s));
+    RET(dev_malloc((void **)&ridx, 4 * (NL + 1), s));
+    RET(dev_malloc((void **)&lmask, 4 * (NL + 1), s));
     F fr2{s, rflag, ridx, lmask};
     RET(cudaMemsetAsync(rflag, 0, 4 * (NL + 1), s));
     k_local_maps<<<nb(N), kT, 0, s>>>(mask, g2l, N, me, P.loc2glob, P.remote, P.owned, rflag, lmask);
@@ -158,10 +158,10 @@ cudaError_t build_partition_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t 
     std::vector<uint32_t> ifm((size_t)nif + 1);
     if (nif > 0) {
         uint32_t *d_ifm = nullptr;
-        RET(cudaMallocAsync((void **)&d_ifm, 4 * (nif + 1), s));
+        RET(dev_malloc((void **)&d_ifm, 4 * (nif + 1), s));
         k_if_masks<<<nb(NL), kT, 0, s>>>(rflag, ridx, lmask, NL, d_ifm);
         RET(cudaMemcpyAsync(ifm.data(), d_ifm, 4 * nif, cudaMemcpyDeviceToHost, s));
-        cudaFreeAsync(d_ifm, s);
+        dev_free(d_ifm, s);
         RET(cudaStreamSynchronize(s));
     }
     // neighbours, per-neighbour send lists, rank-ordered summation lists (as partition.cpp)
@@ -207,8 +207,8 @@ cudaError_t partition_io_maps(const DevPartition &P, const int32_t *d_node_perm,
     RET(dalloc((void **)loc_can, 4 * (size_t)(NL + 1)));
     k_loc_can<<<nb(NL), kT, 0, s>>>(P.loc2glob, d_node_perm, NL, *loc_can);
     int32_t *f = nullptr, *idx = nullptr;
-    RET(cudaMallocAsync((void **)&f, 4 * (NL + 1), s));
-    RET(cudaMallocAsync((void **)&idx, 4 * (NL + 1), s));
+    RET(dev_malloc((void **)&f, 4 * (NL + 1), s));
+    RET(dev_malloc((void **)&idx, 4 * (NL + 1), s));
     k_owned_flag<<<nb(NL + 1), kT, 0, s>>>(P.owned, NL, f);
     RET(excl_scan(f, idx, NL + 1, s));
     int32_t no = 0;
@@ -219,8 +219,8 @@ cudaError_t partition_io_maps(const DevPartition &P, const int32_t *d_node_perm,
     RET(dalloc((void **)own_can, 4 * (size_t)(no + 1)));
     RET(dalloc((void **)own_ft, 4 * (size_t)(no + 1)));
     k_owned_lists<<<nb(NL), kT, 0, s>>>(f, idx, NL, d_loc_int, *loc_can, P.loc2glob, *own_int, *own_can, *own_ft);
-    cudaFreeAsync(f, s);
-    cudaFreeAsync(idx, s);
+    dev_free(f, s);
+    dev_free(idx, s);
     return cudaGetLastError();
 }
 

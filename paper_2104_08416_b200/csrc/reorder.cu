@@ -467,8 +467,8 @@ struct Tmp {
     void *p = nullptr;
     cudaStream_t s;
     explicit Tmp(cudaStream_t st) : s(st) {}
-    cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, n ? n : 16, s); }
-    ~Tmp() { if (p) cudaFreeAsync(p, s); }
+    cudaError_t alloc(size_t n) { return dev_malloc(&p, n ? n : 16, s); }
+    ~Tmp() { if (p) dev_free(p, s); }
 };
 
 #define RET(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)
@@ -641,11 +641,11 @@ cudaError_t build_node_graph(const int32_t *mu, int64_t E, int Np, int64_t N, bo
     RET(scr.alloc(bytes));
     RET(cub::DeviceScan::ExclusiveSum(scr.p, bytes, (int32_t *)cnt.p, (int32_t *)iptr.p, N + 1, s));
     k_incidence<<<blocks_for(n), kThreads, 0, s>>>(mu, n, (int32_t *)iptr.p, (int32_t *)fill.p, (int32_t *)inc.p);
-    RET(cudaMallocAsync((void **)&g.deg, sizeof(int32_t) * (N + 1), s));
+    RET(dev_malloc((void **)&g.deg, sizeof(int32_t) * (N + 1), s));
     k_node_nbrs<<<blocks_for(N, 128), 128, 0, s>>>(mu, Np, (int32_t *)iptr.p, (int32_t *)inc.p, N, g.deg, nullptr,
                                                    nullptr, (int32_t *)dbad.p);
     if (want_adj) {
-        RET(cudaMallocAsync((void **)&g.aptr, sizeof(int64_t) * (N + 1), s));
+        RET(dev_malloc((void **)&g.aptr, sizeof(int64_t) * (N + 1), s));
         Tmp deg64(s), scr2(s);
         RET(deg64.alloc(sizeof(int64_t) * (N + 1)));
         k_i32_to_i64<<<blocks_for(N + 1), kThreads, 0, s>>>(g.deg, N, (int64_t *)deg64.p);
@@ -655,7 +655,7 @@ cudaError_t build_node_graph(const int32_t *mu, int64_t E, int Np, int64_t N, bo
         RET(cub::DeviceScan::ExclusiveSum(scr2.p, bytes, (int64_t *)deg64.p, g.aptr, N + 1, s));
         RET(cudaMemcpyAsync(&g.nadj, g.aptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         RET(cudaStreamSynchronize(s));
-        RET(cudaMallocAsync((void **)&g.adj, sizeof(int32_t) * (g.nadj + 1), s));
+        RET(dev_malloc((void **)&g.adj, sizeof(int32_t) * (g.nadj + 1), s));
         k_node_nbrs<<<blocks_for(N, 128), 128, 0, s>>>(mu, Np, (int32_t *)iptr.p, (int32_t *)inc.p, N, nullptr,
                                                        g.aptr, g.adj, (int32_t *)dbad.p);
     }
@@ -667,9 +667,9 @@ cudaError_t build_node_graph(const int32_t *mu, int64_t E, int Np, int64_t N, bo
 }
 
 void free_node_graph(DevGraph &g, cudaStream_t s) {
-    if (g.deg) cudaFreeAsync(g.deg, s);
-    if (g.aptr) cudaFreeAsync(g.aptr, s);
-    if (g.adj) cudaFreeAsync(g.adj, s);
+    if (g.deg) dev_free(g.deg, s);
+    if (g.aptr) dev_free(g.aptr, s);
+    if (g.adj) dev_free(g.adj, s);
     g = DevGraph{};
 }
 

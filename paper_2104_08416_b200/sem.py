@@ -61,6 +61,35 @@ class sem_info(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class sem_allocator(C.Structure):
+    """The device-memory hook of include/sem.h."""
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("user", C.c_void_p)]
+
+
+def torch_allocator(device: int = 0) -> sem_allocator:
+    """A sem_allocator that takes the library's device memory from PyTorch's caching
+    allocator (stream-ordered on the context's stream).  Keep the returned object alive
+    as long as the context (SemContext does)."""
+    import torch
+
+    def _alloc(nbytes, stream, user):
+        try:
+            with torch.cuda.device(device):
+                return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+        except Exception:  # out of memory etc.: libsem reports SEM_E_CUDA
+            return None
+
+    def _free(ptr, stream, user):
+        with torch.cuda.device(device):
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+    return sem_allocator(_ALLOC_FN(_alloc), _FREE_FN(_free), None)
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -97,7 +126,7 @@ def load(path: str = LIB_PATH):
                 os.environ["SEM_NCCL_LIB"] = f
         L = C.CDLL(path)
         P, i64, i32, u64, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_double
-        L.sem_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, P, P]
+        L.sem_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, P, P, C.POINTER(sem_allocator)]
         L.sem_free.argtypes = [P]
         L.sem_free.restype = None
         L.sem_last_error.argtypes = [P]
@@ -144,12 +173,18 @@ class SemContext:
     """One libsem context (one GPU / rank)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None,
-                 stream: int | None = None):
+                 stream: int | None = None, allocator: sem_allocator | str | None = None):
+        """allocator: None (the library's stream-ordered pool), "torch" (PyTorch's caching
+        allocator) or a sem_allocator."""
         self.L = load()
         h = C.c_void_p()
         idbuf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
+        if allocator == "torch":
+            allocator = torch_allocator(device)
+        self._allocator = allocator  # the callbacks must outlive the context
         st = self.L.sem_create(C.byref(h), device, rank, world_size, idbuf,
-                               None if stream is None else C.c_void_p(stream))
+                               None if stream is None else C.c_void_p(stream),
+                               None if allocator is None else C.byref(allocator))
         self.h = h
         if st != SEM_OK:
             msg = self.L.sem_last_error(h).decode() if h.value else ""
@@ -348,8 +383,11 @@ def nccl_unique_id() -> bytes:
 class LoopbackGroup:
     """G in-process partitions (loopback exchange, SURVEY §8e test transport)."""
 
-    def __init__(self, world: int, device: int = 0):
-        self.ctxs = [SemContext(device, r, world) for r in range(world)]
+    def __init__(self, world: int, device: int = 0, allocator=None):
+        if allocator == "torch":
+            allocator = torch_allocator(device)
+        self._allocator = allocator
+        self.ctxs = [SemContext(device, r, world, allocator=allocator) for r in range(world)]
         self.world = world
         self._arr = (C.c_void_p * world)(*[c.h.value for c in self.ctxs])
 

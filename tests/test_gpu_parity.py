@@ -380,3 +380,45 @@ def test_degenerate_inputs(ctx):
     with pytest.raises(S.SemError) as e:
         S.LoopbackGroup(2).sem_mesh_reorder(vxy[:3], tri, 2)  # 1 element, 2 ranks
     assert e.value.status == S.SEM_E_ARG
+
+
+def test_torch_allocator_hook_bitwise():
+    """SURVEY §8(b)'s allocator hook: with PyTorch's caching allocator behind sem_allocator,
+    every device array of the context is torch memory (torch.cuda.memory_allocated grows by
+    at least the mesh and operator arrays while the context lives and returns when it is
+    freed) and the field is bitwise the same as with the library's own pool."""
+    import torch
+    pb = mg.config("C2", 8)
+    m = pb.mesh
+    rng = np.random.default_rng(3)
+
+    def run(allocator):
+        with S.SemContext(0, allocator=allocator) as c:
+            r = c.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+            c.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+            U0 = np.random.default_rng(3).standard_normal(r["n_nodes"])
+            c.sem_write_state(U0, U0)
+            c.sem_step_n(40)
+            held = torch.cuda.memory_allocated(0)
+            U, _ = c.sem_read_field()
+        return U, held
+
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(0)
+    Ua, _ = run(None)
+    Ut, held = run("torch")
+    torch.cuda.synchronize()
+    assert np.array_equal(Ua, Ut)
+    # mu-sized chunk tables, G, U^n, U^{n-1}, dt^2/M at least: > 24 B per element
+    assert held - base > 24 * m.ne
+    assert torch.cuda.memory_allocated(0) == base
+    g = S.LoopbackGroup(2, allocator="torch")
+    try:
+        g.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+        g.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        g.sem_step_n(5)
+        Ug, _ = g.sem_read_field()
+        assert not np.isnan(Ug).any()
+    finally:
+        g.close()
+    del rng
