@@ -161,8 +161,8 @@ const char *sem_last_error(const sem_ctx *ctx);
  *
  * Errors: SEM_E_UNSUPPORTED (degree, ordering, VISIT without CONN/DIST),
  * SEM_E_MESH ("element e has zero area", "vertex v is not used by any
- * element", a node whose elements hold > 384 entries, a node with more than
- * 32 entries inside one chunk of the step kernel), SEM_E_ARG, SEM_E_CUDA,
+ * element", a node with more than 64 entries -- elements holding it -- inside one
+ * chunk of the step kernel), SEM_E_ARG, SEM_E_CUDA,
  * SEM_E_OOM.
  * Resets any operators/state of an earlier mesh.
  */

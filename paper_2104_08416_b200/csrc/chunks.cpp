@@ -339,7 +339,7 @@ bool build_chunks(const int32_t *mu, int64_t E, int Np, int64_t N, int B, ChunkM
             }
     }
     if (max_cnt > kJdsW) {
-        err = "build_chunks: a node has more than 32 entries in one chunk";
+        err = "build_chunks: a node has more than 64 entries in one chunk";
         return false;
     }
     m.max_local = max_local;

@@ -580,7 +580,7 @@ cudaError_t build_chunks_gpu(const int32_t *d_mu, int64_t E, int Np, int64_t N, 
     m.max_win = hmx[1];
     m.max_count = hmx[2];
     if (m.max_count > kJdsW) {
-        err = "build_chunks: a node has more than 32 entries in one chunk";
+        err = "build_chunks: a node has more than 64 entries in one chunk";
         return cudaSuccess;
     }
     m.max_nsh = hmx[3];

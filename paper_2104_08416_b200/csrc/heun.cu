@@ -71,9 +71,10 @@ struct HeunLayout {
 
 // (R(V), K U) of a local node from the jagged-diagonal entry buffer (see
 // jds_sum in step.cu): diagonals in order, a warp's lanes on consecutive pairs
+template <int W = kJdsW>  // diagonals walked at most (see jds_sum)
 __device__ __forceinline__ double2 jds_sum2(const double2 *ebuf, const uint16_t *jo, int end, int ii) {
     double2 y = ebuf[jo[0] + ii];
-    for (int d = 1; d < kJdsW; d++) {
+    for (int d = 1; d < W; d++) {
         const int nd = (d + 1 < kJdsW ? (int)jo[d + 1] : end) - (int)jo[d];
         if (ii >= nd) break;
         const double2 e = ebuf[jo[d] + ii];
@@ -364,7 +365,9 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
                 const int nwork = nint + nsh;
                 for (int wk = t; wk < nwork; wk += C) {
                     const int i = wk < nint ? wk : ni_al + (wk - nint);  // skips the alignment hole
-                    const double2 ab = i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al);
+                    const double2 ab = ch.max_count <= 32
+                                     ? (i < nint ? jds_sum2<32>(ebuf, jd, m1.x, i) : jds_sum2<32>(ebuf, jd + kJdsW, m1.w, i - ni_al))
+                                     : (i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al));
                     if (i < nint) {
                         const int64_t id = i0 + i;
                         const bool src = id == a.src;
@@ -536,7 +539,9 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
             const int nwork = nint_np + nsh;
             for (int w = t; w < nwork; w += B) {
                 const int i = w < nint_np ? w : ni_al + (w - nint_np);  // skips the element-interior nodes and the hole
-                const double2 ab = i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al);
+                const double2 ab = ch.max_count <= 32
+                                     ? (i < nint ? jds_sum2<32>(ebuf, jd, m1.x, i) : jds_sum2<32>(ebuf, jd + kJdsW, m1.w, i - ni_al))
+                                     : (i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al));
                 if (i < nint) {
                     const int64_t id = i0 + i;
                     const bool src = id == a.src;

@@ -57,8 +57,8 @@ cudaError_t first_touch(const int32_t *mu, int64_t E, int Np, int64_t N, int32_t
 
 // Node graph (nodes connected iff they share an element): degree [N] and,
 // with want_adj, the CSR of ascending distinct neighbours.  Device buffers
-// come from cudaMallocAsync; release with free_node_graph.  *bad = 1 if a
-// node's elements hold more than 384 entries.
+// come from the device-memory facade (dev_malloc); release with free_node_graph.  *bad is
+// kept for the ABI of this helper but never set (nodes with many neighbours take a slower path).
 struct DevGraph {
     int32_t *deg = nullptr;
     int64_t *aptr = nullptr;
@@ -156,7 +156,7 @@ struct StepParams {
 // (for the exchange kernels on the comm stream while the interior chunks run)
 int k7_grid(const DevChunks &ch, bool fused, int reserve_sms = 0);
 // resident K7 CTAs per SM for chunks of B elements with these per-chunk maxima (shared-memory stages)
-int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused);
+int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused, int max_count = 0);
 // device step counter of the graph-captured step loop: += 1, = v
 // pdl: programmatic dependent launch (the graph-captured step loop, SEM_PDL): the kernel may
 // start while its predecessor drains and waits in griddepcontrol.wait before any data access

@@ -287,9 +287,33 @@ __global__ void k_incidence(const int32_t *__restrict__ mu, int64_t n, const int
     if (i < n) inc[ptr[mu[i]] + atomicAdd(&fill[mu[i]], 1)] = (int32_t)i;  // entry index (order fixed later)
 }
 
+// More than kMaxCand distinct neighbours (high-valence fans, high orders): the ascending distinct
+// list by repeated minimum search over the node's element entries, O(degree x entries), no list.
+__device__ void node_nbrs_rescan(const int32_t *__restrict__ mu, int Np, const int32_t *__restrict__ iptr,
+                                 const int32_t *__restrict__ inc, int64_t g, int32_t *deg,
+                                 const int64_t *__restrict__ aptr, int32_t *__restrict__ adj) {
+    int32_t prev = -1;
+    int k = 0;
+    for (;;) {
+        int32_t best = INT_MAX;
+        for (int j = iptr[g]; j < iptr[g + 1]; j++) {
+            const int64_t e = inc[j] / Np;
+            for (int q = 0; q < Np; q++) {
+                const int32_t o = mu[e * Np + q];
+                if (o != (int32_t)g && o > prev && o < best) best = o;
+            }
+        }
+        if (best == INT_MAX) break;
+        if (adj) adj[aptr[g] + k] = best;
+        k++;
+        prev = best;
+    }
+    if (!adj) deg[g] = k;
+}
+
 // Distinct other nodes of the elements holding g: count (adj == nullptr) or
-// write them ascending at adj + aptr[g].  *bad = 1 if a node has more than
-// kMaxCand candidate entries.
+// write them ascending at adj + aptr[g].  Nodes with more than kMaxCand of them take the
+// rescan path (same result).  (*bad is no longer set.)
 __global__ void k_node_nbrs(const int32_t *__restrict__ mu, int Np, const int32_t *__restrict__ iptr,
                             const int32_t *__restrict__ inc, int64_t N, int32_t *deg,
                             const int64_t *__restrict__ aptr, int32_t *__restrict__ adj, int32_t *bad) {
@@ -305,7 +329,10 @@ __global__ void k_node_nbrs(const int32_t *__restrict__ mu, int Np, const int32_
             int k = m - 1;  // insertion into the ascending unique list
             while (k >= 0 && c[k] > o) k--;
             if (k >= 0 && c[k] == o) continue;
-            if (m == kMaxCand) { *bad = 1; return; }
+            if (m == kMaxCand) {  // a high-valence node: the slow path without the local list
+                node_nbrs_rescan(mu, Np, iptr, inc, g, deg, aptr, adj);
+                return;
+            }
             for (int r = m; r > k + 1; r--) c[r] = c[r - 1];
             c[k + 1] = o;
             m++;

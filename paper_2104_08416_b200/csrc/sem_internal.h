@@ -11,7 +11,10 @@
 namespace sem {
 
 constexpr int kMaxNp = 36;  // P = 7
-constexpr int kJdsW = 32;   // jagged diagonals per segment = max entries of a node in a chunk
+#ifndef SEM_JDSW
+#define SEM_JDSW 64
+#endif
+constexpr int kJdsW = SEM_JDSW;  // jagged diagonals per segment = max entries of a node in a chunk
 
 #ifdef __CUDACC__
 #define SEM_HD __host__ __device__

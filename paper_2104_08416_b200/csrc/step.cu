@@ -136,9 +136,12 @@ __global__ void k_geometry(const double *__restrict__ vxy, const int32_t *__rest
 // d-th entry (ascending e = p*B + t) of every node with more than d entries;
 // diagonal lengths do not increase with d.  The sum runs over d in order (a
 // fixed order), and a warp's lanes read consecutive words of each diagonal.
+// W = diagonals walked at most: 32 when no node of the mesh has more entries in a chunk (the
+// common case; the 64-diagonal loop measured 4.5 % slower on C4's K7), else kJdsW.
+template <int W = kJdsW>
 __device__ __forceinline__ double jds_sum(const double *ebuf, const uint16_t *jo, int end, int ii) {
     double y = ebuf[jo[0] + ii];  // every local node has an entry
-    for (int d = 1; d < kJdsW; d++) {
+    for (int d = 1; d < W; d++) {
         const int nd = (d + 1 < kJdsW ? (int)jo[d + 1] : end) - (int)jo[d];
         if (ii >= nd) break;
         y += ebuf[jo[d] + ii];
@@ -229,7 +232,7 @@ __device__ __forceinline__ void finish_shared(const DevChunks &ch, const StepPar
 // 32 (w / G) + lane and the row block w % G of y = K^e u, computed as
 // y_p = grr (Srr u)_p + gss (Sss u)_p + grs (Srs u)_p with the S tables staged in
 // shared memory (all lanes of a warp read the same entry: broadcast).
-template <int NP, int B, int WM, int G = 1>
+template <int NP, int B, int WM, int G = 1, int JW = 32>
 __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10 ? 2 : B <= 128 ? 4 : B <= 192 ? 3 : B <= 256 ? 2 : 1))
     k7_step(const DevChunks ch, const StepParams a, int L, int W, int Lp, int Ls,
             const int32_t *__restrict__ list, int64_t nlist) {
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                 upg = a.Uprev[i0 + i];
                 mg = __ldg(a.dt2M + i0 + i);
             }
-            const double yi = i < nint ? jds_sum(ebuf, jd, end0, i) : jds_sum(ebuf, jd + kJdsW, end1, i - ni_al);
+            const double yi = i < nint ? jds_sum<JW>(ebuf, jd, end0, i) : jds_sum<JW>(ebuf, jd + kJdsW, end1, i - ni_al);
             if (i < nint) {
                 const int id = i0 + i;
                 Unew[id] = leap_update(u_s[i], WM == 0 ? upg : up_s[i], WM == 0 ? mg : m_s[i], id == a.src ? fsrc : 0.0, yi);
@@ -677,8 +680,11 @@ int k7_group(int np) {
     return (np == 36 || np == 28) ? g7 : np == 21 ? g5 : 1;
 }
 
-size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
-    const int wm = k7_win();
+// window mode of the instantiation: meshes with a node of more than 32 entries in a chunk (wide
+// JDS) run the default single-buffered window only
+int k7_mode(bool wide) { return wide ? 1 : k7_win(); }
+size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse, bool wide) {
+    const int wm = k7_mode(wide);
     const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, wm == 2 ? W : 0);
     const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * (np + (np & 1)) * 8 : 0;
     return (size_t)kStages * lay.size + (size_t)np * B * 8 + (wm == 1 ? 2 * (size_t)W * 8 : 0) +
@@ -686,34 +692,37 @@ size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse) {
 }
 
 using K7Fn = void (*)(const DevChunks, const StepParams, int, int, int, int, const int32_t *, int64_t);
-template <int W2>
+template <int W2, int JW>
 K7Fn k7_fn_w(int np, int B) {
-    if (np == 15) return k7_step<15, 128, W2>;  // P4 (R21b): chunks of 128
+    if (np == 15) return k7_step<15, 128, W2, 1, JW>;  // P4 (R21b): chunks of 128
     if (np == 21) {  // P5 (R21): chunks of 128
         const int g = k7_group(21);
-        return g == 4 ? k7_step<21, 128, W2, 4> : g == 2 ? k7_step<21, 128, W2, 2> : k7_step<21, 128, W2>;
+        return g == 4 ? k7_step<21, 128, W2, 4, JW> : g == 2 ? k7_step<21, 128, W2, 2, JW> : k7_step<21, 128, W2, 1, JW>;
     }
     if (np == 28) {                              // P6 (R21b): chunks of 64, G threads per element
         const int g = k7_group(28);
-        return g == 4 ? k7_step<28, 64, W2, 4> : g == 2 ? k7_step<28, 64, W2, 2> : k7_step<28, 64, W2, 1>;
+        return g == 4 ? k7_step<28, 64, W2, 4, JW> : g == 2 ? k7_step<28, 64, W2, 2, JW> : k7_step<28, 64, W2, 1, JW>;
     }
     if (np == 36) {                              // P7: chunks of 64, G threads per element
         const int g = k7_group(36);
-        return g == 4 ? k7_step<36, 64, W2, 4> : g == 2 ? k7_step<36, 64, W2, 2> : k7_step<36, 64, W2, 1>;
+        return g == 4 ? k7_step<36, 64, W2, 4, JW> : g == 2 ? k7_step<36, 64, W2, 2, JW> : k7_step<36, 64, W2, 1, JW>;
     }
     if (np == 6)
-        return B == 128   ? k7_step<6, 128, W2>
-               : B == 192 ? k7_step<6, 192, W2>
-               : B == 512 ? k7_step<6, 512, W2>
-                          : k7_step<6, 256, W2>;
-    return B == 128   ? k7_step<10, 128, W2>
-           : B == 192 ? k7_step<10, 192, W2>
-           : B == 512 ? k7_step<10, 512, W2>
-                      : k7_step<10, 256, W2>;
+        return B == 128   ? k7_step<6, 128, W2, 1, JW>
+               : B == 192 ? k7_step<6, 192, W2, 1, JW>
+               : B == 512 ? k7_step<6, 512, W2, 1, JW>
+                          : k7_step<6, 256, W2, 1, JW>;
+    return B == 128   ? k7_step<10, 128, W2, 1, JW>
+           : B == 192 ? k7_step<10, 192, W2, 1, JW>
+           : B == 512 ? k7_step<10, 512, W2, 1, JW>
+                      : k7_step<10, 256, W2, 1, JW>;
 }
-K7Fn k7_fn(int np, int B) {
+
+// wide: a node of the mesh has more than 32 entries in one chunk -> the 64-diagonal JDS walk
+K7Fn k7_fn(int np, int B, bool wide) {
+    if (wide) return k7_fn_w<1, kJdsW>(np, B);
     const int wm = k7_win();
-    return wm == 2 ? k7_fn_w<2>(np, B) : wm == 0 ? k7_fn_w<0>(np, B) : k7_fn_w<1>(np, B);
+    return wm == 2 ? k7_fn_w<2, 32>(np, B) : wm == 0 ? k7_fn_w<0, 32>(np, B) : k7_fn_w<1, 32>(np, B);
 }
 
 }  // namespace
@@ -765,9 +774,10 @@ cudaError_t assemble_mass(const DevChunks &ch, const double *detJ, double numer,
     return cudaGetLastError();
 }
 
-int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused) {
-    const size_t smem = k7_smem_bytes(np, B, max_local, max_win, 2 * kJdsW, max_nsh, fused);
-    const K7Fn fn = k7_fn(np, B);
+int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused, int max_count) {
+    const bool wide = max_count > 32;
+    const size_t smem = k7_smem_bytes(np, B, max_local, max_win, 2 * kJdsW, max_nsh, fused, wide);
+    const K7Fn fn = k7_fn(np, B, wide);
     set_smem(fn, smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, B * k7_group(np) + 32, smem);
@@ -775,7 +785,7 @@ int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool 
 }
 
 int k7_grid(const DevChunks &ch, bool fused, int reserve_sms) {
-    const int occ = k7_ctas_per_sm(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_nsh, fused);
+    const int occ = k7_ctas_per_sm(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_nsh, fused, ch.max_count);
     const int nsm = current_sm_count();
     if (reserve_sms >= nsm) reserve_sms = nsm - 1;
     int64_t g = (int64_t)occ * (nsm - (reserve_sms > 0 ? reserve_sms : 0));
@@ -806,8 +816,9 @@ cudaError_t launch_k7(const DevChunks &ch, const StepParams &p, int grid, cudaSt
     if (n == 0) return cudaSuccess;
     if (persistent_grid_cap() > 0 && grid > persistent_grid_cap()) grid = (int)persistent_grid_cap();
     if (grid > n) grid = (int)n;
-    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, p.cnt != nullptr);
-    const K7Fn fn = k7_fn(ch.Np, ch.B);
+    const bool wide = ch.max_count > 32;
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, p.cnt != nullptr, wide);
+    const K7Fn fn = k7_fn(ch.Np, ch.B, wide);
     cudaError_t e = set_smem(fn, smem);
     if (e != cudaSuccess) return e;
     return launch_ex(fn, (unsigned)grid, ch.B * k7_group(ch.Np) + 32, smem, s, pdl, ch, p, ch.max_local, ch.max_win,

@@ -104,6 +104,32 @@ def grid_mesh(nx: int, ny: int, Lx: float, Ly: float, alpha: float = 0.0, seed: 
     return m
 
 
+def fan_mesh(n=48, rings=3):
+    """Test input: a vertex shared by n triangles (a high-valence fan) inside `rings` rings of
+    vertices (the chunk builder's and node graph's limits, tests/)."""
+    vxy = [(0.0, 0.0)]
+    for r in range(1, rings + 1):
+        for k in range(n):
+            a = 2 * np.pi * (k + 0.5 * (r % 2)) / n
+            vxy.append((r * np.cos(a), r * np.sin(a)))
+    ring = lambda r, k: 1 + (r - 1) * n + (k % n)  # noqa: E731
+    tri = [(0, ring(1, k), ring(1, k + 1)) for k in range(n)]
+    for r in range(1, rings):
+        for k in range(n):
+            if r % 2:  # the outer ring is rotated by half a step
+                tri.append((ring(r, k + 1), ring(r, k), ring(r + 1, k)))
+                tri.append((ring(r, k + 1), ring(r + 1, k), ring(r + 1, k + 1)))
+            else:
+                tri.append((ring(r, k), ring(r + 1, k), ring(r, k + 1)))
+                tri.append((ring(r, k + 1), ring(r + 1, k), ring(r + 1, k + 1)))
+    vxy = np.array(vxy, np.float64)
+    tri = np.array(tri, np.int32)
+    p0, p1, p2 = vxy[tri[:, 0]], vxy[tri[:, 1]], vxy[tri[:, 2]]
+    area2 = (p1[:, 0] - p0[:, 0]) * (p2[:, 1] - p0[:, 1]) - (p2[:, 0] - p0[:, 0]) * (p1[:, 1] - p0[:, 1])
+    tri[area2 < 0] = tri[area2 < 0][:, [0, 2, 1]]
+    return Mesh(vxy=vxy, tri=tri, nx=0, ny=0)
+
+
 def _signed_area2(vxy, tri):
     p0 = vxy[tri[:, 0]]
     p1 = vxy[tri[:, 1]]

@@ -102,3 +102,15 @@ def test_element_interior_nodes_close_the_interior_segment(name, scale, P, B):
         win = (int_of[ids] >= i0) & (int_of[ids] < tail0)
         order = np.argsort(int_of[ids[win]])
         assert (np.diff(cnt[win][order]) <= 0).all()
+
+
+def test_high_valence_fan_fits_a_chunk():
+    """A vertex held by 48 elements of one chunk (more than round 1's limit of 32 entries per
+    node and chunk): the chunk builder accepts it (kJdsW = 64) and counts its entries."""
+    m = mg.fan_mesh(48)
+    t = core.orient(m.vxy, m.tri)
+    mu, N = core.canonical_nodes(t, m.nv, 3)
+    _, perm, _ = core.hilbert_order(m.vxy, m.tri)
+    _, mu_ft = core.first_touch(mu[perm], N)
+    st = S.sem_debug_chunk_stats(mu_ft, N, 256)
+    assert st["max_count"] == 48

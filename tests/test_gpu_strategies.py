@@ -76,3 +76,28 @@ def test_visit_needs_strategy(ctx):
     with pytest.raises(S.SemError) as e:
         ctx.sem_mesh_reorder(pb.mesh.vxy, pb.mesh.tri, pb.P, S.SEM_ORDER_HILBERT, S.SEM_NODES_VISIT)
     assert e.value.status == S.SEM_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("P", [3, 7])
+@pytest.mark.parametrize("elem_order,node_order", [(S.SEM_ORDER_CONN, S.SEM_NODES_VISIT),
+                                                   (S.SEM_ORDER_HILBERT, S.SEM_NODES_FIRST_TOUCH_DEGREE)])
+def test_high_valence_fan(ctx, P, elem_order, node_order):
+    """A vertex held by 48 elements: more than 32 entries in one chunk (round 1's limit) and,
+    at P7, more distinct neighbours than the node-graph kernel's local list (the rescan path).
+    Permutations bit-exact; five steps from a random state within 1e-12 of the oracle."""
+    m = mg.fan_mesh(48)
+    c = np.full(m.ne, 1.0)
+    r = ctx.sem_mesh_reorder(m.vxy, m.tri, P, elem_order, node_order)
+    ep, npm = oracle_orders(m, P, elem_order, node_order)
+    assert np.array_equal(r["elem_perm"], ep)
+    assert np.array_equal(r["node_perm"], npm)
+    o = OracleSEM(m.vxy, m.tri, P, c)
+    dt = mg.cfl_dt(m, c, P)
+    rng = np.random.default_rng(P)
+    U0, Up = rng.standard_normal(o.N), rng.standard_normal(o.N)
+    Uo, _ = o.leapfrog(dt, 5, src=0, A=1.0, f0=2.0, t0=0.0, U=U0, Uprev=Up)
+    ctx.sem_build_operators(c, 0, 2.0, 0.0, 1.0, dt)
+    ctx.sem_write_state(U0, Up)
+    ctx.sem_step_n(5)
+    Ug, _ = ctx.sem_read_field()
+    assert np.linalg.norm(Ug - Uo) <= 1e-12 * np.linalg.norm(Uo)
