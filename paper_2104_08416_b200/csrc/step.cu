@@ -45,6 +45,24 @@ constexpr int kStages = SEM_KSTAGES;  // pipeline depth of K7 (A/B: -DSEM_KSTAGE
 #define SEM_K7_IDS_TMA 1
 #endif
 constexpr bool kIdsTma = SEM_K7_IDS_TMA != 0;
+// High orders (P5-P7, G > 1): the element products y = grr (Srr u) + gss (Sss u) + grs (Srs u)
+// of a chunk are three dense [Np x Np] x [Np x B] contractions, run on the FP64 tensor cores
+// (mma.sync m8n8k4 f64, SASS DMMA) instead of DFMA with one table read per two FMAs
+// (A/B: -DSEM_K7_TC=0)
+#ifndef SEM_K7_TC
+#define SEM_K7_TC 1
+#endif
+constexpr bool kTcOn = SEM_K7_TC != 0;
+__host__ __device__ constexpr bool k7_tc(int np, int g) { return kTcOn && g > 1 && np >= 21; }
+__host__ __device__ constexpr int pad_to(int v, int m) { return (v + m - 1) / m * m; }
+
+// D = A B + C for one 8x8x4 fp64 tile (per-thread fragments: A[lane / 4][lane % 4],
+// B[lane % 4][lane / 4], C / D[lane / 4][2 (lane % 4) + i], i = 0, 1)
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 // S tables packed densely for the current degree ([p * Np + q]): at P3 the three
 // tables span 2.4 KB of the constant cache instead of rows strided by kMaxNp
@@ -260,7 +278,15 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
     pdl_trigger();  // the next kernel (K8) may be scheduled; it waits for this grid to complete
 
     constexpr int kNPp = NP + (NP & 1);  // G > 1: S table rows padded to an even length (16-byte pairs)
-    if (G > 1) {
+    constexpr bool kTc = k7_tc(NP, G);
+    constexpr int kMP = pad_to(NP, 8), kKP = pad_to(NP, 4);  // tensor-core tiles: rows to 8, columns to 4
+    if (kTc) {  // Srr, Sss, Srs as [3][kMP][kKP], zero-padded (the A operands of the tile products)
+        for (int i = t; i < 3 * kMP * kKP; i += blockDim.x) {
+            const int tb = i / (kMP * kKP), r = (i / kKP) % kMP, q = i % kKP;
+            const double *src = tb == 0 ? c_Srr : tb == 1 ? c_Sss : c_Srs;
+            S_s[i] = (r < NP && q < NP) ? src[r * NP + q] : 0.0;
+        }
+    } else if (G > 1) {
         for (int i = t; i < NP * NP; i += blockDim.x) {
             const int p = i / NP, q = i % NP;
             S_s[p * kNPp + q] = c_Srr[i];
@@ -410,7 +436,42 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             for (int j = t; j < nsh; j += C) SEM_DCHECK(shs[j] >= 0 && shs[j] < ch.n_slots, "slot id in range");
         }
 
-        if (G > 1) {
+        if (kTc) {
+            // (E, tensor cores) warp wi takes the element tiles nt = wi, wi + C/32, ... of 8 elements
+            // each; per tile the three products over k-steps of 4 nodes, then the G_e combination
+            constexpr int MT = kMP / 8, KT = kKP / 4, NT = B / 8;
+            const int lane = t & 31;
+            for (int nt = t >> 5; nt < NT; nt += C / 32) {
+                const int eb = nt * 8 + (lane >> 2);  // element of this lane's B-fragment column
+                double acc[MT][3][2];
+#pragma unroll
+                for (int m = 0; m < MT; m++)
+#pragma unroll
+                    for (int tb = 0; tb < 3; tb++) acc[m][tb][0] = acc[m][tb][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KT; ks++) {
+                    const int q = ks * 4 + (lane & 3);
+                    const double b = (q < NP && eb < ne) ? u_s[li_s[q * B + eb]] : 0.0;
+#pragma unroll
+                    for (int m = 0; m < MT; m++)
+#pragma unroll
+                        for (int tb = 0; tb < 3; tb++)
+                            dmma_8x8x4(acc[m][tb][0], acc[m][tb][1], S_s[(tb * kMP + m * 8 + (lane >> 2)) * kKP + q], b);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const int e = nt * 8 + 2 * (lane & 3) + i;
+                    if (e < ne) {
+                        const double grr = g_s[e], gss = g_s[B + e], grs = g_s[2 * B + e];
+#pragma unroll
+                        for (int m = 0; m < MT; m++) {
+                            const int p = m * 8 + (lane >> 2);
+                            if (p < NP) ebuf[lpo[p * B + e]] = fma(grr, acc[m][0][i], fma(gss, acc[m][1][i], grs * acc[m][2][i]));
+                        }
+                    }
+                }
+            }
+        } else if (G > 1) {
             // (E, wide) this thread: element te, rows [p0, p1) of y = K^e u
             constexpr int R = (NP + G - 1) / G;
             const int w = t >> 5, te = ((w / G) << 5) + (t & 31), p0 = (w % G) * R;
@@ -676,6 +737,8 @@ int k7_win() {
 int k7_group(int np) {
     static int g7 = -1, g5 = -1;
     if (g7 < 0) { const char *e = getenv("SEM_K7_G"); g7 = e ? atoi(e) : 4; if (g7 != 1 && g7 != 2 && g7 != 4) g7 = 4; }
+    // P5: one thread per element with the symmetric K^e build (B1 0.202 ms per step; the tensor-core
+    // path with 2 threads per element: 0.264 ms); SEM_K7_G5=2|4 selects the wide / tensor-core one
     if (g5 < 0) { const char *e = getenv("SEM_K7_G5"); g5 = e ? atoi(e) : 1; if (g5 != 1 && g5 != 2 && g5 != 4) g5 = 1; }
     return (np == 36 || np == 28) ? g7 : np == 21 ? g5 : 1;
 }
@@ -686,7 +749,10 @@ int k7_mode(bool wide) { return wide ? 1 : k7_win(); }
 size_t k7_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, bool fuse, bool wide) {
     const int wm = k7_mode(wide);
     const StageLayout lay(np, B, L, Lp, Ls, fuse ? Ls : 0, wm == 2 ? W : 0);
-    const size_t stab = k7_group(np) > 1 ? 3 * (size_t)np * (np + (np & 1)) * 8 : 0;
+    const int g = k7_group(np);
+    const size_t stab = k7_tc(np, g) ? 3 * (size_t)pad_to(np, 8) * pad_to(np, 4) * 8
+                        : g > 1    ? 3 * (size_t)np * (np + (np & 1)) * 8
+                                   : 0;
     return (size_t)kStages * lay.size + (size_t)np * B * 8 + (wm == 1 ? 2 * (size_t)W * 8 : 0) +
            (4 * kStages + 2) * 8 + stab;
 }
