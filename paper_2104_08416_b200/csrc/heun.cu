@@ -52,6 +52,20 @@ __constant__ double h_wK[kMaxNp];
 // The producer reads the gathers' shared-node ids from a TMA copy in the stage at P >= 5
 // (B1 Heun P5 1.102 -> 1.045 ms); at P2/P3 the dependent global loads measured 0.7 % faster.
 __host__ __device__ constexpr bool ids_tma(int np) { return np > 10; }
+// P5 / P7 with several consumer threads per element: the element products on the FP64 tensor
+// cores (A/B: -DSEM_HEUN_TC=0)
+#ifndef SEM_HEUN_TC
+#define SEM_HEUN_TC 1
+#endif
+__host__ __device__ constexpr bool heun_tc(int np, int g) { return SEM_HEUN_TC != 0 && g >= 4 && np >= 21; }
+
+// D = A B + C for one 8x8x4 fp64 tile (mma.sync, SASS DMMA); per-lane fragments A[lane / 4][lane % 4],
+// B[lane % 4][lane / 4], C / D[lane / 4][2 (lane % 4) + i]
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 struct HeunLayout {
     int lidx, lpos, jds, shs, shn, g, meta, u, w, size;
@@ -118,8 +132,20 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
     // G > 1: the five tables in shared memory, rows padded to an even length (16-byte pairs):
     // Dr, Ds, Srr, Sss, Srs at tab + k * NP * kNPp.  Warp-uniform row, broadcast reads.
     constexpr int kNPp = NP + (NP & 1);
+    constexpr bool kTcH = heun_tc(NP, G);
+    constexpr int kMP = (NP + 7) / 8 * 8, kKP = (NP + 3) / 4 * 4;  // tensor-core tiles: rows to 8, columns to 4
     double *tab = reinterpret_cast<double *>(idb + kStagesH);
-    if (G > 1) {
+    if (kTcH) {  // Dr, Ds, Dr^T, Ds^T, Srr, Sss, Srs zero-padded to [kMP][kKP] (A operands)
+        for (int i = threadIdx.x; i < 7 * kMP * kKP; i += blockDim.x) {
+            const int tb = i / (kMP * kKP), r = (i / kKP) % kMP, q = i % kKP;
+            double v = 0.0;
+            if (r < NP && q < NP) {
+                const double *src[7] = {h_Dr, h_Ds, h_Dr, h_Ds, h_Srr, h_Sss, h_Srs};
+                v = (tb == 2 || tb == 3) ? src[tb][q * NP + r] : src[tb][r * NP + q];
+            }
+            tab[i] = v;
+        }
+    } else if (G > 1) {
         for (int i = threadIdx.x; i < NP * NP; i += blockDim.x) {
             const int p = i / NP, q = i % NP;
             tab[p * kNPp + q] = h_Dr[i];
@@ -209,7 +235,179 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
         return;
     }
 
-    if constexpr (G > 1) {
+    if constexpr (kTcH) {
+        // ===== consumer warps, tensor cores (P5, P7) =====
+        // Every per-element product of the step is a dense [Np x Np] x [Np x 8] tile product per
+        // warp (warp wi: elements 8 wi .. 8 wi + 7 of the chunk), on mma.sync m8n8k4 f64 (DMMA):
+        //   (1) Algorithm 1 on W: (gr, gs) = (Dr, Ds) W, the lagged V update in the epilogue
+        //       (V read and written straight from / to global, fragment by fragment), which
+        //       also forms Algorithm 2's aux = -detJ w J^-1 V into shared memory;
+        //   (2) r = Dr^T ar + Ds^T as (aux from shared memory) and Srr u, Sss u, Srs u;
+        //       y = grr Srr u + gss Sss u + grs Srs u in the epilogue.
+        // Fragments (per lane): A[lane / 4][lane % 4], B[lane % 4][lane / 4], C[lane / 4][2 (lane % 4) + i].
+        constexpr int MT = kMP / 8, KT = kKP / 4;
+        static_assert(B / 8 <= C / 32, "one 8-element tile per consumer warp");
+        const int lane = t & 31, nt = t >> 5;
+        const bool tile = nt < B / 8;
+        const int eb = nt * 8 + (lane >> 2);  // this lane's B-fragment element
+        const double f_n = src_term(a, a.src, a.n), f_n1 = src_term(a, a.src, a.n + 1);
+        double *xs = reinterpret_cast<double *>(ebuf);  // aux [NP][2][B], aliases the entry buffer
+        auto At = [&](int tb, int m, int ks) { return tab[(tb * kMP + m * 8 + (lane >> 2)) * kKP + ks * 4 + (lane & 3)]; };
+        int k = 0;
+        for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
+            const int64_t c = list ? list[pos] : pos;
+            const int s = k % kStagesH;
+            mbar_wait(&full[s], (k / kStagesH) & 1);
+            mbar_wait(&gath[s], (k / kStagesH) & 1);
+            const unsigned char *st = sm + s * lay.size;
+            const int4 m0 = reinterpret_cast<const int4 *>(st + lay.meta)[0];
+            const int4 m1 = reinterpret_cast<const int4 *>(st + lay.meta)[1];
+            const int i0 = m0.x, nint = m0.y, nsh = m0.w, ne = m1.y, ni_al = m1.z;
+            const uint16_t *li_s = reinterpret_cast<const uint16_t *>(st + lay.lidx);
+            const double *g_s = reinterpret_cast<const double *>(st + lay.g);
+            double *Vc = a.V + (c * 2 * NP) * B;  // this chunk's V, [2 NP][B]
+            if (kChecked) {
+                const int4 r0 = reinterpret_cast<const int4 *>(ch.cmeta)[2 * c];
+                SEM_DCHECK(r0.x == m0.x && r0.y == m0.y && r0.z == m0.z && r0.w == m0.w, "stage meta is this chunk's");
+            }
+            // (1) lagged V update (and aux) per tile
+            if (kLag && tile) {
+                const double *w_s = reinterpret_cast<const double *>(st + lay.w);
+                double gr[MT][2], gs[MT][2];
+#pragma unroll
+                for (int m = 0; m < MT; m++) gr[m][0] = gr[m][1] = gs[m][0] = gs[m][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KT; ks++) {
+                    const int q = ks * 4 + (lane & 3);
+                    const double b = (q < NP && eb < ne) ? w_s[li_s[q * B + eb]] : 0.0;
+#pragma unroll
+                    for (int m = 0; m < MT; m++) {
+                        dmma_8x8x4(gr[m][0], gr[m][1], At(0, m, ks), b);
+                        dmma_8x8x4(gs[m][0], gs[m][1], At(1, m, ks), b);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const int e = nt * 8 + 2 * (lane & 3) + i;
+                    if (e < ne) {
+                        const double F00 = g_s[e], F01 = g_s[B + e], F10 = g_s[2 * B + e], F11 = g_s[3 * B + e];
+                        const double sd = g_s[4 * B + e];
+                        const double hF00 = a.h * F00, hF01 = a.h * F01, hF10 = a.h * F10, hF11 = a.h * F11;
+#pragma unroll
+                        for (int m = 0; m < MT; m++) {
+                            const int p = m * 8 + (lane >> 2);
+                            if (p < NP) {
+                                double v0 = Vc[p * B + e], v1 = Vc[(NP + p) * B + e];
+                                v0 = fma(hF00, gr[m][i], fma(hF10, gs[m][i], v0));
+                                v1 = fma(hF01, gr[m][i], fma(hF11, gs[m][i], v1));
+                                Vc[p * B + e] = v0;
+                                Vc[(NP + p) * B + e] = v1;
+                                if (kStep) {
+                                    const double sw = -sd * h_wK[p];
+                                    xs[(2 * p) * B + e] = sw * fma(F00, v0, F01 * v1);
+                                    xs[(2 * p + 1) * B + e] = sw * fma(F10, v0, F11 * v1);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (kStep) {
+                if (!kLag) {  // V as stored: aux straight from it
+                    for (int idx = t; idx < NP * ne; idx += C) {
+                        const int p = idx / ne, e = idx % ne;
+                        const double F00 = g_s[e], F01 = g_s[B + e], F10 = g_s[2 * B + e], F11 = g_s[3 * B + e];
+                        const double sw = -g_s[4 * B + e] * h_wK[p];
+                        const double v0 = Vc[p * B + e], v1 = Vc[(NP + p) * B + e];
+                        xs[(2 * p) * B + e] = sw * fma(F00, v0, F01 * v1);
+                        xs[(2 * p + 1) * B + e] = sw * fma(F10, v0, F11 * v1);
+                    }
+                }
+                consumer_sync<C>();
+                // (2) r = Dr^T ar + Ds^T as; Srr u, Sss u, Srs u
+                const double *u_s = reinterpret_cast<const double *>(st + lay.u);
+                double rr[MT][2], yr[MT][2], ys[MT][2], yx[MT][2];
+#pragma unroll
+                for (int m = 0; m < MT; m++)
+                    rr[m][0] = rr[m][1] = yr[m][0] = yr[m][1] = ys[m][0] = ys[m][1] = yx[m][0] = yx[m][1] = 0.0;
+                if (tile) {
+#pragma unroll
+                    for (int ks = 0; ks < KT; ks++) {
+                        const int q = ks * 4 + (lane & 3);
+                        const bool ok = q < NP && eb < ne;
+                        const double bar = ok ? xs[(2 * q) * B + eb] : 0.0;
+                        const double bas = ok ? xs[(2 * q + 1) * B + eb] : 0.0;
+                        const double bu = ok ? u_s[li_s[q * B + eb]] : 0.0;
+#pragma unroll
+                        for (int m = 0; m < MT; m++) {
+                            dmma_8x8x4(rr[m][0], rr[m][1], At(2, m, ks), bar);
+                            dmma_8x8x4(rr[m][0], rr[m][1], At(3, m, ks), bas);
+                            dmma_8x8x4(yr[m][0], yr[m][1], At(4, m, ks), bu);
+                            dmma_8x8x4(ys[m][0], ys[m][1], At(5, m, ks), bu);
+                            dmma_8x8x4(yx[m][0], yx[m][1], At(6, m, ks), bu);
+                        }
+                    }
+                }
+                consumer_sync<C>();  // every aux read before the entries overwrite it
+                const uint16_t *lpo = reinterpret_cast<const uint16_t *>(st + lay.lpos);
+                if (tile) {
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        const int e = nt * 8 + 2 * (lane & 3) + i;
+                        if (e < ne) {
+                            const double F00 = g_s[e], F01 = g_s[B + e], F10 = g_s[2 * B + e], F11 = g_s[3 * B + e];
+                            const double sd = g_s[4 * B + e];
+                            const double grr = sd * fma(F00, F00, F01 * F01);
+                            const double gss = sd * fma(F10, F10, F11 * F11);
+                            const double grs = sd * fma(F00, F10, F01 * F11);
+#pragma unroll
+                            for (int m = 0; m < MT; m++) {
+                                const int p = m * 8 + (lane >> 2);
+                                if (p < NP)
+                                    ebuf[lpo[p * B + e]] =
+                                        make_double2(rr[m][i], fma(grr, yr[m][i], fma(gss, ys[m][i], grs * yx[m][i])));
+                            }
+                        }
+                    }
+                }
+                consumer_sync<C>();
+                mbar_wait(wfull, k & 1);
+                // (4) node-centric reduction in fixed (JDS diagonal) order + fused Heun update
+                const uint16_t *jd = reinterpret_cast<const uint16_t *>(st + lay.jds);
+                const int32_t *shs = reinterpret_cast<const int32_t *>(st + lay.shs);
+                const int nwork = nint + nsh;
+                for (int wk = t; wk < nwork; wk += C) {
+                    const int i = wk < nint ? wk : ni_al + (wk - nint);  // skips the alignment hole
+                    const double2 ab = ch.max_count <= 32
+                                           ? (i < nint ? jds_sum2<32>(ebuf, jd, m1.x, i) : jds_sum2<32>(ebuf, jd + kJdsW, m1.w, i - ni_al))
+                                           : (i < nint ? jds_sum2(ebuf, jd, m1.x, i) : jds_sum2(ebuf, jd + kJdsW, m1.w, i - ni_al));
+                    if (i < nint) {
+                        const int64_t id = i0 + i;
+                        const bool src = id == a.src;
+                        heun_update(u_s[i], m_s[i], ab.x, ab.y, src ? f_n : 0.0, src ? f_n1 : 0.0, a.h, a.W[id],
+                                    a.U[id]);
+                    } else {
+                        reinterpret_cast<double2 *>(a.slot)[shs[i - ni_al]] = ab;
+                    }
+                }
+            }
+            consumer_sync<C>();
+            if (kChecked) {
+                unsigned char *stw = sm + s * lay.size;
+                double *uw = reinterpret_cast<double *>(stw + lay.u);
+                double *ww = reinterpret_cast<double *>(stw + lay.w);
+                for (int i = t; i < ni_al + nsh; i += C) { uw[i] = poison_f64(); ww[i] = poison_f64(); }
+                if (kStep) for (int i = t; i < ni_al; i += C) m_s[i] = poison_f64();
+                consumer_sync<C>();
+            }
+            if (t == 0) {
+                mbar_arrive(&empty[s]);
+                if (kStep) mbar_arrive(wempty);
+            }
+        }
+        return;
+    }
+    if constexpr (G > 1 && !kTcH) {
         // ===== consumer warps, G threads per element (high orders: P5 optionally, P7) =====
         // Warp wi takes elements 32 (wi / G) + lane and the row block rb = wi % G (rows
         // p = rb R + r) of every per-element product: the lagged V update (Algorithm 1) on its
@@ -653,7 +851,10 @@ int heun_group(int np, int B);
 size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
     const HeunLayout lay(np, B, L, Lp, Ls);
     const bool step = mode <= 1;
-    const size_t tabs = heun_group(np, B) > 1 ? 5 * (size_t)np * (np + (np & 1)) * 8 : 0;
+    const int g = heun_group(np, B);
+    const size_t tabs = heun_tc(np, g) ? 7 * (size_t)((np + 7) / 8 * 8) * ((np + 3) / 4 * 4) * 8
+                        : g > 1        ? 5 * (size_t)np * (np + (np & 1)) * 8
+                                       : 0;
     return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8 +
            tabs;
 }
