@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2104_08416_b200 import meshgen as mg, sem as S
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
-for P in (2, 5, 7):
+for P in [int(x) for x in (sys.argv[1:] or ["2", "5", "7"])]:
     pb = mg.config("B1", 1, degree=P) if P != 2 else mg.config("C5", 4)
     m = pb.mesh
     with S.SemContext(0, stream=st.cuda_stream) as ctx:
