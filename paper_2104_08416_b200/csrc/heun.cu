@@ -113,7 +113,7 @@ __device__ __forceinline__ void heun_update(double u0, double hm, double r, doub
 
 // MODE 0: step with V^n stored (no lag); 1: step with V lagged by one W
 // update; 2: finalise V only.
-template <int NP, int B, int MODE, int G = 1>
+template <int NP, int B, int MODE, int G = 1, bool TC = true>
 __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
     k_heun(const DevChunks ch, const HeunParams a, int L, int W, int Lp, int Ls, const int32_t *__restrict__ list,
            int64_t nlist) {
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
     // G > 1: the five tables in shared memory, rows padded to an even length (16-byte pairs):
     // Dr, Ds, Srr, Sss, Srs at tab + k * NP * kNPp.  Warp-uniform row, broadcast reads.
     constexpr int kNPp = NP + (NP & 1);
-    constexpr bool kTcH = heun_tc(NP, G);
+    constexpr bool kTcH = TC && heun_tc(NP, G);
     constexpr int kMP = (NP + 7) / 8 * 8, kKP = (NP + 3) / 4 * 4;  // tensor-core tiles: rows to 8, columns to 4
     double *tab = reinterpret_cast<double *>(idb + kStagesH);
     if (kTcH) {  // Dr, Ds, Dr^T, Ds^T, Srr, Sss, Srs zero-padded to [kMP][kKP] (A operands)
@@ -848,11 +848,11 @@ cudaError_t set_smem_h(K kernel, size_t bytes) {
 }
 
 int heun_group(int np, int B);
-size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
+size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode, bool tc) {
     const HeunLayout lay(np, B, L, Lp, Ls);
     const bool step = mode <= 1;
     const int g = heun_group(np, B);
-    const size_t tabs = heun_tc(np, g) ? 7 * (size_t)((np + 7) / 8 * 8) * ((np + 3) / 4 * 4) * 8
+    const size_t tabs = tc && heun_tc(np, g) ? 7 * (size_t)((np + 7) / 8 * 8) * ((np + 3) / 4 * 4) * 8
                         : g > 1        ? 5 * (size_t)np * (np + (np & 1)) * 8
                                        : 0;
     return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8 +
@@ -860,9 +860,13 @@ size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode) {
 }
 
 using HFn = void (*)(const DevChunks, const HeunParams, int, int, int, int, const int32_t *, int64_t);
-template <int NP, int B, int G = 1>
+template <int NP, int B, int G = 1, bool TC = true>
 HFn heun_fn_b(int mode) {
-    return mode == 0 ? k_heun<NP, B, 0, G> : mode == 1 ? k_heun<NP, B, 1, G> : k_heun<NP, B, 2, G>;
+    return mode == 0 ? k_heun<NP, B, 0, G, TC> : mode == 1 ? k_heun<NP, B, 1, G, TC> : k_heun<NP, B, 2, G, TC>;
+}
+template <int NP, int B, int G>
+HFn heun_fn_tc(int mode, bool tc) {
+    return tc ? heun_fn_b<NP, B, G, true>(mode) : heun_fn_b<NP, B, G, false>(mode);
 }
 // consumer threads per element of the Heun kernel: P7 4 (chunks of 64), P5 SEM_HEUN_G5 (default 4:
 // B1 1.044 -> 0.779 ms per step against 1 thread per element; 2: 0.803)
@@ -874,13 +878,16 @@ int heun_group(int np) {
 int heun_group(int np, int B) {
     return np == 21 && B < 128 ? 4 : heun_group(np);
 }
-HFn heun_fn(int np, int B, int mode) {
-    if (np == 36) return B == 32 ? heun_fn_b<36, 32, 4>(mode) : heun_fn_b<36, 64, 4>(mode);  // P7
+// tc: the tensor-core element products (only where heun_tc holds); heun_use_tc falls back to the
+// DFMA wide path when the tensor-core tables do not fit beside the stages (meshes with large chunks
+// of local nodes, e.g. the shuffled order at P7)
+HFn heun_fn(int np, int B, int mode, bool tc) {
+    if (np == 36) return B == 32 ? heun_fn_tc<36, 32, 4>(mode, tc) : heun_fn_tc<36, 64, 4>(mode, tc);  // P7
     if (np == 21) {                                      // P5 (the paper's Benchmark 1 order)
         const int g = heun_group(21);
-        if (B == 64) return heun_fn_b<21, 64, 4>(mode);
-        if (B == 32) return heun_fn_b<21, 32, 4>(mode);
-        return g == 4 ? heun_fn_b<21, 128, 4>(mode) : g == 2 ? heun_fn_b<21, 128, 2>(mode) : heun_fn_b<21, 128>(mode);
+        if (B == 64) return heun_fn_tc<21, 64, 4>(mode, tc);
+        if (B == 32) return heun_fn_tc<21, 32, 4>(mode, tc);
+        return g == 4 ? heun_fn_tc<21, 128, 4>(mode, tc) : g == 2 ? heun_fn_b<21, 128, 2>(mode) : heun_fn_b<21, 128>(mode);
     }
     if (np == 6) return B == 128 ? heun_fn_b<6, 128>(mode) : heun_fn_b<6, 256>(mode);
     return B == 128 ? heun_fn_b<10, 128>(mode) : heun_fn_b<10, 256>(mode);
@@ -921,9 +928,18 @@ cudaError_t launch_geometry_heun(const double *vxy, const int32_t *tri_or, const
     return cudaGetLastError();
 }
 
+bool heun_use_tc(const DevChunks &ch, int mode) {
+    if (!heun_tc(ch.Np, heun_group(ch.Np, ch.B))) return false;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode, true) <= (size_t)optin;
+}
+
 int heun_grid(const DevChunks &ch, int mode) {
-    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode);
-    const HFn fn = heun_fn(ch.Np, ch.B, mode);
+    const bool tc = heun_use_tc(ch, mode);
+    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode, tc);
+    const HFn fn = heun_fn(ch.Np, ch.B, mode, tc);
     set_smem_h(fn, smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ch.B * heun_group(ch.Np, ch.B) + 32, smem);
@@ -938,8 +954,9 @@ cudaError_t launch_heun(const DevChunks &ch, const HeunParams &p, int mode, cuda
                         int64_t nlist) {
     const int64_t n = list ? nlist : ch.nchunks;
     if (n == 0) return cudaSuccess;
-    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode);
-    const HFn fn = heun_fn(ch.Np, ch.B, mode);
+    const bool tc = heun_use_tc(ch, mode);
+    const size_t smem = heun_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, mode, tc);
+    const HFn fn = heun_fn(ch.Np, ch.B, mode, tc);
     cudaError_t e = set_smem_h(fn, smem);
     if (e != cudaSuccess) return e;
     int grid = heun_grid(ch, mode);

@@ -107,6 +107,7 @@ def main():
     if "heun" in which:
         heun(mg.config("C2", 16), 3, steps)
         heun(mg.config("B1", 40, degree=5), 5, steps)
+        heun(mg.config("B1", 40, degree=7), 7, steps)  # tensor-core Heun, chunks of 64
     if "mr" in which:
         loopback(mg.config("C2", 16), 2, steps)
     print("pipeline_cases ok", flush=True)
