@@ -134,10 +134,13 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
     constexpr int kNPp = NP + (NP & 1);
     constexpr bool kTcH = TC && heun_tc(NP, G);
     constexpr int kMP = (NP + 7) / 8 * 8, kKP = (NP + 3) / 4 * 4;  // tensor-core tiles: rows to 8, columns to 4
+    // table row stride = 4 or 12 mod 16 doubles: a warp's A-fragment reads (8 rows x 4 columns) hit
+    // distinct banks per half-warp
+    constexpr int kKS = (kKP % 16 == 4 || kKP % 16 == 12) ? kKP : kKP + 4;
     double *tab = reinterpret_cast<double *>(idb + kStagesH);
     if (kTcH) {  // Dr, Ds, Dr^T, Ds^T, Srr, Sss, Srs zero-padded to [kMP][kKP] (A operands)
-        for (int i = threadIdx.x; i < 7 * kMP * kKP; i += blockDim.x) {
-            const int tb = i / (kMP * kKP), r = (i / kKP) % kMP, q = i % kKP;
+        for (int i = threadIdx.x; i < 7 * kMP * kKS; i += blockDim.x) {
+            const int tb = i / (kMP * kKS), r = (i / kKS) % kMP, q = i % kKS;
             double v = 0.0;
             if (r < NP && q < NP) {
                 const double *src[7] = {h_Dr, h_Ds, h_Dr, h_Ds, h_Srr, h_Sss, h_Srs};
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
         const int eb = nt * 8 + (lane >> 2);  // this lane's B-fragment element
         const double f_n = src_term(a, a.src, a.n), f_n1 = src_term(a, a.src, a.n + 1);
         double *xs = reinterpret_cast<double *>(ebuf);  // aux [NP][2][B], aliases the entry buffer
-        auto At = [&](int tb, int m, int ks) { return tab[(tb * kMP + m * 8 + (lane >> 2)) * kKP + ks * 4 + (lane & 3)]; };
+        auto At = [&](int tb, int m, int ks) { return tab[(tb * kMP + m * 8 + (lane >> 2)) * kKS + ks * 4 + (lane & 3)]; };
         int k = 0;
         for (int64_t pos = blockIdx.x; pos < nch; pos += gridDim.x, k++) {
             const int64_t c = list ? list[pos] : pos;
@@ -273,6 +276,19 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
             // (1) lagged V update (and aux) per tile
             if (kLag && tile) {
                 const double *w_s = reinterpret_cast<const double *>(st + lay.w);
+                // this lane's V entries of the epilogue, loaded before the products
+                double vv[MT][2][2];
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const int e = nt * 8 + 2 * (lane & 3) + i;
+#pragma unroll
+                    for (int m = 0; m < MT; m++) {
+                        const int p = m * 8 + (lane >> 2);
+                        const bool ok = e < ne && p < NP;
+                        vv[m][i][0] = ok ? Vc[p * B + e] : 0.0;
+                        vv[m][i][1] = ok ? Vc[(NP + p) * B + e] : 0.0;
+                    }
+                }
                 double gr[MT][2], gs[MT][2];
 #pragma unroll
                 for (int m = 0; m < MT; m++) gr[m][0] = gr[m][1] = gs[m][0] = gs[m][1] = 0.0;
@@ -297,7 +313,7 @@ __global__ void __launch_bounds__(B * G + 32, G > 1 ? 1 : B <= 128 ? 2 : 1)
                         for (int m = 0; m < MT; m++) {
                             const int p = m * 8 + (lane >> 2);
                             if (p < NP) {
-                                double v0 = Vc[p * B + e], v1 = Vc[(NP + p) * B + e];
+                                double v0 = vv[m][i][0], v1 = vv[m][i][1];
                                 v0 = fma(hF00, gr[m][i], fma(hF10, gs[m][i], v0));
                                 v1 = fma(hF01, gr[m][i], fma(hF11, gs[m][i], v1));
                                 Vc[p * B + e] = v0;
@@ -852,7 +868,8 @@ size_t heun_smem_bytes(int np, int B, int L, int W, int Lp, int Ls, int mode, bo
     const HeunLayout lay(np, B, L, Lp, Ls);
     const bool step = mode <= 1;
     const int g = heun_group(np, B);
-    const size_t tabs = tc && heun_tc(np, g) ? 7 * (size_t)((np + 7) / 8 * 8) * ((np + 3) / 4 * 4) * 8
+    const int kp = (np + 3) / 4 * 4, ks = (kp % 16 == 4 || kp % 16 == 12) ? kp : kp + 4;
+    const size_t tabs = tc && heun_tc(np, g) ? 7 * (size_t)((np + 7) / 8 * 8) * ks * 8
                         : g > 1        ? 5 * (size_t)np * (np + (np & 1)) * 8
                                        : 0;
     return (size_t)kStagesH * lay.size + (step ? (size_t)np * B * 16 + (size_t)W * 8 : 0) + (4 * kStagesH + 2) * 8 +
