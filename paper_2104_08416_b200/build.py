@@ -40,16 +40,38 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
-    """Compile the library (out/defines: experiment variants, e.g. out=libsem_alt.so)."""
+    """Compile the library (out/defines: experiment variants, e.g. out=libsem_alt.so).
+
+    Each source compiles to its own object in parallel (build/<variant>/), then one link."""
     if not force and out == LIB and not stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", out + ".tmp", "-lgomp", "-ldl"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    log = r.stdout + r.stderr
+    from concurrent.futures import ThreadPoolExecutor
+
+    tag = os.path.splitext(os.path.basename(out))[0]
+    odir = os.path.join(ROOT, "build", tag)
+    os.makedirs(odir, exist_ok=True)
+    base = [_nvcc(), *[f for f in NVCC_FLAGS if f != "-shared"], *["-D" + d for d in defines],
+            "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+
+    def compile_one(src):
+        obj = os.path.join(odir, src + ".o")
+        cmd = [*base, "-c", os.path.join(CSRC, src), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r.returncode, " ".join(cmd) + "\n" + r.stdout + r.stderr
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    log = "".join(r[3] for r in results)
+    ok = all(r[2] == 0 for r in results)
+    if ok:
+        link = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC,-fopenmp",
+                *[r[1] for r in results], "-o", out + ".tmp", "-lgomp", "-ldl"]
+        r = subprocess.run(link, capture_output=True, text=True)
+        log += " ".join(link) + "\n" + r.stdout + r.stderr
+        ok = r.returncode == 0
     with open(os.path.join(CSRC, "build.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + log)
-    if r.returncode != 0:
+        f.write(log)
+    if not ok:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed (see %s)" % os.path.join(CSRC, "build.log"))
     os.replace(out + ".tmp", out)

@@ -37,6 +37,44 @@ SEM_HD constexpr bool lattice_interior(int np, int p) {
             if (q == p) return i >= 1 && j >= 1 && i + j <= P - 1;
     return false;
 }
+// Reflection r <-> s of the reference triangle on the lattice order: node (i, j) -> (j, i).
+// The stiffness factors satisfy Sss = Pi Srr Pi and Srs = Pi Srs Pi under it (bit for bit at
+// P4-P7, to one ulp at P2/P3, where the tables come from a different derivation).
+SEM_HD constexpr int lattice_mirror(int np, int p) {
+    const int P = lattice_degree(np);
+    int q = 0, pi = 0, pj = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, q++)
+            if (q == p) { pi = i; pj = j; }
+    q = 0;
+    for (int j = 0; j <= P; j++)
+        for (int i = 0; i <= P - j; i++, q++)
+            if (i == pj && j == pi) return q;
+    return -1;
+}
+// Pairs (p <= q) of K^e's upper triangle grouped with their mirror pair (sorted (pi p, pi q)):
+// MirrorTable<NP>: the canonical pairs (the lexicographically smaller of the two) in order,
+// p, q and the mirror pair mp, mq of each; n = their number.
+constexpr int kMirMax = 128;  // canonical pairs held in constant memory (P <= 5: at most 123)
+template <int NP>
+struct MirrorTable {
+    int n = 0;
+    int p[kMirMax] = {}, q[kMirMax] = {}, mp[kMirMax] = {}, mq[kMirMax] = {};
+    constexpr MirrorTable() {
+        int pi[NP] = {};
+        for (int k = 0; k < NP; k++) pi[k] = lattice_mirror(NP, k);
+        for (int a = 0; a < NP; a++)
+            for (int b = a; b < NP; b++) {
+                int x = pi[a], y = pi[b];
+                if (x > y) { const int z = x; x = y; y = z; }
+                if ((a < x || (a == x && b <= y)) && n < kMirMax) {
+                    p[n] = a; q[n] = b; mp[n] = x; mq[n] = y;
+                    n++;
+                }
+            }
+    }
+};
+
 SEM_HD constexpr int lattice_n_interior(int np) {
     const int P = lattice_degree(np);
     return P >= 3 ? (P - 1) * (P - 2) / 2 : 0;

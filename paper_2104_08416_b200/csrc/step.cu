@@ -70,6 +70,43 @@ __constant__ double c_Srr[kMaxNp * kMaxNp];
 __constant__ double c_Sss[kMaxNp * kMaxNp];
 __constant__ double c_Srs[kMaxNp * kMaxNp];
 __constant__ double c_wM[kMaxNp];
+// (Srr, Sss, Srs, 0) of the canonical mirror pairs (mirror_pair, sem_internal.h), P <= 5
+__constant__ double c_mir[4 * kMirMax];
+
+// One-thread-per-element K^e u (P3-P5) with the reflection symmetry of the reference triangle:
+// pair (p, q) and its mirror (p', q') share their three factors (Srr_p'q' = Sss_pq,
+// Sss_p'q' = Srr_pq, Srs_p'q' = Srs_pq), so each canonical pair reads 3 constants and forms
+// grs Srs once for both K^e entries (A/B: -DSEM_K7_MIRROR=0).
+#ifndef SEM_K7_MIRROR
+#define SEM_K7_MIRROR 1
+#endif
+template <int NP, int K>
+__device__ __forceinline__ void mirror_products(double (&y)[NP], const double (&u)[NP], double grr, double gss,
+                                                double grs) {
+    constexpr MirrorTable<NP> T{};
+    if constexpr (K < T.n) {
+        constexpr int p = T.p[K], q = T.q[K], mp = T.mp[K], mq = T.mq[K];
+        const double A = c_mir[4 * K], Bs = c_mir[4 * K + 1], Cs = c_mir[4 * K + 2];
+        const double g = grs * Cs;
+        const double k1 = fma(grr, A, fma(gss, Bs, g));
+        if constexpr (p == q) {
+            y[p] = fma(k1, u[p], y[p]);
+        } else {
+            y[p] = fma(k1, u[q], y[p]);
+            y[q] = fma(k1, u[p], y[q]);
+        }
+        if constexpr (!(mp == p && mq == q)) {
+            const double k2 = fma(grr, Bs, fma(gss, A, g));
+            if constexpr (mp == mq) {
+                y[mp] = fma(k2, u[mp], y[mp]);
+            } else {
+                y[mp] = fma(k2, u[mq], y[mp]);
+                y[mq] = fma(k2, u[mp], y[mq]);
+            }
+        }
+        mirror_products<NP, K + 1>(y, u, grr, gss, grs);
+    }
+}
 
 // step index of U: from device memory when the step loop runs as a CUDA graph
 // (one graph replays many steps; k_step_inc advances the counter), else the
@@ -514,6 +551,9 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
             double u[NP];
 #pragma unroll
             for (int p = 0; p < NP; p++) u[p] = u_s[li_s[p * B + t]];
+            if constexpr (SEM_K7_MIRROR != 0 && NP >= 10 && NP <= 21) {  // P2: 66 -> 76 registers cost its third CTA per SM (C5/4 0.447 -> 0.546 ms)
+                mirror_products<NP, 0>(y, u, grr, gss, grs);
+            } else {
 #pragma unroll
             for (int p = 0; p < NP; p++) {
 #pragma unroll
@@ -526,6 +566,7 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
                         y[q] = fma(kk, u[p], y[q]);
                     }
                 }
+            }
             }
         }
         const double *up_s = WIN2 ? reinterpret_cast<const double *>(st + lay.up) : up_w;
@@ -804,6 +845,26 @@ cudaError_t upload_ref_tables(const RefTables &T, cudaStream_t s) {
     if ((e = cudaMemcpyToSymbolAsync(c_Srr, rr.data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
     if ((e = cudaMemcpyToSymbolAsync(c_Sss, ss.data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
     if ((e = cudaMemcpyToSymbolAsync(c_Srs, rs.data(), sizeof(double) * n * n, 0, cudaMemcpyHostToDevice, s))) return e;
+    if (n <= 21) {  // the canonical mirror pairs of the one-thread K7 (P <= 5)
+        static constexpr MirrorTable<6> t6{};
+        static constexpr MirrorTable<10> t10{};
+        static constexpr MirrorTable<15> t15{};
+        static constexpr MirrorTable<21> t21{};
+        static_assert(t21.n <= kMirMax, "mirror pairs fit c_mir");
+        const int cnt = n == 6 ? t6.n : n == 10 ? t10.n : n == 15 ? t15.n : t21.n;
+        const int *tp = n == 6 ? t6.p : n == 10 ? t10.p : n == 15 ? t15.p : t21.p;
+        const int *tq = n == 6 ? t6.q : n == 10 ? t10.q : n == 15 ? t15.q : t21.q;
+        std::vector<double> mir(4 * kMirMax, 0.0);
+        for (int k = 0; k < cnt; k++) {
+            const int p = tp[k], q = tq[k];
+            mir[4 * k] = T.Srr[p][q];
+            mir[4 * k + 1] = T.Sss[p][q];
+            mir[4 * k + 2] = T.Srs[p][q];
+        }
+        if ((e = cudaMemcpyToSymbolAsync(c_mir, mir.data(), sizeof(double) * 4 * kMirMax, 0, cudaMemcpyHostToDevice, s)))
+            return e;
+        // Host copies above are pageable: the call returns once staged, so `mir` may go out of scope.
+    }
     return cudaMemcpyToSymbolAsync(c_wM, T.wM, sizeof(T.wM), 0, cudaMemcpyHostToDevice, s);
 }
 
