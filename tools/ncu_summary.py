@@ -4,6 +4,7 @@
   python tools/ncu_summary.py launches <launches.csv>        # per-kernel share of device time
   python tools/ncu_summary.py full <report.ncu-rep>          # key counters of one captured launch
   python tools/ncu_summary.py source <report.ncu-rep> [N]    # top-N source lines by stall samples
+  python tools/ncu_summary.py mix <report.ncu-rep>           # SASS opcode mix: executed, stall samples, smem
 """
 import collections
 import csv
@@ -102,5 +103,29 @@ def source(path, top=15):
         print("| %.1f%% | %s | `%s` | %s |" % (100.0 * x / T, ln, text.get(ln, "").strip()[:80].replace("|", "\\|"), st))
 
 
+def mix(path, top=20):
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hi = [i for i, r in enumerate(rows) if len(r) > 4 and r[0] == "Address"][0]
+    h = rows[hi]
+    ix = {n: i for i, n in enumerate(h)}
+    ex, sm, wf = collections.Counter(), collections.Counter(), collections.Counter()
+    for r in rows[hi + 1:]:
+        if len(r) < len(h):
+            continue
+        src = r[ix["Source"]].split()
+        if not src:
+            continue
+        op = (src[1] if src[0].startswith("@") and len(src) > 1 else src[0]).split(".")[0]
+        ex[op] += int(r[ix["Instructions Executed"]] or 0)
+        sm[op] += int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+        wf[op] += int(r[ix["L1 Wavefronts Shared"]] or 0)
+    TE, TS = sum(ex.values()), sum(sm.values())
+    print("| opcode | warp instructions executed | share | stall samples | share | shared wavefronts |")
+    print("|---|---|---|---|---|---|")
+    for op, c in ex.most_common(top):
+        print("| %s | %d | %.1f%% | %d | %.1f%% | %d |" % (op, c, 100.0 * c / TE, sm[op], 100.0 * sm[op] / max(TS, 1), wf[op]))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full, "source": source}[sys.argv[1]](*sys.argv[2:3])
+    {"launches": launches, "full": full, "source": source, "mix": mix}[sys.argv[1]](*sys.argv[2:3])
