@@ -27,8 +27,11 @@ using namespace sem;
 namespace {
 int g_const_P = 0;  // degree whose tables currently sit in __constant__ memory
 
-// Elements per chunk (one CTA iteration of K7): 256 at P2/P3 (128 for Heun); SEM_CHUNK=128|192|512
-// selects the other compiled variants (design experiments, chunk size).
+// Elements per chunk (one CTA iteration of K7): 512 at P3 (one CTA of 17 warps per SM; half the
+// shared nodes of 256: C4 step 0.3862 -> 0.3792 ms, C3 0.1926 -> 0.1906 ms), 256 at P2 (C5/4 0.445
+// at 256 against 0.569 ms at 512), 128 for Heun; SEM_CHUNK=128|192|256|512 selects the other
+// compiled variants (design experiments, chunk size).  A mesh whose largest
+// chunks of 512 would not fit one CTA's shared memory is rebuilt with 256 (sem_mesh_reorder).
 int chunk_elems(int P, bool heun) {
     const char *v = getenv("SEM_CHUNK");
     if (heun && (P == 5 || P == 7)) {  // Heun's wide kernel: SEM_CHUNK=32|64|128 (A/B)
@@ -38,7 +41,7 @@ int chunk_elems(int P, bool heun) {
     if (P == 4 || P == 5) return 128;  // shared-memory budget of the stage at 15 / 21 nodes per element
     if (P == 6 || P == 7) return 64;   // ... and at 28 / 36
     // Heun (integrator selected before sem_mesh_reorder): 128 runs 2 CTAs per SM
-    const int b = v ? atoi(v) : (heun ? 128 : 256);
+    const int b = v ? atoi(v) : (heun ? 128 : P == 3 ? 512 : 256);
     return (b == 128 || b == 192 || b == 512) ? b : 256;
 }
 
@@ -1302,14 +1305,33 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
         tr.mark(s, "partition");
 
         // ---- chunk metadata for the step kernel ----
-        const int B_chunk = chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN);
+        int B_chunk = chunk_elems(degree, ctx->integrator == SEM_INTEGRATOR_HEUN);
         ChunkMeta m;
         DevChunks &d = ctx->dch;
+        const size_t mark = L.size();  // the chunk arrays start here (fallback rebuild)
+        // chunks of 512 whose largest members overflow one CTA's shared memory: rebuild with 256
+        const auto too_big = [&](const ChunkMeta &mm) {
+            if (B_chunk != 512 || ctx->integrator == SEM_INTEGRATOR_HEUN) return false;
+            DevChunks t{};
+            t.Np = Np; t.B = B_chunk;
+            t.max_local = mm.max_local; t.max_win = mm.max_win; t.max_count = mm.max_count; t.max_nsh = mm.max_nsh;
+            return !k7_fits(t, false);
+        };
+    build_chunk_arrays:
         if (gpu_chunks) {
             CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, B_chunk,
                                 one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd, &ctx->d_intc,
                                 err, s));
             if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
+            if (too_big(m)) {
+                CK(cudaStreamSynchronize(s));
+                L.release_from(mark);
+                m = ChunkMeta();
+                d = DevChunks{};
+                B_chunk = 256;
+                tr.mark(s, "chunks of 512 do not fit one CTA: rebuilt with 256");
+                goto build_chunk_arrays;
+            }
             if (check_chunks) {
                 ChunkMeta h;
                 if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, h,
@@ -1320,9 +1342,15 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             }
             std::vector<int32_t>().swap(mu_h);
             tr.mark(s, "chunk builder (GPU)");
-        } else if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m,
-                                 err, one ? nullptr : part.remote.data())) {
-            return fail(ctx, SEM_E_MESH, err);
+        } else {
+            if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m, err,
+                              one ? nullptr : part.remote.data()))
+                return fail(ctx, SEM_E_MESH, err);
+            if (too_big(m)) {
+                m = ChunkMeta();
+                B_chunk = 256;
+                goto build_chunk_arrays;
+            }
         }
         if (!gpu_chunks) {
             if (ctx->scatter != SEM_SCATTER_CHUNK) ST(prepare_ablation(ctx, mu_h, E, Np, N, degree, one, m, s));

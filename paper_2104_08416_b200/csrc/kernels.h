@@ -155,6 +155,8 @@ struct StepParams {
 // persistent K7 grid: resident CTAs per SM x SMs; reserve_sms SMs' worth of CTA slots are left free
 // (for the exchange kernels on the comm stream while the interior chunks run)
 int k7_grid(const DevChunks &ch, bool fused, int reserve_sms = 0);
+// K7's shared memory for these chunks fits one CTA on the current device
+bool k7_fits(const DevChunks &ch, bool fused);
 // resident K7 CTAs per SM for chunks of B elements with these per-chunk maxima (shared-memory stages)
 int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool fused, int max_count = 0);
 // device step counter of the graph-captured step loop: += 1, = v

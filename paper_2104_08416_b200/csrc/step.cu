@@ -911,6 +911,19 @@ int k7_ctas_per_sm(int np, int B, int max_local, int max_win, int max_nsh, bool 
     return occ < 1 ? 1 : occ;
 }
 
+bool k7_fits(const DevChunks &ch, bool fused) {
+    const bool wide = ch.max_count > 32;
+    const size_t smem = k7_smem_bytes(ch.Np, ch.B, ch.max_local, ch.max_win, 2 * kJdsW, ch.max_nsh, fused, wide);
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return false;
+    // SEM_K7_SMEM_CAP (bytes, tests): a smaller budget than the device's, to exercise the fallback
+    const char *cap = getenv("SEM_K7_SMEM_CAP");
+    if (cap && atol(cap) > 0 && atol(cap) < optin) optin = (int)atol(cap);
+    return smem <= (size_t)optin;
+}
+
 int k7_grid(const DevChunks &ch, bool fused, int reserve_sms) {
     const int occ = k7_ctas_per_sm(ch.Np, ch.B, ch.max_local, ch.max_win, ch.max_nsh, fused, ch.max_count);
     const int nsm = current_sm_count();

@@ -49,3 +49,33 @@ def test_single_element_and_tiny(ctx):
         for P in (2, 3, 5, 7):
             r = ctx.sem_mesh_reorder(vxy[:3] if len(tri) == 1 else vxy, tri, P)
             assert r["n_nodes"] > 0
+
+
+def test_chunks_of_512_fall_back_to_256(monkeypatch):
+    """P3 defaults to chunks of 512 (api.cu chunk_elems); a mesh whose largest chunks would
+    not fit one K7 CTA's shared memory is rebuilt with 256 (SEM_K7_SMEM_CAP lowers the budget
+    to force it).  Both builds keep the oracle parity of a few steps from a random state."""
+    import numpy as np
+    from oracle.core import OracleSEM
+
+    monkeypatch.delenv("SEM_CHUNK", raising=False)
+    pb = mg.config("C2", 8)
+    m = pb.mesh
+    o = OracleSEM(m.vxy, m.tri, pb.P, pb.c)
+    rng = np.random.default_rng(11)
+    U0 = rng.standard_normal(o.N)
+    Up = U0 + 0.1 * rng.standard_normal(o.N)
+    Uo, _ = o.leapfrog(pb.dt, 5, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=0.0, U=U0, Uprev=Up, step0=3)
+    for cap, want in ((None, 512), ("150000", 256)):
+        if cap:
+            monkeypatch.setenv("SEM_K7_SMEM_CAP", cap)
+        with S.SemContext(0) as c:
+            c.sem_mesh_reorder(m.vxy, m.tri, pb.P)
+            assert c.sem_get_info()["chunk_elems"] == want
+            c.sem_build_operators(pb.c, pb.src_vertex, pb.f0, 0.0, 1.0, pb.dt)
+            c.sem_write_state(U0, Up)
+            c.sem_set_step(3)
+            c.sem_step_n(5)
+            Ug, n = c.sem_read_field()
+        assert n == 8
+        assert float(np.linalg.norm(Ug - Uo) / np.linalg.norm(Uo)) <= 1e-13

@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 @pytest.mark.parametrize("env", [{"SEM_K7_WIN": "0"}, {"SEM_K7_WIN": "2"}, {"SEM_FUSE_K8": "1"},
                                  {"SEM_HOST_CHUNKS": "1"}, {"SEM_GRAPH": "0"}, {"SEM_PDL": "1"},
-                                 {"SEM_CHUNK": "128"}, {"SEM_CHUNK": "192"}, {"SEM_CHUNK": "512"},
+                                 {"SEM_CHUNK": "128"}, {"SEM_CHUNK": "192"}, {"SEM_CHUNK": "256"}, {"SEM_CHUNK": "512"},
+                                 {"SEM_K7_SMEM_CAP": "150000"}, {"SEM_K7_SMEM_CAP": "150000", "SEM_HOST_CHUNKS": "1"},
                                  {"SEM_K7_G5": "2"}])
 def test_knob_keeps_parity(env):
     e = dict(os.environ)

@@ -260,7 +260,7 @@ def test_full_size_bench_configuration(ctx, name):
     Up = U0 + 0.1 * rng.standard_normal(o.N)
     Uo, _ = o.leapfrog(pb.dt, 1, src=pb.src_vertex, A=1.0, f0=pb.f0, t0=pb.t0, U=U0, Uprev=Up, step0=5)
     Ug = run_gpu(ctx, pb, 1, state=(U0, Up), step0=5)
-    assert ctx.sem_get_info()["chunk_elems"] == 256
+    assert ctx.sem_get_info()["chunk_elems"] == 512  # the P3 default (api.cu chunk_elems)
     assert rel_l2(Ug, Uo) <= 1e-13, rel_l2(Ug, Uo)
     pb2 = mg.Problem(**{**pb.__dict__, "t0": 3 * pb.dt, "f0": 1.0 / (8 * pb.dt)})
     Uo, _ = o.leapfrog(pb2.dt, 10, src=pb2.src_vertex, A=1.0, f0=pb2.f0, t0=pb2.t0)
