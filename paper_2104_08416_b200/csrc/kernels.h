@@ -222,5 +222,7 @@ cudaError_t launch_abl_update(int64_t n, const StepParams &p, double *KU, cudaSt
 cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,
                                double *out, cudaStream_t s);
 cudaError_t launch_nonfinite(const double *a, int64_t n, int32_t *flag, cudaStream_t s);
+// *first = min(*first, smallest i < n with !(a[i] > 0) or a[i] not finite)
+cudaError_t launch_check_positive(const double *a, int64_t n, int32_t *first, cudaStream_t s);
 
 }  // namespace sem

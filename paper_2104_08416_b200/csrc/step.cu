@@ -709,6 +709,11 @@ __global__ void k_permute_f64(const double *__restrict__ in, const int32_t *__re
     out[omap ? omap[i] : i] = in[imap ? imap[i] : i];
 }
 
+__global__ void k_positive(const double *__restrict__ a, int64_t n, int32_t *first) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && !(a[i] > 0.0 && isfinite(a[i]))) atomicMin(first, (int32_t)i);
+}
+
 __global__ void k_nonfinite(const double *__restrict__ a, int64_t n, int32_t *flag) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n && !isfinite(a[i])) atomicMin(flag, (int32_t)i);
@@ -1039,6 +1044,11 @@ cudaError_t launch_step_set(int64_t *n, int64_t v, cudaStream_t s) {
 cudaError_t launch_permute_f64(const double *in, const int32_t *imap, const int32_t *omap, int64_t n,
                                double *out, cudaStream_t s) {
     k_permute_f64<<<blocks_for(n), kThreads, 0, s>>>(in, imap, omap, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_positive(const double *a, int64_t n, int32_t *first, cudaStream_t s) {
+    if (n > 0) k_positive<<<blocks_for(n), kThreads, 0, s>>>(a, n, first);
     return cudaGetLastError();
 }
 

@@ -216,6 +216,13 @@ def test_errors(ctx):
     with pytest.raises(S.SemError) as e:
         ctx.sem_build_operators(c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
     assert e.value.status == S.SEM_E_ARG and "element 3" in e.value.msg
+    for k, v in ((9, np.nan), (11, 0.0), (12, np.inf)):  # checked on the device: the smallest bad index
+        c = pb.c.copy()
+        c[k] = v
+        c[k + 5] = -2.0
+        with pytest.raises(S.SemError) as e:
+            ctx.sem_build_operators(c, pb.src_vertex, pb.f0, pb.t0, 1.0, pb.dt)
+        assert e.value.status == S.SEM_E_ARG and ("element %d " % k) in e.value.msg, e.value.msg
     with pytest.raises(S.SemError) as e:
         ctx.sem_build_operators(pb.c, pb.src_vertex, pb.f0, pb.t0, 1.0, -1.0)
     assert e.value.status == S.SEM_E_ARG
