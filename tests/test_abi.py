@@ -88,6 +88,30 @@ def test_library_stiffness_tables_equal_oracle(P):
             assert np.abs(g[k] - ref[k]).max() <= 1e-13 * np.abs(ref[k]).max(), k
 
 
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7])
+def test_stiffness_tables_reflection_symmetry(P):
+    # K7's one-thread element products (P3-P5, step.cu mirror_products) read one set of
+    # (Srr, Sss, Srs) per mirror pair: the reflection r <-> s of the reference triangle,
+    # lattice node (i, j) -> (j, i), maps Srr onto Sss and Srs onto itself.  The identity is
+    # exact in the library's P4-P7 tables and holds to a few ulp at P2/P3 (DESIGN.md v12).
+    g = sem.sem_debug_ref_stiffness(P)
+    lat = [(i, j) for j in range(P + 1) for i in range(P + 1 - j)]
+    idx = {n: k for k, n in enumerate(lat)}
+    pi = np.array([idx[(j, i)] for (i, j) in lat])
+    A = np.ix_(pi, pi)
+    scale = max(np.abs(g[k]).max() for k in ("Srr", "Sss", "Srs"))
+    tol = 0.0 if P >= 4 else 4 * np.finfo(float).eps * scale
+    assert np.abs(g["Sss"] - g["Srr"][A]).max() <= tol
+    assert np.abs(g["Srs"] - g["Srs"][A]).max() <= tol
+    # the rotation (i, j) -> (P - i - j, i) maps K^e(G) onto K^e(T(G)) with
+    # T(G) = (gss, grr + 2 grs + gss, -(grs + gss)) (the six-symmetry form of section 6)
+    rho = np.array([idx[(P - i - j, i)] for (i, j) in lat])
+    grr, gss, grs = 1.3, 0.7, -0.2
+    K = grr * g["Srr"] + gss * g["Sss"] + grs * g["Srs"]
+    KT = gss * g["Srr"] + (grr + 2 * grs + gss) * g["Sss"] - (grs + gss) * g["Srs"]
+    assert np.abs(K[np.ix_(rho, rho)] - KT).max() <= 64 * np.finfo(float).eps * np.abs(K).max()
+
+
 @pytest.mark.parametrize("P", [1, 8])
 def test_library_rejects_unsupported_degrees(P):
     with pytest.raises(sem.SemError) as e:
