@@ -210,6 +210,8 @@ struct sem_ctx {
     int64_t step = 0;
     cudaEvent_t xev = nullptr;  // loopback: phase-1 done on this rank
     cudaStream_t comm_stream = nullptr;           // NCCL exchange, overlapped with interior chunks
+    cudaStream_t io_stream = nullptr;             // sem_mesh_reorder's output copies, overlapped with the chunk builder
+    cudaEvent_t io_ev = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
     int32_t *d_bnd = nullptr, *d_intc = nullptr;  // boundary / interior chunk lists
     int64_t n_bnd = 0, n_intc = 0;
@@ -1062,6 +1064,8 @@ void sem_free(sem_ctx *ctx) {
     if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
     if (ctx->ev_exchanged) cudaEventDestroy(ctx->ev_exchanged);
     if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->io_stream) cudaStreamDestroy(ctx->io_stream);
+    if (ctx->io_ev) cudaEventDestroy(ctx->io_ev);
     for (auto &e : ctx->pev)
         if (e) cudaEventDestroy(e);
     if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
@@ -1248,14 +1252,32 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             node_perm.resize(N);
             CK(cudaMemcpyAsync(node_perm.data(), d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
         }
-        if (node_perm_out)
-            CK(cudaMemcpyAsync(node_perm_out, d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+        // the caller's permutations go out on a side stream while the chunk builder runs (pinned
+        // destinations overlap; pageable ones are staged by the copy call); every return below
+        // waits for them first (io_sync, destroyed before the temporaries)
+        struct IoSync {
+            cudaStream_t st = nullptr;
+            ~IoSync() {
+                if (st) cudaStreamSynchronize(st);
+            }
+        } io_sync;
+        if (node_perm_out || elem_perm_out) {
+            if (!ctx->io_stream) CK(cudaStreamCreateWithFlags(&ctx->io_stream, cudaStreamNonBlocking));
+            if (!ctx->io_ev) CK(cudaEventCreateWithFlags(&ctx->io_ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->io_ev, s));
+            CK(cudaStreamWaitEvent(ctx->io_stream, ctx->io_ev, 0));
+            io_sync.st = ctx->io_stream;
+            if (node_perm_out)
+                CK(cudaMemcpyAsync(node_perm_out, d_node_perm, sizeof(int32_t) * N, cudaMemcpyDeviceToHost,
+                                   ctx->io_stream));
+            if (elem_perm_out)
+                CK(cudaMemcpyAsync(elem_perm_out, ctx->d_perm, sizeof(int32_t) * E, cudaMemcpyDeviceToHost,
+                                   ctx->io_stream));
+        }
         if (!gpu_chunks || check_chunks) {
             mu_h.resize((size_t)E * Np);
             CK(cudaMemcpyAsync(mu_h.data(), d_mu_ft, sizeof(int32_t) * E * Np, cudaMemcpyDeviceToHost, s));
         }
-        if (elem_perm_out)
-            CK(cudaMemcpyAsync(elem_perm_out, ctx->d_perm, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (n_nodes_out) *n_nodes_out = N;
         if (grid_wh_out) { grid_wh_out[0] = ctx->grid[0]; grid_wh_out[1] = ctx->grid[1]; }
