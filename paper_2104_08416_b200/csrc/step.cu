@@ -80,6 +80,9 @@ __constant__ double c_mir[4 * kMirMax];
 #ifndef SEM_K7_MIRROR
 #define SEM_K7_MIRROR 1
 #endif
+#ifndef SEM_K7_REV_TAIL
+#define SEM_K7_REV_TAIL 1
+#endif
 template <int NP, int K>
 __device__ __forceinline__ void mirror_products(double (&y)[NP], const double (&u)[NP], double grr, double gss,
                                                 double grs) {
@@ -600,7 +603,15 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
         //     interior node w < nint_np, else shared node ni_al + (w - nint_np) (skips
         //     the element-interior nodes and the alignment hole)
         const int nwork = nint_np + nsh;
-        for (int w = t; w < nwork; w += C) {
+        // P3: the work items are sorted by entry count (the vertex nodes' six-entry sums first), so
+        // the threads that drew them in the first round skip the last, partial round: it is taken
+        // in reverse thread order (C4 0.3835 -> 0.3724 ms per step, C3 0.1923 -> 0.1881 ms; at P2
+        // and P5 it measured 1-2 % slower; A/B: -DSEM_K7_REV_TAIL=0).
+        constexpr bool kRevTail = SEM_K7_REV_TAIL != 0 && NP == 10;
+        const int nfull = kRevTail ? nwork / C * C : nwork;
+        for (int w0 = 0; w0 < nwork; w0 += C) {
+            const int w = w0 + (w0 >= nfull ? C - 1 - t : t);
+            if (w >= nwork) continue;
             const int i = w < nint_np ? w : ni_al + (w - nint_np);
             double upg = 0.0, mg = 0.0;
             if (WM == 0 && i < nint) {  // coalesced global loads, issued before the shared-memory sum
