@@ -39,6 +39,8 @@ def lib():
             L = C.CDLL(_LIB)
             P = C.c_void_p
             i64, i32, u64, dbl = C.c_int64, C.c_int32, C.c_uint64, C.c_double
+            L.orc_splitmix64_value.argtypes = [C.c_uint64]
+            L.orc_splitmix64_value.restype = C.c_uint64
             L.orc_gilbert_path.argtypes = [i32, i32, P, P]
             L.orc_gilbert_path.restype = i64
             L.orc_orient.argtypes = [P, P, i64, P, P]
@@ -122,6 +124,11 @@ def hilbert_order(vxy: np.ndarray, tri: np.ndarray):
     if rc != 0:
         raise OracleError("hilbert_order rc=%d" % rc)
     return key, perm, (int(grid[0]), int(grid[1]))
+
+
+def splitmix64(x: int) -> int:
+    """The oracle's key mixer of reading R16 (sem_oracle.c orc_splitmix64)."""
+    return int(lib().orc_splitmix64_value(x & (2**64 - 1)))
 
 
 def random_order(ne: int, seed: int) -> np.ndarray:

@@ -198,6 +198,8 @@ static uint64_t orc_splitmix64(uint64_t x) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);
 }
+/* the mixer alone, for its pin against the published SplitMix64 sequence (tests) */
+uint64_t orc_splitmix64_value(uint64_t x) { return orc_splitmix64(x); }
 typedef struct { uint64_t k; int32_t id; } orc_kv;
 static int cmp_kv(const void *a, const void *b) {
     const orc_kv *x = (const orc_kv *)a, *y = (const orc_kv *)b;

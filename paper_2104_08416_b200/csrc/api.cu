@@ -1345,40 +1345,43 @@ sem_status sem_mesh_reorder(sem_ctx *ctx, const double *vxy_host, int64_t n_vert
             t.max_local = mm.max_local; t.max_win = mm.max_win; t.max_count = mm.max_count; t.max_nsh = mm.max_nsh;
             return !k7_fits(t, false);
         };
-    build_chunk_arrays:
-        if (gpu_chunks) {
-            CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, B_chunk,
-                                one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd, &ctx->d_intc,
-                                err, s));
-            if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
-            if (too_big(m)) {
-                CK(cudaStreamSynchronize(s));
-                L.release_from(mark);
-                m = ChunkMeta();
-                d = DevChunks{};
-                B_chunk = 256;
-                tr.mark(s, "chunks of 512 do not fit one CTA: rebuilt with 256");
-                goto build_chunk_arrays;
-            }
-            if (check_chunks) {
-                ChunkMeta h;
-                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, h,
-                                  err, one ? nullptr : part.remote.data()))
+        for (;;) {  // one pass, or two when chunks of 512 fall back to 256
+            if (gpu_chunks) {
+                CK(build_chunks_gpu(one ? d_mu_ft : dpart.mu_local, ctx->E, Np, ctx->N, B_chunk,
+                                    one ? nullptr : dpart.remote, da, m, d, &ctx->d_loc_int, &ctx->d_bnd,
+                                    &ctx->d_intc, err, s));
+                if (!err.empty()) return fail(ctx, SEM_E_MESH, err);
+                if (too_big(m)) {
+                    CK(cudaStreamSynchronize(s));
+                    L.release_from(mark);
+                    m = ChunkMeta();
+                    d = DevChunks{};
+                    B_chunk = 256;
+                    tr.mark(s, "chunks of 512 do not fit one CTA: rebuilt with 256");
+                    continue;
+                }
+                if (check_chunks) {
+                    ChunkMeta h;
+                    if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, h,
+                                      err, one ? nullptr : part.remote.data()))
+                        return fail(ctx, SEM_E_MESH, err);
+                    const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
+                    if (!diff.empty())
+                        return fail(ctx, SEM_E_MESH, "GPU chunk builder differs from the host's: " + diff);
+                }
+                std::vector<int32_t>().swap(mu_h);
+                tr.mark(s, "chunk builder (GPU)");
+            } else {
+                if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m, err,
+                                  one ? nullptr : part.remote.data()))
                     return fail(ctx, SEM_E_MESH, err);
-                const std::string diff = compare_chunks(h, m, d, ctx->d_loc_int, s);
-                if (!diff.empty()) return fail(ctx, SEM_E_MESH, "GPU chunk builder differs from the host's: " + diff);
+                if (too_big(m)) {
+                    m = ChunkMeta();
+                    B_chunk = 256;
+                    continue;
+                }
             }
-            std::vector<int32_t>().swap(mu_h);
-            tr.mark(s, "chunk builder (GPU)");
-        } else {
-            if (!build_chunks(one ? mu_h.data() : part.mu_local.data(), ctx->E, Np, ctx->N, B_chunk, m, err,
-                              one ? nullptr : part.remote.data()))
-                return fail(ctx, SEM_E_MESH, err);
-            if (too_big(m)) {
-                m = ChunkMeta();
-                B_chunk = 256;
-                goto build_chunk_arrays;
-            }
+            break;
         }
         if (!gpu_chunks) {
             if (ctx->scatter != SEM_SCATTER_CHUNK) ST(prepare_ablation(ctx, mu_h, E, Np, N, degree, one, m, s));

@@ -130,6 +130,19 @@ def test_random_order_is_bijection_and_seeded():
     assert (a == b).all() and not (a == c).all()
 
 
+def test_splitmix64_published_sequence():
+    # Reading R16 keys the library-side random order by SplitMix64 (Steele, Lea and Flood 2014).
+    # The generator's published reference output for state 0 starts e220a8397b1dcdaf,
+    # 6e789e6aa1b965f4: output k is the mixer of k times the golden-ratio increment.
+    g = 0x9E3779B97F4A7C15
+    assert core.splitmix64(0) == 0xE220A8397B1DCDAF
+    assert core.splitmix64(g) == 0x6E789E6AA1B965F4
+    # the order is the stable sort of ids by splitmix64(seed ^ id)
+    perm = core.random_order(300, 5)
+    keys = [core.splitmix64(5 ^ e) for e in range(300)]
+    assert perm.tolist() == sorted(range(300), key=lambda e: (keys[e], e))
+
+
 def test_first_touch_brute_force():
     rng = np.random.default_rng(3)
     N = 40
