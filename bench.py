@@ -111,13 +111,23 @@ def ncu_traffic(config, kernel):
         return None
 
 
+def graph_split(steps):
+    """sem_step_n's one-rank graph replays (api.cu) after the warm-up's sem_step_n(0) captured
+    them all: (size, replays) for the graphs of 32, 16, 8, 4, 2 and 1 steps."""
+    out, left = [], steps
+    for sz in (32, 16, 8, 4, 2, 1):
+        if left // sz:
+            out.append((sz, left // sz))
+            left -= (left // sz) * sz
+    return out
+
+
 def gpu_launches(steps, info, world):
     """Kernels of this library launched in the timed region: per step K7 + K8
     (+ the interface kernels with several ranks); the one-rank graph loop adds a
-    step-counter kernel per captured step and one counter reset per call."""
+    step-counter kernel per captured step and one counter reset per graph size used."""
     if world == 1 and os.environ.get("SEM_GRAPH", "1") != "0":
-        g = (steps // 32) * 32
-        return int(g * 3 + (steps - g) * info["launches_per_step"] + (1 if g else 0))
+        return int(steps * 3 + len(graph_split(steps)))
     return int(steps * info["launches_per_step"])
 
 
@@ -174,14 +184,16 @@ def run_ours(args):
     info = ctx.sem_get_info()
     E_glob = info["n_elements_global"]
 
-    # warm-up (untimed); sem_step_n(0) captures the step loop's CUDA graph outside the timed region
-    ctx.sem_step_n(args.warmup)
+    # sem_step_n(0) captures the step loop's CUDA graphs outside the timed region; the clock
+    # sampler starts next, and the W warm-up steps run right before the timed region (after the
+    # sampler's start-up pause, so the timed steps do not begin on an idle GPU)
     ctx.sem_step_n(0)
     ctx.sem_sync()
-
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    ctx.sem_step_n(args.warmup)
+    ctx.sem_sync()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -272,16 +284,12 @@ def run_ours(args):
 
 
 def step_loop_label(steps, world):
-    """How sem_step_n(steps) launches (api.cu: sem_step_n): one rank replays a captured CUDA
-    graph of 32 steps for each whole block of 32, the rest as stream launches."""
+    """How sem_step_n(steps) launches (api.cu: sem_step_n): one rank replays captured CUDA
+    graphs of 32 steps for each whole block of 32, then one of 16, 8, 4, 2, 1 steps each as
+    needed for the rest."""
     if world > 1 or os.environ.get("SEM_GRAPH", "1") == "0":
         return "stream launches (%d steps)" % steps
-    g, r = divmod(steps, 32)
-    parts = []
-    if g:
-        parts.append("%d replays of a 32-step CUDA graph" % g)
-    if r:
-        parts.append("%d steps as stream launches" % r)
+    parts = ["%d replay%s of a %d-step CUDA graph" % (n, "s" if n > 1 else "", sz) for sz, n in graph_split(steps)]
     return " + ".join(parts) or "none"
 
 

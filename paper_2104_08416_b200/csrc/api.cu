@@ -185,7 +185,7 @@ struct sem_ctx {
     double *d_U[2] = {nullptr, nullptr};
     double *d_slot = nullptr;
     int32_t *d_cnt = nullptr;  // shared-node arrival counters (K8 fused into K7, SEM_FUSE_K8=1)
-    cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};  // captured step loop per U parity
+    cudaGraphExec_t graph_exec[6][2] = {};  // captured step loops of 32, 16, .., 1 steps per U parity
     // kernel timing inside the graph: the same step loop with event-record nodes around K7 and
     // K8 of every step (gev[3 j .. 3 j + 2] = before K7, after K7, after K8 of step j)
     cudaGraphExec_t graph_exec_t[2] = {nullptr, nullptr};
@@ -565,12 +565,16 @@ StepParams step_params(sem_ctx *ctx) {
     return p;
 }
 
-// ---- CUDA-graph step loop (one rank, leapfrog, chunk scatter, timing off) ----------
+// ---- CUDA-graph step loop (one rank, leapfrog, chunk scatter) --------------------------
 // kGraphSteps consecutive steps (K7, K8, counter += 1 each; an even count, so the
 // U / U^{n-1} ping-pong returns to the same parity) are captured once per parity
 // and replayed; the step index comes from a device counter.  Removes the
-// per-launch host overhead that dominates small meshes.  SEM_GRAPH=0 disables.
+// per-launch host overhead that dominates small meshes.  The remainder of a call
+// (n mod 32 steps) replays the graphs of 16, 8, 4, 2 and 1 steps (an odd one flips
+// the parity); sem_step_n(0) captures all twelve.  Kernel timing mode: 32-step graphs
+// with event nodes, the remainder launched step by step.  SEM_GRAPH=0 disables.
 constexpr int kGraphSteps = 32;
+constexpr int kNGraph = 6;  // graph sizes kGraphSteps >> si
 
 // SEM_COMM_SMS: SMs left to the exchange kernels (NCCL send/recv on the comm stream) while the
 // interior chunks run; SEM_OVERLAP_PROBE_US: one-rank overlap probe (stand-in comm kernel)
@@ -593,17 +597,24 @@ bool graph_ok(sem_ctx *ctx) {
 }
 
 void destroy_graphs(sem_ctx *ctx) {
-    for (auto *set : {ctx->graph_exec, ctx->graph_exec_t})
+    for (int si = 0; si < kNGraph; si++)
         for (int i = 0; i < 2; i++)
-            if (set[i]) { cudaGraphExecDestroy(set[i]); set[i] = nullptr; }
+            if (ctx->graph_exec[si][i]) { cudaGraphExecDestroy(ctx->graph_exec[si][i]); ctx->graph_exec[si][i] = nullptr; }
+    for (int i = 0; i < 2; i++)
+        if (ctx->graph_exec_t[i]) { cudaGraphExecDestroy(ctx->graph_exec_t[i]); ctx->graph_exec_t[i] = nullptr; }
 }
 
-sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
+// the step loop graph of kGraphSteps >> si steps starting at U parity par (timing mode: si = 0
+// with the event nodes), captured on first use
+sem_status graph_steps(sem_ctx *ctx, int64_t reps, int si = 0, int par = -1) {
     CK(cudaSetDevice(ctx->device));
     ST(ensure_tables(ctx));
     cudaStream_t s = ctx->stream;
     const bool timed = ctx->timing;
-    cudaGraphExec_t &ex = (timed ? ctx->graph_exec_t : ctx->graph_exec)[ctx->cur];
+    if (timed) si = 0;
+    if (par < 0) par = ctx->cur;
+    const int nsteps = kGraphSteps >> si;
+    cudaGraphExec_t &ex = timed ? ctx->graph_exec_t[par] : ctx->graph_exec[si][par];
     if (timed && ctx->gev.empty()) {
         ctx->gev.resize(3 * kGraphSteps);
         for (auto &e : ctx->gev) CK(cudaEventCreate(&e));
@@ -619,10 +630,10 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
         const bool pdl = pv && pv[0] == '1';
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         cudaError_t e = cudaSuccess;
-        for (int k = 0; k < kGraphSteps && e == cudaSuccess; k++) {
+        for (int k = 0; k < nsteps && e == cudaSuccess; k++) {
             StepParams p = step_params(ctx);
-            p.U = ctx->d_U[(ctx->cur + k) & 1];
-            p.Uprev = ctx->d_U[1 - ((ctx->cur + k) & 1)];
+            p.U = ctx->d_U[(par + k) & 1];
+            p.Uprev = ctx->d_U[1 - ((par + k) & 1)];
             p.n_dev = ctx->d_nstep;
             if (timed) e = cudaEventRecordWithFlags(ctx->gev[3 * k], s, cudaEventRecordExternal);
             if (e == cudaSuccess) e = launch_k7(ctx->dch, p, ctx->k7_grid, s, nullptr, 0, pdl);
@@ -639,6 +650,7 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
     }
     if (reps == 0) return SEM_OK;
+    if (par != ctx->cur) return fail(ctx, SEM_E_STATE, "graph replay at the other U parity");
     CK(launch_step_set(ctx->d_nstep, ctx->step, s));
     for (int64_t r = 0; r < reps; r++) {
         CK(cudaGraphLaunch(ex, s));
@@ -655,7 +667,8 @@ sem_status graph_steps(sem_ctx *ctx, int64_t reps) {
             }
         }
     }
-    ctx->step += reps * kGraphSteps;
+    ctx->step += reps * nsteps;
+    if (nsteps & 1) ctx->cur ^= (int)(reps & 1);
     return SEM_OK;
 }
 
@@ -1501,11 +1514,27 @@ sem_status sem_step_n(sem_ctx *ctx, int64_t n_steps) {
         return SEM_OK;
     }
     int64_t k = 0;
-    if (n_steps == 0 && graph_ok(ctx)) return graph_steps(ctx, 0);  // capture only (warm-up)
-    if (graph_ok(ctx) && n_steps >= kGraphSteps) {
+    if (n_steps == 0 && graph_ok(ctx)) {  // capture only (warm-up): every size, both parities
+        if (ctx->timing) return graph_steps(ctx, 0);
+        for (int si = 0; si < kNGraph; si++)
+            for (int par = 0; par < 2; par++) ST(graph_steps(ctx, 0, si, par));
+        return SEM_OK;
+    }
+    if (graph_ok(ctx) && ctx->timing && n_steps >= kGraphSteps) {
         const int64_t reps = n_steps / kGraphSteps;
         ST(graph_steps(ctx, reps));
         k = reps * kGraphSteps;
+    } else if (graph_ok(ctx) && !ctx->timing) {
+        for (int si = 0; si < kNGraph; si++) {
+            const int64_t sz = kGraphSteps >> si, reps = (n_steps - k) / sz;
+            // the remainder graphs only once captured (sem_step_n(0)): a first capture costs more
+            // than a few steps' launch gaps save
+            if (si > 0 && reps > 0 && !ctx->graph_exec[si][ctx->cur]) break;
+            if (reps > 0) {
+                ST(graph_steps(ctx, reps, si));
+                k += reps * sz;
+            }
+        }
     }
     for (; k < n_steps; k++) {
         ST(step_phase1(ctx, ctx->world > 1));

@@ -295,8 +295,8 @@ with S.SemContext(0) as c:
 
 
 def test_graph_step_loop_bitwise_equal(tmp_path):
-    """The CUDA-graph step loop (32 captured steps per replay, device step
-    counter) gives the same bits as launching step by step (SEM_GRAPH=0, read once
+    """The CUDA-graph step loop (32 captured steps per replay, the remainder from the
+    16/8/4/2/1-step graphs, device step counter) gives the same bits as launching step by step (SEM_GRAPH=0, read once
     per process: a child process), with and without the kernel-timing events in
     the graph and with a capture-only sem_step_n(0), and matches the oracle."""
     import subprocess
@@ -314,9 +314,9 @@ def test_graph_step_loop_bitwise_equal(tmp_path):
             c.sem_step_n(0)    # capture only: advances nothing
             assert c.sem_read_field()[1] == 0
             c.sem_set_kernel_timing(timing)  # timing: the graph with event-record nodes
-            c.sem_step_n(70)   # 2 graph replays + 6 plain steps
-            c.sem_step_n(3)
-            c.sem_step_n(77)   # odd parity at entry: the other captured graph
+            c.sem_step_n(70)   # 2 replays of the 32-step graph + the 4- and 2-step graphs (timing: 6 plain steps)
+            c.sem_step_n(3)    # the 2- and 1-step graphs: the parity flips
+            c.sem_step_n(77)   # odd parity at entry: the other captured graphs (64 + 8 + 4 + 1)
             U, n = c.sem_read_field()
             assert n == 150
             if timing:
