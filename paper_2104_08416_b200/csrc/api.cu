@@ -552,6 +552,15 @@ sem_status exchange_loopback(sem_ctx **ctxs, int n, int w = 1) {
     return SEM_OK;
 }
 
+// K8 takes the shared nodes in descending order, starting with the slots K7's last chunks wrote
+// (still in L2): C4 K8 0.0275 -> 0.0270 ms, C3 step 0.1861 -> 0.1854 ms with two nodes per
+// thread (profiles/r2s4_k8_ab.md); SEM_K8_REV=0 takes them ascending (A/B)
+bool k8_rev() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("SEM_K8_REV"); v = e && e[0] == '0' ? 0 : 1; }
+    return v == 1;
+}
+
 StepParams step_params(sem_ctx *ctx) {
     StepParams p;
     p.Grr = ctx->d_Grr; p.Gss = ctx->d_Gss; p.Grs = ctx->d_Grs; p.dt2M = ctx->d_dt2M;
@@ -562,6 +571,7 @@ StepParams step_params(sem_ctx *ctx) {
     p.Uprev = ctx->d_U[1 - ctx->cur];
     p.n = ctx->step;
     p.n_dev = nullptr;
+    p.k8_rev = k8_rev() ? 1 : 0;
     return p;
 }
 

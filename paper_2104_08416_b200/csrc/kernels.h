@@ -151,6 +151,8 @@ struct StepParams {
     double amp, f0, t0, dt;
     int64_t n;         // step index of U
     const int64_t *n_dev;  // if set: the step index lives in device memory (CUDA-graph step loop)
+    int32_t k8_rev;        // K8 walks the shared nodes from the last block down (the slots K7's
+                           // last chunks wrote are the ones still in L2)
 };
 // persistent K7 grid: resident CTAs per SM x SMs; reserve_sms SMs' worth of CTA slots are left free
 // (for the exchange kernels on the comm stream while the interior chunks run)

@@ -656,7 +656,8 @@ __global__ void __launch_bounds__(B * G + 32, (G > 1 ? 1 : NP > 21 ? 1 : NP > 10
 __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     pdl_trigger();
     pdl_wait();
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t blk = a.k8_rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int64_t s = blk * (int64_t)blockDim.x + threadIdx.x;
     if (s >= ch.N_sh - ch.N_if) return;  // interface nodes: k_if_partial / k8_if
     const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1];
     SEM_DCHECK(j0 >= 0 && j0 < j1 && j1 <= ch.n_slots, "slot run of a shared node");
@@ -671,6 +672,85 @@ __global__ void k8_fix(const DevChunks ch, const StepParams a) {
     for (int j = j0 + 4; j < j1; j++) y += a.slot[j];
     const double f = (id == a.src) ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
     a.Uprev[id] = leap_update(u, up, m, f, y);
+}
+
+// K8 with two consecutive shared nodes per thread (the default): the three slot-run bounds and
+// both nodes' U^n / U^{n-1} / dt^2/M loads are issued before any slot is read, so a thread keeps
+// twice the independent loads in flight; the same sums in the same order per node as k8_fix
+// (identical bits).  C4: K8 0.0307 -> 0.0275 ms (profiles/r2s4_k8_ab.md).
+__global__ void k8_fix2(const DevChunks ch, const StepParams a) {
+    pdl_trigger();
+    pdl_wait();
+    const int64_t nsh = ch.N_sh - ch.N_if;
+    const int64_t blk = a.k8_rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int64_t s = 2 * (blk * (int64_t)blockDim.x + threadIdx.x);
+    if (s >= nsh) return;  // interface nodes: k_if_partial / k8_if
+    const bool two = s + 1 < nsh;
+    const int j0 = ch.sh_pstart[s], j1 = ch.sh_pstart[s + 1], j2 = two ? ch.sh_pstart[s + 2] : j1;
+    SEM_DCHECK(j0 >= 0 && j0 < j1 && (!two || j1 < j2) && j2 <= ch.n_slots, "slot run of a shared node");
+    const int64_t id = ch.N_int + s;
+    const double u0 = a.U[id], up0 = a.Uprev[id], m0 = a.dt2M[id];
+    double u1 = 0.0, up1 = 0.0, m1 = 0.0;
+    if (two) { u1 = a.U[id + 1]; up1 = a.Uprev[id + 1]; m1 = a.dt2M[id + 1]; }
+    double p0[4], p1[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        p0[d] = (j0 + d < j1) ? a.slot[j0 + d] : 0.0;
+        p1[d] = (j1 + d < j2) ? a.slot[j1 + d] : 0.0;
+    }
+    double y0 = p0[0], y1 = p1[0];  // contiguous slots, ascending chunk order
+#pragma unroll
+    for (int d = 1; d < 4; d++) { y0 += p0[d]; y1 += p1[d]; }
+    for (int j = j0 + 4; j < j1; j++) y0 += a.slot[j];
+    for (int j = j1 + 4; j < j2; j++) y1 += a.slot[j];
+    const bool hs = id == a.src || id + 1 == a.src;
+    const double fs = hs ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
+    a.Uprev[id] = leap_update(u0, up0, m0, id == a.src ? fs : 0.0, y0);
+    if (two) a.Uprev[id + 1] = leap_update(u1, up1, m1, id + 1 == a.src ? fs : 0.0, y1);
+}
+
+// K8 with NPT consecutive shared nodes per thread (SEM_K8_NPT=4, A/B): the k8_fix2 scheme for
+// any NPT (same sums, same order per node).
+template <int NPT>
+__global__ void k8_fixn(const DevChunks ch, const StepParams a) {
+    pdl_trigger();
+    pdl_wait();
+    const int64_t nsh = ch.N_sh - ch.N_if;
+    const int64_t blk = a.k8_rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int64_t s = NPT * (blk * (int64_t)blockDim.x + threadIdx.x);
+    if (s >= nsh) return;  // interface nodes: k_if_partial / k8_if
+    const int nn = nsh - s < NPT ? (int)(nsh - s) : NPT;  // nodes of this thread
+    int j[NPT + 1];
+    j[0] = ch.sh_pstart[s];
+#pragma unroll
+    for (int q = 1; q <= NPT; q++) j[q] = q <= nn ? ch.sh_pstart[s + q] : j[q - 1];
+    const int64_t id = ch.N_int + s;
+    double u[NPT], up[NPT], m[NPT];
+#pragma unroll
+    for (int q = 0; q < NPT; q++) {
+        SEM_DCHECK(q >= nn || (j[q] >= 0 && j[q] < j[q + 1] && j[q + 1] <= ch.n_slots), "slot run of a shared node");
+        u[q] = q < nn ? a.U[id + q] : 0.0;
+        up[q] = q < nn ? a.Uprev[id + q] : 0.0;
+        m[q] = q < nn ? a.dt2M[id + q] : 0.0;
+    }
+    double y[NPT];
+#pragma unroll
+    for (int q = 0; q < NPT; q++) {
+        double part[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) part[d] = (j[q] + d < j[q + 1]) ? a.slot[j[q] + d] : 0.0;
+        y[q] = part[0];  // contiguous slots, ascending chunk order
+#pragma unroll
+        for (int d = 1; d < 4; d++) y[q] += part[d];
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; q++)
+        for (int k = j[q] + 4; k < j[q + 1]; k++) y[q] += a.slot[k];
+    const bool hs = a.src >= id && a.src < id + nn;
+    const double fs = hs ? a.amp * ricker_dev((double)step_index(a) * a.dt, a.f0, a.t0) : 0.0;
+#pragma unroll
+    for (int q = 0; q < NPT; q++)
+        if (q < nn) a.Uprev[id + q] = leap_update(u[q], up[q], m[q], id + q == a.src ? fs : 0.0, y[q]);
 }
 
 // ---- multi-GPU interface -----------------------------------------
@@ -990,6 +1070,16 @@ cudaError_t launch_k8(const DevChunks &ch, const StepParams &p, cudaStream_t s, 
         const int b = v ? atoi(v) : 128;
         return (b == 64 || b == 128 || b == 256 || b == 512 || b == 1024) ? b : 128;
     }();
+    // shared nodes per thread: 2 (C4 step 0.3782 -> 0.3763 ms, C3 0.1875 -> 0.1861 ms against 1;
+    // profiles/r2s4_k8_ab.md); SEM_K8_NPT=1|2|4 overrides (A/B)
+    static const int npt = [] {
+        const char *v = getenv("SEM_K8_NPT");
+        const int n = v ? atoi(v) : 2;
+        return (n == 1 || n == 2 || n == 4) ? n : 2;
+    }();
+    const int64_t nsh = ch.N_sh - ch.N_if;
+    if (npt == 2) return launch_ex(k8_fix2, blocks_for((nsh + 1) / 2, bt), (unsigned)bt, 0, s, pdl, ch, p);
+    if (npt == 4) return launch_ex(k8_fixn<4>, blocks_for((nsh + 3) / 4, bt), (unsigned)bt, 0, s, pdl, ch, p);
     return launch_ex(k8_fix, blocks_for(ch.N_sh - ch.N_if, bt), (unsigned)bt, 0, s, pdl, ch, p);
 }
 
