@@ -1,4 +1,5 @@
 #!/bin/bash
+# (SEM_K7_DYN exists only in the experiment build profiles/experiments/r2s4_k7_ticket_schedule.diff, removed from the library)
 # Session-4 A/B on a GPU box: HEAD build (libsem_base.so) against the working tree's libsem.so
 # on C4 and C3 (defaults), then the prefetched ticket schedule against round-robin.
 mkdir -p gpurun_out

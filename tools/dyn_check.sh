@@ -1,4 +1,5 @@
 #!/bin/bash
+# (SEM_K7_DYN exists only in the experiment build profiles/experiments/r2s4_k7_ticket_schedule.diff, removed from the library)
 # Ticket-scheduled K7 (SEM_K7_DYN=1) on a GPU box: the K7 parity tests under it, then an
 # alternating A/B against the round-robin default on C4 and C3.
 mkdir -p gpurun_out

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (SEM_K7_DYN exists only in the experiment build profiles/experiments/r2s4_k7_ticket_schedule.diff, removed from the library)
 # A/B of the K7 ticket schedule (SEM_K7_DYN) and K8's descending node order (SEM_K8_REV) on a
 # GPU box: parity tests under both knobs, then alternating bench runs of the four combinations.
 #   tools/sched_ab.sh [config] [steps]
