@@ -661,6 +661,10 @@ def run_reference(args):
     from oracle.core import OracleSEM
     from paper_2104_08416_b200 import meshgen as mg
     budget_s = 60.0
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 is the only one that works here,
+    # so it takes the host's cores as the N=1 launch (plain `python bench.py`) does
+    if "TORCHELASTIC_RUN_ID" in os.environ and os.environ.get("OMP_NUM_THREADS") == "1":
+        core.set_num_threads(len(os.sched_getaffinity(0)))
     nthr = core.num_threads()
     # calibrate the oracle's element-update rate on a small sample of the recipe
     cal = mg.config(args.config, 16)
